@@ -1,0 +1,188 @@
+/*
+ * hp.h — C ABI of the B200-native swarm scorer for arXiv 2005.07068
+ * ("Recognition of 26 Degrees of Freedom of Hands Using Model-based approach and
+ * Depth-Color Images").  Library: paper_2005_07068_b200/libhp.so (sm_100a).
+ *
+ * Citations: P:Lnn = /root/reference/PAPER.md line nn; DESIGN §n = /root/repo/DESIGN.md.
+ *
+ * Conventions for every entry point
+ *  - Every function returns hp_status; no exception or exit crosses the ABI.  On failure
+ *    the message is available from hp_last_error(ctx) (thread-local global text when ctx
+ *    is NULL or creation failed).
+ *  - Units: mm for positions and depths, radians for angles, depth 0 = undefined.
+ *  - Pose layout (Eq. (1)-(3); flattening order S:L122): 26 values
+ *    [x_c, y_c, z_c, th_x, th_y, th_z, then thumb, index, middle, ring, little each
+ *    (th_MP^x, th_MP^z, th_PIP, th_DIP)], row-major [N][26].
+ *  - Streams: `stream` is a cudaStream_t (passed as void*; NULL = the legacy default
+ *    stream).  Device-pointer calls are enqueued on it and return without synchronising
+ *    unless stated otherwise.
+ *  - Ownership: the context owns its device workspace (sized by max_particles at
+ *    creation) and a copy of the observation.  Caller buffers are only read/written
+ *    during the call (host pointers) or until the enqueued work completes (device
+ *    pointers); the library never frees or retains them.
+ *  - Threads: one host thread per context at a time; distinct contexts are independent.
+ *  - There is no CPU fallback: without a usable sm_100 device hp_create fails.
+ */
+#ifndef HP_H
+#define HP_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HP_NDOF 26  /* Eq. (3): h = (q_i, q_c), 5 x 4 finger angles + 6 wrist DOF */
+#define HP_NPRIM 38 /* 3 palm + 5 x (3 segments + 4 spheres) */
+#define HP_REC_FLOATS 24
+
+typedef struct hp_ctx hp_ctx;
+
+typedef enum {
+  HP_OK = 0,
+  HP_ERR_INVALID_ARG = 1, /* null pointer, bad size, bad parameter (see each call) */
+  HP_ERR_CUDA = 2,        /* a CUDA runtime / driver call failed                   */
+  HP_ERR_OOM = 3,         /* device or pinned-host allocation failed               */
+  HP_ERR_NCCL = 4,        /* NCCL failure in the sharded mode                      */
+  HP_ERR_STATE = 5,       /* call not valid in the context's current state         */
+  HP_ERR_NO_DEVICE = 6    /* no sm_100 device / library built for another arch     */
+} hp_status;
+
+/* Camera C ("focal length and viewing direction"): pinhole, pixel (u, v) casts the
+ * ray d = ((u + 0.5 - cx)/fx, (v + 0.5 - cy)/fy, 1); depth = camera z.  The per-pixel
+ * arithmetic is fp32.  Errors: width/height < 1, fx/fy <= 0, !(0 < z_near < z_far). */
+typedef struct {
+  int32_t width, height;
+  float fx, fy, cx, cy;
+  float z_near_mm, z_far_mm;
+} hp_intrinsics;
+
+/* Hand model dimensions ("measured from a real hand"; values DESIGN §2). */
+typedef struct {
+  float palm_half_w, palm_half_t, palm_len, palm_cap_half_len;
+  float base[5][3];    /* MCP centres in the hand frame H             */
+  float seg_len[5][3]; /* L1, L2, L3                                  */
+  float radius[5][4];  /* joint spheres MCP, PIP, DIP, tip            */
+  float thumb_ell_x, thumb_ell_z;       /* thumb proximal ellipsoid cross semi-axes */
+  float thumb_yaw_deg, thumb_pitch_deg; /* R_T0 = Rz(yaw) Ry(pitch)                 */
+} hp_hand_dims;
+
+/* Eq. (4)-(5) constants and readings. */
+typedef struct {
+  double d_m;         /* r_m threshold, mm (10)                           */
+  double d_M;         /* numerator clamp, mm (40) — AMB-1                 */
+  double lambda;      /* area weight (20)                                 */
+  double lambda_k;    /* collision weight (10)                            */
+  double depth_scale; /* mm -> cm (0.1) — AMB-2                           */
+  double kc_rest;     /* rho in phi = MPz(radial) - MPz(ulnar) + rho (0)  */
+  int32_t clamp_at_dm;/* 1 = literal Eq. (4) clamp at d_m                 */
+} hp_cost_params;
+
+/* PSO (Eq. (6)-(7)); DESIGN §4. */
+typedef struct {
+  uint64_t seed;
+  int32_t particles;       /* >= 1 and <= max_particles (paper: 64)   */
+  int32_t generations;     /* >= 1 (paper: 30)                        */
+  int32_t mutation_period; /* >= 0, 0 = off (paper: 3)                */
+  int32_t per_dim_r;       /* 0: scalar r1, r2 per particle (AMB-15)          */
+  double c1, c2;           /* c1 + c2 > 4 (paper: 2.8, 1.3)           */
+  double mutation_fraction;/* [0, 1] (paper: 0.5)                             */
+  double stop_threshold;   /* stop when G's cost < this; -INFINITY = off      */
+  const double* init_center; /* host [26] or NULL: init box = centre +- radius  */
+  const double* init_radius; /* host [26] or NULL   intersected with Tables 1-2 */
+} hp_pso_params;
+
+/* Fill with the defaults of DESIGN §2 / P:L130 / P:L148-152.  Errors: NULL. */
+hp_status hp_default_dims(hp_hand_dims* out);
+hp_status hp_default_cost(hp_cost_params* out);
+hp_status hp_default_pso(hp_pso_params* out);
+/* AMB-12 Kinect-like intrinsics for a width x height frame (fx = 525 * width / 640). */
+hp_status hp_default_intrinsics(int32_t width, int32_t height, hp_intrinsics* out);
+/* Tables 1-2 in pose units (rad, mm), host arrays of 26. */
+hp_status hp_bounds(double lo[26], double hi[26]);
+
+/* Create a context on `device` (the current CUDA device if < 0) with a workspace for up
+ * to max_particles poses per call.  dims/cost may be NULL (defaults).  The observation
+ * starts empty (all undefined); set it with hp_set_observation.
+ * Errors: INVALID_ARG (NULL out/cam, bad intrinsics, max_particles < 1), NO_DEVICE, OOM. */
+hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims,
+                    const hp_cost_params* cost, int32_t max_particles, int32_t device,
+                    hp_ctx** out);
+
+/* Observation O = (O_s, O_d): depth [H][W] fp32 mm (0, negative or non-finite =
+ * undefined) and skin mask [H][W] u8 (nonzero = hand).  Both host (on_device = 0) or both
+ * device (on_device = 1) pointers, row-major, no padding.  The context copies and packs
+ * them into one u32 per pixel and computes S_o = sum o_s (DESIGN §1 row A0); the caller
+ * may free its buffers when the call returns (the call synchronises `stream`).
+ * Errors: INVALID_ARG (NULL ctx/depth/mask), CUDA. */
+hp_status hp_set_observation(hp_ctx* ctx, const float* depth_mm, const uint8_t* mask,
+                             int32_t on_device, void* stream);
+
+/* Simulation protocol: render pose h_ref (host fp64 [26]) with this context's
+ * camera and model into depth_dev [H][W] fp32 (0 = no hit) and mask_dev [H][W] u8
+ * (silhouette), both device buffers (mask_dev may be NULL).  Async on `stream`. */
+hp_status hp_render_observation(hp_ctx* ctx, const double* h_ref, float* depth_dev,
+                                uint8_t* mask_dev, void* stream);
+
+/* Objective E(h, O) = D(O, h, C) + lambda_k kc(h) (Eq. (4)-(5)) of n poses.
+ * poses_dev: device fp32 [n][26]; costs_dev: device fp32 [n].  Poses are scored as given
+ * (no clamping); non-finite poses give NaN.  n = 0 is a no-op.  Async on `stream`.
+ * Errors: INVALID_ARG (NULL ctx/pointers with n > 0, n < 0 or n > max_particles). */
+hp_status hp_eval_costs(hp_ctx* ctx, const float* poses_dev, int64_t n, float* costs_dev,
+                        void* stream);
+
+/* Same with HOST buffers: copies poses in, scores, copies costs out, then synchronises
+ * `stream` (the end-to-end path a host application calls). */
+hp_status hp_eval_costs_host(hp_ctx* ctx, const float* poses_host, int64_t n,
+                             float* costs_host, void* stream);
+
+/* Per-pose integer sums behind Eq. (4) (test hook, async): sums_dev [n][4] u64 =
+ * (sum r_m, sum (o_s AND r_m), sum over both-defined pixels of rint(min(|o_d - r_d|,
+ * clamp) * 2^20), number of both-defined pixels); costs64_dev [n] fp64 may be NULL. */
+hp_status hp_eval_sums(hp_ctx* ctx, const float* poses_dev, int64_t n, uint64_t* sums_dev,
+                       double* costs64_dev, void* stream);
+
+/* Full PSO fit on the GPU: init, K generations of update +
+ * mutation + evaluation + bookkeeping captured in one CUDA graph, one device->host copy at
+ * the end.  Synchronous.  Outputs (host): best_pose [26] (G), best_cost (its E), trace
+ * [generations] (G's cost after each generation; entries after an early stop repeat the
+ * last value, may be NULL), gens_run (may be NULL).
+ * Errors: INVALID_ARG (particles < 1 or > max_particles, generations < 1, c1 + c2 <= 4,
+ * mutation_fraction outside [0, 1], mutation_period < 0, NULL outputs), CUDA. */
+hp_status hp_pso_fit(hp_ctx* ctx, const hp_pso_params* params, double* best_pose,
+                     double* best_cost, double* trace, int32_t* gens_run, void* stream);
+
+/* Final swarm state of the last hp_pso_fit / hp_debug_pso_sphere (host, synchronous):
+ * X, V, P [particles][D] and Pcost [particles]; any pointer may be NULL. */
+hp_status hp_pso_state(hp_ctx* ctx, double* X, double* V, double* P, double* Pcost);
+
+/* ---- test hooks ------------------------------------------------------------------- */
+/* FK of one host fp64 pose on the device (the same device function hp_eval_costs runs):
+ * records [38][24] fp32 (layout DESIGN §9), boxes [38][4] int32 (x0, y0, x1, y1 inclusive,
+ * x0 > x1 = empty), joints [5][4][3] fp64 camera-frame joint centres, kc (fp64).  Any
+ * output may be NULL.  Synchronous. */
+hp_status hp_debug_fk(hp_ctx* ctx, const double* pose, float* records, int32_t* boxes,
+                      double* joints, double* kc);
+/* Depth image [H][W] fp32 (device) of the pose pose_dev (device fp32 [26]) produced by
+ * the same tile/culling/intersection code as hp_eval_costs.  Async. */
+hp_status hp_debug_render(hp_ctx* ctx, const float* pose_dev, float* depth_dev, void* stream);
+/* The PSO of hp_pso_fit on f(x) = sum_d (x_d - centre_d)^2 (fp64, left to right, no FMA)
+ * over D <= 64 dims with bounds lo/hi, init box, mutation dims [mut_lo, mut_hi); host
+ * arrays.  Same outputs as hp_pso_fit.  Synchronous. */
+hp_status hp_debug_pso_sphere(hp_ctx* ctx, int32_t D, const double* lo, const double* hi,
+                              const double* init_lo, const double* init_hi, int32_t mut_lo,
+                              int32_t mut_hi, const double* centre, const hp_pso_params* params,
+                              double* best_x, double* best_cost, double* trace,
+                              int32_t* gens_run, void* stream);
+
+/* Number of kernel launches the last hp_eval_costs / hp_pso_fit enqueued (bench). */
+int64_t hp_last_launch_count(const hp_ctx* ctx);
+/* Split factor S (CTAs per particle) used for n poses. */
+int32_t hp_splits_for(const hp_ctx* ctx, int64_t n);
+
+const char* hp_last_error(const hp_ctx* ctx);
+void hp_destroy(hp_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

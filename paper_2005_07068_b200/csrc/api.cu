@@ -1,0 +1,714 @@
+// api.cu — the C ABI of include/hp.h: context, observation upload, TMA descriptor,
+// evaluation entry points, the CUDA-graph PSO driver and the test hooks.
+#include <cudaTypedefs.h>
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/hp.h"
+#include "common.cuh"
+
+using namespace hp;
+
+namespace {
+
+thread_local std::string g_err = "";
+
+struct Graph {
+  cudaGraphExec_t exec = nullptr;
+  int N = -1, D = -1, K = -1, period = -1, per_dim_r = -1, nmut = -1, mut_lo = -1, mut_hi = -1;
+  int sphere = -1;
+};
+
+}  // namespace
+
+struct hp_ctx {
+  int device = 0, sm_count = 0;
+  hp_intrinsics cam{};
+  hp_hand_dims dims{};
+  hp_cost_params cost{};
+  int max_n = 0;
+  CamParams camp{};
+  DimsD dimsd{};
+  CostD costd{};
+  // observation
+  uint32_t* obs = nullptr;
+  int pitch_words = 0;
+  unsigned long long* S_o = nullptr;
+  CUtensorMap tmap{};
+  float* up_depth = nullptr;  // staging for host uploads
+  uint8_t* up_mask = nullptr;
+  // evaluation workspace
+  unsigned long long* acc = nullptr;
+  unsigned int* counters = nullptr;
+  float* poses32 = nullptr;
+  float* costs32 = nullptr;
+  float* h_poses = nullptr;  // pinned
+  float* h_costs = nullptr;  // pinned
+  double* scratch = nullptr; // 26 + 38*24 + ... device scratch for hooks
+  // PSO
+  double *X = nullptr, *V = nullptr, *P = nullptr, *Pc = nullptr, *E = nullptr;
+  double *G = nullptr, *Gc = nullptr, *trace = nullptr, *bnd = nullptr, *centre = nullptr;
+  int* mark = nullptr;
+  int* flags = nullptr;  // [0] done, [1] gens_run
+  PsoDyn* dyn = nullptr;
+  double* h_out = nullptr;  // pinned: G[64], Gc, trace[K], gens_run
+  int trace_cap = 0;
+  int last_N = 0, last_D = 0;
+  Graph graph;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev = nullptr;
+  int64_t last_launches = 0;
+  CUtensorMap* tmap_g = nullptr;
+  int use_tma = 1;   // HP_NO_TMA=1 in the environment selects plain loads (A/B, debugging)
+  int sync_debug = 0;  // HP_SYNC_DEBUG=1: synchronise after every launch
+  std::string err;
+};
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e__ = (call);                                                          \
+    if (e__ != cudaSuccess) {                                                          \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e__);                  \
+      return e__ == cudaErrorMemoryAllocation ? HP_ERR_OOM : HP_ERR_CUDA;              \
+    }                                                                                  \
+  } while (0)
+
+#define ARG(cond, msg)                \
+  do {                                \
+    if (!(cond)) {                    \
+      if (ctx) ctx->err = (msg);      \
+      g_err = (msg);                  \
+      return HP_ERR_INVALID_ARG;      \
+    }                                 \
+  } while (0)
+
+static double deg2rad(double d) { return d * (M_PI / 180.0); }
+
+extern "C" {
+
+hp_status hp_default_dims(hp_hand_dims* d) {
+  if (!d) return HP_ERR_INVALID_ARG;
+  static const float base[5][3] = {{30, -10, -8}, {27, -88, 0}, {9, -92, 0}, {-9, -89, 0}, {-26, -83, 0}};
+  static const float len[5][3] = {{45, 32, 27}, {45, 27, 22}, {48, 30, 24}, {45, 28, 23}, {36, 21, 20}};
+  static const float rad[5][4] = {
+      {11, 10, 8.5f, 7.5f}, {9, 8, 7, 6}, {9.5f, 8.5f, 7.5f, 6.5f}, {9, 8, 7, 6}, {8, 7, 6.5f, 5.5f}};
+  d->palm_half_w = 45;
+  d->palm_half_t = 15;
+  d->palm_len = 80;
+  d->palm_cap_half_len = 10;
+  memcpy(d->base, base, sizeof base);
+  memcpy(d->seg_len, len, sizeof len);
+  memcpy(d->radius, rad, sizeof rad);
+  d->thumb_ell_x = 12;
+  d->thumb_ell_z = 10;
+  d->thumb_yaw_deg = 40;
+  d->thumb_pitch_deg = 90;
+  return HP_OK;
+}
+
+hp_status hp_default_cost(hp_cost_params* c) {
+  if (!c) return HP_ERR_INVALID_ARG;
+  c->d_m = 10.0;  // 1 cm
+  c->d_M = 40.0;  // 4 cm
+  c->lambda = 20.0;
+  c->lambda_k = 10.0;
+  c->depth_scale = 0.1;
+  c->kc_rest = 0.0;
+  c->clamp_at_dm = 0;
+  return HP_OK;
+}
+
+hp_status hp_default_pso(hp_pso_params* p) {
+  if (!p) return HP_ERR_INVALID_ARG;
+  p->seed = 0;
+  p->particles = 64;
+  p->generations = 30;
+  p->mutation_period = 3;
+  p->per_dim_r = 0;
+  p->c1 = 2.8;
+  p->c2 = 1.3;
+  p->mutation_fraction = 0.5;
+  p->stop_threshold = -INFINITY;
+  p->init_center = nullptr;
+  p->init_radius = nullptr;
+  return HP_OK;
+}
+
+hp_status hp_default_intrinsics(int32_t w, int32_t h, hp_intrinsics* o) {
+  if (!o || w < 1 || h < 1) return HP_ERR_INVALID_ARG;
+  const float s = (float)w / 640.f;
+  o->width = w;
+  o->height = h;
+  o->fx = 525.f * s;
+  o->fy = 525.f * s;
+  o->cx = 0.5f * (float)w;
+  o->cy = 0.5f * (float)h;
+  o->z_near_mm = 300.f;
+  o->z_far_mm = 2000.f;
+  return HP_OK;
+}
+
+hp_status hp_bounds(double lo[26], double hi[26]) {
+  if (!lo || !hi) return HP_ERR_INVALID_ARG;
+  // Tables 1-2
+  static const double wl[6] = {-900, -680, 500, -30, -70, -35};
+  static const double wh[6] = {900, 680, 1500, 120, 75, 20};
+  static const double fl[5][4] = {{0, -15, 0, -15}, {0, -15, 0, 0}, {0, -10, 0, 0}, {0, -30, 0, 0}, {0, -45, 0, 0}};
+  static const double fh[5][4] = {{90, 60, 50, 70}, {90, 15, 100, 60}, {90, 10, 100, 60}, {90, 0, 100, 60}, {90, 0, 100, 60}};
+  for (int i = 0; i < 6; i++) {
+    lo[i] = i < 3 ? wl[i] : deg2rad(wl[i]);
+    hi[i] = i < 3 ? wh[i] : deg2rad(wh[i]);
+  }
+  for (int f = 0; f < 5; f++)
+    for (int j = 0; j < 4; j++) {
+      lo[6 + 4 * f + j] = deg2rad(fl[f][j]);
+      hi[6 + 4 * f + j] = deg2rad(fh[f][j]);
+    }
+  return HP_OK;
+}
+
+const char* hp_last_error(const hp_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+int64_t hp_last_launch_count(const hp_ctx* ctx) { return ctx ? ctx->last_launches : -1; }
+
+int32_t hp_splits_for(const hp_ctx* ctx, int64_t n) {
+  if (!ctx || n <= 0) return 1;
+  // enough CTAs for ~4 resident 8-warp CTAs per SM; each split strides over the tiles
+  const int64_t target = (int64_t)ctx->sm_count * 4;
+  int64_t s = (target + n - 1) / n;
+  if (s < 1) s = 1;
+  if (s > 32) s = 32;
+  return (int32_t)s;
+}
+
+void hp_destroy(hp_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->graph.exec) cudaGraphExecDestroy(ctx->graph.exec);
+  void* dev[] = {ctx->obs, ctx->S_o, ctx->up_depth, ctx->up_mask, ctx->acc, ctx->counters,
+                 ctx->poses32, ctx->costs32, ctx->scratch, ctx->X, ctx->V, ctx->P, ctx->Pc,
+                 ctx->E, ctx->G, ctx->Gc, ctx->trace, ctx->bnd, ctx->centre, ctx->mark,
+                 ctx->flags, ctx->dyn, ctx->tmap_g};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  if (ctx->h_poses) cudaFreeHost(ctx->h_poses);
+  if (ctx->h_costs) cudaFreeHost(ctx->h_costs);
+  if (ctx->h_out) cudaFreeHost(ctx->h_out);
+  if (ctx->ev) cudaEventDestroy(ctx->ev);
+  if (ctx->st) cudaStreamDestroy(ctx->st);
+  delete ctx;
+}
+
+static hp_status make_tmap(hp_ctx* ctx) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) {
+      ctx->err = "cuTensorMapEncodeTiled unavailable";
+      return HP_ERR_CUDA;
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t gdim[2] = {(cuuint64_t)ctx->cam.width, (cuuint64_t)ctx->cam.height};
+  cuuint64_t gstride[1] = {(cuuint64_t)ctx->pitch_words * 4};
+  cuuint32_t box[2] = {(cuuint32_t)kTileW, (cuuint32_t)kTileH};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode(&ctx->tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, ctx->obs, gdim, gstride,
+                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    ctx->err = "cuTensorMapEncodeTiled failed: " + std::to_string((int)r);
+    return HP_ERR_CUDA;
+  }
+  return HP_OK;
+}
+
+hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp_cost_params* cost,
+                    int32_t max_particles, int32_t device, hp_ctx** out) {
+  hp_ctx* ctx = nullptr;
+  ARG(out && cam, "hp_create: NULL argument");
+  *out = nullptr;
+  ARG(cam->width >= 1 && cam->height >= 1, "hp_create: width/height < 1");
+  ARG(cam->fx > 0 && cam->fy > 0, "hp_create: fx/fy <= 0");
+  ARG(cam->z_near_mm > 0 && cam->z_far_mm > cam->z_near_mm, "hp_create: need 0 < z_near < z_far");
+  ARG(max_particles >= 1, "hp_create: max_particles < 1");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    g_err = "hp_create: no CUDA device";
+    return HP_ERR_NO_DEVICE;
+  }
+  if (device < 0) cudaGetDevice(&device);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10 || prop.minor != 0) {
+    g_err = "hp_create: libhp is built for sm_100a (B200); device is sm_" +
+            std::to_string(prop.major) + std::to_string(prop.minor);
+    return HP_ERR_NO_DEVICE;
+  }
+  ctx = new hp_ctx();
+  ctx->device = device;
+  ctx->sm_count = prop.multiProcessorCount;
+  ctx->cam = *cam;
+  if (dims) ctx->dims = *dims; else hp_default_dims(&ctx->dims);
+  if (cost) ctx->cost = *cost; else hp_default_cost(&ctx->cost);
+  ctx->max_n = max_particles;
+  if (const char* e = getenv("HP_NO_TMA")) ctx->use_tma = atoi(e) ? 0 : 1;
+  if (const char* e = getenv("HP_TMA_MODE")) ctx->use_tma = atoi(e);
+  if (const char* e = getenv("HP_SYNC_DEBUG")) ctx->sync_debug = atoi(e);
+  hp_status st = HP_OK;
+#define CKC(call)                                 \
+  do {                                            \
+    cudaError_t e__ = (call);                     \
+    if (e__ != cudaSuccess) {                     \
+      g_err = std::string(#call) + ": " + cudaGetErrorString(e__); \
+      hp_destroy(ctx);                            \
+      return e__ == cudaErrorMemoryAllocation ? HP_ERR_OOM : HP_ERR_CUDA; \
+    }                                             \
+  } while (0)
+  CKC(cudaSetDevice(device));
+  CKC(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
+  CKC(cudaEventCreateWithFlags(&ctx->ev, cudaEventDisableTiming));
+  // device parameter blocks
+  ctx->camp = CamParams{cam->width, cam->height, cam->fx, cam->fy, cam->cx, cam->cy,
+                        cam->z_near_mm, cam->z_far_mm};
+  const hp_hand_dims& d = ctx->dims;
+  DimsD& dd = ctx->dimsd;
+  dd.palm_half_w = d.palm_half_w;
+  dd.palm_half_t = d.palm_half_t;
+  dd.palm_len = d.palm_len;
+  dd.cap_half = d.palm_cap_half_len;
+  for (int f = 0; f < 5; f++) {
+    for (int i = 0; i < 3; i++) {
+      dd.base[f][i] = d.base[f][i];
+      dd.len[f][i] = d.seg_len[f][i];
+    }
+    for (int i = 0; i < 4; i++) dd.rad[f][i] = d.radius[f][i];
+  }
+  dd.th_x = d.thumb_ell_x;
+  dd.th_z = d.thumb_ell_z;
+  {  // R_T0 = Rz(yaw) Ry(pitch)
+    const double a = deg2rad(d.thumb_yaw_deg), b = deg2rad(d.thumb_pitch_deg);
+    const double ca = cos(a), sa = sin(a), cb = cos(b), sb = sin(b);
+    const double Rz[3][3] = {{ca, -sa, 0}, {sa, ca, 0}, {0, 0, 1}};
+    const double Ry[3][3] = {{cb, 0, sb}, {0, 1, 0}, {-sb, 0, cb}};
+    for (int i = 0; i < 3; i++)
+      for (int j = 0; j < 3; j++)
+        dd.RT0[i][j] = Rz[i][0] * Ry[0][j] + Rz[i][1] * Ry[1][j] + Rz[i][2] * Ry[2][j];
+  }
+  const hp_cost_params& c = ctx->cost;
+  ctx->costd = CostD{(float)c.d_m, (float)(c.clamp_at_dm ? c.d_m : c.d_M), c.lambda, c.lambda_k,
+                     c.depth_scale, c.kc_rest};
+  // observation buffers
+  const int W = cam->width, H = cam->height;
+  ctx->pitch_words = (W + 3) & ~3;  // 16-byte row pitch for TMA
+  CKC(cudaMalloc(&ctx->obs, (size_t)ctx->pitch_words * H * 4));
+  CKC(cudaMemset(ctx->obs, 0, (size_t)ctx->pitch_words * H * 4));
+  CKC(cudaMalloc(&ctx->S_o, sizeof(unsigned long long)));
+  CKC(cudaMemset(ctx->S_o, 0, sizeof(unsigned long long)));
+  CKC(cudaMalloc(&ctx->up_depth, (size_t)W * H * 4));
+  CKC(cudaMalloc(&ctx->up_mask, (size_t)W * H));
+  st = make_tmap(ctx);
+  if (st != HP_OK) {
+    g_err = ctx->err;
+    hp_destroy(ctx);
+    return st;
+  }
+  CKC(cudaMalloc(&ctx->tmap_g, sizeof(CUtensorMap)));
+  CKC(cudaMemcpy(ctx->tmap_g, &ctx->tmap, sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  // evaluation workspace
+  const size_t N = (size_t)max_particles;
+  CKC(cudaMalloc(&ctx->acc, N * 4 * sizeof(unsigned long long)));
+  CKC(cudaMemset(ctx->acc, 0, N * 4 * sizeof(unsigned long long)));
+  CKC(cudaMalloc(&ctx->counters, N * sizeof(unsigned int)));
+  CKC(cudaMemset(ctx->counters, 0, N * sizeof(unsigned int)));
+  CKC(cudaMalloc(&ctx->poses32, N * kNdof * sizeof(float)));
+  CKC(cudaMalloc(&ctx->costs32, N * sizeof(float)));
+  CKC(cudaMallocHost(&ctx->h_poses, N * kNdof * sizeof(float)));
+  CKC(cudaMallocHost(&ctx->h_costs, N * sizeof(float)));
+  CKC(cudaMalloc(&ctx->scratch, 4096 * sizeof(double)));
+  // PSO state (D <= 64 for the generic hook, 26 for the hand)
+  const size_t ND = N * 64;
+  CKC(cudaMalloc(&ctx->X, ND * sizeof(double)));
+  CKC(cudaMalloc(&ctx->V, ND * sizeof(double)));
+  CKC(cudaMalloc(&ctx->P, ND * sizeof(double)));
+  CKC(cudaMalloc(&ctx->Pc, N * sizeof(double)));
+  CKC(cudaMalloc(&ctx->E, N * sizeof(double)));
+  CKC(cudaMalloc(&ctx->mark, N * sizeof(int)));
+  CKC(cudaMalloc(&ctx->G, 64 * sizeof(double)));
+  CKC(cudaMalloc(&ctx->Gc, sizeof(double)));
+  CKC(cudaMalloc(&ctx->bnd, 4 * 64 * sizeof(double)));
+  CKC(cudaMalloc(&ctx->centre, 64 * sizeof(double)));
+  CKC(cudaMalloc(&ctx->flags, 2 * sizeof(int)));
+  CKC(cudaMalloc(&ctx->dyn, sizeof(PsoDyn)));
+  ctx->trace_cap = 0;
+  CKC(cudaDeviceSynchronize());
+#undef CKC
+  *out = ctx;
+  return HP_OK;
+}
+
+hp_status hp_set_observation(hp_ctx* ctx, const float* depth, const uint8_t* mask,
+                             int32_t on_device, void* stream) {
+  ARG(ctx && depth && mask, "hp_set_observation: NULL argument");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int W = ctx->cam.width, H = ctx->cam.height;
+  const float* dd = depth;
+  const uint8_t* dm = mask;
+  if (!on_device) {
+    CK(cudaMemcpyAsync(ctx->up_depth, depth, (size_t)W * H * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->up_mask, mask, (size_t)W * H, cudaMemcpyHostToDevice, s));
+    dd = ctx->up_depth;
+    dm = ctx->up_mask;
+  }
+  CK(cudaMemsetAsync(ctx->S_o, 0, sizeof(unsigned long long), s));
+  CK(launch_pack_obs(dd, dm, ctx->obs, W, H, ctx->pitch_words, ctx->S_o, s));
+  CK(cudaStreamSynchronize(s));
+  return HP_OK;
+}
+
+static EvalArgs base_args(hp_ctx* ctx) {
+  EvalArgs a{};
+  a.cam = ctx->camp;
+  a.dims = ctx->dimsd;
+  a.cost = ctx->costd;
+  a.S_o = ctx->S_o;
+  a.acc = ctx->acc;
+  a.counters = ctx->counters;
+  a.obs = ctx->obs;
+  a.obs_pitch = ctx->pitch_words;
+  a.use_tma = ctx->use_tma;
+  a.tmap_g = ctx->tmap_g;
+  return a;
+}
+
+static hp_status render_depth(hp_ctx* ctx, const void* pose, bool pose_double, float* depth,
+                              cudaStream_t s) {
+  const int W = ctx->cam.width, H = ctx->cam.height;
+  CK(cudaMemsetAsync(depth, 0, (size_t)W * H * 4, s));
+  EvalArgs a = base_args(ctx);
+  a.poses = pose;
+  a.n = 1;
+  a.S = 64;
+  a.depth_out = depth;
+  CK(launch_eval(a, pose_double, kModeDepth, &ctx->tmap, s));
+  return HP_OK;
+}
+
+hp_status hp_render_observation(hp_ctx* ctx, const double* h_ref, float* depth_dev,
+                                uint8_t* mask_dev, void* stream) {
+  ARG(ctx && h_ref && depth_dev, "hp_render_observation: NULL argument");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(ctx->scratch, h_ref, kNdof * sizeof(double), cudaMemcpyHostToDevice, s));
+  hp_status r = render_depth(ctx, ctx->scratch, true, depth_dev, s);
+  if (r != HP_OK) return r;
+  if (mask_dev) CK(launch_depth_to_mask(depth_dev, mask_dev, ctx->cam.width * ctx->cam.height, s));
+  CK(cudaStreamSynchronize(s));  // h_ref staging is reused
+  return HP_OK;
+}
+
+hp_status hp_debug_render(hp_ctx* ctx, const float* pose_dev, float* depth_dev, void* stream) {
+  ARG(ctx && pose_dev && depth_dev, "hp_debug_render: NULL argument");
+  cudaSetDevice(ctx->device);
+  return render_depth(ctx, pose_dev, false, depth_dev, (cudaStream_t)stream);
+}
+
+static hp_status eval_common(hp_ctx* ctx, const float* poses, int64_t n, float* costs32,
+                             double* costs64, uint64_t* sums, cudaStream_t s) {
+  EvalArgs a = base_args(ctx);
+  a.poses = poses;
+  a.n = (int)n;
+  a.S = hp_splits_for(ctx, n);
+  a.costs32 = costs32;
+  a.costs64 = costs64;
+  a.sums_out = reinterpret_cast<unsigned long long*>(sums);
+  CK(launch_eval(a, false, kModeCost, &ctx->tmap, s));
+  if (ctx->sync_debug) CK(cudaStreamSynchronize(s));
+  ctx->last_launches = 1;
+  return HP_OK;
+}
+
+hp_status hp_eval_costs(hp_ctx* ctx, const float* poses, int64_t n, float* costs, void* stream) {
+  ARG(ctx, "hp_eval_costs: NULL ctx");
+  ARG(n >= 0 && n <= ctx->max_n, "hp_eval_costs: n < 0 or n > max_particles");
+  if (n == 0) return HP_OK;
+  ARG(poses && costs, "hp_eval_costs: NULL buffer");
+  cudaSetDevice(ctx->device);
+  return eval_common(ctx, poses, n, costs, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+hp_status hp_eval_costs_host(hp_ctx* ctx, const float* poses, int64_t n, float* costs,
+                             void* stream) {
+  ARG(ctx, "hp_eval_costs_host: NULL ctx");
+  ARG(n >= 0 && n <= ctx->max_n, "hp_eval_costs_host: n < 0 or n > max_particles");
+  if (n == 0) return HP_OK;
+  ARG(poses && costs, "hp_eval_costs_host: NULL buffer");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  // pinned staging so the copies are true async DMA
+  memcpy(ctx->h_poses, poses, (size_t)n * kNdof * sizeof(float));
+  CK(cudaMemcpyAsync(ctx->poses32, ctx->h_poses, (size_t)n * kNdof * sizeof(float),
+                     cudaMemcpyHostToDevice, s));
+  hp_status r = eval_common(ctx, ctx->poses32, n, ctx->costs32, nullptr, nullptr, s);
+  if (r != HP_OK) return r;
+  CK(cudaMemcpyAsync(ctx->h_costs, ctx->costs32, (size_t)n * sizeof(float),
+                     cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  memcpy(costs, ctx->h_costs, (size_t)n * sizeof(float));
+  return HP_OK;
+}
+
+hp_status hp_eval_sums(hp_ctx* ctx, const float* poses, int64_t n, uint64_t* sums,
+                       double* costs64, void* stream) {
+  ARG(ctx, "hp_eval_sums: NULL ctx");
+  ARG(n >= 0 && n <= ctx->max_n, "hp_eval_sums: n < 0 or n > max_particles");
+  if (n == 0) return HP_OK;
+  ARG(poses && sums, "hp_eval_sums: NULL buffer");
+  cudaSetDevice(ctx->device);
+  return eval_common(ctx, poses, n, nullptr, costs64, sums, (cudaStream_t)stream);
+}
+
+hp_status hp_debug_fk(hp_ctx* ctx, const double* pose, float* records, int32_t* boxes,
+                      double* joints, double* kc) {
+  ARG(ctx && pose, "hp_debug_fk: NULL argument");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->st;
+  double* dpose = ctx->scratch;                              // 26
+  float* drec = reinterpret_cast<float*>(ctx->scratch + 32); // 38*24 floats = 456 doubles
+  int* dbox = reinterpret_cast<int*>(ctx->scratch + 32 + 456);  // 152 ints = 76 doubles
+  double* djoint = ctx->scratch + 32 + 456 + 80;             // 60
+  double* dkc = djoint + 64;
+  CK(cudaMemcpyAsync(dpose, pose, kNdof * sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(launch_fk_debug(dpose, ctx->dimsd, ctx->camp, drec, dbox, djoint, dkc, s));
+  if (records) CK(cudaMemcpyAsync(records, drec, kNprim * kRec * 4, cudaMemcpyDeviceToHost, s));
+  if (boxes) CK(cudaMemcpyAsync(boxes, dbox, kNprim * 16, cudaMemcpyDeviceToHost, s));
+  if (joints) CK(cudaMemcpyAsync(joints, djoint, 60 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (kc) CK(cudaMemcpyAsync(kc, dkc, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return HP_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// PSO driver
+// ---------------------------------------------------------------------------------------
+static hp_status validate_pso(hp_ctx* ctx, const hp_pso_params* p) {
+  ARG(p, "pso: NULL params");
+  ARG(p->particles >= 1 && p->particles <= ctx->max_n, "pso: particles < 1 or > max_particles");
+  ARG(p->generations >= 1, "pso: generations < 1");
+  ARG(p->c1 + p->c2 > 4.0, "pso: c1 + c2 must exceed 4 (P:L150 constriction)");
+  ARG(p->mutation_fraction >= 0.0 && p->mutation_fraction <= 1.0, "pso: mutation_fraction");
+  ARG(p->mutation_period >= 0, "pso: mutation_period < 0");
+  return HP_OK;
+}
+
+static PsoDev pso_dev(hp_ctx* ctx, int N, int D, const hp_pso_params* p, int mut_lo, int mut_hi) {
+  PsoDev d{};
+  d.N = N;
+  d.D = D;
+  d.K = p->generations;
+  d.period = p->mutation_period;
+  d.per_dim_r = p->per_dim_r ? 1 : 0;
+  d.nmut = (int)floor((double)N * p->mutation_fraction);
+  d.mut_lo = mut_lo;
+  d.mut_hi = mut_hi;
+  d.dyn = ctx->dyn;
+  d.lo = ctx->bnd;
+  d.hi = ctx->bnd + 64;
+  d.ilo = ctx->bnd + 128;
+  d.ihi = ctx->bnd + 192;
+  d.X = ctx->X;
+  d.V = ctx->V;
+  d.P = ctx->P;
+  d.Pc = ctx->Pc;
+  d.E = ctx->E;
+  d.G = ctx->G;
+  d.Gc = ctx->Gc;
+  d.trace = ctx->trace;
+  d.mark = ctx->mark;
+  d.done = ctx->flags;
+  d.gens_run = ctx->flags + 1;
+  return d;
+}
+
+// Enqueue the whole fit on `s` (captured into a graph by the caller).
+static hp_status enqueue_fit(hp_ctx* ctx, const PsoDev& d, bool sphere, cudaStream_t s,
+                             int64_t* launches) {
+  int64_t n = 0;
+  EvalArgs a = base_args(ctx);
+  a.poses = d.X;
+  a.n = d.N;
+  a.S = hp_splits_for(ctx, d.N);
+  a.costs64 = d.E;
+  a.done = d.done;
+  auto eval = [&]() -> hp_status {
+    if (sphere) CK(launch_sphere_eval(d, ctx->centre, s));
+    else CK(launch_eval(a, true, kModeCost, &ctx->tmap, s));
+    n++;
+    return HP_OK;
+  };
+  CK(launch_pso_init(d, s));
+  n++;
+  hp_status r = eval();
+  if (r != HP_OK) return r;
+  CK(launch_pso_book(d, 0, s));
+  n++;
+  for (int k = 1; k < d.K; k++) {
+    CK(launch_pso_update(d, k, s));
+    n++;
+    r = eval();
+    if (r != HP_OK) return r;
+    CK(launch_pso_book(d, k, s));
+    n++;
+  }
+  *launches = n;
+  return HP_OK;
+}
+
+static hp_status run_fit(hp_ctx* ctx, const hp_pso_params* p, int D, const double* lo,
+                         const double* hi, const double* ilo, const double* ihi, int mut_lo,
+                         int mut_hi, bool sphere, double* best, double* best_cost, double* trace,
+                         int32_t* gens_run, cudaStream_t user) {
+  const int N = p->particles, K = p->generations;
+  cudaStream_t s = ctx->st;
+  if (K > ctx->trace_cap) {
+    if (ctx->trace) cudaFree(ctx->trace);
+    if (ctx->h_out) cudaFreeHost(ctx->h_out);
+    ctx->trace = nullptr;
+    ctx->h_out = nullptr;
+    CK(cudaMalloc(&ctx->trace, (size_t)K * sizeof(double)));
+    CK(cudaMallocHost(&ctx->h_out, (size_t)(K + 72) * sizeof(double)));
+    ctx->trace_cap = K;
+    if (ctx->graph.exec) {
+      cudaGraphExecDestroy(ctx->graph.exec);
+      ctx->graph.exec = nullptr;
+    }
+  }
+  // per-fit parameters into device memory (the captured graph reads them); pageable
+  // source: cudaMemcpyAsync stages it before returning
+  std::vector<double> hbv(256, 0.0);
+  for (int i = 0; i < D; i++) {
+    hbv[i] = lo[i];
+    hbv[64 + i] = hi[i];
+    hbv[128 + i] = ilo[i];
+    hbv[192 + i] = ihi[i];
+  }
+  PsoDyn dyn{p->seed, p->c1, p->c2, 0.0, p->stop_threshold};
+  {
+    const double psi = p->c1 + p->c2;  // w = 2 / |2 - psi - sqrt(psi^2 - 4 psi)|
+    dyn.w = 2.0 / fabs(2.0 - psi - sqrt(psi * psi - 4.0 * psi));
+  }
+  CK(cudaEventRecord(ctx->ev, user));
+  CK(cudaStreamWaitEvent(s, ctx->ev, 0));
+  CK(cudaMemcpyAsync(ctx->bnd, hbv.data(), 256 * sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->dyn, &dyn, sizeof dyn, cudaMemcpyHostToDevice, s));
+  PsoDev d = pso_dev(ctx, N, D, p, mut_lo, mut_hi);
+  Graph& g = ctx->graph;
+  const bool same = g.exec && g.N == N && g.D == D && g.K == K && g.period == d.period &&
+                    g.per_dim_r == d.per_dim_r && g.nmut == d.nmut && g.mut_lo == mut_lo &&
+                    g.mut_hi == mut_hi && g.sphere == (int)sphere;
+  int64_t launches = 0;
+  if (!same) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr;
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    hp_status r = enqueue_fit(ctx, d, sphere, s, &launches);
+    cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    if (r != HP_OK) return r;
+    CK(ce);
+    CK(cudaGraphInstantiate(&g.exec, graph, 0));
+    cudaGraphDestroy(graph);
+    g.N = N;
+    g.D = D;
+    g.K = K;
+    g.period = d.period;
+    g.per_dim_r = d.per_dim_r;
+    g.nmut = d.nmut;
+    g.mut_lo = mut_lo;
+    g.mut_hi = mut_hi;
+    g.sphere = sphere;
+  } else {
+    launches = 3 * (int64_t)K;
+  }
+  CK(cudaGraphLaunch(g.exec, s));
+  double* ho = ctx->h_out;
+  CK(cudaMemcpyAsync(ho, ctx->G, D * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(ho + 64, ctx->Gc, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(ho + 65, ctx->flags + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(ho + 72, ctx->trace, K * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  ctx->last_launches = launches;
+  ctx->last_N = N;
+  ctx->last_D = D;
+  memcpy(best, ho, D * sizeof(double));
+  *best_cost = ho[64];
+  int gr = 0;
+  memcpy(&gr, ho + 65, sizeof(int));
+  if (gens_run) *gens_run = gr;
+  if (trace) {
+    for (int k = 0; k < K; k++) trace[k] = k < gr ? ho[72 + k] : ho[72 + gr - 1];
+  }
+  return HP_OK;
+}
+
+hp_status hp_pso_fit(hp_ctx* ctx, const hp_pso_params* p, double* best_pose, double* best_cost,
+                     double* trace, int32_t* gens_run, void* stream) {
+  ARG(ctx, "hp_pso_fit: NULL ctx");
+  hp_status r = validate_pso(ctx, p);
+  if (r != HP_OK) return r;
+  ARG(best_pose && best_cost, "hp_pso_fit: NULL output");
+  cudaSetDevice(ctx->device);
+  double lo[26], hi[26], ilo[26], ihi[26];
+  hp_bounds(lo, hi);
+  for (int i = 0; i < 26; i++) {
+    ilo[i] = lo[i];
+    ihi[i] = hi[i];
+    if (p->init_center && p->init_radius) {  // centre +- radius intersected with the bounds
+      ilo[i] = fmax(lo[i], p->init_center[i] - p->init_radius[i]);
+      ihi[i] = fmin(hi[i], p->init_center[i] + p->init_radius[i]);
+    }
+  }
+  return run_fit(ctx, p, 26, lo, hi, ilo, ihi, 6, 26, false, best_pose, best_cost, trace,
+                 gens_run, (cudaStream_t)stream);
+}
+
+hp_status hp_debug_pso_sphere(hp_ctx* ctx, int32_t D, const double* lo, const double* hi,
+                              const double* init_lo, const double* init_hi, int32_t mut_lo,
+                              int32_t mut_hi, const double* centre, const hp_pso_params* p,
+                              double* best_x, double* best_cost, double* trace,
+                              int32_t* gens_run, void* stream) {
+  ARG(ctx, "hp_debug_pso_sphere: NULL ctx");
+  hp_status r = validate_pso(ctx, p);
+  if (r != HP_OK) return r;
+  ARG(D >= 1 && D <= 64 && lo && hi && init_lo && init_hi && centre && best_x && best_cost,
+      "hp_debug_pso_sphere: bad argument");
+  ARG(mut_lo >= 0 && mut_lo <= mut_hi && mut_hi <= D, "hp_debug_pso_sphere: mutation dims");
+  cudaSetDevice(ctx->device);
+  CK(cudaMemcpyAsync(ctx->centre, centre, D * sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  return run_fit(ctx, p, D, lo, hi, init_lo, init_hi, mut_lo, mut_hi, true, best_x, best_cost,
+                 trace, gens_run, (cudaStream_t)stream);
+}
+
+hp_status hp_pso_state(hp_ctx* ctx, double* X, double* V, double* P, double* Pcost) {
+  ARG(ctx, "hp_pso_state: NULL ctx");
+  if (ctx->last_N == 0) {
+    ctx->err = "hp_pso_state: no fit has run";
+    return HP_ERR_STATE;
+  }
+  cudaSetDevice(ctx->device);
+  const size_t nd = (size_t)ctx->last_N * ctx->last_D * sizeof(double);
+  if (X) CK(cudaMemcpy(X, ctx->X, nd, cudaMemcpyDeviceToHost));
+  if (V) CK(cudaMemcpy(V, ctx->V, nd, cudaMemcpyDeviceToHost));
+  if (P) CK(cudaMemcpy(P, ctx->P, nd, cudaMemcpyDeviceToHost));
+  if (Pcost) CK(cudaMemcpy(Pcost, ctx->Pc, ctx->last_N * sizeof(double), cudaMemcpyDeviceToHost));
+  return HP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,154 @@
+// common.cuh — device-side parameter blocks, record layout and PTX helpers for libhp.
+//
+// This is product code (CUDA for sm_100a).  It shares nothing with oracle/: both follow
+// DESIGN.md §2 (frozen model) and §3 (readings) independently.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hp {
+
+constexpr int kNdof = 26;
+constexpr int kNprim = 38;
+constexpr int kRec = 24;   // floats per primitive record (96 B)
+constexpr int kTileW = 16; // warp tile: 16 x 8 pixels, 4 pixels per lane
+constexpr int kTileH = 8;
+constexpr int kPxPerLane = 4;
+
+// Primitive order on the device (sorted by kind so a cull mask splits by bit range):
+//   0..19  spheres   (finger f, joint k) -> 4 f + k
+//   20..31 cones     fingers 1..4, segment k -> 20 + 3 (f - 1) + k
+//   32, 33 cones     thumb segments 2, 3
+//   34     palm elliptic cylinder (same code path as the cones, k = 0)
+//   35     thumb proximal ellipsoid
+//   36, 37 palm cap ellipsoids
+constexpr int kSphere0 = 0, kCone0 = 20, kCyl = 34, kEll0 = 35;
+constexpr uint64_t kSphereMask = (1ull << 20) - 1;
+constexpr uint64_t kConeMask = ((1ull << 35) - 1) ^ kSphereMask;
+constexpr uint64_t kEllMask = ((1ull << 38) - 1) ^ ((1ull << 35) - 1);
+
+// Record layout, all camera frame, fp32:
+//   [0..2]  c: local origin (sphere/ellipsoid centre, cone/cylinder axis midpoint)
+//   [3]     r^2 (sphere)
+//   [4..12] M row-major: camera offset -> local (ellipsoid: diag(1/s) R^T;
+//           cone: rows e1, e2, axis; cylinder: x_H/a, z_H/b, y_H)
+//   [13..15] c_l = M c
+//   [16] r_mid  [17] slope k  [18] half length (cone / cylinder)
+enum RecField { kC = 0, kR2 = 3, kM = 4, kCl = 13, kRm = 16, kK = 17, kHl = 18 };
+
+struct CamParams {
+  int W, H;
+  float fx, fy, cx, cy, znear, zfar;
+};
+
+struct DimsD {
+  double palm_half_w, palm_half_t, palm_len, cap_half;
+  double base[5][3], len[5][3], rad[5][4];
+  double th_x, th_z;
+  double RT0[3][3];  // thumb base frame Rz(yaw) Ry(pitch), host fp64
+};
+
+struct CostD {
+  float d_m, clampv;  // per-pixel fp32 compare / clamp
+  double lambda, lambda_k, depth_scale, kc_rest;
+};
+
+enum EvalMode { kModeCost = 0, kModeDepth = 1 };
+
+struct EvalArgs {
+  const void* poses;          // [n][26] float or double
+  int n, S;                   // poses, CTAs per pose
+  CamParams cam;
+  DimsD dims;
+  CostD cost;
+  const unsigned long long* S_o;  // device scalar: sum o_s
+  unsigned long long* acc;        // [n][4] accumulators (zero between launches)
+  unsigned int* counters;         // [n] CTA arrival counters (zero between launches)
+  float* costs32;                 // optional [n]
+  double* costs64;                // optional [n]
+  unsigned long long* sums_out;   // optional [n][4]
+  float* depth_out;               // kModeDepth: [H][W]
+  const int* done;                // optional PSO stop flag: skip work when *done
+  const uint32_t* obs;            // packed observation (plain-load path)
+  int obs_pitch;                  // words per row
+  int use_tma;                    // 1: TMA tile loads (default), 0: plain loads
+  const CUtensorMap* tmap_g;      // the same descriptor in global memory (use_tma = 2)
+};
+
+// --------------------------------------------------------------------------------------
+// PTX helpers: mbarrier + TMA (cp.async.bulk.tensor), sm_90+ / sm_100a
+// --------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// --------------------------------------------------------------------------------------
+// Launchers (kernels.cu)
+// --------------------------------------------------------------------------------------
+cudaError_t launch_pack_obs(const float* depth, const uint8_t* mask, uint32_t* obs, int W,
+                            int H, int pitch_words, unsigned long long* S_o, cudaStream_t st);
+cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUtensorMap* map,
+                        cudaStream_t st);
+cudaError_t launch_fk_debug(const double* pose_dev, const DimsD& dims, const CamParams& cam,
+                            float* rec, int* boxes, double* joints, double* kc,
+                            cudaStream_t st);
+cudaError_t launch_depth_to_mask(const float* depth, uint8_t* mask, int npx, cudaStream_t st);
+int eval_warps_per_cta();
+
+// PSO (pso.cu)
+struct PsoDyn {  // per-fit values, read from device memory so a captured graph is reusable
+  uint64_t seed;
+  double c1, c2, w, stop;
+};
+struct PsoDev {
+  int N, D, K, period, per_dim_r, nmut, mut_lo, mut_hi;
+  const PsoDyn* dyn;
+  const double *lo, *hi, *ilo, *ihi;  // [D]
+  double *X, *V, *P, *Pc, *E, *G, *Gc, *trace;
+  int* mark;
+  int* done;
+  int* gens_run;
+};
+cudaError_t launch_pso_init(const PsoDev& p, cudaStream_t st);
+cudaError_t launch_pso_update(const PsoDev& p, int k, cudaStream_t st);
+cudaError_t launch_pso_book(const PsoDev& p, int k, cudaStream_t st);
+cudaError_t launch_sphere_eval(const PsoDev& p, const double* centre, cudaStream_t st);
+
+}  // namespace hp

@@ -1,0 +1,321 @@
+// fk.cuh — forward kinematics on one warp (fp64) -> 38 fp32 primitive records,
+// conservative screen boxes, the union box and kc(h).
+//
+// Follows DESIGN §2 (frames, chain, dimensions) for Eq. (1)-(3) and the
+// primitive geometry of P:L82; kc per P:L130 with reading AMB-7.  Runs inside k_eval
+// (warp 0 of every CTA) so the records never leave shared memory.
+#pragma once
+#include "common.cuh"
+
+namespace hp {
+
+struct FkScratch {
+  double h[kNdof];
+  double sn[kNdof], cs[kNdof];
+  double RW[3][3];
+  double J[5][4][3];        // joint centres, camera frame
+  double Rs[5][3][3][3];    // segment frames R_W R_k^H (k = 1..3), camera frame
+  int bad;                  // non-finite pose
+};
+
+struct FkOut {
+  float rec[kNprim][kRec];
+  int4 box[kNprim];  // x0, y0, x1, y1 inclusive; x0 > x1 = empty
+  int4 ubox;
+  double kc;
+};
+
+__device__ __forceinline__ void mat3_mul(const double a[3][3], const double b[3][3],
+                                         double o[3][3]) {
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) o[i][j] = a[i][0] * b[0][j] + a[i][1] * b[1][j] + a[i][2] * b[2][j];
+}
+
+// Bounds of the body {c + E q : |q| <= 1}, A = E E^T, on the image: the tangent planes
+// through the camera centre containing an image axis satisfy
+// (cz^2 - Azz) u^2 - 2 (ca cz - Aaz) u + (ca^2 - Aaa) = 0.  Accumulates into [u0,u1]x[v0,v1]
+// (normalised image coordinates); returns 0 behind the camera, 2 if straddling z = 0.
+__device__ __forceinline__ int gen_bounds(const double c[3], const double A[3][3], double& u0,
+                                          double& u1, double& v0, double& v1) {
+  double zext = sqrt(fmax(A[2][2], 0.0));
+  if (c[2] + zext <= 0.0) return 0;
+  if (c[2] - zext <= 0.0) return 2;
+  double qa = c[2] * c[2] - A[2][2];
+#pragma unroll
+  for (int ax = 0; ax < 2; ax++) {
+    double qb = c[ax] * c[2] - A[ax][2];
+    double qc = c[ax] * c[ax] - A[ax][ax];
+    double sq = sqrt(fmax(qb * qb - qa * qc, 0.0));
+    double lo = (qb - sq) / qa, hi = (qb + sq) / qa;
+    if (ax == 0) {
+      u0 = fmin(u0, lo);
+      u1 = fmax(u1, hi);
+    } else {
+      v0 = fmin(v0, lo);
+      v1 = fmax(v1, hi);
+    }
+  }
+  return 1;
+}
+
+// A = R diag(s^2) R^T with R given by its columns.
+__device__ __forceinline__ void shape_from_axes(const double col[3][3], const double s[3],
+                                                double A[3][3]) {
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++)
+      A[i][j] = col[0][i] * col[0][j] * s[0] * s[0] + col[1][i] * col[1][j] * s[1] * s[1] +
+                col[2][i] * col[2][j] * s[2] * s[2];
+}
+
+// Disc of radius r centred at c with unit normal a: A = r^2 (I - a a^T).
+__device__ __forceinline__ void disc_shape(const double a[3], double r, double A[3][3]) {
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) A[i][j] = r * r * ((i == j ? 1.0 : 0.0) - a[i] * a[j]);
+}
+
+__device__ __forceinline__ int4 finish_box(int st_any, int full, double u0, double u1, double v0,
+                                           double v1, const CamParams& cam) {
+  int4 b = make_int4(1, 1, 0, 0);  // empty
+  if (!st_any) return b;
+  if (full) return make_int4(0, 0, cam.W - 1, cam.H - 1);
+  double fx = cam.fx, fy = cam.fy, cx = cam.cx, cy = cam.cy;
+  // pixel i is a candidate iff its centre i + 0.5 lies within the bounds; 1 px margin
+  double x0 = ceil(fx * u0 + cx - 0.5) - 1.0, x1 = floor(fx * u1 + cx - 0.5) + 1.0;
+  double y0 = ceil(fy * v0 + cy - 0.5) - 1.0, y1 = floor(fy * v1 + cy - 0.5) + 1.0;
+  x0 = fmax(x0, 0.0);
+  y0 = fmax(y0, 0.0);
+  x1 = fmin(x1, (double)(cam.W - 1));
+  y1 = fmin(y1, (double)(cam.H - 1));
+  if (!(x0 <= x1 && y0 <= y1)) return b;
+  return make_int4((int)x0, (int)y0, (int)x1, (int)y1);
+}
+
+// Bounds of a primitive from up to two generator bodies.
+__device__ __forceinline__ int4 prim_box(int ng, const double c[2][3], const double A[2][3][3],
+                                         const CamParams& cam) {
+  double u0 = 1e300, u1 = -1e300, v0 = 1e300, v1 = -1e300;
+  int any = 0, full = 0;
+  for (int g = 0; g < ng; g++) {
+    int st = gen_bounds(c[g], A[g], u0, u1, v0, v1);
+    if (st) any = 1;
+    if (st == 2) full = 1;
+  }
+  return finish_box(any, full, u0, u1, v0, v1, cam);
+}
+
+__device__ __forceinline__ void put3(float* r, int off, const double v[3]) {
+  r[off + 0] = (float)v[0];
+  r[off + 1] = (float)v[1];
+  r[off + 2] = (float)v[2];
+}
+
+// Build record + box of device primitive j (see common.cuh for the order).
+__device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const CamParams& cam,
+                           float* rec, int4& box) {
+#pragma unroll
+  for (int i = 0; i < kRec; i++) rec[i] = 0.f;
+  double gc[2][3], gA[2][3][3];
+  int ng = 0;
+  if (j < kCone0) {  // sphere at joint (f, k)
+    int f = j >> 2, k = j & 3;
+    double r = dm.rad[f][k];
+    const double* c = s.J[f][k];
+    put3(rec, kC, c);
+    rec[kR2] = (float)(r * r);
+    for (int i = 0; i < 3; i++) gc[0][i] = c[i];
+    for (int a = 0; a < 3; a++)
+      for (int b = 0; b < 3; b++) gA[0][a][b] = (a == b) ? r * r : 0.0;
+    ng = 1;
+  } else if (j < kCyl) {  // truncated cone J_k -> J_{k+1}
+    int f, k;
+    if (j < 32) {
+      f = 1 + (j - kCone0) / 3;
+      k = (j - kCone0) % 3;
+    } else {
+      f = 0;
+      k = j - 32 + 1;
+    }
+    const double* J0 = s.J[f][k];
+    const double* J1 = s.J[f][k + 1];
+    double L = dm.len[f][k], r0 = dm.rad[f][k], r1 = dm.rad[f][k + 1];
+    // segment frame columns: e1 = col0, axis = -col1 (the segment runs along -y_k), e2 = col2
+    double e1[3], e2[3], ax[3], m[3];
+    for (int i = 0; i < 3; i++) {
+      e1[i] = s.Rs[f][k][i][0];
+      ax[i] = -s.Rs[f][k][i][1];
+      e2[i] = s.Rs[f][k][i][2];
+      m[i] = 0.5 * (J0[i] + J1[i]);
+    }
+    put3(rec, kC, m);
+    double rows[3][3] = {{e1[0], e1[1], e1[2]}, {e2[0], e2[1], e2[2]}, {ax[0], ax[1], ax[2]}};
+    for (int a = 0; a < 3; a++) {
+      put3(rec, kM + 3 * a, rows[a]);
+      rec[kCl + a] = (float)(rows[a][0] * m[0] + rows[a][1] * m[1] + rows[a][2] * m[2]);
+    }
+    rec[kRm] = (float)(0.5 * (r0 + r1));
+    rec[kK] = (float)((r1 - r0) / L);
+    rec[kHl] = (float)(0.5 * L);
+    for (int i = 0; i < 3; i++) {
+      gc[0][i] = J0[i];
+      gc[1][i] = J1[i];
+    }
+    disc_shape(ax, r0, gA[0]);
+    disc_shape(ax, r1, gA[1]);
+    ng = 2;
+  } else if (j == kCyl) {  // palm: elliptic cylinder y_H in [-len, 0]
+    double cx[3], cy[3], cz[3], m[3];
+    for (int i = 0; i < 3; i++) {
+      cx[i] = s.RW[i][0];
+      cy[i] = s.RW[i][1];
+      cz[i] = s.RW[i][2];
+      m[i] = s.h[i] - 0.5 * dm.palm_len * cy[i];
+    }
+    put3(rec, kC, m);
+    double rows[3][3];
+    for (int i = 0; i < 3; i++) {
+      rows[0][i] = cx[i] / dm.palm_half_w;
+      rows[1][i] = cz[i] / dm.palm_half_t;
+      rows[2][i] = cy[i];
+    }
+    for (int a = 0; a < 3; a++) {
+      put3(rec, kM + 3 * a, rows[a]);
+      rec[kCl + a] = (float)(rows[a][0] * m[0] + rows[a][1] * m[1] + rows[a][2] * m[2]);
+    }
+    rec[kRm] = 1.f;
+    rec[kK] = 0.f;
+    rec[kHl] = (float)(0.5 * dm.palm_len);
+    double cols[3][3] = {{cx[0], cx[1], cx[2]}, {cy[0], cy[1], cy[2]}, {cz[0], cz[1], cz[2]}};
+    double sd[3] = {dm.palm_half_w, 0.0, dm.palm_half_t};
+    for (int e = 0; e < 2; e++) {
+      double yc = e == 0 ? 0.0 : -dm.palm_len;
+      for (int i = 0; i < 3; i++) gc[e][i] = s.h[i] + yc * cy[i];
+      shape_from_axes(cols, sd, gA[e]);
+    }
+    ng = 2;
+  } else {  // ellipsoids: thumb proximal (35), palm caps (36, 37)
+    double c[3], cols[3][3], sd[3];
+    if (j == kEll0) {
+      for (int i = 0; i < 3; i++) c[i] = 0.5 * (s.J[0][0][i] + s.J[0][1][i]);
+      for (int a = 0; a < 3; a++)
+        for (int i = 0; i < 3; i++) cols[a][i] = s.Rs[0][0][i][a];
+      sd[0] = dm.th_x;
+      sd[1] = 0.5 * dm.len[0][0];
+      sd[2] = dm.th_z;
+    } else {
+      double yc = j == kEll0 + 1 ? 0.0 : -dm.palm_len;
+      for (int i = 0; i < 3; i++) c[i] = s.h[i] + yc * s.RW[i][1];
+      for (int a = 0; a < 3; a++)
+        for (int i = 0; i < 3; i++) cols[a][i] = s.RW[i][a];
+      sd[0] = dm.palm_half_w;
+      sd[1] = dm.cap_half;
+      sd[2] = dm.palm_half_t;
+    }
+    put3(rec, kC, c);
+    for (int a = 0; a < 3; a++) {
+      double row[3] = {cols[a][0] / sd[a], cols[a][1] / sd[a], cols[a][2] / sd[a]};
+      put3(rec, kM + 3 * a, row);
+      rec[kCl + a] = (float)(row[0] * c[0] + row[1] * c[1] + row[2] * c[2]);
+    }
+    for (int i = 0; i < 3; i++) gc[0][i] = c[i];
+    shape_from_axes(cols, sd, gA[0]);
+    ng = 1;
+  }
+  box = prim_box(ng, gc, gA, cam);
+}
+
+// Whole-warp FK.  pose: 26 values (float or double); writes `out` (shared) and, if
+// `scratch_out` is true, leaves joints in `s` for the debug hook.
+template <typename PoseT>
+__device__ void fk_warp(const PoseT* pose, const DimsD& dm, const CamParams& cam, double kc_rest,
+                        FkScratch& s, FkOut& out) {
+  const int lane = threadIdx.x & 31;
+  if (lane < kNdof) {
+    double v = (double)pose[lane];
+    s.h[lane] = v;
+    if (lane >= 3) sincos(v, &s.sn[lane], &s.cs[lane]);
+  }
+  __syncwarp();
+  int bad = 0;
+  if (lane < kNdof) bad = !isfinite(s.h[lane]);
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) {
+    // R_W = Rz(th_z) Ry(th_y) Rx(th_x)  (AMB-10)
+    double cx = s.cs[3], sx = s.sn[3], cy = s.cs[4], sy = s.sn[4], cz = s.cs[5], sz = s.sn[5];
+    double Rx[3][3] = {{1, 0, 0}, {0, cx, -sx}, {0, sx, cx}};
+    double Ry[3][3] = {{cy, 0, sy}, {0, 1, 0}, {-sy, 0, cy}};
+    double Rz[3][3] = {{cz, -sz, 0}, {sz, cz, 0}, {0, 0, 1}};
+    double t[3][3];
+    mat3_mul(Ry, Rx, t);
+    mat3_mul(Rz, t, s.RW);
+    s.bad = bad;
+  }
+  __syncwarp();
+  if (lane < 5) {
+    const int f = lane;
+    const int o = 6 + 4 * f;  // (MPx, MPz, PIP, DIP), Eq. (1)
+    double R0[3][3];
+    for (int a = 0; a < 3; a++)
+      for (int b = 0; b < 3; b++) R0[a][b] = f == 0 ? dm.RT0[a][b] : (a == b ? 1.0 : 0.0);
+    double cz = s.cs[o + 1], sz = s.sn[o + 1];
+    double Rz[3][3] = {{cz, -sz, 0}, {sz, cz, 0}, {0, 0, 1}};
+    double RH[3][3], t[3][3];
+    mat3_mul(R0, Rz, t);
+    double JH[3] = {dm.base[f][0], dm.base[f][1], dm.base[f][2]};
+    double Jc[3];
+    for (int i = 0; i < 3; i++)
+      Jc[i] = s.h[i] + s.RW[i][0] * JH[0] + s.RW[i][1] * JH[1] + s.RW[i][2] * JH[2];
+    for (int i = 0; i < 3; i++) s.J[f][0][i] = Jc[i];
+    for (int k = 0; k < 3; k++) {
+      double c = s.cs[k == 0 ? o : o + 1 + k], sn = s.sn[k == 0 ? o : o + 1 + k];
+      double Rx[3][3] = {{1, 0, 0}, {0, c, -sn}, {0, sn, c}}, Rn[3][3];
+      mat3_mul(k == 0 ? t : RH, Rx, Rn);  // R1 = R0 Rz Rx(MPx); R2 = R1 Rx(PIP); ...
+      for (int a = 0; a < 3; a++)
+        for (int b = 0; b < 3; b++) RH[a][b] = Rn[a][b];
+      double L = dm.len[f][k];
+      for (int i = 0; i < 3; i++) JH[i] -= L * RH[i][1];  // J += R (0, -L, 0)
+      for (int i = 0; i < 3; i++)
+        s.J[f][k + 1][i] = s.h[i] + s.RW[i][0] * JH[0] + s.RW[i][1] * JH[1] + s.RW[i][2] * JH[2];
+      mat3_mul(s.RW, RH, s.Rs[f][k]);
+    }
+  }
+  __syncwarp();
+  for (int j = lane; j < kNprim; j += 32) build_prim(j, s, dm, cam, out.rec[j], out.box[j]);
+  __syncwarp();
+  // union box
+  int4 u = make_int4(1 << 30, 1 << 30, -1, -1);
+  for (int j = lane; j < kNprim; j += 32) {
+    int4 b = out.box[j];
+    if (b.x <= b.z) {
+      u.x = min(u.x, b.x);
+      u.y = min(u.y, b.y);
+      u.z = max(u.z, b.z);
+      u.w = max(u.w, b.w);
+    }
+  }
+  for (int off = 16; off; off >>= 1) {
+    u.x = min(u.x, __shfl_xor_sync(0xffffffffu, u.x, off));
+    u.y = min(u.y, __shfl_xor_sync(0xffffffffu, u.y, off));
+    u.z = max(u.z, __shfl_xor_sync(0xffffffffu, u.z, off));
+    u.w = max(u.w, __shfl_xor_sync(0xffffffffu, u.w, off));
+  }
+  if (lane == 0) {
+    if (s.bad || u.z < u.x) u = make_int4(1, 1, 0, 0);
+    out.ubox = u;
+    // kc(h) = sum over (index,middle), (middle,ring), (ring,little) of -min(phi, 0)
+    double kc = 0.0;
+    for (int f = 1; f <= 3; f++) {
+      double phi = s.h[6 + 4 * f + 1] - s.h[6 + 4 * (f + 1) + 1] + kc_rest;
+      kc += -fmin(phi, 0.0);
+    }
+    out.kc = s.bad ? __longlong_as_double(0x7ff8000000000000ll) : kc;
+  }
+  __syncwarp();
+}
+
+}  // namespace hp

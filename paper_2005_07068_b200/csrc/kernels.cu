@@ -1,0 +1,385 @@
+// kernels.cu — the hot path of libhp on sm_100a.
+//
+//   k_pack_obs : observation O = (O_s, O_d) -> one u32 per pixel (fp32 depth bits, bit 31 =
+//                o_s) and S_o = sum o_s                     (DESIGN §1 row A0)
+//   k_eval     : fused FK + render + score + cost finalize   (rows A2-A5; P:L114-130,
+//                P:L162-171).  One CTA per (particle, split); warp 0 runs FK in fp64 into
+//                shared memory, then every warp walks 16x8-pixel tiles of the particle's
+//                screen box: TMA-loads the observation tile, culls the 38 primitive boxes
+//                with two ballots, ray-casts the surviving primitives analytically (fp32,
+//                re-centred at the closest approach), resolves the min depth and scores the
+//                pixel.  Sums are integers (fixed point 2^-20 mm for the numerator): warp
+//                shuffles, one atomic per sum per CTA, and the last CTA of each particle
+//                computes Eq. (4)-(5) in fp64 and resets the accumulators.
+//   k_fk_debug : the same FK for the hp_debug_fk test hook.
+#include <math.h>
+
+#include "common.cuh"
+#include "fk.cuh"
+
+namespace hp {
+
+// ---------------------------------------------------------------------------------------
+// Observation packing
+// ---------------------------------------------------------------------------------------
+__global__ void k_pack_obs(const float* __restrict__ depth, const uint8_t* __restrict__ mask,
+                           uint32_t* __restrict__ obs, int W, int H, int pitch,
+                           unsigned long long* S_o) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long npx = (long long)W * H;
+  unsigned int cnt = 0;
+  if (i < npx) {
+    const int y = (int)(i / W), x = (int)(i % W);
+    const float d = depth[i];
+    const uint32_t bits = (d > 0.f && isfinite(d)) ? __float_as_uint(d) : 0u;
+    const uint32_t s = mask[i] ? 1u : 0u;
+    obs[(long long)y * pitch + x] = bits | (s << 31);
+    cnt = s;
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(S_o, (unsigned long long)cnt);
+}
+
+__global__ void k_depth_to_mask(const float* __restrict__ depth, uint8_t* __restrict__ mask,
+                                int npx) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < npx) mask[i] = depth[i] > 0.f ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------------------
+// Per-primitive analytic first hit for the 4 pixels of a lane (DESIGN §5 formulas).
+// Pixel ray d = (dx, dy_j, 1); t_c = (d.c)/|d|^2 re-centres the quadratic at the closest
+// approach to the primitive's local origin, so its coefficients are O(primitive size)
+// and fp32 does not cancel (a camera-origin quadratic has |c|^2 ~ 1e6 mm^2 against
+// r^2 ~ 1e2).  Depth = t (d_z = 1).
+// ---------------------------------------------------------------------------------------
+struct Lane4 {
+  float dx;
+  float dy[kPxPerLane];
+  float inv_dd[kPxPerLane];
+  float zb[kPxPerLane];
+};
+
+__device__ __forceinline__ float fast_sqrt(float x) { return x * rsqrtf(x); }
+
+__device__ __forceinline__ void keep(float z, float& zb, float znear, float zfar) {
+  if (z >= znear && z <= zfar && z < zb) zb = z;
+}
+
+__device__ __forceinline__ void isect_sphere(const float* __restrict__ r, Lane4& L, float znear,
+                                             float zfar) {
+  const float4 q = *reinterpret_cast<const float4*>(r);  // c, r^2
+  const float bx = fmaf(L.dx, q.x, q.z);
+#pragma unroll
+  for (int j = 0; j < kPxPerLane; j++) {
+    const float tc = fmaf(L.dy[j], q.y, bx) * L.inv_dd[j];
+    const float ox = fmaf(tc, L.dx, -q.x), oy = fmaf(tc, L.dy[j], -q.y), oz = tc - q.z;
+    const float disc = q.w - fmaf(ox, ox, fmaf(oy, oy, oz * oz));
+    if (disc >= 0.f) keep(tc - fast_sqrt(disc * L.inv_dd[j]), L.zb[j], znear, zfar);
+  }
+}
+
+__device__ __forceinline__ void isect_ellipsoid(const float* __restrict__ r, Lane4& L,
+                                                float znear, float zfar) {
+  const float4 r0 = *reinterpret_cast<const float4*>(r + 0);   // c, -
+  const float4 r1 = *reinterpret_cast<const float4*>(r + 4);   // M00 M01 M02 M10
+  const float4 r2 = *reinterpret_cast<const float4*>(r + 8);   // M11 M12 M20 M21
+  const float4 r3 = *reinterpret_cast<const float4*>(r + 12);  // M22 cl0 cl1 cl2
+  // d_l = M (dx, dy, 1): the dx part is shared by the lane's 4 pixels
+  const float px = fmaf(r1.x, L.dx, r1.z), py = fmaf(r1.w, L.dx, r2.y),
+              pz = fmaf(r2.z, L.dx, r3.x);
+  const float bx = fmaf(L.dx, r0.x, r0.z);
+#pragma unroll
+  for (int j = 0; j < kPxPerLane; j++) {
+    const float dy = L.dy[j];
+    const float tc = fmaf(dy, r0.y, bx) * L.inv_dd[j];
+    const float lx = fmaf(r1.y, dy, px), ly = fmaf(r2.x, dy, py), lz = fmaf(r2.w, dy, pz);
+    const float ox = fmaf(tc, lx, -r3.y), oy = fmaf(tc, ly, -r3.z), oz = fmaf(tc, lz, -r3.w);
+    const float A = fmaf(lx, lx, fmaf(ly, ly, lz * lz));
+    const float B = fmaf(ox, lx, fmaf(oy, ly, oz * lz));
+    const float C = fmaf(ox, ox, fmaf(oy, oy, fmaf(oz, oz, -1.f)));
+    const float disc = fmaf(B, B, -A * C);
+    if (disc >= 0.f) {
+      const float qq = -(B + copysignf(fast_sqrt(disc), B));
+      const float s = fminf(__fdividef(qq, A), __fdividef(C, qq));
+      keep(tc + s, L.zb[j], znear, zfar);
+    }
+  }
+}
+
+// Cone (and the elliptic cylinder with k = 0 in scaled coordinates):
+// x^2 + y^2 - (r_m + k z)^2 = 0 with |z| <= half length; the smaller root whose axial
+// coordinate is in range (the far-nappe case needs the larger one).  No cap tests: every
+// cap disc is the equator of a joint sphere / cap ellipsoid that is hit first.
+__device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L, float znear,
+                                           float zfar) {
+  const float4 r0 = *reinterpret_cast<const float4*>(r + 0);
+  const float4 r1 = *reinterpret_cast<const float4*>(r + 4);
+  const float4 r2 = *reinterpret_cast<const float4*>(r + 8);
+  const float4 r3 = *reinterpret_cast<const float4*>(r + 12);
+  const float4 r4 = *reinterpret_cast<const float4*>(r + 16);  // rm, k, hl, -
+  const float px = fmaf(r1.x, L.dx, r1.z), py = fmaf(r1.w, L.dx, r2.y),
+              pz = fmaf(r2.z, L.dx, r3.x);
+  const float bx = fmaf(L.dx, r0.x, r0.z);
+  const float rm = r4.x, k = r4.y, hl = r4.z;
+#pragma unroll
+  for (int j = 0; j < kPxPerLane; j++) {
+    const float dy = L.dy[j];
+    const float tc = fmaf(dy, r0.y, bx) * L.inv_dd[j];
+    const float lx = fmaf(r1.y, dy, px), ly = fmaf(r2.x, dy, py), lz = fmaf(r2.w, dy, pz);
+    const float ox = fmaf(tc, lx, -r3.y), oy = fmaf(tc, ly, -r3.z), oz = fmaf(tc, lz, -r3.w);
+    const float g = fmaf(k, oz, rm), kd = k * lz;
+    const float A = fmaf(lx, lx, fmaf(ly, ly, -kd * kd));
+    const float B = fmaf(ox, lx, fmaf(oy, ly, -kd * g));
+    const float C = fmaf(ox, ox, fmaf(oy, oy, -g * g));
+    const float disc = fmaf(B, B, -A * C);
+    if (disc >= 0.f) {
+      const float qq = -(B + copysignf(fast_sqrt(disc), B));
+      const float s1 = __fdividef(qq, A), s2 = __fdividef(C, qq);
+      const float sa = fminf(s1, s2), sb = fmaxf(s1, s2);
+      const float za = fmaf(sa, lz, oz), zb = fmaf(sb, lz, oz);
+      const float s = fabsf(za) <= hl ? sa : (fabsf(zb) <= hl ? sb : __int_as_float(0x7fc00000));
+      keep(tc + s, L.zb[j], znear, zfar);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// The fused evaluation kernel
+// ---------------------------------------------------------------------------------------
+template <int NW, typename PoseT, int MODE>
+__global__ void __launch_bounds__(NW * 32)
+    k_eval(const EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
+  __shared__ FkScratch s_fk;
+  __shared__ __align__(16) FkOut s_out;
+  __shared__ __align__(128) uint32_t s_obs[NW][kTileW * kTileH];
+  __shared__ __align__(8) uint64_t s_bar[NW];
+  __shared__ unsigned long long s_red[NW][4];
+
+  if (a.done && *a.done) return;  // PSO stop rule reached (grid-uniform)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = blockIdx.x / a.S, sidx = blockIdx.x % a.S;
+
+  if (MODE == kModeCost && warp == NW - 1 && lane == 0) {
+    // one thread initialises every warp's TMA barrier (count 1: the expect_tx arrival)
+    for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);
+    fence_mbar_init();
+    if (a.use_tma == 1) prefetch_tmap(&tmap);
+  }
+  if (warp == 0) {
+    const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
+    fk_warp<PoseT>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
+  }
+  __syncthreads();
+
+  // tile origin: the union box's x0 rounded down to 4 px, because a TMA box must start
+  // 16-byte aligned in global memory (an unaligned start faults on sm_100a)
+  int4 ub = s_out.ubox;
+  ub.x &= ~3;
+  const int bw = ub.z - ub.x + 1, bh = ub.w - ub.y + 1;
+  const int tx = bw > 0 ? (bw + kTileW - 1) / kTileW : 0;
+  const int ty = bh > 0 ? (bh + kTileH - 1) / kTileH : 0;
+  const int ntiles = tx * ty;
+  const int col = lane & 15, rowb = lane >> 4;
+  const float znear = a.cam.znear, zfar = a.cam.zfar;
+  const float d_m = a.cost.d_m, clampv = a.cost.clampv;
+  unsigned int c_rm = 0, c_and = 0, c_both = 0;
+  unsigned long long c_num = 0;
+  uint32_t phase = 0;
+
+  for (int t = sidx * NW + warp; t < ntiles; t += a.S * NW) {
+    const int X0 = ub.x + (t % tx) * kTileW, Y0 = ub.y + (t / tx) * kTileH;
+    if (MODE == kModeCost && a.use_tma && lane == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(&s_bar[warp], kTileW * kTileH * 4);
+      tma_load_2d(s_obs[warp], a.use_tma == 2 ? a.tmap_g : &tmap, X0, Y0, &s_bar[warp]);
+    }
+    // cull the 38 conservative boxes against the tile: two ballots -> 64-bit mask
+    uint64_t mask;
+    {
+      const int4 b = s_out.box[lane];
+      const bool ov = b.x <= X0 + kTileW - 1 && b.z >= X0 && b.y <= Y0 + kTileH - 1 && b.w >= Y0;
+      bool ov2 = false;
+      if (lane < kNprim - 32) {
+        const int4 c = s_out.box[32 + lane];
+        ov2 = c.x <= X0 + kTileW - 1 && c.z >= X0 && c.y <= Y0 + kTileH - 1 && c.w >= Y0;
+      }
+      mask = (uint64_t)__ballot_sync(0xffffffffu, ov) |
+             ((uint64_t)__ballot_sync(0xffffffffu, ov2) << 32);
+    }
+    Lane4 L;
+    const int x = X0 + col;
+    L.dx = __fdiv_rn((float)x + 0.5f - a.cam.cx, a.cam.fx);
+#pragma unroll
+    for (int j = 0; j < kPxPerLane; j++) {
+      const int y = Y0 + rowb + 2 * j;
+      L.dy[j] = __fdiv_rn((float)y + 0.5f - a.cam.cy, a.cam.fy);
+      L.inv_dd[j] = __frcp_rn(fmaf(L.dx, L.dx, fmaf(L.dy[j], L.dy[j], 1.f)));
+      L.zb[j] = INFINITY;
+    }
+    for (uint64_t m = mask & kSphereMask; m; m &= m - 1)
+      isect_sphere(s_out.rec[__ffsll((long long)m) - 1], L, znear, zfar);
+    for (uint64_t m = mask & kConeMask; m; m &= m - 1)
+      isect_cone(s_out.rec[__ffsll((long long)m) - 1], L, znear, zfar);
+    for (uint64_t m = mask & kEllMask; m; m &= m - 1)
+      isect_ellipsoid(s_out.rec[__ffsll((long long)m) - 1], L, znear, zfar);
+
+    if (MODE == kModeDepth) {
+#pragma unroll
+      for (int j = 0; j < kPxPerLane; j++) {
+        const int y = Y0 + rowb + 2 * j;
+        if (x < a.cam.W && y < a.cam.H)
+          a.depth_out[(size_t)y * a.cam.W + x] = L.zb[j] < INFINITY ? L.zb[j] : 0.f;
+      }
+    } else {
+      if (a.use_tma) {
+        mbar_wait(&s_bar[warp], phase);
+        phase ^= 1u;
+      } else {
+#pragma unroll
+        for (int j = 0; j < kPxPerLane; j++) {
+          const int y = Y0 + rowb + 2 * j;
+          s_obs[warp][(rowb + 2 * j) * kTileW + col] =
+              (x < a.cam.W && y < a.cam.H) ? a.obs[(size_t)y * a.obs_pitch + x] : 0u;
+        }
+        __syncwarp();
+      }
+#pragma unroll
+      for (int j = 0; j < kPxPerLane; j++) {
+        const int y = Y0 + rowb + 2 * j;
+        if (x < a.cam.W && y < a.cam.H && L.zb[j] < INFINITY) {
+          const uint32_t w = s_obs[warp][(rowb + 2 * j) * kTileW + col];
+          const float od = __uint_as_float(w & 0x7fffffffu);
+          const unsigned int os = w >> 31;
+          const float diff = fabsf(od - L.zb[j]);
+          // r_m = 1 where |r_d - o_d| < d_m or o_d undefined (AMB-4, AMB-5)
+          const unsigned int rm = (od == 0.f) | (diff < d_m);
+          c_rm += rm;
+          c_and += rm & os;
+          if (od > 0.f) {
+            c_both += 1;
+            c_num += __float2ull_rn(fminf(diff, clampv) * 1048576.f);  // 2^-20 mm fixed point
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  if (MODE != kModeCost) return;
+  // ---- reduction: warp shuffles, one atomic per sum per CTA ----
+  c_rm = __reduce_add_sync(0xffffffffu, c_rm);
+  c_and = __reduce_add_sync(0xffffffffu, c_and);
+  c_both = __reduce_add_sync(0xffffffffu, c_both);
+#pragma unroll
+  for (int off = 16; off; off >>= 1) c_num += __shfl_xor_sync(0xffffffffu, c_num, off);
+  if (lane == 0) {
+    s_red[warp][0] = c_rm;
+    s_red[warp][1] = c_and;
+    s_red[warp][2] = c_num;
+    s_red[warp][3] = c_both;
+  }
+  __syncthreads();
+  unsigned long long* acc = a.acc + (size_t)p * 4;
+  if (threadIdx.x == 0) {
+    unsigned long long v[4] = {0, 0, 0, 0};
+    for (int w = 0; w < NW; w++)
+      for (int k = 0; k < 4; k++) v[k] += s_red[w][k];
+    int last = 1;
+    if (a.S > 1) {
+      for (int k = 0; k < 4; k++)
+        if (v[k]) atomicAdd(acc + k, v[k]);
+      __threadfence();
+      last = atomicAdd(a.counters + p, 1u) == (unsigned)(a.S - 1);
+      if (last) {
+        __threadfence();
+        for (int k = 0; k < 4; k++) v[k] = atomicExch(acc + k, 0ull);  // read + reset
+        a.counters[p] = 0;
+      }
+    }
+    if (last) {
+      // ---- Eq. (4)-(5) in fp64 (AMB-1, -2, -3, -6) ----
+      const long long s_rm = (long long)v[0], s_and = (long long)v[1];
+      const long long s_or = (long long)*a.S_o + s_rm - s_and;
+      double D = 0.0;
+      if (s_or > 0) {
+        const double num = (double)v[2] * (1.0 / 1048576.0);
+        const double sor = (double)s_or, sand = (double)s_and;
+        D = a.cost.depth_scale * num / sor + a.cost.lambda * (1.0 - 2.0 * sand / (sand + sor));
+      }
+      const double E = D + a.cost.lambda_k * s_out.kc;
+      if (a.costs32) a.costs32[p] = (float)E;
+      if (a.costs64) a.costs64[p] = E;
+      if (a.sums_out)
+        for (int k = 0; k < 4; k++) a.sums_out[(size_t)p * 4 + k] = v[k];
+    }
+  }
+}
+
+__global__ void k_fk_debug(const double* pose, const DimsD dims, const CamParams cam,
+                           float* rec, int* boxes, double* joints, double* kc) {
+  __shared__ FkScratch s;
+  __shared__ __align__(16) FkOut o;
+  fk_warp<double>(pose, dims, cam, 0.0, s, o);
+  for (int j = threadIdx.x; j < kNprim; j += 32) {
+    if (rec)
+      for (int i = 0; i < kRec; i++) rec[j * kRec + i] = o.rec[j][i];
+    if (boxes) {
+      boxes[j * 4 + 0] = o.box[j].x;
+      boxes[j * 4 + 1] = o.box[j].y;
+      boxes[j * 4 + 2] = o.box[j].z;
+      boxes[j * 4 + 3] = o.box[j].w;
+    }
+  }
+  if (joints)
+    for (int i = threadIdx.x; i < 60; i += 32) joints[i] = (&s.J[0][0][0])[i];
+  if (kc && threadIdx.x == 0) *kc = o.kc;
+}
+
+// ---------------------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------------------
+constexpr int kEvalWarps = 8;
+int eval_warps_per_cta() { return kEvalWarps; }
+
+cudaError_t launch_pack_obs(const float* depth, const uint8_t* mask, uint32_t* obs, int W,
+                            int H, int pitch_words, unsigned long long* S_o, cudaStream_t st) {
+  const long long npx = (long long)W * H;
+  const int threads = 256;
+  const long long blocks = (npx + threads - 1) / threads;
+  k_pack_obs<<<(unsigned)blocks, threads, 0, st>>>(depth, mask, obs, W, H, pitch_words, S_o);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_depth_to_mask(const float* depth, uint8_t* mask, int npx, cudaStream_t st) {
+  k_depth_to_mask<<<(npx + 255) / 256, 256, 0, st>>>(depth, mask, npx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUtensorMap* map,
+                        cudaStream_t st) {
+  const long long blocks = (long long)a.n * a.S;
+  if (blocks == 0) return cudaSuccess;
+  const dim3 grid((unsigned)blocks), block(kEvalWarps * 32);
+  if (mode == kModeCost) {
+    if (pose_double)
+      k_eval<kEvalWarps, double, kModeCost><<<grid, block, 0, st>>>(a, *map);
+    else
+      k_eval<kEvalWarps, float, kModeCost><<<grid, block, 0, st>>>(a, *map);
+  } else {
+    if (pose_double)
+      k_eval<kEvalWarps, double, kModeDepth><<<grid, block, 0, st>>>(a, *map);
+    else
+      k_eval<kEvalWarps, float, kModeDepth><<<grid, block, 0, st>>>(a, *map);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fk_debug(const double* pose_dev, const DimsD& dims, const CamParams& cam,
+                            float* rec, int* boxes, double* joints, double* kc,
+                            cudaStream_t st) {
+  k_fk_debug<<<1, 32, 0, st>>>(pose_dev, dims, cam, rec, boxes, joints, kc);
+  return cudaGetLastError();
+}
+
+}  // namespace hp

@@ -1,0 +1,356 @@
+"""ctypes binding of libhp.so (include/hp.h) — argument marshalling only.
+
+Every step of the path (FK, rendering, scoring, PSO) runs in the CUDA kernels behind the C
+ABI; this module converts torch tensors to device pointers and the current CUDA stream to
+a ``cudaStream_t``.  There is no CPU fallback: if ``libhp.so`` is missing or no sm_100
+device is present, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhp.so")
+NDOF = 26
+NPRIM = 38
+REC_FLOATS = 24
+
+HP_OK, HP_ERR_INVALID_ARG, HP_ERR_CUDA, HP_ERR_OOM, HP_ERR_NCCL, HP_ERR_STATE, \
+    HP_ERR_NO_DEVICE = range(7)
+
+
+class HPError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"hp status {status}: {msg}")
+        self.status = status
+
+
+class Intrinsics(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("fx", C.c_float), ("fy", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("z_near_mm", C.c_float),
+                ("z_far_mm", C.c_float)]
+
+
+class HandDims(C.Structure):
+    _fields_ = [("palm_half_w", C.c_float), ("palm_half_t", C.c_float), ("palm_len", C.c_float),
+                ("palm_cap_half_len", C.c_float), ("base", (C.c_float * 3) * 5),
+                ("seg_len", (C.c_float * 3) * 5), ("radius", (C.c_float * 4) * 5),
+                ("thumb_ell_x", C.c_float), ("thumb_ell_z", C.c_float),
+                ("thumb_yaw_deg", C.c_float), ("thumb_pitch_deg", C.c_float)]
+
+
+class CostParams(C.Structure):
+    _fields_ = [("d_m", C.c_double), ("d_M", C.c_double), ("lam", C.c_double),
+                ("lambda_k", C.c_double), ("depth_scale", C.c_double), ("kc_rest", C.c_double),
+                ("clamp_at_dm", C.c_int32)]
+
+
+class PsoParams(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("particles", C.c_int32), ("generations", C.c_int32),
+                ("mutation_period", C.c_int32), ("per_dim_r", C.c_int32), ("c1", C.c_double),
+                ("c2", C.c_double), ("mutation_fraction", C.c_double),
+                ("stop_threshold", C.c_double), ("init_center", C.POINTER(C.c_double)),
+                ("init_radius", C.POINTER(C.c_double))]
+
+
+_lib = None
+_VP = C.c_void_p
+
+
+def lib() -> C.CDLL:
+    """Load libhp.so (raises if it was not built: run ``python -m paper_2005_07068_b200.build``)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not found: build it with "
+                              "`python -m paper_2005_07068_b200.build` (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        sig = {
+            "hp_default_dims": [C.POINTER(HandDims)],
+            "hp_default_cost": [C.POINTER(CostParams)],
+            "hp_default_pso": [C.POINTER(PsoParams)],
+            "hp_default_intrinsics": [C.c_int32, C.c_int32, C.POINTER(Intrinsics)],
+            "hp_bounds": [_VP, _VP],
+            "hp_create": [C.POINTER(Intrinsics), C.POINTER(HandDims), C.POINTER(CostParams),
+                          C.c_int32, C.c_int32, C.POINTER(_VP)],
+            "hp_set_observation": [_VP, _VP, _VP, C.c_int32, _VP],
+            "hp_render_observation": [_VP, _VP, _VP, _VP, _VP],
+            "hp_eval_costs": [_VP, _VP, C.c_int64, _VP, _VP],
+            "hp_eval_costs_host": [_VP, _VP, C.c_int64, _VP, _VP],
+            "hp_eval_sums": [_VP, _VP, C.c_int64, _VP, _VP, _VP],
+            "hp_pso_fit": [_VP, C.POINTER(PsoParams), _VP, _VP, _VP, _VP, _VP],
+            "hp_pso_state": [_VP, _VP, _VP, _VP, _VP],
+            "hp_debug_fk": [_VP, _VP, _VP, _VP, _VP, _VP],
+            "hp_debug_render": [_VP, _VP, _VP, _VP],
+            "hp_debug_pso_sphere": [_VP, C.c_int32, _VP, _VP, _VP, _VP, C.c_int32, C.c_int32, _VP,
+                                    C.POINTER(PsoParams), _VP, _VP, _VP, _VP, _VP],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        L.hp_last_error.argtypes = [_VP]
+        L.hp_last_error.restype = C.c_char_p
+        L.hp_last_launch_count.argtypes = [_VP]
+        L.hp_last_launch_count.restype = C.c_int64
+        L.hp_splits_for.argtypes = [_VP, C.c_int64]
+        L.hp_splits_for.restype = C.c_int32
+        L.hp_destroy.argtypes = [_VP]
+        L.hp_destroy.restype = None
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    """Names of every function include/hp.h declares (used by the CPU load test)."""
+    return ["hp_default_dims", "hp_default_cost", "hp_default_pso", "hp_default_intrinsics",
+            "hp_bounds", "hp_create", "hp_set_observation", "hp_render_observation",
+            "hp_eval_costs", "hp_eval_costs_host", "hp_eval_sums", "hp_pso_fit", "hp_pso_state",
+            "hp_debug_fk", "hp_debug_render", "hp_debug_pso_sphere", "hp_last_launch_count",
+            "hp_splits_for", "hp_last_error", "hp_destroy"]
+
+
+def _check(status: int, ctx=None):
+    if status != HP_OK:
+        msg = lib().hp_last_error(ctx)
+        raise HPError(status, msg.decode() if msg else "")
+
+
+def default_dims() -> HandDims:
+    d = HandDims()
+    _check(lib().hp_default_dims(C.byref(d)))
+    return d
+
+
+def default_cost(**kw) -> CostParams:
+    c = CostParams()
+    _check(lib().hp_default_cost(C.byref(c)))
+    for k, v in kw.items():
+        setattr(c, "lam" if k == "lambda_" else k, v)
+    return c
+
+
+def default_intrinsics(width: int, height: int) -> Intrinsics:
+    i = Intrinsics()
+    _check(lib().hp_default_intrinsics(width, height, C.byref(i)))
+    return i
+
+
+def intrinsics_from(d: dict) -> Intrinsics:
+    return Intrinsics(d["width"], d["height"], d["fx"], d["fy"], d["cx"], d["cy"], d["z_near"],
+                      d["z_far"])
+
+
+def bounds():
+    lo = np.zeros(NDOF)
+    hi = np.zeros(NDOF)
+    _check(lib().hp_bounds(lo.ctypes.data, hi.ctypes.data))
+    return lo, hi
+
+
+def _dptr(t) -> int:
+    """Device pointer of a contiguous CUDA tensor."""
+    assert t.is_cuda and t.is_contiguous(), "expected a contiguous CUDA tensor"
+    return t.data_ptr()
+
+
+def _stream(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+@dataclass
+class FitResult:
+    best_pose: np.ndarray
+    best_cost: float
+    trace: np.ndarray
+    gens_run: int
+
+
+class Context:
+    """One hp_ctx: a camera, a hand model, cost constants and a workspace for up to
+    ``max_particles`` poses per call (include/hp.h hp_create)."""
+
+    def __init__(self, width: int = 640, height: int = 480, max_particles: int = 4096,
+                 intrinsics: Intrinsics | None = None, dims: HandDims | None = None,
+                 cost: CostParams | None = None, device: int = -1):
+        self._L = lib()
+        self.cam = intrinsics or default_intrinsics(width, height)
+        self.width, self.height = self.cam.width, self.cam.height
+        self.max_particles = max_particles
+        h = _VP()
+        st = self._L.hp_create(C.byref(self.cam), C.byref(dims) if dims else None,
+                               C.byref(cost) if cost else None, max_particles, device,
+                               C.byref(h))
+        _check(st, None)
+        self._h = h
+
+    # -- lifetime
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.hp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- observation
+    def set_observation(self, depth, mask, stream=None):
+        """O = (O_s, O_d): depth fp32 [H][W] mm (0 = undefined), mask u8 [H][W]; numpy
+        arrays (host) or CUDA tensors (device)."""
+        if isinstance(depth, np.ndarray):
+            d = np.ascontiguousarray(depth, dtype=np.float32)
+            m = np.ascontiguousarray(mask, dtype=np.uint8)
+            assert d.shape == (self.height, self.width) and m.shape == d.shape
+            _check(self._L.hp_set_observation(self._h, d.ctypes.data, m.ctypes.data, 0,
+                                              _stream(stream)), self._h)
+        else:
+            assert tuple(depth.shape) == (self.height, self.width)
+            _check(self._L.hp_set_observation(self._h, _dptr(depth), _dptr(mask), 1,
+                                              _stream(stream)), self._h)
+
+    def render_observation(self, h_ref, stream=None):
+        """Simulation protocol: render h_ref on the GPU -> (depth, mask) tensors."""
+        import torch
+
+        h = np.ascontiguousarray(h_ref, dtype=np.float64)
+        depth = torch.empty((self.height, self.width), dtype=torch.float32, device="cuda")
+        mask = torch.empty((self.height, self.width), dtype=torch.uint8, device="cuda")
+        _check(self._L.hp_render_observation(self._h, h.ctypes.data, _dptr(depth), _dptr(mask),
+                                             _stream(stream)), self._h)
+        return depth, mask
+
+    # -- evaluation
+    def eval_costs(self, poses, out=None, stream=None):
+        """E(h, O) for poses [N][26] fp32 CUDA tensor -> costs [N] fp32 (async)."""
+        import torch
+
+        assert poses.dtype == torch.float32 and poses.shape[-1] == NDOF
+        n = poses.shape[0]
+        if out is None:
+            out = torch.empty(n, dtype=torch.float32, device=poses.device)
+        _check(self._L.hp_eval_costs(self._h, _dptr(poses), n, _dptr(out), _stream(stream)),
+               self._h)
+        return out
+
+    def eval_costs_host(self, poses: np.ndarray, stream=None) -> np.ndarray:
+        """Host-buffer variant: copies in, scores, copies out, synchronises."""
+        p = np.ascontiguousarray(poses, dtype=np.float32).reshape(-1, NDOF)
+        out = np.empty(p.shape[0], dtype=np.float32)
+        _check(self._L.hp_eval_costs_host(self._h, p.ctypes.data, p.shape[0], out.ctypes.data,
+                                          _stream(stream)), self._h)
+        return out
+
+    def eval_sums(self, poses, stream=None):
+        """(sums [N][4] u64 as int64 tensor, costs fp64 [N]) — test hook."""
+        import torch
+
+        n = poses.shape[0]
+        sums = torch.zeros((n, 4), dtype=torch.int64, device=poses.device)
+        costs = torch.empty(n, dtype=torch.float64, device=poses.device)
+        _check(self._L.hp_eval_sums(self._h, _dptr(poses), n, _dptr(sums), _dptr(costs),
+                                    _stream(stream)), self._h)
+        return sums, costs
+
+    def splits_for(self, n: int) -> int:
+        return self._L.hp_splits_for(self._h, n)
+
+    def last_launch_count(self) -> int:
+        return self._L.hp_last_launch_count(self._h)
+
+    # -- PSO
+    def pso_fit(self, seed: int = 0, particles: int = 64, generations: int = 30,
+                mutation_period: int = 3, c1: float = 2.8, c2: float = 1.3,
+                mutation_fraction: float = 0.5, per_dim_r: bool = False,
+                stop_threshold: float = -math.inf, init_center=None, init_radius=None,
+                stream=None) -> FitResult:
+        """The paper's PSO fit on the GPU; synchronous."""
+        p = PsoParams()
+        _check(self._L.hp_default_pso(C.byref(p)))
+        p.seed, p.particles, p.generations = seed, particles, generations
+        p.mutation_period, p.c1, p.c2 = mutation_period, c1, c2
+        p.mutation_fraction, p.per_dim_r, p.stop_threshold = mutation_fraction, int(per_dim_r), \
+            stop_threshold
+        keep = []
+        if init_center is not None:
+            ic = np.ascontiguousarray(init_center, dtype=np.float64)
+            ir = np.ascontiguousarray(init_radius, dtype=np.float64)
+            keep += [ic, ir]
+            p.init_center = ic.ctypes.data_as(C.POINTER(C.c_double))
+            p.init_radius = ir.ctypes.data_as(C.POINTER(C.c_double))
+        best = np.zeros(NDOF)
+        cost = C.c_double()
+        trace = np.zeros(generations)
+        gr = C.c_int32()
+        _check(self._L.hp_pso_fit(self._h, C.byref(p), best.ctypes.data, C.byref(cost),
+                                  trace.ctypes.data, C.byref(gr), _stream(stream)), self._h)
+        return FitResult(best, cost.value, trace, gr.value)
+
+    def pso_state(self, particles: int, D: int = NDOF):
+        X = np.zeros((particles, D))
+        V = np.zeros((particles, D))
+        P = np.zeros((particles, D))
+        Pc = np.zeros(particles)
+        _check(self._L.hp_pso_state(self._h, X.ctypes.data, V.ctypes.data, P.ctypes.data,
+                                    Pc.ctypes.data), self._h)
+        return X, V, P, Pc
+
+    def debug_pso_sphere(self, D, lo, hi, init_lo, init_hi, mut_lo, mut_hi, centre, seed=0,
+                         particles=64, generations=30, mutation_period=3, c1=2.8, c2=1.3,
+                         mutation_fraction=0.5, per_dim_r=False, stop_threshold=-math.inf):
+        p = PsoParams()
+        _check(self._L.hp_default_pso(C.byref(p)))
+        p.seed, p.particles, p.generations = seed, particles, generations
+        p.mutation_period, p.c1, p.c2 = mutation_period, c1, c2
+        p.mutation_fraction, p.per_dim_r, p.stop_threshold = mutation_fraction, int(per_dim_r), \
+            stop_threshold
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (lo, hi, init_lo, init_hi,
+                                                                     centre)]
+        best = np.zeros(D)
+        cost = C.c_double()
+        trace = np.zeros(generations)
+        gr = C.c_int32()
+        _check(self._L.hp_debug_pso_sphere(self._h, D, *[a.ctypes.data for a in arrs[:4]],
+                                           mut_lo, mut_hi, arrs[4].ctypes.data, C.byref(p),
+                                           best.ctypes.data, C.byref(cost), trace.ctypes.data,
+                                           C.byref(gr), None), self._h)
+        return FitResult(best, cost.value, trace, gr.value)
+
+    # -- test hooks
+    def debug_fk(self, pose):
+        h = np.ascontiguousarray(pose, dtype=np.float64)
+        rec = np.zeros((NPRIM, REC_FLOATS), dtype=np.float32)
+        boxes = np.zeros((NPRIM, 4), dtype=np.int32)
+        joints = np.zeros((5, 4, 3))
+        kc = C.c_double()
+        _check(self._L.hp_debug_fk(self._h, h.ctypes.data, rec.ctypes.data, boxes.ctypes.data,
+                                   joints.ctypes.data, C.byref(kc)), self._h)
+        return rec, boxes, joints, kc.value
+
+    def debug_render(self, pose_dev, stream=None):
+        import torch
+
+        depth = torch.empty((self.height, self.width), dtype=torch.float32, device="cuda")
+        _check(self._L.hp_debug_render(self._h, _dptr(pose_dev), _dptr(depth), _stream(stream)),
+               self._h)
+        return depth
