@@ -42,13 +42,15 @@ WIDTH, HEIGHT = 640, 480
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--fit-seeds", type=int, default=10)
     ap.add_argument("--no-fit", action="store_true")
+    ap.add_argument("--clock-ramp", type=float, default=1.0,
+                    help="seconds of untimed load before the timed region (clock sampling)")
     return ap.parse_args()
 
 
@@ -121,7 +123,9 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "window": "nvidia-smi every 200 ms over a 1 s untimed load ramp + the timed "
+                          "region"}
 
 
 def cpu_baseline(seconds: float, swarm: np.ndarray):
@@ -214,6 +218,12 @@ def run_ours(args):
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     with ClockSampler(local) as clk:
+        # ~1 s of untimed load first: nvidia-smi needs ~0.2 s per sample and the clocks ramp
+        t_load = time.perf_counter()
+        while time.perf_counter() - t_load < args.clock_ramp:
+            for _ in range(20):
+                step()
+            torch.cuda.synchronize()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()

@@ -12,9 +12,13 @@ namespace hp {
 constexpr int kNdof = 26;
 constexpr int kNprim = 38;
 constexpr int kRec = 24;   // floats per primitive record (96 B)
-constexpr int kTileW = 16; // warp tile: 16 x 8 pixels, 4 pixels per lane
-constexpr int kTileH = 8;
-constexpr int kPxPerLane = 4;
+#ifndef HP_PX
+#define HP_PX 4
+#endif
+constexpr int kPxPerLane = HP_PX;       // pixels per lane (one column, every other row)
+constexpr int kTileW = 16;              // warp tile: 16 x (2 * kPxPerLane) pixels
+constexpr int kTileH = 2 * kPxPerLane;
+constexpr int kRayPad = 16;             // ray-table slack for tiles overhanging the image
 
 // Primitive order on the device (sorted by kind so a cull mask splits by bit range):
 //   0..19  spheres   (finger f, joint k) -> 4 f + k

@@ -60,10 +60,12 @@ struct Lane4 {
   float zb[kPxPerLane];
 };
 
-__device__ __forceinline__ float fast_sqrt(float x) { return x * rsqrtf(x); }
+__device__ __forceinline__ float fast_sqrt(float x) { return x * rsqrtf(x); }  // NaN if x < 0
 
+// Branch-free min-depth update: a NaN z (no real root / out of range) never wins.
 __device__ __forceinline__ void keep(float z, float& zb, float znear, float zfar) {
-  if (z >= znear && z <= zfar && z < zb) zb = z;
+  const bool ok = (z >= znear) & (z <= zfar) & (z < zb);
+  zb = ok ? z : zb;
 }
 
 __device__ __forceinline__ void isect_sphere(const float* __restrict__ r, Lane4& L, float znear,
@@ -75,7 +77,7 @@ __device__ __forceinline__ void isect_sphere(const float* __restrict__ r, Lane4&
     const float tc = fmaf(L.dy[j], q.y, bx) * L.inv_dd[j];
     const float ox = fmaf(tc, L.dx, -q.x), oy = fmaf(tc, L.dy[j], -q.y), oz = tc - q.z;
     const float disc = q.w - fmaf(ox, ox, fmaf(oy, oy, oz * oz));
-    if (disc >= 0.f) keep(tc - fast_sqrt(disc * L.inv_dd[j]), L.zb[j], znear, zfar);
+    keep(tc - fast_sqrt(disc * L.inv_dd[j]), L.zb[j], znear, zfar);
   }
 }
 
@@ -85,7 +87,7 @@ __device__ __forceinline__ void isect_ellipsoid(const float* __restrict__ r, Lan
   const float4 r1 = *reinterpret_cast<const float4*>(r + 4);   // M00 M01 M02 M10
   const float4 r2 = *reinterpret_cast<const float4*>(r + 8);   // M11 M12 M20 M21
   const float4 r3 = *reinterpret_cast<const float4*>(r + 12);  // M22 cl0 cl1 cl2
-  // d_l = M (dx, dy, 1): the dx part is shared by the lane's 4 pixels
+  // d_l = M (dx, dy, 1): the dx part is shared by the lane's pixels
   const float px = fmaf(r1.x, L.dx, r1.z), py = fmaf(r1.w, L.dx, r2.y),
               pz = fmaf(r2.z, L.dx, r3.x);
   const float bx = fmaf(L.dx, r0.x, r0.z);
@@ -99,11 +101,9 @@ __device__ __forceinline__ void isect_ellipsoid(const float* __restrict__ r, Lan
     const float B = fmaf(ox, lx, fmaf(oy, ly, oz * lz));
     const float C = fmaf(ox, ox, fmaf(oy, oy, fmaf(oz, oz, -1.f)));
     const float disc = fmaf(B, B, -A * C);
-    if (disc >= 0.f) {
-      const float qq = -(B + copysignf(fast_sqrt(disc), B));
-      const float s = fminf(__fdividef(qq, A), __fdividef(C, qq));
-      keep(tc + s, L.zb[j], znear, zfar);
-    }
+    const float qq = -(B + copysignf(fast_sqrt(disc), B));
+    const float s = fminf(__fdividef(qq, A), __fdividef(C, qq));
+    keep(tc + s, L.zb[j], znear, zfar);
   }
 }
 
@@ -133,14 +133,12 @@ __device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L
     const float B = fmaf(ox, lx, fmaf(oy, ly, -kd * g));
     const float C = fmaf(ox, ox, fmaf(oy, oy, -g * g));
     const float disc = fmaf(B, B, -A * C);
-    if (disc >= 0.f) {
-      const float qq = -(B + copysignf(fast_sqrt(disc), B));
-      const float s1 = __fdividef(qq, A), s2 = __fdividef(C, qq);
-      const float sa = fminf(s1, s2), sb = fmaxf(s1, s2);
-      const float za = fmaf(sa, lz, oz), zb = fmaf(sb, lz, oz);
-      const float s = fabsf(za) <= hl ? sa : (fabsf(zb) <= hl ? sb : __int_as_float(0x7fc00000));
-      keep(tc + s, L.zb[j], znear, zfar);
-    }
+    const float qq = -(B + copysignf(fast_sqrt(disc), B));
+    const float s1 = __fdividef(qq, A), s2 = __fdividef(C, qq);
+    const float sa = fminf(s1, s2), sb = fmaxf(s1, s2);
+    const float za = fmaf(sa, lz, oz), zb = fmaf(sb, lz, oz);
+    const float s = fabsf(za) <= hl ? sa : (fabsf(zb) <= hl ? sb : __int_as_float(0x7fc00000));
+    keep(tc + s, L.zb[j], znear, zfar);
   }
 }
 
@@ -148,27 +146,40 @@ __device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L
 // The fused evaluation kernel
 // ---------------------------------------------------------------------------------------
 template <int NW, typename PoseT, int MODE>
-__global__ void __launch_bounds__(NW * 32)
+__global__ void __launch_bounds__(NW * 32, 24 / NW)
     k_eval(const EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
   __shared__ FkScratch s_fk;
   __shared__ __align__(16) FkOut s_out;
   __shared__ __align__(128) uint32_t s_obs[NW][kTileW * kTileH];
   __shared__ __align__(8) uint64_t s_bar[NW];
   __shared__ unsigned long long s_red[NW][4];
+  __shared__ int s_next;
+  extern __shared__ float s_ray[];  // dx per column [W + pad], dy per row [H + pad]
 
   if (a.done && *a.done) return;  // PSO stop rule reached (grid-uniform)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.x / a.S, sidx = blockIdx.x % a.S;
+  float* s_dx = s_ray;
+  float* s_dy = s_ray + a.cam.W + kRayPad;
 
-  if (MODE == kModeCost && warp == NW - 1 && lane == 0) {
-    // one thread initialises every warp's TMA barrier (count 1: the expect_tx arrival)
-    for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);
-    fence_mbar_init();
-    if (a.use_tma == 1) prefetch_tmap(&tmap);
-  }
   if (warp == 0) {
     const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
     fk_warp<PoseT>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
+  } else {
+    // while warp 0 runs FK: per-column / per-row ray directions, correctly rounded
+    // d = ((u + 0.5 - cx)/fx, (v + 0.5 - cy)/fy, 1)  (P:L114 camera C)
+    const int nx = a.cam.W + kRayPad, ny = a.cam.H + kRayPad;
+    for (int i = threadIdx.x - 32; i < nx + ny; i += (NW - 1) * 32) {
+      if (i < nx) s_dx[i] = __fdiv_rn((float)i + 0.5f - a.cam.cx, a.cam.fx);
+      else s_dy[i - nx] = __fdiv_rn((float)(i - nx) + 0.5f - a.cam.cy, a.cam.fy);
+    }
+    if (MODE == kModeCost && warp == NW - 1 && lane == 0) {
+      // one thread initialises every warp's TMA barrier (count 1: the expect_tx arrival)
+      for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);
+      fence_mbar_init();
+      if (a.use_tma == 1) prefetch_tmap(&tmap);
+    }
+    if (threadIdx.x == 32) s_next = NW;
   }
   __syncthreads();
 
@@ -180,6 +191,9 @@ __global__ void __launch_bounds__(NW * 32)
   const int tx = bw > 0 ? (bw + kTileW - 1) / kTileW : 0;
   const int ty = bh > 0 ? (bh + kTileH - 1) / kTileH : 0;
   const int ntiles = tx * ty;
+  // this CTA owns tiles sidx, sidx + S, ...; warps take them dynamically (load balance)
+  const int nmine = ntiles > sidx ? (ntiles - sidx + a.S - 1) / a.S : 0;
+  const float inv_tx = 1.0f / (float)(tx > 0 ? tx : 1);
   const int col = lane & 15, rowb = lane >> 4;
   const float znear = a.cam.znear, zfar = a.cam.zfar;
   const float d_m = a.cost.d_m, clampv = a.cost.clampv;
@@ -187,13 +201,22 @@ __global__ void __launch_bounds__(NW * 32)
   unsigned long long c_num = 0;
   uint32_t phase = 0;
 
-  for (int t = sidx * NW + warp; t < ntiles; t += a.S * NW) {
-    const int X0 = ub.x + (t % tx) * kTileW, Y0 = ub.y + (t / tx) * kTileH;
+  int j = warp;
+  while (j < nmine) {
+    const int t = sidx + j * a.S;
+    int qy = (int)((float)t * inv_tx);  // t / tx, corrected below
+    int qx = t - qy * tx;
+    if (qx < 0) { qy--; qx += tx; }
+    if (qx >= tx) { qy++; qx -= tx; }
+    const int X0 = ub.x + qx * kTileW, Y0 = ub.y + qy * kTileH;
     if (MODE == kModeCost && a.use_tma && lane == 0) {
       fence_proxy_async();
       mbar_expect_tx(&s_bar[warp], kTileW * kTileH * 4);
       tma_load_2d(s_obs[warp], a.use_tma == 2 ? a.tmap_g : &tmap, X0, Y0, &s_bar[warp]);
     }
+    // next tile for this warp (dynamic): fetched early, used at the loop end
+    int jn = 0;
+    if (lane == 0) jn = atomicAdd(&s_next, 1);
     // cull the 38 conservative boxes against the tile: two ballots -> 64-bit mask
     uint64_t mask;
     {
@@ -209,13 +232,12 @@ __global__ void __launch_bounds__(NW * 32)
     }
     Lane4 L;
     const int x = X0 + col;
-    L.dx = __fdiv_rn((float)x + 0.5f - a.cam.cx, a.cam.fx);
+    L.dx = s_dx[x];
 #pragma unroll
-    for (int j = 0; j < kPxPerLane; j++) {
-      const int y = Y0 + rowb + 2 * j;
-      L.dy[j] = __fdiv_rn((float)y + 0.5f - a.cam.cy, a.cam.fy);
-      L.inv_dd[j] = __frcp_rn(fmaf(L.dx, L.dx, fmaf(L.dy[j], L.dy[j], 1.f)));
-      L.zb[j] = INFINITY;
+    for (int q = 0; q < kPxPerLane; q++) {
+      L.dy[q] = s_dy[Y0 + rowb + 2 * q];
+      L.inv_dd[q] = __fdividef(1.f, fmaf(L.dx, L.dx, fmaf(L.dy[q], L.dy[q], 1.f)));
+      L.zb[q] = INFINITY;
     }
     for (uint64_t m = mask & kSphereMask; m; m &= m - 1)
       isect_sphere(s_out.rec[__ffsll((long long)m) - 1], L, znear, zfar);
@@ -226,10 +248,10 @@ __global__ void __launch_bounds__(NW * 32)
 
     if (MODE == kModeDepth) {
 #pragma unroll
-      for (int j = 0; j < kPxPerLane; j++) {
-        const int y = Y0 + rowb + 2 * j;
+      for (int q = 0; q < kPxPerLane; q++) {
+        const int y = Y0 + rowb + 2 * q;
         if (x < a.cam.W && y < a.cam.H)
-          a.depth_out[(size_t)y * a.cam.W + x] = L.zb[j] < INFINITY ? L.zb[j] : 0.f;
+          a.depth_out[(size_t)y * a.cam.W + x] = L.zb[q] < INFINITY ? L.zb[q] : 0.f;
       }
     } else {
       if (a.use_tma) {
@@ -237,21 +259,21 @@ __global__ void __launch_bounds__(NW * 32)
         phase ^= 1u;
       } else {
 #pragma unroll
-        for (int j = 0; j < kPxPerLane; j++) {
-          const int y = Y0 + rowb + 2 * j;
-          s_obs[warp][(rowb + 2 * j) * kTileW + col] =
+        for (int q = 0; q < kPxPerLane; q++) {
+          const int y = Y0 + rowb + 2 * q;
+          s_obs[warp][(rowb + 2 * q) * kTileW + col] =
               (x < a.cam.W && y < a.cam.H) ? a.obs[(size_t)y * a.obs_pitch + x] : 0u;
         }
         __syncwarp();
       }
 #pragma unroll
-      for (int j = 0; j < kPxPerLane; j++) {
-        const int y = Y0 + rowb + 2 * j;
-        if (x < a.cam.W && y < a.cam.H && L.zb[j] < INFINITY) {
-          const uint32_t w = s_obs[warp][(rowb + 2 * j) * kTileW + col];
+      for (int q = 0; q < kPxPerLane; q++) {
+        const int y = Y0 + rowb + 2 * q;
+        if (x < a.cam.W && y < a.cam.H && L.zb[q] < INFINITY) {
+          const uint32_t w = s_obs[warp][(rowb + 2 * q) * kTileW + col];
           const float od = __uint_as_float(w & 0x7fffffffu);
           const unsigned int os = w >> 31;
-          const float diff = fabsf(od - L.zb[j]);
+          const float diff = fabsf(od - L.zb[q]);
           // r_m = 1 where |r_d - o_d| < d_m or o_d undefined (AMB-4, AMB-5)
           const unsigned int rm = (od == 0.f) | (diff < d_m);
           c_rm += rm;
@@ -264,6 +286,7 @@ __global__ void __launch_bounds__(NW * 32)
       }
     }
     __syncwarp();
+    j = __shfl_sync(0xffffffffu, jn, 0);
   }
 
   if (MODE != kModeCost) return;
@@ -339,7 +362,10 @@ __global__ void k_fk_debug(const double* pose, const DimsD dims, const CamParams
 // ---------------------------------------------------------------------------------------
 // Launchers
 // ---------------------------------------------------------------------------------------
-constexpr int kEvalWarps = 8;
+#ifndef HP_NW
+#define HP_NW 8
+#endif
+constexpr int kEvalWarps = HP_NW;
 int eval_warps_per_cta() { return kEvalWarps; }
 
 cudaError_t launch_pack_obs(const float* depth, const uint8_t* mask, uint32_t* obs, int W,
@@ -361,16 +387,17 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
   const long long blocks = (long long)a.n * a.S;
   if (blocks == 0) return cudaSuccess;
   const dim3 grid((unsigned)blocks), block(kEvalWarps * 32);
+  const size_t dyn = (size_t)(a.cam.W + a.cam.H + 2 * kRayPad) * sizeof(float);
   if (mode == kModeCost) {
     if (pose_double)
-      k_eval<kEvalWarps, double, kModeCost><<<grid, block, 0, st>>>(a, *map);
+      k_eval<kEvalWarps, double, kModeCost><<<grid, block, dyn, st>>>(a, *map);
     else
-      k_eval<kEvalWarps, float, kModeCost><<<grid, block, 0, st>>>(a, *map);
+      k_eval<kEvalWarps, float, kModeCost><<<grid, block, dyn, st>>>(a, *map);
   } else {
     if (pose_double)
-      k_eval<kEvalWarps, double, kModeDepth><<<grid, block, 0, st>>>(a, *map);
+      k_eval<kEvalWarps, double, kModeDepth><<<grid, block, dyn, st>>>(a, *map);
     else
-      k_eval<kEvalWarps, float, kModeDepth><<<grid, block, 0, st>>>(a, *map);
+      k_eval<kEvalWarps, float, kModeDepth><<<grid, block, dyn, st>>>(a, *map);
   }
   return cudaGetLastError();
 }

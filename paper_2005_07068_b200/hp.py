@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhp.so")
+LIB_PATH = os.environ.get("HP_LIB") or os.path.join(_HERE, "libhp.so")  # HP_LIB: A/B builds
 NDOF = 26
 NPRIM = 38
 REC_FLOATS = 24

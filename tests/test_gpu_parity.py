@@ -250,7 +250,7 @@ def test_pso_sphere_bitwise_parity(N, D, period, per_dim):
     r = O.pso_sphere(D, lo, hi, ilo, ihi, mlo, D, centre,
                      O.default_pso(seed=42, particles=N, generations=12, mutation_period=period,
                                    per_dim_r=per_dim))
-    assert np.array_equal(g.best_x, r.best_x)
+    assert np.array_equal(g.best_pose, r.best_x)
     assert np.array_equal(g.trace, r.trace) and g.best_cost == r.best_cost
     assert np.array_equal(X, r.X) and np.array_equal(V, r.V)
     assert np.array_equal(P, r.P) and np.array_equal(Pc, r.Pcost)
