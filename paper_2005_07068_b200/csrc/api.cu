@@ -64,6 +64,9 @@ struct hp_ctx {
   cudaEvent_t ev = nullptr;
   int64_t last_launches = 0;
   CUtensorMap* tmap_g = nullptr;
+  float* ray = nullptr;  // per-column / per-row ray directions (k_ray_table)
+  unsigned int* pcount = nullptr;  // persistent-kernel counters (zero between launches)
+  int persist_grid = 0;            // CTAs of k_eval_persist (0 = never use it)
   int use_tma = 1;   // HP_NO_TMA=1 in the environment selects plain loads (A/B, debugging)
   int sync_debug = 0;  // HP_SYNC_DEBUG=1: synchronise after every launch
   std::string err;
@@ -193,7 +196,7 @@ void hp_destroy(hp_ctx* ctx) {
   void* dev[] = {ctx->obs, ctx->S_o, ctx->up_depth, ctx->up_mask, ctx->acc, ctx->counters,
                  ctx->poses32, ctx->costs32, ctx->scratch, ctx->X, ctx->V, ctx->P, ctx->Pc,
                  ctx->E, ctx->G, ctx->Gc, ctx->trace, ctx->bnd, ctx->centre, ctx->mark,
-                 ctx->flags, ctx->dyn, ctx->tmap_g};
+                 ctx->flags, ctx->dyn, ctx->tmap_g, ctx->ray, ctx->pcount};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_poses) cudaFreeHost(ctx->h_poses);
@@ -319,6 +322,14 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
     hp_destroy(ctx);
     return st;
   }
+  // ray table, padded to a multiple of 4 floats for the float4 staging copy
+  CKC(cudaMalloc(&ctx->ray, (size_t)((W + H + 2 * kRayPad + 3) & ~3) * sizeof(float)));
+  CKC(launch_ray_table(ctx->camp, ctx->ray, ctx->st));
+  CKC(cudaMalloc(&ctx->pcount, 2 * sizeof(unsigned int)));
+  CKC(cudaMemset(ctx->pcount, 0, 2 * sizeof(unsigned int)));
+  ctx->persist_grid = ctx->sm_count * persist_blocks_per_sm(ctx->camp);
+  if (const char* e = getenv("HP_NO_PERSIST"))
+    if (atoi(e)) ctx->persist_grid = 0;
   CKC(cudaMalloc(&ctx->tmap_g, sizeof(CUtensorMap)));
   CKC(cudaMemcpy(ctx->tmap_g, &ctx->tmap, sizeof(CUtensorMap), cudaMemcpyHostToDevice));
   // evaluation workspace
@@ -385,6 +396,9 @@ static EvalArgs base_args(hp_ctx* ctx) {
   a.obs_pitch = ctx->pitch_words;
   a.use_tma = ctx->use_tma;
   a.tmap_g = ctx->tmap_g;
+  a.ray = ctx->ray;
+  a.pcount = ctx->pcount;
+  a.persist_grid = ctx->persist_grid;
   return a;
 }
 

@@ -19,6 +19,7 @@ constexpr int kPxPerLane = HP_PX;       // pixels per lane (one column, every ot
 constexpr int kTileW = 16;              // warp tile: 16 x (2 * kPxPerLane) pixels
 constexpr int kTileH = 2 * kPxPerLane;
 constexpr int kRayPad = 16;             // ray-table slack for tiles overhanging the image
+                                        // (W + H + 2 kRayPad is a multiple of 4 when W, H are)
 
 // Primitive order on the device (sorted by kind so a cull mask splits by bit range):
 //   0..19  spheres   (finger f, joint k) -> 4 f + k
@@ -78,6 +79,9 @@ struct EvalArgs {
   int obs_pitch;                  // words per row
   int use_tma;                    // 1: TMA tile loads (default), 0: plain loads
   const CUtensorMap* tmap_g;      // the same descriptor in global memory (use_tma = 2)
+  const float* ray;               // k_ray_table output: dx[W + pad], dy[H + pad]
+  unsigned int* pcount;           // [2] persistent kernel: particle counter, CTA exit counter
+  int persist_grid;               // > 0: use k_eval_persist with this many CTAs
 };
 
 // --------------------------------------------------------------------------------------
@@ -99,6 +103,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
@@ -133,8 +140,10 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
 cudaError_t launch_fk_debug(const double* pose_dev, const DimsD& dims, const CamParams& cam,
                             float* rec, int* boxes, double* joints, double* kc,
                             cudaStream_t st);
+cudaError_t launch_ray_table(const CamParams& cam, float* ray, cudaStream_t st);
 cudaError_t launch_depth_to_mask(const float* depth, uint8_t* mask, int npx, cudaStream_t st);
 int eval_warps_per_cta();
+int persist_blocks_per_sm(const CamParams& cam);
 
 // PSO (pso.cu)
 struct PsoDyn {  // per-fit values, read from device memory so a captured graph is reusable

@@ -35,34 +35,40 @@ __device__ __forceinline__ void mat3_mul(const double a[3][3], const double b[3]
 
 // Bounds of the body {c + E q : |q| <= 1}, A = E E^T, on the image: the tangent planes
 // through the camera centre containing an image axis satisfy
-// (cz^2 - Azz) u^2 - 2 (ca cz - Aaz) u + (ca^2 - Aaa) = 0.  Accumulates into [u0,u1]x[v0,v1]
-// (normalised image coordinates); returns 0 behind the camera, 2 if straddling z = 0.
-__device__ __forceinline__ int gen_bounds(const double c[3], const double A[3][3], double& u0,
-                                          double& u1, double& v0, double& v1) {
-  double zext = sqrt(fmax(A[2][2], 0.0));
-  if (c[2] + zext <= 0.0) return 0;
-  if (c[2] - zext <= 0.0) return 2;
-  double qa = c[2] * c[2] - A[2][2];
+// (cz^2 - Azz) u^2 - 2 (ca cz - Aaz) u + (ca^2 - Aaa) = 0.  Evaluated in fp32 (the boxes only
+// need to be conservative, and carry a 1 px margin) with the discriminant expanded so the
+// ca^2 cz^2 terms cancel analytically:
+//   disc = Aaa cz^2 + Azz ca^2 - 2 Aaz ca cz + Aaz^2 - Aaa Azz.
+// Accumulates into [u0,u1]x[v0,v1] (normalised image coordinates); returns 0 behind the
+// camera, 2 if the body straddles z = 0.
+__device__ __forceinline__ int gen_bounds(const float c[3], const float A[3][3], float& u0,
+                                          float& u1, float& v0, float& v1) {
+  const float zext = sqrtf(fmaxf(A[2][2], 0.f));
+  if (c[2] + zext <= 0.f) return 0;
+  if (c[2] - zext <= 0.f) return 2;
+  const float qa = fmaf(c[2], c[2], -A[2][2]), inv = 1.f / qa;
 #pragma unroll
   for (int ax = 0; ax < 2; ax++) {
-    double qb = c[ax] * c[2] - A[ax][2];
-    double qc = c[ax] * c[ax] - A[ax][ax];
-    double sq = sqrt(fmax(qb * qb - qa * qc, 0.0));
-    double lo = (qb - sq) / qa, hi = (qb + sq) / qa;
+    const float ca = c[ax], Aaa = A[ax][ax], Aaz = A[ax][2], Azz = A[2][2];
+    const float qb = fmaf(ca, c[2], -Aaz);
+    const float disc = Aaa * c[2] * c[2] + Azz * ca * ca - 2.f * Aaz * ca * c[2] + Aaz * Aaz -
+                       Aaa * Azz;
+    const float sq = sqrtf(fmaxf(disc, 0.f));
+    const float lo = (qb - sq) * inv, hi = (qb + sq) * inv;
     if (ax == 0) {
-      u0 = fmin(u0, lo);
-      u1 = fmax(u1, hi);
+      u0 = fminf(u0, lo);
+      u1 = fmaxf(u1, hi);
     } else {
-      v0 = fmin(v0, lo);
-      v1 = fmax(v1, hi);
+      v0 = fminf(v0, lo);
+      v1 = fmaxf(v1, hi);
     }
   }
   return 1;
 }
 
 // A = R diag(s^2) R^T with R given by its columns.
-__device__ __forceinline__ void shape_from_axes(const double col[3][3], const double s[3],
-                                                double A[3][3]) {
+__device__ __forceinline__ void shape_from_axes(const float col[3][3], const float s[3],
+                                                float A[3][3]) {
 #pragma unroll
   for (int i = 0; i < 3; i++)
 #pragma unroll
@@ -72,37 +78,38 @@ __device__ __forceinline__ void shape_from_axes(const double col[3][3], const do
 }
 
 // Disc of radius r centred at c with unit normal a: A = r^2 (I - a a^T).
-__device__ __forceinline__ void disc_shape(const double a[3], double r, double A[3][3]) {
+__device__ __forceinline__ void disc_shape(const float a[3], float r, float A[3][3]) {
 #pragma unroll
   for (int i = 0; i < 3; i++)
 #pragma unroll
-    for (int j = 0; j < 3; j++) A[i][j] = r * r * ((i == j ? 1.0 : 0.0) - a[i] * a[j]);
+    for (int j = 0; j < 3; j++) A[i][j] = r * r * ((i == j ? 1.f : 0.f) - a[i] * a[j]);
 }
 
-__device__ __forceinline__ int4 finish_box(int st_any, int full, double u0, double u1, double v0,
-                                           double v1, const CamParams& cam) {
+__device__ __forceinline__ int4 finish_box(int st_any, int full, float u0, float u1, float v0,
+                                           float v1, const CamParams& cam) {
   int4 b = make_int4(1, 1, 0, 0);  // empty
   if (!st_any) return b;
   if (full) return make_int4(0, 0, cam.W - 1, cam.H - 1);
-  double fx = cam.fx, fy = cam.fy, cx = cam.cx, cy = cam.cy;
   // pixel i is a candidate iff its centre i + 0.5 lies within the bounds; 1 px margin
-  double x0 = ceil(fx * u0 + cx - 0.5) - 1.0, x1 = floor(fx * u1 + cx - 0.5) + 1.0;
-  double y0 = ceil(fy * v0 + cy - 0.5) - 1.0, y1 = floor(fy * v1 + cy - 0.5) + 1.0;
-  x0 = fmax(x0, 0.0);
-  y0 = fmax(y0, 0.0);
-  x1 = fmin(x1, (double)(cam.W - 1));
-  y1 = fmin(y1, (double)(cam.H - 1));
+  float x0 = ceilf(fmaf(cam.fx, u0, cam.cx) - 0.5f) - 1.f;
+  float x1 = floorf(fmaf(cam.fx, u1, cam.cx) - 0.5f) + 1.f;
+  float y0 = ceilf(fmaf(cam.fy, v0, cam.cy) - 0.5f) - 1.f;
+  float y1 = floorf(fmaf(cam.fy, v1, cam.cy) - 0.5f) + 1.f;
+  x0 = fmaxf(x0, 0.f);
+  y0 = fmaxf(y0, 0.f);
+  x1 = fminf(x1, (float)(cam.W - 1));
+  y1 = fminf(y1, (float)(cam.H - 1));
   if (!(x0 <= x1 && y0 <= y1)) return b;
   return make_int4((int)x0, (int)y0, (int)x1, (int)y1);
 }
 
 // Bounds of a primitive from up to two generator bodies.
-__device__ __forceinline__ int4 prim_box(int ng, const double c[2][3], const double A[2][3][3],
+__device__ __forceinline__ int4 prim_box(int ng, const float c[2][3], const float A[2][3][3],
                                          const CamParams& cam) {
-  double u0 = 1e300, u1 = -1e300, v0 = 1e300, v1 = -1e300;
+  float u0 = 3e38f, u1 = -3e38f, v0 = 3e38f, v1 = -3e38f;
   int any = 0, full = 0;
   for (int g = 0; g < ng; g++) {
-    int st = gen_bounds(c[g], A[g], u0, u1, v0, v1);
+    const int st = gen_bounds(c[g], A[g], u0, u1, v0, v1);
     if (st) any = 1;
     if (st == 2) full = 1;
   }
@@ -120,7 +127,7 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
                            float* rec, int4& box) {
 #pragma unroll
   for (int i = 0; i < kRec; i++) rec[i] = 0.f;
-  double gc[2][3], gA[2][3][3];
+  float gc[2][3], gA[2][3][3];
   int ng = 0;
   if (j < kCone0) {  // sphere at joint (f, k)
     int f = j >> 2, k = j & 3;
@@ -128,9 +135,9 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
     const double* c = s.J[f][k];
     put3(rec, kC, c);
     rec[kR2] = (float)(r * r);
-    for (int i = 0; i < 3; i++) gc[0][i] = c[i];
+    for (int i = 0; i < 3; i++) gc[0][i] = (float)c[i];
     for (int a = 0; a < 3; a++)
-      for (int b = 0; b < 3; b++) gA[0][a][b] = (a == b) ? r * r : 0.0;
+      for (int b = 0; b < 3; b++) gA[0][a][b] = (a == b) ? (float)(r * r) : 0.f;
     ng = 1;
   } else if (j < kCyl) {  // truncated cone J_k -> J_{k+1}
     int f, k;
@@ -161,12 +168,13 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
     rec[kRm] = (float)(0.5 * (r0 + r1));
     rec[kK] = (float)((r1 - r0) / L);
     rec[kHl] = (float)(0.5 * L);
+    float axf[3] = {(float)ax[0], (float)ax[1], (float)ax[2]};
     for (int i = 0; i < 3; i++) {
-      gc[0][i] = J0[i];
-      gc[1][i] = J1[i];
+      gc[0][i] = (float)J0[i];
+      gc[1][i] = (float)J1[i];
     }
-    disc_shape(ax, r0, gA[0]);
-    disc_shape(ax, r1, gA[1]);
+    disc_shape(axf, (float)r0, gA[0]);
+    disc_shape(axf, (float)r1, gA[1]);
     ng = 2;
   } else if (j == kCyl) {  // palm: elliptic cylinder y_H in [-len, 0]
     double cx[3], cy[3], cz[3], m[3];
@@ -190,11 +198,15 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
     rec[kRm] = 1.f;
     rec[kK] = 0.f;
     rec[kHl] = (float)(0.5 * dm.palm_len);
-    double cols[3][3] = {{cx[0], cx[1], cx[2]}, {cy[0], cy[1], cy[2]}, {cz[0], cz[1], cz[2]}};
-    double sd[3] = {dm.palm_half_w, 0.0, dm.palm_half_t};
+    float cols[3][3], sd[3] = {(float)dm.palm_half_w, 0.f, (float)dm.palm_half_t};
+    for (int i = 0; i < 3; i++) {
+      cols[0][i] = (float)cx[i];
+      cols[1][i] = (float)cy[i];
+      cols[2][i] = (float)cz[i];
+    }
     for (int e = 0; e < 2; e++) {
       double yc = e == 0 ? 0.0 : -dm.palm_len;
-      for (int i = 0; i < 3; i++) gc[e][i] = s.h[i] + yc * cy[i];
+      for (int i = 0; i < 3; i++) gc[e][i] = (float)(s.h[i] + yc * cy[i]);
       shape_from_axes(cols, sd, gA[e]);
     }
     ng = 2;
@@ -222,8 +234,11 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
       put3(rec, kM + 3 * a, row);
       rec[kCl + a] = (float)(row[0] * c[0] + row[1] * c[1] + row[2] * c[2]);
     }
-    for (int i = 0; i < 3; i++) gc[0][i] = c[i];
-    shape_from_axes(cols, sd, gA[0]);
+    float colf[3][3], sdf[3] = {(float)sd[0], (float)sd[1], (float)sd[2]};
+    for (int a = 0; a < 3; a++)
+      for (int i = 0; i < 3; i++) colf[a][i] = (float)cols[a][i];
+    for (int i = 0; i < 3; i++) gc[0][i] = (float)c[i];
+    shape_from_axes(colf, sdf, gA[0]);
     ng = 1;
   }
   box = prim_box(ng, gc, gA, cam);

@@ -40,6 +40,22 @@ __global__ void k_pack_obs(const float* __restrict__ depth, const uint8_t* __res
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(S_o, (unsigned long long)cnt);
 }
 
+// Per-column / per-row ray directions, correctly rounded:
+// d = ((u + 0.5 - cx)/fx, (v + 0.5 - cy)/fy, 1)  (P:L114 camera C).
+// Layout: dx[W + kRayPad] then dy[H + kRayPad] (the pad covers tiles overhanging the image).
+__global__ void k_ray_table(const CamParams cam, float* ray) {
+  const int nx = cam.W + kRayPad, ny = cam.H + kRayPad;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nx) ray[i] = __fdiv_rn((float)i + 0.5f - cam.cx, cam.fx);
+  else if (i < nx + ny) ray[i] = __fdiv_rn((float)(i - nx) + 0.5f - cam.cy, cam.fy);
+}
+
+cudaError_t launch_ray_table(const CamParams& cam, float* ray, cudaStream_t st) {
+  const int n = cam.W + cam.H + 2 * kRayPad;
+  k_ray_table<<<(n + 255) / 256, 256, 0, st>>>(cam, ray);
+  return cudaGetLastError();
+}
+
 __global__ void k_depth_to_mask(const float* __restrict__ depth, uint8_t* __restrict__ mask,
                                 int npx) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -62,14 +78,13 @@ struct Lane4 {
 
 __device__ __forceinline__ float fast_sqrt(float x) { return x * rsqrtf(x); }  // NaN if x < 0
 
-// Branch-free min-depth update: a NaN z (no real root / out of range) never wins.
-__device__ __forceinline__ void keep(float z, float& zb, float znear, float zfar) {
-  const bool ok = (z >= znear) & (z <= zfar) & (z < zb);
-  zb = ok ? z : zb;
+// Branch-free min-depth update.  zb starts just above z_far, so z < zb also enforces
+// z <= z_far; a NaN z (no real root / axial range miss) never wins.
+__device__ __forceinline__ void keep(float z, float& zb, float znear) {
+  zb = (z >= znear) & (z < zb) ? z : zb;
 }
 
-__device__ __forceinline__ void isect_sphere(const float* __restrict__ r, Lane4& L, float znear,
-                                             float zfar) {
+__device__ __forceinline__ void isect_sphere(const float* __restrict__ r, Lane4& L, float znear) {
   const float4 q = *reinterpret_cast<const float4*>(r);  // c, r^2
   const float bx = fmaf(L.dx, q.x, q.z);
 #pragma unroll
@@ -77,12 +92,12 @@ __device__ __forceinline__ void isect_sphere(const float* __restrict__ r, Lane4&
     const float tc = fmaf(L.dy[j], q.y, bx) * L.inv_dd[j];
     const float ox = fmaf(tc, L.dx, -q.x), oy = fmaf(tc, L.dy[j], -q.y), oz = tc - q.z;
     const float disc = q.w - fmaf(ox, ox, fmaf(oy, oy, oz * oz));
-    keep(tc - fast_sqrt(disc * L.inv_dd[j]), L.zb[j], znear, zfar);
+    keep(tc - fast_sqrt(disc * L.inv_dd[j]), L.zb[j], znear);
   }
 }
 
 __device__ __forceinline__ void isect_ellipsoid(const float* __restrict__ r, Lane4& L,
-                                                float znear, float zfar) {
+                                                float znear) {
   const float4 r0 = *reinterpret_cast<const float4*>(r + 0);   // c, -
   const float4 r1 = *reinterpret_cast<const float4*>(r + 4);   // M00 M01 M02 M10
   const float4 r2 = *reinterpret_cast<const float4*>(r + 8);   // M11 M12 M20 M21
@@ -101,9 +116,10 @@ __device__ __forceinline__ void isect_ellipsoid(const float* __restrict__ r, Lan
     const float B = fmaf(ox, lx, fmaf(oy, ly, oz * lz));
     const float C = fmaf(ox, ox, fmaf(oy, oy, fmaf(oz, oz, -1.f)));
     const float disc = fmaf(B, B, -A * C);
-    const float qq = -(B + copysignf(fast_sqrt(disc), B));
-    const float s = fminf(__fdividef(qq, A), __fdividef(C, qq));
-    keep(tc + s, L.zb[j], znear, zfar);
+    // A > 0: the smaller root; only the absolute error of s matters (z = t_c + s), so the
+    // plain form is accurate to ~1e-6 mm here
+    const float s = (-B - fast_sqrt(disc)) * __fdividef(1.f, A);
+    keep(tc + s, L.zb[j], znear);
   }
 }
 
@@ -111,8 +127,7 @@ __device__ __forceinline__ void isect_ellipsoid(const float* __restrict__ r, Lan
 // x^2 + y^2 - (r_m + k z)^2 = 0 with |z| <= half length; the smaller root whose axial
 // coordinate is in range (the far-nappe case needs the larger one).  No cap tests: every
 // cap disc is the equator of a joint sphere / cap ellipsoid that is hit first.
-__device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L, float znear,
-                                           float zfar) {
+__device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L, float znear) {
   const float4 r0 = *reinterpret_cast<const float4*>(r + 0);
   const float4 r1 = *reinterpret_cast<const float4*>(r + 4);
   const float4 r2 = *reinterpret_cast<const float4*>(r + 8);
@@ -133,17 +148,164 @@ __device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L
     const float B = fmaf(ox, lx, fmaf(oy, ly, -kd * g));
     const float C = fmaf(ox, ox, fmaf(oy, oy, -g * g));
     const float disc = fmaf(B, B, -A * C);
-    const float qq = -(B + copysignf(fast_sqrt(disc), B));
-    const float s1 = __fdividef(qq, A), s2 = __fdividef(C, qq);
+    const float sq = fast_sqrt(disc), inv = __fdividef(1.f, A);  // NaN when disc < 0
+    const float s1 = (-B - sq) * inv, s2 = (-B + sq) * inv;     // A < 0: far nappe first
     const float sa = fminf(s1, s2), sb = fmaxf(s1, s2);
     const float za = fmaf(sa, lz, oz), zb = fmaf(sb, lz, oz);
     const float s = fabsf(za) <= hl ? sa : (fabsf(zb) <= hl ? sb : __int_as_float(0x7fc00000));
-    keep(tc + s, L.zb[j], znear, zfar);
+    keep(tc + s, L.zb[j], znear);
   }
 }
 
 // ---------------------------------------------------------------------------------------
-// The fused evaluation kernel
+// One warp tile: TMA the observation tile, cull, ray-cast, min-depth, score.
+// ---------------------------------------------------------------------------------------
+struct TileSums {
+  unsigned int rm = 0, both = 0, and_ = 0;
+  unsigned long long num = 0;
+};
+
+// Tile geometry of a particle: the union box's x0 rounded down to 4 px, because a TMA box
+// must start 16-byte aligned in global memory (an unaligned start faults on sm_100a).
+struct TileGrid {
+  int x0, y0, tx, ntiles;
+  float inv_tx;
+  __device__ __forceinline__ explicit TileGrid(int4 ub) {
+    x0 = ub.x & ~3;
+    y0 = ub.y;
+    const int bw = ub.z - x0 + 1, bh = ub.w - ub.y + 1;
+    tx = bw > 0 ? (bw + kTileW - 1) / kTileW : 0;
+    const int ty = bh > 0 ? (bh + kTileH - 1) / kTileH : 0;
+    ntiles = tx * ty;
+    inv_tx = 1.0f / (float)(tx > 0 ? tx : 1);
+  }
+  __device__ __forceinline__ void origin(int t, int& X0, int& Y0) const {
+    int qy = (int)((float)t * inv_tx);  // t / tx, corrected below
+    int qx = t - qy * tx;
+    if (qx < 0) { qy--; qx += tx; }
+    if (qx >= tx) { qy++; qx -= tx; }
+    X0 = x0 + qx * kTileW;
+    Y0 = y0 + qy * kTileH;
+  }
+};
+
+template <int MODE>
+__device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tmap,
+                                        const FkOut& fo, int X0, int Y0, uint32_t* obs_buf,
+                                        uint64_t* bar, uint32_t& phase, const float* s_dx,
+                                        const float* s_dy, TileSums& acc) {
+  const int lane = threadIdx.x & 31;
+  const int col = lane & 15, rowb = lane >> 4;
+  const float znear = a.cam.znear, zfar = a.cam.zfar;
+  const float zinit = __uint_as_float(__float_as_uint(zfar) + 1u);  // next float above z_far
+  if (MODE == kModeCost && a.use_tma && lane == 0) {
+    fence_proxy_async();
+    mbar_expect_tx(bar, kTileW * kTileH * 4);
+    tma_load_2d(obs_buf, a.use_tma == 2 ? a.tmap_g : tmap, X0, Y0, bar);
+  }
+  // cull the 38 conservative boxes against the tile: two ballots -> 64-bit mask
+  uint64_t mask;
+  {
+    const int4 b = fo.box[lane];
+    const bool ov = b.x <= X0 + kTileW - 1 && b.z >= X0 && b.y <= Y0 + kTileH - 1 && b.w >= Y0;
+    bool ov2 = false;
+    if (lane < kNprim - 32) {
+      const int4 c = fo.box[32 + lane];
+      ov2 = c.x <= X0 + kTileW - 1 && c.z >= X0 && c.y <= Y0 + kTileH - 1 && c.w >= Y0;
+    }
+    mask = (uint64_t)__ballot_sync(0xffffffffu, ov) |
+           ((uint64_t)__ballot_sync(0xffffffffu, ov2) << 32);
+  }
+  Lane4 L;
+  const int x = X0 + col;
+  L.dx = s_dx[x];
+#pragma unroll
+  for (int q = 0; q < kPxPerLane; q++) {
+    L.dy[q] = s_dy[Y0 + rowb + 2 * q];
+    L.inv_dd[q] = __fdividef(1.f, fmaf(L.dx, L.dx, fmaf(L.dy[q], L.dy[q], 1.f)));
+    L.zb[q] = zinit;
+  }
+  for (uint64_t m = mask & kSphereMask; m; m &= m - 1)
+    isect_sphere(fo.rec[__ffsll((long long)m) - 1], L, znear);
+  for (uint64_t m = mask & kConeMask; m; m &= m - 1)
+    isect_cone(fo.rec[__ffsll((long long)m) - 1], L, znear);
+  for (uint64_t m = mask & kEllMask; m; m &= m - 1)
+    isect_ellipsoid(fo.rec[__ffsll((long long)m) - 1], L, znear);
+
+  if (MODE == kModeDepth) {
+#pragma unroll
+    for (int q = 0; q < kPxPerLane; q++) {
+      const int y = Y0 + rowb + 2 * q;
+      if (x < a.cam.W && y < a.cam.H)
+        a.depth_out[(size_t)y * a.cam.W + x] = L.zb[q] <= zfar ? L.zb[q] : 0.f;
+    }
+  } else {
+    if (a.use_tma) {
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+    } else {
+#pragma unroll
+      for (int q = 0; q < kPxPerLane; q++) {
+        const int y = Y0 + rowb + 2 * q;
+        obs_buf[(rowb + 2 * q) * kTileW + col] =
+            (x < a.cam.W && y < a.cam.H) ? a.obs[(size_t)y * a.obs_pitch + x] : 0u;
+      }
+      __syncwarp();
+    }
+    const float d_m = a.cost.d_m, clampv = a.cost.clampv;
+#pragma unroll
+    for (int q = 0; q < kPxPerLane; q++) {
+      const int y = Y0 + rowb + 2 * q;
+      if (x < a.cam.W && y < a.cam.H && L.zb[q] <= zfar) {
+        const uint32_t w = obs_buf[(rowb + 2 * q) * kTileW + col];
+        const float od = __uint_as_float(w & 0x7fffffffu);
+        const unsigned int os = w >> 31;
+        const float diff = fabsf(od - L.zb[q]);
+        // r_m = 1 where |r_d - o_d| < d_m or o_d undefined (AMB-4, AMB-5)
+        const unsigned int rm = (od == 0.f) | (diff < d_m);
+        acc.rm += rm;
+        acc.and_ += rm & os;
+        if (od > 0.f) {
+          acc.both += 1;
+          acc.num += __float2ull_rn(fminf(diff, clampv) * 1048576.f);  // 2^-20 mm fixed point
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void warp_reduce(TileSums& s) {
+  s.rm = __reduce_add_sync(0xffffffffu, s.rm);
+  s.and_ = __reduce_add_sync(0xffffffffu, s.and_);
+  s.both = __reduce_add_sync(0xffffffffu, s.both);
+#pragma unroll
+  for (int off = 16; off; off >>= 1) s.num += __shfl_xor_sync(0xffffffffu, s.num, off);
+}
+
+// Eq. (4)-(5) in fp64 from the integer sums v = (sum r_m, sum o_s AND r_m, numerator in
+// 2^-20 mm, both-defined count)  (AMB-1, -2, -3, -6).
+__device__ __forceinline__ void finalize_cost(const EvalArgs& a, int p, const unsigned long long v[4],
+                                              double kc) {
+  const long long s_rm = (long long)v[0], s_and = (long long)v[1];
+  const long long s_or = (long long)*a.S_o + s_rm - s_and;
+  double D = 0.0;
+  if (s_or > 0) {
+    const double num = (double)v[2] * (1.0 / 1048576.0);
+    const double sor = (double)s_or, sand = (double)s_and;
+    D = a.cost.depth_scale * num / sor + a.cost.lambda * (1.0 - 2.0 * sand / (sand + sor));
+  }
+  const double E = D + a.cost.lambda_k * kc;
+  if (a.costs32) a.costs32[p] = (float)E;
+  if (a.costs64) a.costs64[p] = E;
+  if (a.sums_out)
+    for (int k = 0; k < 4; k++) a.sums_out[(size_t)p * 4 + k] = v[k];
+}
+
+// ---------------------------------------------------------------------------------------
+// k_eval: one CTA per (particle, split).  Warp 0 runs FK into shared memory while the other
+// warps stage the ray table; then all warps take tiles dynamically.  Used for small swarms
+// (S > 1 splits per particle keep every SM busy) and for the depth-image hooks.
 // ---------------------------------------------------------------------------------------
 template <int NW, typename PoseT, int MODE>
 __global__ void __launch_bounds__(NW * 32, 24 / NW)
@@ -159,23 +321,19 @@ __global__ void __launch_bounds__(NW * 32, 24 / NW)
   if (a.done && *a.done) return;  // PSO stop rule reached (grid-uniform)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.x / a.S, sidx = blockIdx.x % a.S;
-  float* s_dx = s_ray;
-  float* s_dy = s_ray + a.cam.W + kRayPad;
+  const float* s_dx = s_ray;
+  const float* s_dy = s_ray + a.cam.W + kRayPad;
 
   if (warp == 0) {
     const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
     fk_warp<PoseT>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
   } else {
-    // while warp 0 runs FK: per-column / per-row ray directions, correctly rounded
-    // d = ((u + 0.5 - cx)/fx, (v + 0.5 - cy)/fy, 1)  (P:L114 camera C)
-    const int nx = a.cam.W + kRayPad, ny = a.cam.H + kRayPad;
-    for (int i = threadIdx.x - 32; i < nx + ny; i += (NW - 1) * 32) {
-      if (i < nx) s_dx[i] = __fdiv_rn((float)i + 0.5f - a.cam.cx, a.cam.fx);
-      else s_dy[i - nx] = __fdiv_rn((float)(i - nx) + 0.5f - a.cam.cy, a.cam.fy);
-    }
+    // while warp 0 runs FK: stage the per-column / per-row ray directions (k_ray_table)
+    const int n4 = (a.cam.W + a.cam.H + 2 * kRayPad + 3) / 4;
+    for (int i = threadIdx.x - 32; i < n4; i += (NW - 1) * 32)
+      reinterpret_cast<float4*>(s_ray)[i] = __ldg(reinterpret_cast<const float4*>(a.ray) + i);
     if (MODE == kModeCost && warp == NW - 1 && lane == 0) {
-      // one thread initialises every warp's TMA barrier (count 1: the expect_tx arrival)
-      for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);
+      for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);  // count 1: the expect_tx arrival
       fence_mbar_init();
       if (a.use_tma == 1) prefetch_tmap(&tmap);
     }
@@ -183,127 +341,32 @@ __global__ void __launch_bounds__(NW * 32, 24 / NW)
   }
   __syncthreads();
 
-  // tile origin: the union box's x0 rounded down to 4 px, because a TMA box must start
-  // 16-byte aligned in global memory (an unaligned start faults on sm_100a)
-  int4 ub = s_out.ubox;
-  ub.x &= ~3;
-  const int bw = ub.z - ub.x + 1, bh = ub.w - ub.y + 1;
-  const int tx = bw > 0 ? (bw + kTileW - 1) / kTileW : 0;
-  const int ty = bh > 0 ? (bh + kTileH - 1) / kTileH : 0;
-  const int ntiles = tx * ty;
+  const TileGrid g(s_out.ubox);
   // this CTA owns tiles sidx, sidx + S, ...; warps take them dynamically (load balance)
-  const int nmine = ntiles > sidx ? (ntiles - sidx + a.S - 1) / a.S : 0;
-  const float inv_tx = 1.0f / (float)(tx > 0 ? tx : 1);
-  const int col = lane & 15, rowb = lane >> 4;
-  const float znear = a.cam.znear, zfar = a.cam.zfar;
-  const float d_m = a.cost.d_m, clampv = a.cost.clampv;
-  unsigned int c_rm = 0, c_and = 0, c_both = 0;
-  unsigned long long c_num = 0;
+  const int nmine = g.ntiles > sidx ? (g.ntiles - sidx + a.S - 1) / a.S : 0;
+  TileSums acc;
   uint32_t phase = 0;
-
   int j = warp;
   while (j < nmine) {
-    const int t = sidx + j * a.S;
-    int qy = (int)((float)t * inv_tx);  // t / tx, corrected below
-    int qx = t - qy * tx;
-    if (qx < 0) { qy--; qx += tx; }
-    if (qx >= tx) { qy++; qx -= tx; }
-    const int X0 = ub.x + qx * kTileW, Y0 = ub.y + qy * kTileH;
-    if (MODE == kModeCost && a.use_tma && lane == 0) {
-      fence_proxy_async();
-      mbar_expect_tx(&s_bar[warp], kTileW * kTileH * 4);
-      tma_load_2d(s_obs[warp], a.use_tma == 2 ? a.tmap_g : &tmap, X0, Y0, &s_bar[warp]);
-    }
-    // next tile for this warp (dynamic): fetched early, used at the loop end
     int jn = 0;
-    if (lane == 0) jn = atomicAdd(&s_next, 1);
-    // cull the 38 conservative boxes against the tile: two ballots -> 64-bit mask
-    uint64_t mask;
-    {
-      const int4 b = s_out.box[lane];
-      const bool ov = b.x <= X0 + kTileW - 1 && b.z >= X0 && b.y <= Y0 + kTileH - 1 && b.w >= Y0;
-      bool ov2 = false;
-      if (lane < kNprim - 32) {
-        const int4 c = s_out.box[32 + lane];
-        ov2 = c.x <= X0 + kTileW - 1 && c.z >= X0 && c.y <= Y0 + kTileH - 1 && c.w >= Y0;
-      }
-      mask = (uint64_t)__ballot_sync(0xffffffffu, ov) |
-             ((uint64_t)__ballot_sync(0xffffffffu, ov2) << 32);
-    }
-    Lane4 L;
-    const int x = X0 + col;
-    L.dx = s_dx[x];
-#pragma unroll
-    for (int q = 0; q < kPxPerLane; q++) {
-      L.dy[q] = s_dy[Y0 + rowb + 2 * q];
-      L.inv_dd[q] = __fdividef(1.f, fmaf(L.dx, L.dx, fmaf(L.dy[q], L.dy[q], 1.f)));
-      L.zb[q] = INFINITY;
-    }
-    for (uint64_t m = mask & kSphereMask; m; m &= m - 1)
-      isect_sphere(s_out.rec[__ffsll((long long)m) - 1], L, znear, zfar);
-    for (uint64_t m = mask & kConeMask; m; m &= m - 1)
-      isect_cone(s_out.rec[__ffsll((long long)m) - 1], L, znear, zfar);
-    for (uint64_t m = mask & kEllMask; m; m &= m - 1)
-      isect_ellipsoid(s_out.rec[__ffsll((long long)m) - 1], L, znear, zfar);
-
-    if (MODE == kModeDepth) {
-#pragma unroll
-      for (int q = 0; q < kPxPerLane; q++) {
-        const int y = Y0 + rowb + 2 * q;
-        if (x < a.cam.W && y < a.cam.H)
-          a.depth_out[(size_t)y * a.cam.W + x] = L.zb[q] < INFINITY ? L.zb[q] : 0.f;
-      }
-    } else {
-      if (a.use_tma) {
-        mbar_wait(&s_bar[warp], phase);
-        phase ^= 1u;
-      } else {
-#pragma unroll
-        for (int q = 0; q < kPxPerLane; q++) {
-          const int y = Y0 + rowb + 2 * q;
-          s_obs[warp][(rowb + 2 * q) * kTileW + col] =
-              (x < a.cam.W && y < a.cam.H) ? a.obs[(size_t)y * a.obs_pitch + x] : 0u;
-        }
-        __syncwarp();
-      }
-#pragma unroll
-      for (int q = 0; q < kPxPerLane; q++) {
-        const int y = Y0 + rowb + 2 * q;
-        if (x < a.cam.W && y < a.cam.H && L.zb[q] < INFINITY) {
-          const uint32_t w = s_obs[warp][(rowb + 2 * q) * kTileW + col];
-          const float od = __uint_as_float(w & 0x7fffffffu);
-          const unsigned int os = w >> 31;
-          const float diff = fabsf(od - L.zb[q]);
-          // r_m = 1 where |r_d - o_d| < d_m or o_d undefined (AMB-4, AMB-5)
-          const unsigned int rm = (od == 0.f) | (diff < d_m);
-          c_rm += rm;
-          c_and += rm & os;
-          if (od > 0.f) {
-            c_both += 1;
-            c_num += __float2ull_rn(fminf(diff, clampv) * 1048576.f);  // 2^-20 mm fixed point
-          }
-        }
-      }
-    }
-    __syncwarp();
+    if (lane == 0) jn = atomicAdd(&s_next, 1);  // next tile, fetched early
+    int X0, Y0;
+    g.origin(sidx + j * a.S, X0, Y0);
+    do_tile<MODE>(a, &tmap, s_out, X0, Y0, s_obs[warp], &s_bar[warp], phase, s_dx, s_dy, acc);
     j = __shfl_sync(0xffffffffu, jn, 0);
   }
 
   if (MODE != kModeCost) return;
   // ---- reduction: warp shuffles, one atomic per sum per CTA ----
-  c_rm = __reduce_add_sync(0xffffffffu, c_rm);
-  c_and = __reduce_add_sync(0xffffffffu, c_and);
-  c_both = __reduce_add_sync(0xffffffffu, c_both);
-#pragma unroll
-  for (int off = 16; off; off >>= 1) c_num += __shfl_xor_sync(0xffffffffu, c_num, off);
+  warp_reduce(acc);
   if (lane == 0) {
-    s_red[warp][0] = c_rm;
-    s_red[warp][1] = c_and;
-    s_red[warp][2] = c_num;
-    s_red[warp][3] = c_both;
+    s_red[warp][0] = acc.rm;
+    s_red[warp][1] = acc.and_;
+    s_red[warp][2] = acc.num;
+    s_red[warp][3] = acc.both;
   }
   __syncthreads();
-  unsigned long long* acc = a.acc + (size_t)p * 4;
+  unsigned long long* gacc = a.acc + (size_t)p * 4;
   if (threadIdx.x == 0) {
     unsigned long long v[4] = {0, 0, 0, 0};
     for (int w = 0; w < NW; w++)
@@ -311,30 +374,134 @@ __global__ void __launch_bounds__(NW * 32, 24 / NW)
     int last = 1;
     if (a.S > 1) {
       for (int k = 0; k < 4; k++)
-        if (v[k]) atomicAdd(acc + k, v[k]);
+        if (v[k]) atomicAdd(gacc + k, v[k]);
       __threadfence();
       last = atomicAdd(a.counters + p, 1u) == (unsigned)(a.S - 1);
       if (last) {
         __threadfence();
-        for (int k = 0; k < 4; k++) v[k] = atomicExch(acc + k, 0ull);  // read + reset
+        for (int k = 0; k < 4; k++) v[k] = atomicExch(gacc + k, 0ull);  // read + reset
         a.counters[p] = 0;
       }
     }
-    if (last) {
-      // ---- Eq. (4)-(5) in fp64 (AMB-1, -2, -3, -6) ----
-      const long long s_rm = (long long)v[0], s_and = (long long)v[1];
-      const long long s_or = (long long)*a.S_o + s_rm - s_and;
-      double D = 0.0;
-      if (s_or > 0) {
-        const double num = (double)v[2] * (1.0 / 1048576.0);
-        const double sor = (double)s_or, sand = (double)s_and;
-        D = a.cost.depth_scale * num / sor + a.cost.lambda * (1.0 - 2.0 * sand / (sand + sor));
+    if (last) finalize_cost(a, p, v, s_out.kc);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// k_eval_persist: persistent, warp-specialised version for large swarms (one CTA per SM
+// slot, one particle at a time per CTA).  Warp 0 is the FK producer: it fetches the next
+// particle from a global counter and runs FK into one of two shared-memory slots while
+// warps 1..NW-1 (consumers) render the particle in the other slot, so FK latency is hidden
+// behind rendering.  Slots are handed over with mbarriers (full: producer -> consumers,
+// empty: consumers -> producer).  The consumers accumulate a particle's sums in shared
+// memory; the last consumer warp to finish computes Eq. (4)-(5).
+// ---------------------------------------------------------------------------------------
+template <int NW, typename PoseT>
+__global__ void __launch_bounds__(NW * 32, 24 / NW)
+    k_eval_persist(const EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
+  constexpr int NC = NW - 1;  // consumer warps
+  __shared__ FkScratch s_fk;
+  __shared__ __align__(16) FkOut s_out[2];
+  __shared__ __align__(128) uint32_t s_obs[NW][kTileW * kTileH];
+  __shared__ __align__(8) uint64_t s_bar[NW];
+  __shared__ __align__(8) uint64_t s_full[2], s_empty[2];
+  __shared__ unsigned long long s_acc[2][4];
+  __shared__ int s_next[2], s_done[2], s_pid[2];
+  extern __shared__ float s_ray[];
+
+  if (a.done && *a.done) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* s_dx = s_ray;
+  const float* s_dy = s_ray + a.cam.W + kRayPad;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&s_full[b], 32);       // every producer lane arrives (releases its writes)
+      mbar_init(&s_empty[b], NC * 32); // every consumer lane arrives (its reads are done)
+      s_next[b] = 0;
+      s_done[b] = 0;
+      for (int k = 0; k < 4; k++) s_acc[b][k] = 0;
+    }
+    fence_mbar_init();
+    if (a.use_tma == 1) prefetch_tmap(&tmap);
+  }
+  {
+    const int n4 = (a.cam.W + a.cam.H + 2 * kRayPad + 3) / 4;
+    for (int i = threadIdx.x; i < n4; i += NW * 32)
+      reinterpret_cast<float4*>(s_ray)[i] = __ldg(reinterpret_cast<const float4*>(a.ray) + i);
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---- producer: particle fetch + FK ----
+    for (int i = 0;; i++) {
+      const int b = i & 1;
+      if (i >= 2) mbar_wait(&s_empty[b], ((i >> 1) - 1) & 1);
+      int p = 0;
+      if (lane == 0) p = (int)atomicAdd(a.pcount, 1u);
+      p = __shfl_sync(0xffffffffu, p, 0);
+      if (lane == 0) s_pid[b] = p;
+      if (p < a.n) {
+        const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
+        fk_warp<PoseT>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out[b]);
       }
-      const double E = D + a.cost.lambda_k * s_out.kc;
-      if (a.costs32) a.costs32[p] = (float)E;
-      if (a.costs64) a.costs64[p] = E;
-      if (a.sums_out)
-        for (int k = 0; k < 4; k++) a.sums_out[(size_t)p * 4 + k] = v[k];
+      mbar_arrive(&s_full[b]);
+      if (p >= a.n) break;
+    }
+  } else {
+    // ---- consumers ----
+    uint32_t phase = 0;
+    for (int i = 0;; i++) {
+      const int b = i & 1;
+      mbar_wait(&s_full[b], (i >> 1) & 1);
+      const int p = s_pid[b];
+      if (p >= a.n) break;
+      const FkOut& fo = s_out[b];
+      const TileGrid g(fo.ubox);
+      TileSums acc;
+      int t = 0;
+      if (lane == 0) t = atomicAdd(&s_next[b], 1);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      while (t < g.ntiles) {
+        int tn = 0;
+        if (lane == 0) tn = atomicAdd(&s_next[b], 1);
+        int X0, Y0;
+        g.origin(t, X0, Y0);
+        do_tile<kModeCost>(a, &tmap, fo, X0, Y0, s_obs[warp], &s_bar[warp], phase, s_dx, s_dy,
+                           acc);
+        t = __shfl_sync(0xffffffffu, tn, 0);
+      }
+      warp_reduce(acc);
+      if (lane == 0) {
+        if (acc.rm) atomicAdd(&s_acc[b][0], (unsigned long long)acc.rm);
+        if (acc.and_) atomicAdd(&s_acc[b][1], (unsigned long long)acc.and_);
+        if (acc.num) atomicAdd(&s_acc[b][2], acc.num);
+        if (acc.both) atomicAdd(&s_acc[b][3], (unsigned long long)acc.both);
+        __threadfence_block();
+        if (atomicAdd(&s_done[b], 1) == NC - 1) {  // last consumer warp for this particle
+          __threadfence_block();
+          unsigned long long v[4];
+          for (int k = 0; k < 4; k++) {
+            v[k] = s_acc[b][k];
+            s_acc[b][k] = 0;
+          }
+          finalize_cost(a, p, v, fo.kc);
+          s_next[b] = 0;
+          s_done[b] = 0;
+        }
+      }
+      __syncwarp();
+      mbar_arrive(&s_empty[b]);
+    }
+  }
+  // the last CTA to leave resets the particle counter for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(a.pcount + 1, 1u) == gridDim.x - 1) {
+      a.pcount[0] = 0;
+      a.pcount[1] = 0;
+      __threadfence();
     }
   }
 }
@@ -368,6 +535,15 @@ __global__ void k_fk_debug(const double* pose, const DimsD dims, const CamParams
 constexpr int kEvalWarps = HP_NW;
 int eval_warps_per_cta() { return kEvalWarps; }
 
+int persist_blocks_per_sm(const CamParams& cam) {
+  int nb = 0;
+  const size_t dyn = (size_t)((cam.W + cam.H + 2 * kRayPad + 3) & ~3) * sizeof(float);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_persist<kEvalWarps, float>,
+                                                    kEvalWarps * 32, dyn) != cudaSuccess)
+    return 0;
+  return nb;
+}
+
 cudaError_t launch_pack_obs(const float* depth, const uint8_t* mask, uint32_t* obs, int W,
                             int H, int pitch_words, unsigned long long* S_o, cudaStream_t st) {
   const long long npx = (long long)W * H;
@@ -387,8 +563,14 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
   const long long blocks = (long long)a.n * a.S;
   if (blocks == 0) return cudaSuccess;
   const dim3 grid((unsigned)blocks), block(kEvalWarps * 32);
-  const size_t dyn = (size_t)(a.cam.W + a.cam.H + 2 * kRayPad) * sizeof(float);
-  if (mode == kModeCost) {
+  const size_t dyn = (size_t)((a.cam.W + a.cam.H + 2 * kRayPad + 3) & ~3) * sizeof(float);
+  if (mode == kModeCost && a.S == 1 && a.persist_grid > 0) {
+    const dim3 pgrid((unsigned)(a.persist_grid < a.n ? a.persist_grid : a.n));
+    if (pose_double)
+      k_eval_persist<kEvalWarps, double><<<pgrid, block, dyn, st>>>(a, *map);
+    else
+      k_eval_persist<kEvalWarps, float><<<pgrid, block, dyn, st>>>(a, *map);
+  } else if (mode == kModeCost) {
     if (pose_double)
       k_eval<kEvalWarps, double, kModeCost><<<grid, block, dyn, st>>>(a, *map);
     else

@@ -1,7 +1,9 @@
 #!/bin/bash
-# A/B the kernel variants in build_variants/ against the default build (bench kernel time).
+# A/B kernel variants: default build, env switches, and builds in build_variants/.
 B="python bench.py --steps 100 --warmup 5 --no-fit --no-cpu-baseline --clock-ramp 0.3"
-echo "default: $($B | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["roofline"]["kernel_ms"], d["roofline"]["frac"])')"
+P='import json,sys; d=json.loads(sys.stdin.read()); print("%.3fM hyp/s  kernel %.4f ms  frac %.4f" % (d["value"]/1e6, d["roofline"]["kernel_ms"], d["roofline"]["frac"]))'
+echo "default:            $($B | python -c "$P")"
+echo "HP_NO_PERSIST=1:    $(HP_NO_PERSIST=1 $B | python -c "$P")"
 for f in build_variants/*.so; do
-  echo "$f: $(HP_LIB=$f $B | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["roofline"]["kernel_ms"], d["roofline"]["frac"])')"
+  echo "$f: $(HP_LIB=$f $B | python -c "$P")"
 done
