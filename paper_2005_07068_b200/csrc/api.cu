@@ -242,6 +242,8 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   ARG(cam->fx > 0 && cam->fy > 0, "hp_create: fx/fy <= 0");
   ARG(cam->z_near_mm > 0 && cam->z_far_mm > cam->z_near_mm, "hp_create: need 0 < z_near < z_far");
   ARG(max_particles >= 1, "hp_create: max_particles < 1");
+  ARG(!cost || (cost->d_m > 0 && cost->d_M > 0 && cost->d_m <= 512 && cost->d_M <= 512),
+      "hp_create: need 0 < d_m, d_M <= 512 mm (32-bit per-tile fixed-point numerator)");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     g_err = "hp_create: no CUDA device";

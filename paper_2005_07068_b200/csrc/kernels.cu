@@ -76,7 +76,18 @@ struct Lane4 {
   float zb[kPxPerLane];
 };
 
-__device__ __forceinline__ float fast_sqrt(float x) { return x * rsqrtf(x); }  // NaN if x < 0
+// Single-MUFU approximations (flush-to-zero: denormals never occur in these quantities).
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float fast_sqrt(float x) { return x * rsqrt_approx(x); }  // NaN if x < 0
 
 // Branch-free min-depth update.  zb starts just above z_far, so z < zb also enforces
 // z <= z_far; a NaN z (no real root / axial range miss) never wins.
@@ -118,15 +129,18 @@ __device__ __forceinline__ void isect_ellipsoid(const float* __restrict__ r, Lan
     const float disc = fmaf(B, B, -A * C);
     // A > 0: the smaller root; only the absolute error of s matters (z = t_c + s), so the
     // plain form is accurate to ~1e-6 mm here
-    const float s = (-B - fast_sqrt(disc)) * __fdividef(1.f, A);
+    const float s = (-B - fast_sqrt(disc)) * rcp_approx(A);
     keep(tc + s, L.zb[j], znear);
   }
 }
 
 // Cone (and the elliptic cylinder with k = 0 in scaled coordinates):
-// x^2 + y^2 - (r_m + k z)^2 = 0 with |z| <= half length; the smaller root whose axial
-// coordinate is in range (the far-nappe case needs the larger one).  No cap tests: every
-// cap disc is the equator of a joint sphere / cap ellipsoid that is hit first.
+// x^2 + y^2 - (r_m + k z)^2 = 0 with |z| <= half length.  Only the ENTERING root
+// s = (-B - sqrt(disc)) / A is needed, for A > 0 (interior [s_lo, s_hi]) and for A < 0 (ray
+// inside the double cone's opening, interior (-inf, s_lo] U [s_hi, inf)) alike: if it is
+// outside the axial range the ray can only enter the finite solid through a cap disc, and
+// every cap disc is the equator of a joint sphere / cap ellipsoid that is hit first
+// (DESIGN §2), so the min over primitives is unchanged.
 __device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L, float znear) {
   const float4 r0 = *reinterpret_cast<const float4*>(r + 0);
   const float4 r1 = *reinterpret_cast<const float4*>(r + 4);
@@ -148,12 +162,9 @@ __device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L
     const float B = fmaf(ox, lx, fmaf(oy, ly, -kd * g));
     const float C = fmaf(ox, ox, fmaf(oy, oy, -g * g));
     const float disc = fmaf(B, B, -A * C);
-    const float sq = fast_sqrt(disc), inv = __fdividef(1.f, A);  // NaN when disc < 0
-    const float s1 = (-B - sq) * inv, s2 = (-B + sq) * inv;     // A < 0: far nappe first
-    const float sa = fminf(s1, s2), sb = fmaxf(s1, s2);
-    const float za = fmaf(sa, lz, oz), zb = fmaf(sb, lz, oz);
-    const float s = fabsf(za) <= hl ? sa : (fabsf(zb) <= hl ? sb : __int_as_float(0x7fc00000));
-    keep(tc + s, L.zb[j], znear);
+    const float s = (-B - fast_sqrt(disc)) * rcp_approx(A);  // NaN when disc < 0
+    const float z = fabsf(fmaf(s, lz, oz)) <= hl ? tc + s : __int_as_float(0x7fc00000);
+    keep(z, L.zb[j], znear);
   }
 }
 
@@ -222,7 +233,7 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
 #pragma unroll
   for (int q = 0; q < kPxPerLane; q++) {
     L.dy[q] = s_dy[Y0 + rowb + 2 * q];
-    L.inv_dd[q] = __fdividef(1.f, fmaf(L.dx, L.dx, fmaf(L.dy[q], L.dy[q], 1.f)));
+    L.inv_dd[q] = rcp_approx(fmaf(L.dx, L.dx, fmaf(L.dy[q], L.dy[q], 1.f)));
     L.zb[q] = zinit;
   }
   for (uint64_t m = mask & kSphereMask; m; m &= m - 1)
@@ -253,24 +264,24 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
       __syncwarp();
     }
     const float d_m = a.cost.d_m, clampv = a.cost.clampv;
+    const bool xin = x < a.cam.W;
+    unsigned int num = 0;  // <= 4 px x 40 mm x 2^20 < 2^32
 #pragma unroll
     for (int q = 0; q < kPxPerLane; q++) {
       const int y = Y0 + rowb + 2 * q;
-      if (x < a.cam.W && y < a.cam.H && L.zb[q] <= zfar) {
-        const uint32_t w = obs_buf[(rowb + 2 * q) * kTileW + col];
-        const float od = __uint_as_float(w & 0x7fffffffu);
-        const unsigned int os = w >> 31;
-        const float diff = fabsf(od - L.zb[q]);
-        // r_m = 1 where |r_d - o_d| < d_m or o_d undefined (AMB-4, AMB-5)
-        const unsigned int rm = (od == 0.f) | (diff < d_m);
-        acc.rm += rm;
-        acc.and_ += rm & os;
-        if (od > 0.f) {
-          acc.both += 1;
-          acc.num += __float2ull_rn(fminf(diff, clampv) * 1048576.f);  // 2^-20 mm fixed point
-        }
-      }
+      const uint32_t w = obs_buf[(rowb + 2 * q) * kTileW + col];
+      const float od = __uint_as_float(w & 0x7fffffffu);
+      const float diff = fabsf(od - L.zb[q]);
+      const bool hit = xin & (y < a.cam.H) & (L.zb[q] <= zfar);
+      // r_m = 1 where |r_d - o_d| < d_m or o_d undefined (AMB-4, AMB-5)
+      const unsigned int rm = hit & ((od == 0.f) | (diff < d_m));
+      const bool both = hit & (od > 0.f);
+      acc.rm += rm;
+      acc.and_ += rm & (w >> 31);
+      acc.both += both;
+      num += both ? __float2uint_rn(fminf(diff, clampv) * 1048576.f) : 0u;  // 2^-20 mm
     }
+    acc.num += num;
   }
   __syncwarp();
 }
@@ -436,7 +447,7 @@ __global__ void __launch_bounds__(NW * 32, 24 / NW)
     // ---- producer: particle fetch + FK ----
     for (int i = 0;; i++) {
       const int b = i & 1;
-      if (i >= 2) mbar_wait(&s_empty[b], ((i >> 1) - 1) & 1);
+      if (i >= 2) mbar_wait_sleep(&s_empty[b], ((i >> 1) - 1) & 1);
       int p = 0;
       if (lane == 0) p = (int)atomicAdd(a.pcount, 1u);
       p = __shfl_sync(0xffffffffu, p, 0);

@@ -70,6 +70,11 @@ NAMED = {
     "spread": pose((-30.0, 50.0, 850.0), (-5.0, 5.0, 0.0),
                    ((10, 40, 10, 10), (5, 15, 5, 5), (5, 0, 5, 5), (5, -20, 5, 5),
                     (5, -35, 5, 5))),
+    # fingers pointing (almost) straight at the camera: rays inside the cones' openings
+    "toward_camera": pose((5.0, -3.0, 700.0), (90.0, 0.0, 0.0), ((0, 0, 0, 0),) * 5),
+    "toward_camera_tilt": pose((-5.0, 8.0, 650.0), (88.5, 1.0, 0.5),
+                               ((10, 0, 0, 0), (0, 3, 0, 0), (0, 0, 0, 0), (0, -3, 0, 0),
+                                (0, -5, 0, 0))),
 }
 
 
