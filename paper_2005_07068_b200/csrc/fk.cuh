@@ -23,6 +23,7 @@ struct FkOut {
   int4 box[kNprim];  // x0, y0, x1, y1 inclusive; x0 > x1 = empty
   int4 ubox;
   double kc;
+  int near_ok;  // every primitive lies entirely beyond z_near (fast min-depth path)
 };
 
 __device__ __forceinline__ void mat3_mul(const double a[3][3], const double b[3][3],
@@ -42,8 +43,9 @@ __device__ __forceinline__ void mat3_mul(const double a[3][3], const double b[3]
 // Accumulates into [u0,u1]x[v0,v1] (normalised image coordinates); returns 0 behind the
 // camera, 2 if the body straddles z = 0.
 __device__ __forceinline__ int gen_bounds(const float c[3], const float A[3][3], float& u0,
-                                          float& u1, float& v0, float& v1) {
+                                          float& u1, float& v0, float& v1, float& zmin) {
   const float zext = sqrtf(fmaxf(A[2][2], 0.f));
+  zmin = fminf(zmin, c[2] - zext);
   if (c[2] + zext <= 0.f) return 0;
   if (c[2] - zext <= 0.f) return 2;
   const float qa = fmaf(c[2], c[2], -A[2][2]), inv = 1.f / qa;
@@ -105,11 +107,12 @@ __device__ __forceinline__ int4 finish_box(int st_any, int full, float u0, float
 
 // Bounds of a primitive from up to two generator bodies.
 __device__ __forceinline__ int4 prim_box(int ng, const float c[2][3], const float A[2][3][3],
-                                         const CamParams& cam) {
+                                         const CamParams& cam, float& zmin) {
   float u0 = 3e38f, u1 = -3e38f, v0 = 3e38f, v1 = -3e38f;
   int any = 0, full = 0;
+  zmin = 3e38f;
   for (int g = 0; g < ng; g++) {
-    const int st = gen_bounds(c[g], A[g], u0, u1, v0, v1);
+    const int st = gen_bounds(c[g], A[g], u0, u1, v0, v1, zmin);
     if (st) any = 1;
     if (st == 2) full = 1;
   }
@@ -124,7 +127,7 @@ __device__ __forceinline__ void put3(float* r, int off, const double v[3]) {
 
 // Build record + box of device primitive j (see common.cuh for the order).
 __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const CamParams& cam,
-                           float* rec, int4& box) {
+                           float* rec, int4& box, float& zmin) {
 #pragma unroll
   for (int i = 0; i < kRec; i++) rec[i] = 0.f;
   float gc[2][3], gA[2][3][3];
@@ -241,7 +244,7 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
     shape_from_axes(colf, sdf, gA[0]);
     ng = 1;
   }
-  box = prim_box(ng, gc, gA, cam);
+  box = prim_box(ng, gc, gA, cam, zmin);
 }
 
 // Whole-warp FK.  pose: 26 values (float or double); writes `out` (shared) and, if
@@ -300,7 +303,16 @@ __device__ void fk_warp(const PoseT* pose, const DimsD& dm, const CamParams& cam
     }
   }
   __syncwarp();
-  for (int j = lane; j < kNprim; j += 32) build_prim(j, s, dm, cam, out.rec[j], out.box[j]);
+  int near_ok = 1;
+  for (int j = lane; j < kNprim; j += 32) {
+    float zmin;
+    build_prim(j, s, dm, cam, out.rec[j], out.box[j], zmin);
+    // the solid is the convex hull of its generators, so zmin bounds its nearest point;
+    // 1e-3 relative slack covers the fp32 evaluation
+    near_ok &= zmin > cam.znear * 1.001f;
+  }
+  near_ok = __all_sync(0xffffffffu, near_ok);
+  if (lane == 0) out.near_ok = near_ok && !s.bad;
   __syncwarp();
   // union box
   int4 u = make_int4(1 << 30, 1 << 30, -1, -1);

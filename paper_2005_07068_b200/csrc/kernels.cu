@@ -91,10 +91,15 @@ __device__ __forceinline__ float fast_sqrt(float x) { return x * rsqrt_approx(x)
 
 // Branch-free min-depth update.  zb starts just above z_far, so z < zb also enforces
 // z <= z_far; a NaN z (no real root / axial range miss) never wins.
+// CHK = false when FK proved every primitive lies beyond z_near (the common case): then
+// a plain fminf suffices (fminf ignores a NaN operand, and zb starts above z_far).
+template <bool CHK>
 __device__ __forceinline__ void keep(float z, float& zb, float znear) {
-  zb = (z >= znear) & (z < zb) ? z : zb;
+  if (CHK) zb = (z >= znear) & (z < zb) ? z : zb;
+  else zb = fminf(zb, z);
 }
 
+template <bool CHK>
 __device__ __forceinline__ void isect_sphere(const float* __restrict__ r, Lane4& L, float znear) {
   const float4 q = *reinterpret_cast<const float4*>(r);  // c, r^2
   const float bx = fmaf(L.dx, q.x, q.z);
@@ -103,10 +108,11 @@ __device__ __forceinline__ void isect_sphere(const float* __restrict__ r, Lane4&
     const float tc = fmaf(L.dy[j], q.y, bx) * L.inv_dd[j];
     const float ox = fmaf(tc, L.dx, -q.x), oy = fmaf(tc, L.dy[j], -q.y), oz = tc - q.z;
     const float disc = q.w - fmaf(ox, ox, fmaf(oy, oy, oz * oz));
-    keep(tc - fast_sqrt(disc * L.inv_dd[j]), L.zb[j], znear);
+    keep<CHK>(tc - fast_sqrt(disc * L.inv_dd[j]), L.zb[j], znear);
   }
 }
 
+template <bool CHK>
 __device__ __forceinline__ void isect_ellipsoid(const float* __restrict__ r, Lane4& L,
                                                 float znear) {
   const float4 r0 = *reinterpret_cast<const float4*>(r + 0);   // c, -
@@ -130,7 +136,7 @@ __device__ __forceinline__ void isect_ellipsoid(const float* __restrict__ r, Lan
     // A > 0: the smaller root; only the absolute error of s matters (z = t_c + s), so the
     // plain form is accurate to ~1e-6 mm here
     const float s = (-B - fast_sqrt(disc)) * rcp_approx(A);
-    keep(tc + s, L.zb[j], znear);
+    keep<CHK>(tc + s, L.zb[j], znear);
   }
 }
 
@@ -141,6 +147,7 @@ __device__ __forceinline__ void isect_ellipsoid(const float* __restrict__ r, Lan
 // outside the axial range the ray can only enter the finite solid through a cap disc, and
 // every cap disc is the equator of a joint sphere / cap ellipsoid that is hit first
 // (DESIGN §2), so the min over primitives is unchanged.
+template <bool CHK>
 __device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L, float znear) {
   const float4 r0 = *reinterpret_cast<const float4*>(r + 0);
   const float4 r1 = *reinterpret_cast<const float4*>(r + 4);
@@ -164,7 +171,7 @@ __device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L
     const float disc = fmaf(B, B, -A * C);
     const float s = (-B - fast_sqrt(disc)) * rcp_approx(A);  // NaN when disc < 0
     const float z = fabsf(fmaf(s, lz, oz)) <= hl ? tc + s : __int_as_float(0x7fc00000);
-    keep(z, L.zb[j], znear);
+    keep<CHK>(z, L.zb[j], znear);
   }
 }
 
@@ -236,12 +243,21 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
     L.inv_dd[q] = rcp_approx(fmaf(L.dx, L.dx, fmaf(L.dy[q], L.dy[q], 1.f)));
     L.zb[q] = zinit;
   }
-  for (uint64_t m = mask & kSphereMask; m; m &= m - 1)
-    isect_sphere(fo.rec[__ffsll((long long)m) - 1], L, znear);
-  for (uint64_t m = mask & kConeMask; m; m &= m - 1)
-    isect_cone(fo.rec[__ffsll((long long)m) - 1], L, znear);
-  for (uint64_t m = mask & kEllMask; m; m &= m - 1)
-    isect_ellipsoid(fo.rec[__ffsll((long long)m) - 1], L, znear);
+  if (fo.near_ok) {
+    for (uint64_t m = mask & kSphereMask; m; m &= m - 1)
+      isect_sphere<false>(fo.rec[__ffsll((long long)m) - 1], L, znear);
+    for (uint64_t m = mask & kConeMask; m; m &= m - 1)
+      isect_cone<false>(fo.rec[__ffsll((long long)m) - 1], L, znear);
+    for (uint64_t m = mask & kEllMask; m; m &= m - 1)
+      isect_ellipsoid<false>(fo.rec[__ffsll((long long)m) - 1], L, znear);
+  } else {
+    for (uint64_t m = mask & kSphereMask; m; m &= m - 1)
+      isect_sphere<true>(fo.rec[__ffsll((long long)m) - 1], L, znear);
+    for (uint64_t m = mask & kConeMask; m; m &= m - 1)
+      isect_cone<true>(fo.rec[__ffsll((long long)m) - 1], L, znear);
+    for (uint64_t m = mask & kEllMask; m; m &= m - 1)
+      isect_ellipsoid<true>(fo.rec[__ffsll((long long)m) - 1], L, znear);
+  }
 
   if (MODE == kModeDepth) {
 #pragma unroll
@@ -402,15 +418,14 @@ __global__ void __launch_bounds__(NW * 32, 24 / NW)
 // k_eval_persist: persistent, warp-specialised version for large swarms (one CTA per SM
 // slot, one particle at a time per CTA).  Warp 0 is the FK producer: it fetches the next
 // particle from a global counter and runs FK into one of two shared-memory slots while
-// warps 1..NW-1 (consumers) render the particle in the other slot, so FK latency is hidden
-// behind rendering.  Slots are handed over with mbarriers (full: producer -> consumers,
-// empty: consumers -> producer).  The consumers accumulate a particle's sums in shared
-// memory; the last consumer warp to finish computes Eq. (4)-(5).
+// warps 1..NW-1 render the particle in the other slot, so FK latency is hidden behind
+// rendering; once its FK is done, warp 0 joins the rendering.  Slots are handed over with
+// mbarriers (full: producer -> renderers, empty: all warps -> producer).  A particle's sums
+// accumulate in shared memory; the last warp to finish computes Eq. (4)-(5).
 // ---------------------------------------------------------------------------------------
 template <int NW, typename PoseT>
 __global__ void __launch_bounds__(NW * 32, 24 / NW)
     k_eval_persist(const EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
-  constexpr int NC = NW - 1;  // consumer warps
   __shared__ FkScratch s_fk;
   __shared__ __align__(16) FkOut s_out[2];
   __shared__ __align__(128) uint32_t s_obs[NW][kTileW * kTileH];
@@ -428,7 +443,7 @@ __global__ void __launch_bounds__(NW * 32, 24 / NW)
     for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);
     for (int b = 0; b < 2; b++) {
       mbar_init(&s_full[b], 32);       // every producer lane arrives (releases its writes)
-      mbar_init(&s_empty[b], NC * 32); // every consumer lane arrives (its reads are done)
+      mbar_init(&s_empty[b], NW * 32); // every lane arrives once its reads are done
       s_next[b] = 0;
       s_done[b] = 0;
       for (int k = 0; k < 4; k++) s_acc[b][k] = 0;
@@ -443,11 +458,51 @@ __global__ void __launch_bounds__(NW * 32, 24 / NW)
   }
   __syncthreads();
 
+  // Render (this warp's share of) particle p in slot b; the last of the NW warps to finish
+  // computes Eq. (4)-(5) and resets the slot's shared accumulators.
+  uint32_t phase = 0;
+  auto consume = [&](int p, int b) {
+    const FkOut& fo = s_out[b];
+    const TileGrid g(fo.ubox);
+    TileSums acc;
+    int t = 0;
+    if (lane == 0) t = atomicAdd(&s_next[b], 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    while (t < g.ntiles) {
+      int tn = 0;
+      if (lane == 0) tn = atomicAdd(&s_next[b], 1);
+      int X0, Y0;
+      g.origin(t, X0, Y0);
+      do_tile<kModeCost>(a, &tmap, fo, X0, Y0, s_obs[warp], &s_bar[warp], phase, s_dx, s_dy,
+                         acc);
+      t = __shfl_sync(0xffffffffu, tn, 0);
+    }
+    warp_reduce(acc);
+    if (lane == 0) {
+      if (acc.rm) atomicAdd(&s_acc[b][0], (unsigned long long)acc.rm);
+      if (acc.and_) atomicAdd(&s_acc[b][1], (unsigned long long)acc.and_);
+      if (acc.num) atomicAdd(&s_acc[b][2], acc.num);
+      if (acc.both) atomicAdd(&s_acc[b][3], (unsigned long long)acc.both);
+      __threadfence_block();
+      if (atomicAdd(&s_done[b], 1) == NW - 1) {  // last warp for this particle
+        __threadfence_block();
+        unsigned long long v[4];
+        for (int k = 0; k < 4; k++) {
+          v[k] = s_acc[b][k];
+          s_acc[b][k] = 0;
+        }
+        finalize_cost(a, p, v, fo.kc);
+        s_next[b] = 0;
+        s_done[b] = 0;
+      }
+    }
+    __syncwarp();
+    mbar_arrive(&s_empty[b]);
+  };
+
   if (warp == 0) {
-    // ---- producer: particle fetch + FK ----
-    for (int i = 0;; i++) {
-      const int b = i & 1;
-      if (i >= 2) mbar_wait_sleep(&s_empty[b], ((i >> 1) - 1) & 1);
+    // ---- producer: fetch + FK one particle ahead, then help render the current one ----
+    auto produce = [&](int b) {
       int p = 0;
       if (lane == 0) p = (int)atomicAdd(a.pcount, 1u);
       p = __shfl_sync(0xffffffffu, p, 0);
@@ -457,52 +512,24 @@ __global__ void __launch_bounds__(NW * 32, 24 / NW)
         fk_warp<PoseT>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out[b]);
       }
       mbar_arrive(&s_full[b]);
-      if (p >= a.n) break;
+      return p;
+    };
+    int pcur = produce(0);
+    for (int i = 0; pcur < a.n; i++) {
+      const int b = i & 1;
+      if (i >= 1) mbar_wait(&s_empty[b ^ 1], ((i - 1) >> 1) & 1);  // particle i-1 released
+      const int pnext = produce(b ^ 1);
+      consume(pcur, b);
+      pcur = pnext;
     }
   } else {
     // ---- consumers ----
-    uint32_t phase = 0;
     for (int i = 0;; i++) {
       const int b = i & 1;
       mbar_wait(&s_full[b], (i >> 1) & 1);
       const int p = s_pid[b];
       if (p >= a.n) break;
-      const FkOut& fo = s_out[b];
-      const TileGrid g(fo.ubox);
-      TileSums acc;
-      int t = 0;
-      if (lane == 0) t = atomicAdd(&s_next[b], 1);
-      t = __shfl_sync(0xffffffffu, t, 0);
-      while (t < g.ntiles) {
-        int tn = 0;
-        if (lane == 0) tn = atomicAdd(&s_next[b], 1);
-        int X0, Y0;
-        g.origin(t, X0, Y0);
-        do_tile<kModeCost>(a, &tmap, fo, X0, Y0, s_obs[warp], &s_bar[warp], phase, s_dx, s_dy,
-                           acc);
-        t = __shfl_sync(0xffffffffu, tn, 0);
-      }
-      warp_reduce(acc);
-      if (lane == 0) {
-        if (acc.rm) atomicAdd(&s_acc[b][0], (unsigned long long)acc.rm);
-        if (acc.and_) atomicAdd(&s_acc[b][1], (unsigned long long)acc.and_);
-        if (acc.num) atomicAdd(&s_acc[b][2], acc.num);
-        if (acc.both) atomicAdd(&s_acc[b][3], (unsigned long long)acc.both);
-        __threadfence_block();
-        if (atomicAdd(&s_done[b], 1) == NC - 1) {  // last consumer warp for this particle
-          __threadfence_block();
-          unsigned long long v[4];
-          for (int k = 0; k < 4; k++) {
-            v[k] = s_acc[b][k];
-            s_acc[b][k] = 0;
-          }
-          finalize_cost(a, p, v, fo.kc);
-          s_next[b] = 0;
-          s_done[b] = 0;
-        }
-      }
-      __syncwarp();
-      mbar_arrive(&s_empty[b]);
+      consume(p, b);
     }
   }
   // the last CTA to leave resets the particle counter for the next launch
