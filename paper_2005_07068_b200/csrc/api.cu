@@ -58,7 +58,9 @@ struct hp_ctx {
   PsoDyn* dyn = nullptr;
   double* h_out = nullptr;  // pinned: G[64], Gc, trace[K], gens_run
   int trace_cap = 0;
-  int last_N = 0, last_D = 0;
+  int last_N = 0, last_D = 0, last_gens = 0, last_fused = 0;
+  double *X2 = nullptr, *V2 = nullptr;  // second position / velocity buffers (fused fit)
+  unsigned int* gcount = nullptr;       // grid arrival counter of the fused bookkeeping
   Graph graph;
   cudaStream_t st = nullptr;
   cudaEvent_t ev = nullptr;
@@ -196,7 +198,8 @@ void hp_destroy(hp_ctx* ctx) {
   void* dev[] = {ctx->obs, ctx->S_o, ctx->up_depth, ctx->up_mask, ctx->acc, ctx->counters,
                  ctx->poses32, ctx->costs32, ctx->scratch, ctx->X, ctx->V, ctx->P, ctx->Pc,
                  ctx->E, ctx->G, ctx->Gc, ctx->trace, ctx->bnd, ctx->centre, ctx->mark,
-                 ctx->flags, ctx->dyn, ctx->tmap_g, ctx->ray, ctx->pcount};
+                 ctx->flags, ctx->dyn, ctx->tmap_g, ctx->ray, ctx->pcount, ctx->X2,
+                 ctx->V2, ctx->gcount};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_poses) cudaFreeHost(ctx->h_poses);
@@ -349,6 +352,10 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   const size_t ND = N * 64;
   CKC(cudaMalloc(&ctx->X, ND * sizeof(double)));
   CKC(cudaMalloc(&ctx->V, ND * sizeof(double)));
+  CKC(cudaMalloc(&ctx->X2, ND * sizeof(double)));
+  CKC(cudaMalloc(&ctx->V2, ND * sizeof(double)));
+  CKC(cudaMalloc(&ctx->gcount, sizeof(unsigned int)));
+  CKC(cudaMemset(ctx->gcount, 0, sizeof(unsigned int)));
   CKC(cudaMalloc(&ctx->P, ND * sizeof(double)));
   CKC(cudaMalloc(&ctx->Pc, N * sizeof(double)));
   CKC(cudaMalloc(&ctx->E, N * sizeof(double)));
@@ -557,31 +564,42 @@ static PsoDev pso_dev(hp_ctx* ctx, int N, int D, const hp_pso_params* p, int mut
 static hp_status enqueue_fit(hp_ctx* ctx, const PsoDev& d, bool sphere, cudaStream_t s,
                              int64_t* launches) {
   int64_t n = 0;
-  EvalArgs a = base_args(ctx);
-  a.poses = d.X;
-  a.n = d.N;
-  a.S = hp_splits_for(ctx, d.N);
-  a.costs64 = d.E;
-  a.done = d.done;
-  auto eval = [&]() -> hp_status {
-    if (sphere) CK(launch_sphere_eval(d, ctx->centre, s));
-    else CK(launch_eval(a, true, kModeCost, &ctx->tmap, s));
-    n++;
-    return HP_OK;
-  };
   CK(launch_pso_init(d, s));
   n++;
-  hp_status r = eval();
-  if (r != HP_OK) return r;
-  CK(launch_pso_book(d, 0, s));
-  n++;
-  for (int k = 1; k < d.K; k++) {
-    CK(launch_pso_update(d, k, s));
-    n++;
-    r = eval();
-    if (r != HP_OK) return r;
-    CK(launch_pso_book(d, k, s));
-    n++;
+  if (sphere) {  // test objective: standalone update / evaluate / bookkeeping kernels
+    CK(launch_sphere_eval(d, ctx->centre, s));
+    CK(launch_pso_book(d, 0, s));
+    n += 2;
+    for (int k = 1; k < d.K; k++) {
+      CK(launch_pso_update(d, k, s));
+      CK(launch_sphere_eval(d, ctx->centre, s));
+      CK(launch_pso_book(d, k, s));
+      n += 3;
+    }
+  } else {
+    // the hand: ONE kernel per generation — PSO update (k >= 1) fused before FK in every
+    // CTA, bookkeeping fused into the grid's last CTA; X, V double-buffered by parity
+    EvalArgs a = base_args(ctx);
+    a.persist_grid = 0;
+    a.n = d.N;
+    a.S = hp_splits_for(ctx, d.N);
+    a.costs64 = d.E;
+    a.done = d.done;
+    a.pso_on = 1;
+    a.pso = d;
+    a.gcount = ctx->gcount;
+    double* Xb[2] = {ctx->X, ctx->X2};
+    double* Vb[2] = {ctx->V, ctx->V2};
+    for (int k = 0; k < d.K; k++) {
+      a.pso_k = k;
+      a.poses = Xb[0];
+      a.x_in = Xb[(k + 1) & 1];
+      a.v_in = Vb[(k + 1) & 1];
+      a.x_out = Xb[k & 1];
+      a.v_out = Vb[k & 1];
+      CK(launch_eval(a, true, kModeCost, &ctx->tmap, s));
+      n++;
+    }
   }
   *launches = n;
   return HP_OK;
@@ -651,7 +669,7 @@ static hp_status run_fit(hp_ctx* ctx, const hp_pso_params* p, int D, const doubl
     g.mut_hi = mut_hi;
     g.sphere = sphere;
   } else {
-    launches = 3 * (int64_t)K;
+    launches = sphere ? 3 * (int64_t)K : 1 + (int64_t)K;
   }
   CK(cudaGraphLaunch(g.exec, s));
   double* ho = ctx->h_out;
@@ -668,6 +686,8 @@ static hp_status run_fit(hp_ctx* ctx, const hp_pso_params* p, int D, const doubl
   int gr = 0;
   memcpy(&gr, ho + 65, sizeof(int));
   if (gens_run) *gens_run = gr;
+  ctx->last_gens = gr;
+  ctx->last_fused = !sphere;
   if (trace) {
     for (int k = 0; k < K; k++) trace[k] = k < gr ? ho[72 + k] : ho[72 + gr - 1];
   }
@@ -720,8 +740,10 @@ hp_status hp_pso_state(hp_ctx* ctx, double* X, double* V, double* P, double* Pco
   }
   cudaSetDevice(ctx->device);
   const size_t nd = (size_t)ctx->last_N * ctx->last_D * sizeof(double);
-  if (X) CK(cudaMemcpy(X, ctx->X, nd, cudaMemcpyDeviceToHost));
-  if (V) CK(cudaMemcpy(V, ctx->V, nd, cudaMemcpyDeviceToHost));
+  // the fused hand fit double-buffers X, V: generation g lives in buffer g & 1
+  const bool second = ctx->last_fused && ((ctx->last_gens - 1) & 1);
+  if (X) CK(cudaMemcpy(X, second ? ctx->X2 : ctx->X, nd, cudaMemcpyDeviceToHost));
+  if (V) CK(cudaMemcpy(V, second ? ctx->V2 : ctx->V, nd, cudaMemcpyDeviceToHost));
   if (P) CK(cudaMemcpy(P, ctx->P, nd, cudaMemcpyDeviceToHost));
   if (Pcost) CK(cudaMemcpy(Pcost, ctx->Pc, ctx->last_N * sizeof(double), cudaMemcpyDeviceToHost));
   return HP_OK;

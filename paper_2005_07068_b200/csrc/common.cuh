@@ -59,6 +59,20 @@ struct CostD {
   double lambda, lambda_k, depth_scale, kc_rest;
 };
 
+struct PsoDyn {  // per-fit values, read from device memory so a captured graph is reusable
+  uint64_t seed;
+  double c1, c2, w, stop;
+};
+struct PsoDev {
+  int N, D, K, period, per_dim_r, nmut, mut_lo, mut_hi;
+  const PsoDyn* dyn;
+  const double *lo, *hi, *ilo, *ihi;  // [D]
+  double *X, *V, *P, *Pc, *E, *G, *Gc, *trace;
+  int* mark;
+  int* done;
+  int* gens_run;
+};
+
 enum EvalMode { kModeCost = 0, kModeDepth = 1 };
 
 struct EvalArgs {
@@ -82,6 +96,12 @@ struct EvalArgs {
   const float* ray;               // k_ray_table output: dx[W + pad], dy[H + pad]
   unsigned int* pcount;           // [2] persistent kernel: particle counter, CTA exit counter
   int persist_grid;               // > 0: use k_eval_persist with this many CTAs
+  // PSO generation mode (hp_pso_fit): fused update before FK, fused bookkeeping at the end
+  int pso_on, pso_k;
+  PsoDev pso;
+  const double *x_in, *v_in;      // generation k-1 positions / velocities
+  double *x_out, *v_out;          // generation k (evaluated)
+  unsigned int* gcount;           // grid arrival counter (zero between launches)
 };
 
 // --------------------------------------------------------------------------------------
@@ -159,19 +179,6 @@ int eval_warps_per_cta();
 int persist_blocks_per_sm(const CamParams& cam);
 
 // PSO (pso.cu)
-struct PsoDyn {  // per-fit values, read from device memory so a captured graph is reusable
-  uint64_t seed;
-  double c1, c2, w, stop;
-};
-struct PsoDev {
-  int N, D, K, period, per_dim_r, nmut, mut_lo, mut_hi;
-  const PsoDyn* dyn;
-  const double *lo, *hi, *ilo, *ihi;  // [D]
-  double *X, *V, *P, *Pc, *E, *G, *Gc, *trace;
-  int* mark;
-  int* done;
-  int* gens_run;
-};
 cudaError_t launch_pso_init(const PsoDev& p, cudaStream_t st);
 cudaError_t launch_pso_update(const PsoDev& p, int k, cudaStream_t st);
 cudaError_t launch_pso_book(const PsoDev& p, int k, cudaStream_t st);

@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "fk.cuh"
+#include "pso.cuh"
 
 namespace hp {
 
@@ -352,8 +353,17 @@ __global__ void __launch_bounds__(NW * 32, 24 / NW)
   const float* s_dy = s_ray + a.cam.W + kRayPad;
 
   if (warp == 0) {
-    const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
-    fk_warp<PoseT>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
+    if (a.pso_on && a.pso_k >= 1) {
+      // fused PSO update (Eq. 6-7, row A8) of this particle; every CTA of the particle
+      // computes the same bits, split 0 stores them (double-buffered X, V)
+      __shared__ double s_pose[32];
+      pso_update_warp(a.pso, p, a.pso_k, a.x_in, a.v_in, a.x_out, a.v_out, sidx == 0, s_pose);
+      __syncwarp();
+      fk_warp<double>(s_pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
+    } else {
+      const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
+      fk_warp<PoseT>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
+    }
   } else {
     // while warp 0 runs FK: stage the per-column / per-row ray directions (k_ray_table)
     const int n4 = (a.cam.W + a.cam.H + 2 * kRayPad + 3) / 4;
@@ -412,6 +422,20 @@ __global__ void __launch_bounds__(NW * 32, 24 / NW)
     }
     if (last) finalize_cost(a, p, v, s_out.kc);
   }
+  if (!a.pso_on) return;
+  // ---- fused PSO bookkeeping (row A7): the last CTA of the grid, after every cost ----
+  __shared__ int s_lastcta;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(a.gcount, 1u);
+    s_lastcta = prev == gridDim.x - 1;
+    if (s_lastcta) {
+      __threadfence();
+      *a.gcount = 0;
+    }
+  }
+  __syncthreads();
+  if (s_lastcta) pso_book_block(a.pso, a.pso_k, a.pso_k >= 1 ? a.x_out : a.pso.X);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -7,38 +7,9 @@
 // (particle, dim, generation, tag).
 #include <math.h>
 
-#include "common.cuh"
+#include "pso.cuh"
 
 namespace hp {
-
-__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
-#pragma unroll
-  for (int r = 0; r < 10; r++) {
-    if (r > 0) {
-      k.x += 0x9E3779B9u;
-      k.y += 0xBB67AE85u;
-    }
-    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
-    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
-    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-  }
-  return c;
-}
-
-// 53-bit uniform in [0, 1): every step is exact, so the value is unique.
-__device__ __forceinline__ double u01(uint32_t w0, uint32_t w1) {
-  return ((double)(w0 >> 5) * 67108864.0 + (double)(w1 >> 6)) * (1.0 / 9007199254740992.0);
-}
-
-__device__ __forceinline__ uint4 draw(uint64_t seed, uint32_t i, uint32_t d, uint32_t k,
-                                      uint32_t tag) {
-  return philox4x32_10(make_uint4(i, d, k, tag), make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
-}
-
-// lo + u (hi - lo), rounded after each operation
-__device__ __forceinline__ double lerp_rn(double lo, double hi, double u) {
-  return __dadd_rn(lo, __dmul_rn(u, __dsub_rn(hi, lo)));
-}
 
 __global__ void k_pso_init(const PsoDev p) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -54,125 +25,16 @@ __global__ void k_pso_init(const PsoDev p) {
   p.V[idx] = 0.0;                                          // "initial velocity is 0"
 }
 
-// One warp per particle; lane d handles dims d, d + 32, ...
+// One warp per particle (standalone update; the hand fit fuses it into k_eval).
 __global__ void k_pso_update(const PsoDev p, int k) {
   if (*p.done) return;
-  const int i = blockIdx.x;
-  const int lane = threadIdx.x;
-  const PsoDyn dyn = *p.dyn;
-  double r1 = 0.0, r2 = 0.0;
-  if (!p.per_dim_r) {
-    const uint4 r = draw(dyn.seed, (uint32_t)i, 0u, (uint32_t)k, 1u);
-    r1 = u01(r.x, r.y);
-    r2 = u01(r.z, r.w);
-  }
-  const bool marked = p.mark[i] != 0;
-  for (int d = lane; d < p.D; d += 32) {
-    if (p.per_dim_r) {
-      const uint4 r = draw(dyn.seed, (uint32_t)i, (uint32_t)d, (uint32_t)k, 1u);
-      r1 = u01(r.x, r.y);
-      r2 = u01(r.z, r.w);
-    }
-    const long long id = (long long)i * p.D + d;
-    const double x0 = p.X[id];
-    // Eq. (6): v = w (v + c1 r1 (P - x) + c2 r2 (G - x));  Eq. (7): x = x + v
-    const double t1 = __dmul_rn(__dmul_rn(dyn.c1, r1), __dsub_rn(p.P[id], x0));
-    const double t2 = __dadd_rn(p.V[id], t1);
-    const double t3 = __dmul_rn(__dmul_rn(dyn.c2, r2), __dsub_rn(p.G[d], x0));
-    double v = __dmul_rn(dyn.w, __dadd_rn(t2, t3));
-    double x = __dadd_rn(x0, v);
-    if (x < p.lo[d]) {  // AMB-16: clamp, zero that velocity component
-      x = p.lo[d];
-      v = 0.0;
-    } else if (x > p.hi[d]) {
-      x = p.hi[d];
-      v = 0.0;
-    }
-    if (marked && d >= p.mut_lo && d < p.mut_hi) {  // P:L152 mutation (AMB-17)
-      const uint4 r = draw(dyn.seed, (uint32_t)i, (uint32_t)d, (uint32_t)k, 2u);
-      x = lerp_rn(p.lo[d], p.hi[d], u01(r.x, r.y));
-      v = 0.0;
-    }
-    p.X[id] = x;
-    p.V[id] = v;
-  }
+  pso_update_warp(p, blockIdx.x, k, p.X, p.V, p.X, p.V, true, nullptr);
 }
 
-// Bookkeeping after generation k's evaluation: pbest (strict), gbest (lowest index on
-// ties, NaN = +inf), trace, stop rule, and the mutation marks for generation k + 1.
 constexpr int kBookThreads = 1024;
 __global__ void __launch_bounds__(kBookThreads) k_pso_book(const PsoDev p, int k) {
   if (k > 0 && *p.done) return;
-  __shared__ double s_v[kBookThreads / 32];
-  __shared__ int s_i[kBookThreads / 32];
-  __shared__ int s_g;
-  const int tid = threadIdx.x;
-  for (int i = tid; i < p.N; i += blockDim.x) {
-    double e = p.E[i];
-    if (isnan(e)) e = INFINITY;
-    if (k == 0 || e < p.Pc[i]) {
-      p.Pc[i] = e;
-      for (int d = 0; d < p.D; d++) p.P[(long long)i * p.D + d] = p.X[(long long)i * p.D + d];
-    }
-  }
-  __syncthreads();
-  double bv = INFINITY;
-  int bi = 0x7fffffff;
-  for (int i = tid; i < p.N; i += blockDim.x) {
-    const double v = p.Pc[i];
-    if (v < bv || (v == bv && i < bi)) {
-      bv = v;
-      bi = i;
-    }
-  }
-#pragma unroll
-  for (int off = 16; off; off >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-    if (ov < bv || (ov == bv && oi < bi)) {
-      bv = ov;
-      bi = oi;
-    }
-  }
-  if ((tid & 31) == 0) {
-    s_v[tid >> 5] = bv;
-    s_i[tid >> 5] = bi;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double v = INFINITY;
-    int g = 0x7fffffff;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++)
-      if (s_v[w] < v || (s_v[w] == v && s_i[w] < g)) {
-        v = s_v[w];
-        g = s_i[w];
-      }
-    if (g >= p.N) g = 0;  // all +inf (or NaN): lowest index
-    s_g = g;
-    *p.Gc = p.Pc[g];
-    p.trace[k] = p.Pc[g];
-    *p.gens_run = k + 1;
-    if (p.dyn->stop > -INFINITY && p.Pc[g] < p.dyn->stop) *p.done = 1;  // P:L148 stop rule
-  }
-  __syncthreads();
-  const int g = s_g;
-  for (int d = tid; d < p.D; d += blockDim.x) p.G[d] = p.P[(long long)g * p.D + d];
-  // marks for generation k + 1: worst floor(N frac) by Pcost, ties -> higher index worse
-  const int kn = k + 1;
-  const bool mut = p.period > 0 && kn < p.K && kn % p.period == 0 && p.nmut > 0;
-  for (int i = tid; i < p.N; i += blockDim.x) {
-    int m = 0;
-    if (mut) {
-      const double ci = p.Pc[i];
-      int rank = 0;
-      for (int j = 0; j < p.N; j++) {
-        const double cj = p.Pc[j];
-        rank += (cj < ci) || (cj == ci && j < i);
-      }
-      m = rank >= p.N - p.nmut;
-    }
-    p.mark[i] = m;
-  }
+  pso_book_block(p, k, p.X);
 }
 
 // f(x) = sum_d (x_d - c_d)^2, left to right (hp_debug_pso_sphere).
