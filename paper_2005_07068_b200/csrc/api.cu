@@ -69,6 +69,7 @@ struct hp_ctx {
   float* ray = nullptr;  // per-column / per-row ray directions (k_ray_table)
   unsigned int* pcount = nullptr;  // persistent-kernel counters (zero between launches)
   int persist_grid = 0;            // CTAs of k_eval_persist (0 = never use it)
+  int blocks_per_sm = 0;           // resident k_eval CTAs per SM
   int use_tma = 1;   // HP_NO_TMA=1 in the environment selects plain loads (A/B, debugging)
   int sync_debug = 0;  // HP_SYNC_DEBUG=1: synchronise after every launch
   std::string err;
@@ -183,9 +184,10 @@ int64_t hp_last_launch_count(const hp_ctx* ctx) { return ctx ? ctx->last_launche
 
 int32_t hp_splits_for(const hp_ctx* ctx, int64_t n) {
   if (!ctx || n <= 0) return 1;
-  // enough CTAs for ~4 resident 8-warp CTAs per SM; each split strides over the tiles
-  const int64_t target = (int64_t)ctx->sm_count * 4;
-  int64_t s = (target + n - 1) / n;
+  // as many CTAs per pose as fit in ONE wave of resident CTAs (a second partial wave
+  // doubles the latency of a small swarm); each split strides over the pose's tiles
+  const int64_t target = (int64_t)ctx->sm_count * (ctx->blocks_per_sm > 0 ? ctx->blocks_per_sm : 3);
+  int64_t s = target / n;
   if (s < 1) s = 1;
   if (s > 32) s = 32;
   return (int32_t)s;
@@ -332,7 +334,8 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   CKC(launch_ray_table(ctx->camp, ctx->ray, ctx->st));
   CKC(cudaMalloc(&ctx->pcount, 2 * sizeof(unsigned int)));
   CKC(cudaMemset(ctx->pcount, 0, 2 * sizeof(unsigned int)));
-  ctx->persist_grid = ctx->sm_count * persist_blocks_per_sm(ctx->camp);
+  ctx->blocks_per_sm = persist_blocks_per_sm(ctx->camp);
+  ctx->persist_grid = ctx->sm_count * ctx->blocks_per_sm;
   if (const char* e = getenv("HP_NO_PERSIST"))
     if (atoi(e)) ctx->persist_grid = 0;
   CKC(cudaMalloc(&ctx->tmap_g, sizeof(CUtensorMap)));

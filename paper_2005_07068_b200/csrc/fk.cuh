@@ -16,6 +16,7 @@ struct FkScratch {
   double J[5][4][3];        // joint centres, camera frame
   double Rs[5][3][3][3];    // segment frames R_W R_k^H (k = 1..3), camera frame
   int bad;                  // non-finite pose
+  int nearf[kNprim];        // primitive lies entirely beyond z_near
 };
 
 struct FkOut {
@@ -247,77 +248,117 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
   box = prim_box(ng, gc, gA, cam, zmin);
 }
 
-// Whole-warp FK.  pose: 26 values (float or double); writes `out` (shared) and, if
-// `scratch_out` is true, leaves joints in `s` for the debug hook.
-template <typename PoseT>
-__device__ void fk_warp(const PoseT* pose, const DimsD& dm, const CamParams& cam, double kc_rest,
-                        FkScratch& s, FkOut& out) {
-  const int lane = threadIdx.x & 31;
-  if (lane < kNdof) {
-    double v = (double)pose[lane];
-    s.h[lane] = v;
-    if (lane >= 3) sincos(v, &s.sn[lane], &s.cs[lane]);
-  }
-  __syncwarp();
-  int bad = 0;
-  if (lane < kNdof) bad = !isfinite(s.h[lane]);
-  bad = __any_sync(0xffffffffu, bad);
-  if (lane == 0) {
-    // R_W = Rz(th_z) Ry(th_y) Rx(th_x)  (AMB-10)
-    double cx = s.cs[3], sx = s.sn[3], cy = s.cs[4], sy = s.sn[4], cz = s.cs[5], sz = s.sn[5];
-    double Rx[3][3] = {{1, 0, 0}, {0, cx, -sx}, {0, sx, cx}};
-    double Ry[3][3] = {{cy, 0, sy}, {0, 1, 0}, {-sy, 0, cy}};
-    double Rz[3][3] = {{cz, -sz, 0}, {sz, cz, 0}, {0, 0, 1}};
-    double t[3][3];
-    mat3_mul(Ry, Rx, t);
-    mat3_mul(Rz, t, s.RW);
-    s.bad = bad;
-  }
-  __syncwarp();
-  if (lane < 5) {
-    const int f = lane;
-    const int o = 6 + 4 * f;  // (MPx, MPz, PIP, DIP), Eq. (1)
-    double R0[3][3];
-    for (int a = 0; a < 3; a++)
-      for (int b = 0; b < 3; b++) R0[a][b] = f == 0 ? dm.RT0[a][b] : (a == b ? 1.0 : 0.0);
-    double cz = s.cs[o + 1], sz = s.sn[o + 1];
-    double Rz[3][3] = {{cz, -sz, 0}, {sz, cz, 0}, {0, 0, 1}};
-    double RH[3][3], t[3][3];
-    mat3_mul(R0, Rz, t);
-    double JH[3] = {dm.base[f][0], dm.base[f][1], dm.base[f][2]};
-    double Jc[3];
-    for (int i = 0; i < 3; i++)
-      Jc[i] = s.h[i] + s.RW[i][0] * JH[0] + s.RW[i][1] * JH[1] + s.RW[i][2] * JH[2];
-    for (int i = 0; i < 3; i++) s.J[f][0][i] = Jc[i];
-    for (int k = 0; k < 3; k++) {
-      double c = s.cs[k == 0 ? o : o + 1 + k], sn = s.sn[k == 0 ? o : o + 1 + k];
-      double Rx[3][3] = {{1, 0, 0}, {0, c, -sn}, {0, sn, c}}, Rn[3][3];
-      mat3_mul(k == 0 ? t : RH, Rx, Rn);  // R1 = R0 Rz Rx(MPx); R2 = R1 Rx(PIP); ...
-      for (int a = 0; a < 3; a++)
-        for (int b = 0; b < 3; b++) RH[a][b] = Rn[a][b];
-      double L = dm.len[f][k];
-      for (int i = 0; i < 3; i++) JH[i] -= L * RH[i][1];  // J += R (0, -L, 0)
-      for (int i = 0; i < 3; i++)
-        s.J[f][k + 1][i] = s.h[i] + s.RW[i][0] * JH[0] + s.RW[i][1] * JH[1] + s.RW[i][2] * JH[2];
-      mat3_mul(s.RW, RH, s.Rs[f][k]);
+// FK on a team of 1 or 2 warps (warp 0 = the team leader).  pose: 26 values (float or
+// double).  Writes `out`; `s` keeps the fp64 joints for the debug hook.
+//   phase A (warp 0): load the pose, sincos of the 23 angles (one per lane, fp64)
+//   phase B (warp 0, lanes 0..4): the finger chains directly in the camera frame with
+//           sparse column updates: B <- B Rz(MPz) touches columns 0, 1, B <- B Rx(t)
+//           columns 1, 2 (the segment runs along -B[:,1])
+//   phase C: the 38 records + fp32 screen boxes (TEAM 2: spheres on warp 0, the rest on
+//           warp 1, in parallel), then the union box, the near-plane flag and kc(h)
+template <typename PoseT, int TEAM>
+__device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam,
+                        double kc_rest, FkScratch& s, FkOut& out) {
+  const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 1;
+  if (w == 0) {
+    if (lane < kNdof) {
+      const double v = (double)pose[lane];
+      s.h[lane] = v;
+      if (lane >= 3) sincos(v, &s.sn[lane], &s.cs[lane]);
     }
+    __syncwarp();
+    int bad = 0;
+    if (lane < kNdof) bad = !isfinite(s.h[lane]);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane < 5) {
+      // R_W = Rz(th_z) Ry(th_y) Rx(th_x)  (AMB-10), written out
+      const double cx = s.cs[3], sx = s.sn[3], cy = s.cs[4], sy = s.sn[4], cz = s.cs[5],
+                   sz = s.sn[5];
+      const double r0[3] = {cy, sy * sx, sy * cx}, r1[3] = {0.0, cx, -sx},
+                   r2[3] = {-sy, cy * sx, cy * cx};  // rows of Ry Rx
+      double RW[3][3];
+      for (int j = 0; j < 3; j++) {
+        RW[0][j] = cz * r0[j] - sz * r1[j];
+        RW[1][j] = sz * r0[j] + cz * r1[j];
+        RW[2][j] = r2[j];
+      }
+      const int f = lane;
+      if (f == 0) {
+        for (int i = 0; i < 3; i++)
+          for (int j = 0; j < 3; j++) s.RW[i][j] = RW[i][j];
+        s.bad = bad;
+      }
+      // B = R_W R_f0 (camera-frame base frame of the finger)
+      double B[3][3];
+      if (f == 0) mat3_mul(RW, dm.RT0, B);
+      else
+        for (int i = 0; i < 3; i++)
+          for (int j = 0; j < 3; j++) B[i][j] = RW[i][j];
+      const int o = 6 + 4 * f;  // (MPx, MPz, PIP, DIP), Eq. (1)
+      {                         // B <- B Rz(MPz)
+        const double c = s.cs[o + 1], sn = s.sn[o + 1];
+        for (int i = 0; i < 3; i++) {
+          const double b0 = B[i][0], b1 = B[i][1];
+          B[i][0] = c * b0 + sn * b1;
+          B[i][1] = c * b1 - sn * b0;
+        }
+      }
+      double J[3];
+      for (int i = 0; i < 3; i++)
+        J[i] = s.h[i] + RW[i][0] * dm.base[f][0] + RW[i][1] * dm.base[f][1] +
+               RW[i][2] * dm.base[f][2];
+      for (int i = 0; i < 3; i++) s.J[f][0][i] = J[i];
+      for (int k = 0; k < 3; k++) {  // B <- B Rx(MPx | PIP | DIP); J += B (0, -L, 0)
+        const int ai = k == 0 ? o : o + 1 + k;
+        const double c = s.cs[ai], sn = s.sn[ai];
+        for (int i = 0; i < 3; i++) {
+          const double b1 = B[i][1], b2 = B[i][2];
+          B[i][1] = c * b1 + sn * b2;
+          B[i][2] = c * b2 - sn * b1;
+        }
+        const double L = dm.len[f][k];
+        for (int i = 0; i < 3; i++) {
+          J[i] -= L * B[i][1];
+          s.J[f][k + 1][i] = J[i];
+        }
+        for (int i = 0; i < 3; i++)
+          for (int j = 0; j < 3; j++) s.Rs[f][k][i][j] = B[i][j];
+      }
+    }
+    __syncwarp();
+    if (TEAM == 2) asm volatile("bar.arrive 2, 64;" ::: "memory");
+  } else if (TEAM == 2) {
+    asm volatile("bar.sync 2, 64;" ::: "memory");
   }
-  __syncwarp();
+  // ---- phase C: records + boxes ----
+  if (TEAM == 2) {
+    const int j = w == 0 ? lane : 20 + lane;
+    if ((w == 0 && lane < 20) || (w == 1 && lane < kNprim - 20)) {
+      float zmin;
+      build_prim(j, s, dm, cam, out.rec[j], out.box[j], zmin);
+      s.nearf[j] = zmin > cam.znear * 1.001f;
+    }
+    if (w == 1) {
+      asm volatile("bar.arrive 1, 64;" ::: "memory");
+      return;
+    }
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+  } else {
+    for (int j = lane; j < kNprim; j += 32) {
+      float zmin;
+      build_prim(j, s, dm, cam, out.rec[j], out.box[j], zmin);
+      s.nearf[j] = zmin > cam.znear * 1.001f;
+    }
+    __syncwarp();
+  }
+  // ---- warp 0: union box, near-plane flag, kc ----
+  // (the solid is the convex hull of its generators, so zmin bounds its nearest point; the
+  // 1e-3 relative slack covers the fp32 evaluation)
   int near_ok = 1;
-  for (int j = lane; j < kNprim; j += 32) {
-    float zmin;
-    build_prim(j, s, dm, cam, out.rec[j], out.box[j], zmin);
-    // the solid is the convex hull of its generators, so zmin bounds its nearest point;
-    // 1e-3 relative slack covers the fp32 evaluation
-    near_ok &= zmin > cam.znear * 1.001f;
-  }
-  near_ok = __all_sync(0xffffffffu, near_ok);
-  if (lane == 0) out.near_ok = near_ok && !s.bad;
-  __syncwarp();
-  // union box
   int4 u = make_int4(1 << 30, 1 << 30, -1, -1);
   for (int j = lane; j < kNprim; j += 32) {
-    int4 b = out.box[j];
+    near_ok &= s.nearf[j];
+    const int4 b = out.box[j];
     if (b.x <= b.z) {
       u.x = min(u.x, b.x);
       u.y = min(u.y, b.y);
@@ -325,6 +366,7 @@ __device__ void fk_warp(const PoseT* pose, const DimsD& dm, const CamParams& cam
       u.w = max(u.w, b.w);
     }
   }
+  near_ok = __all_sync(0xffffffffu, near_ok);
   for (int off = 16; off; off >>= 1) {
     u.x = min(u.x, __shfl_xor_sync(0xffffffffu, u.x, off));
     u.y = min(u.y, __shfl_xor_sync(0xffffffffu, u.y, off));
@@ -334,6 +376,7 @@ __device__ void fk_warp(const PoseT* pose, const DimsD& dm, const CamParams& cam
   if (lane == 0) {
     if (s.bad || u.z < u.x) u = make_int4(1, 1, 0, 0);
     out.ubox = u;
+    out.near_ok = near_ok && !s.bad;
     // kc(h) = sum over (index,middle), (middle,ring), (ring,little) of -min(phi, 0)
     double kc = 0.0;
     for (int f = 1; f <= 3; f++) {
@@ -343,6 +386,12 @@ __device__ void fk_warp(const PoseT* pose, const DimsD& dm, const CamParams& cam
     out.kc = s.bad ? __longlong_as_double(0x7ff8000000000000ll) : kc;
   }
   __syncwarp();
+}
+
+template <typename PoseT>
+__device__ __forceinline__ void fk_warp(const PoseT* pose, const DimsD& dm, const CamParams& cam,
+                                        double kc_rest, FkScratch& s, FkOut& out) {
+  fk_team<PoseT, 1>(pose, dm, cam, kc_rest, s, out);
 }
 
 }  // namespace hp

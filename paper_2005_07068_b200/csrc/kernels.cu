@@ -352,29 +352,31 @@ __global__ void __launch_bounds__(NW * 32, 24 / NW)
   const float* s_dx = s_ray;
   const float* s_dy = s_ray + a.cam.W + kRayPad;
 
-  if (warp == 0) {
+  if (warp <= 1) {
+    // FK on warps 0 and 1 (warp 1 builds the non-sphere records in parallel)
+    __shared__ double s_pose[32];
     if (a.pso_on && a.pso_k >= 1) {
       // fused PSO update (Eq. 6-7, row A8) of this particle; every CTA of the particle
       // computes the same bits, split 0 stores them (double-buffered X, V)
-      __shared__ double s_pose[32];
-      pso_update_warp(a.pso, p, a.pso_k, a.x_in, a.v_in, a.x_out, a.v_out, sidx == 0, s_pose);
+      if (warp == 0)
+        pso_update_warp(a.pso, p, a.pso_k, a.x_in, a.v_in, a.x_out, a.v_out, sidx == 0, s_pose);
       __syncwarp();
-      fk_warp<double>(s_pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
+      fk_team<double, 2>(s_pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
     } else {
       const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
-      fk_warp<PoseT>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
+      fk_team<PoseT, 2>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
     }
   } else {
-    // while warp 0 runs FK: stage the per-column / per-row ray directions (k_ray_table)
+    // while warps 0-1 run FK: stage the per-column / per-row ray directions (k_ray_table)
     const int n4 = (a.cam.W + a.cam.H + 2 * kRayPad + 3) / 4;
-    for (int i = threadIdx.x - 32; i < n4; i += (NW - 1) * 32)
+    for (int i = threadIdx.x - 64; i < n4; i += (NW - 2) * 32)
       reinterpret_cast<float4*>(s_ray)[i] = __ldg(reinterpret_cast<const float4*>(a.ray) + i);
     if (MODE == kModeCost && warp == NW - 1 && lane == 0) {
       for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);  // count 1: the expect_tx arrival
       fence_mbar_init();
       if (a.use_tma == 1) prefetch_tmap(&tmap);
     }
-    if (threadIdx.x == 32) s_next = NW;
+    if (threadIdx.x == 64) s_next = NW;
   }
   __syncthreads();
 
