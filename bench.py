@@ -199,13 +199,22 @@ def run_ours(args):
     swarm = rank_swarm(rank, world)
     P = torch.tensor(swarm, device=dev)
     costs = torch.empty(PER_RANK, dtype=torch.float32, device=dev)
-    all_costs = torch.empty(PER_RANK * world, dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    if world > 1:
+        # the product's particle-sharded mode: every rank passes the FULL swarm; the library
+        # scores this rank's slice and NCCL-allgathers all costs (hp_shard)
+        sctx = hp.Context(WIDTH, HEIGHT, max_particles=PER_RANK)
+        sctx.set_observation(depth, mask)
+        sctx.shard(rank, world)
+        P_all = torch.tensor(np.ascontiguousarray(W.swarm_c4(PER_RANK * world), np.float32),
+                             device=dev)
+        all_costs = torch.empty(PER_RANK * world, dtype=torch.float32, device=dev)
 
     def step():
-        ctx.eval_costs(P, out=costs)
         if world > 1:
-            dist.all_gather_into_tensor(all_costs, costs)
+            sctx.eval_costs(P_all, out=all_costs)
+        else:
+            ctx.eval_costs(P, out=costs)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -230,15 +239,18 @@ def run_ours(args):
         for k in range(args.steps):
             flush.zero_()
             evs[k][0].record(stream)
-            kev[k][0].record(stream)
-            ctx.eval_costs(P, out=costs)
-            kev[k][1].record(stream)
-            if world > 1:
-                dist.all_gather_into_tensor(all_costs, costs)
+            step()
             evs[k][1].record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+    # the fused kernel alone (roofline), same slice and launch configuration
+    for k in range(args.steps):
+        flush.zero_()
+        kev[k][0].record(stream)
+        ctx.eval_costs(P, out=costs)
+        kev[k][1].record(stream)
+    torch.cuda.synchronize()
     step_ms = sum(a.elapsed_time(b) for a, b in evs)
     kern_ms = sum(a.elapsed_time(b) for a, b in kev)
     t = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device=dev)
@@ -251,16 +263,15 @@ def run_ours(args):
 
     # ---- end to end through the public host API (pinned host <-> device inside) ----
     host_poses = swarm.copy()
-    for _ in range(2):
-        ctx.eval_costs_host(host_poses)
     e2e_s = 0.0
+    host_all = np.ascontiguousarray(W.swarm_c4(PER_RANK * world), np.float32) if world > 1 \
+        else host_poses
+    ectx = sctx if world > 1 else ctx
     for k in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        out = ctx.eval_costs_host(host_poses)
-        if world > 1:
-            dist.all_gather_into_tensor(all_costs, torch.from_numpy(out).to(dev))
+        out = ectx.eval_costs_host(host_all)  # sharded: slice + NCCL allgather inside
         e2e_s += time.perf_counter() - t0
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
@@ -315,8 +326,9 @@ def run_ours(args):
                          "peak_note": f"FP32 FMA pipe: {sms} SMs x 128 lanes x 2 x "
                                       f"{peak_mhz:.0f} MHz (sm_max_mhz); W_alg "
                                       f"{flops / PER_RANK / 1e6:.3f} MFLOP/hyp (profiles/walg.json)"},
-            "e2e": {"value": e2e, "unit": "hyp/s", "h2d_bytes_per_step": PER_RANK * 26 * 4,
-                    "d2h_bytes_per_step": PER_RANK * 4},
+            "e2e": {"value": e2e, "unit": "hyp/s",
+                    "h2d_bytes_per_step": PER_RANK * 26 * 4,  # this rank's slice
+                    "d2h_bytes_per_step": PER_RANK * world * 4},  # all gathered costs
             "gpu_launches": launches,
             "clocks": clocks,
         }

@@ -174,6 +174,27 @@ hp_status hp_debug_pso_sphere(hp_ctx* ctx, int32_t D, const double* lo, const do
                               double* best_x, double* best_cost, double* trace,
                               int32_t* gens_run, void* stream);
 
+/* ---- particle-sharded multi-GPU mode (one process per GPU) -------------
+ * Only the particles shard: the observation is replicated, rank r scores poses
+ * [r*ceil(N/W), min(N, (r+1)*ceil(N/W))) and NCCL allgathers the costs (over NVLink /
+ * NVSwitch), so every rank holds all N costs.  In hp_pso_fit every rank then runs the
+ * identical update of all particles and the identical bookkeeping, so G is known
+ * everywhere without a broadcast and the result is bitwise independent of W (integer
+ * pixel sums, fp64 swarm state).  NCCL is loaded at run time (libnccl.so.2, or the path in
+ * HP_NCCL_LIB); single-GPU use never needs it. */
+/* The slice of n poses owned by `rank` of `world` (host-only, no GPU needed). */
+hp_status hp_shard_range(int64_t n, int32_t rank, int32_t world, int64_t* begin, int64_t* end);
+/* 1 if libnccl.so.2 could be loaded. */
+hp_status hp_nccl_available(int32_t* available);
+/* A fresh NCCL unique id (128 bytes) on rank 0; broadcast it to the other ranks (the
+ * Python binding uses torch.distributed).  Errors: NCCL. */
+hp_status hp_get_nccl_id(uint8_t* id);
+/* Collective: every rank calls it with the same id.  Afterwards hp_eval_costs takes the
+ * FULL batch (n <= max_particles * world), scores this rank's slice and returns all n
+ * costs on every rank; hp_pso_fit runs sharded (particles >= world).  Errors:
+ * INVALID_ARG, STATE (already sharded), NCCL, OOM. */
+hp_status hp_shard(hp_ctx* ctx, const uint8_t* id, int32_t rank, int32_t world);
+
 /* Number of kernel launches the last hp_eval_costs / hp_pso_fit enqueued (bench). */
 int64_t hp_last_launch_count(const hp_ctx* ctx);
 /* Split factor S (CTAs per particle) used for n poses. */

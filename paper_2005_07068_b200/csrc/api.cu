@@ -1,10 +1,12 @@
 // api.cu — the C ABI of include/hp.h: context, observation upload, TMA descriptor,
 // evaluation entry points, the CUDA-graph PSO driver and the test hooks.
 #include <cudaTypedefs.h>
+#include <dlfcn.h>
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -16,12 +18,50 @@ using namespace hp;
 
 namespace {
 
+// ---- NCCL, loaded at run time (dlopen) so single-GPU use has no NCCL dependency ----
+// ABI subset of nccl.h 2.28 (nvidia-nccl wheel): ncclComm_t is an opaque pointer, the
+// unique id is 128 bytes, ncclSuccess = 0, ncclFloat32 = 7, ncclFloat64 = 8.
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+enum { kNcclFloat32 = 7, kNcclFloat64 = 8 };
+struct NcclApi {
+  void* handle = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    const char* env = getenv("HP_NCCL_LIB");
+    void* h = env ? dlopen(env, RTLD_NOW | RTLD_GLOBAL) : nullptr;
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+      api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+      api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+      api.errorString = (decltype(api.errorString))dlsym(h, "ncclGetErrorString");
+      if (api.getUniqueId && api.commInitRank && api.commDestroy && api.allGather &&
+          api.errorString)
+        api.handle = h;
+    }
+  }
+  return api.handle ? &api : nullptr;
+}
+
 thread_local std::string g_err = "";
 
 struct Graph {
   cudaGraphExec_t exec = nullptr;
   int N = -1, D = -1, K = -1, period = -1, per_dim_r = -1, nmut = -1, mut_lo = -1, mut_hi = -1;
   int sphere = -1;
+  int world = -1;
 };
 
 }  // namespace
@@ -59,6 +99,7 @@ struct hp_ctx {
   double* h_out = nullptr;  // pinned: G[64], Gc, trace[K], gens_run
   int trace_cap = 0;
   int last_N = 0, last_D = 0, last_gens = 0, last_fused = 0;
+  int64_t last_fit_launches = 0;
   double *X2 = nullptr, *V2 = nullptr;  // second position / velocity buffers (fused fit)
   unsigned int* gcount = nullptr;       // grid arrival counter of the fused bookkeeping
   Graph graph;
@@ -70,6 +111,12 @@ struct hp_ctx {
   unsigned int* pcount = nullptr;  // persistent-kernel counters (zero between launches)
   int persist_grid = 0;            // CTAs of k_eval_persist (0 = never use it)
   int blocks_per_sm = 0;           // resident k_eval CTAs per SM
+  // particle-sharded mode (hp_shard): rank r owns poses [r chunk, (r + 1) chunk)
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  float* gat32 = nullptr;    // [chunk * world] allgather buffer (hp_eval_costs)
+  double* gat64 = nullptr;   // [chunk * world] allgather buffer (hp_pso_fit costs)
+  int64_t gat_cap = 0;       // chunk capacity of the buffers
   int use_tma = 1;   // HP_NO_TMA=1 in the environment selects plain loads (A/B, debugging)
   int sync_debug = 0;  // HP_SYNC_DEBUG=1: synchronise after every launch
   std::string err;
@@ -196,6 +243,9 @@ int32_t hp_splits_for(const hp_ctx* ctx, int64_t n) {
 void hp_destroy(hp_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  if (ctx->comm && nccl_api()) nccl_api()->commDestroy(ctx->comm);
+  if (ctx->gat32) cudaFree(ctx->gat32);
+  if (ctx->gat64) cudaFree(ctx->gat64);
   if (ctx->graph.exec) cudaGraphExecDestroy(ctx->graph.exec);
   void* dev[] = {ctx->obs, ctx->S_o, ctx->up_depth, ctx->up_mask, ctx->acc, ctx->counters,
                  ctx->poses32, ctx->costs32, ctx->scratch, ctx->X, ctx->V, ctx->P, ctx->Pc,
@@ -461,23 +511,86 @@ static hp_status eval_common(hp_ctx* ctx, const float* poses, int64_t n, float* 
   return HP_OK;
 }
 
+static inline void shard_range(int64_t n, int rank, int world, int64_t* b, int64_t* e) {
+  const int64_t chunk = (n + world - 1) / world;
+  *b = std::min<int64_t>(n, (int64_t)rank * chunk);
+  *e = std::min<int64_t>(n, *b + chunk);
+}
+
+// Sharded objective: this rank scores its slice of the N poses into its chunk of the
+// allgather buffer; ncclAllGather (in place) gives every rank all N costs.
+static hp_status eval_sharded(hp_ctx* ctx, const float* poses, int64_t n, float* costs,
+                              cudaStream_t s) {
+  const int64_t chunk = (n + ctx->world - 1) / ctx->world;
+  if (chunk > ctx->gat_cap) {
+    ctx->err = "sharded eval: n exceeds max_particles * world";
+    return HP_ERR_INVALID_ARG;
+  }
+  int64_t b, e;
+  shard_range(n, ctx->rank, ctx->world, &b, &e);
+  int64_t launches = 0;
+  if (e > b) {
+    hp_status r = eval_common(ctx, poses + b * kNdof, e - b, ctx->gat32 + ctx->rank * chunk,
+                              nullptr, nullptr, s);
+    if (r != HP_OK) return r;
+    launches = 1;
+  }
+  ncclResult_t nr = nccl_api()->allGather(ctx->gat32 + ctx->rank * chunk, ctx->gat32,
+                                          (size_t)chunk, kNcclFloat32, ctx->comm, s);
+  if (nr != 0) {
+    ctx->err = std::string("ncclAllGather: ") + nccl_api()->errorString(nr);
+    return HP_ERR_NCCL;
+  }
+  CK(cudaMemcpyAsync(costs, ctx->gat32, (size_t)n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  ctx->last_launches = launches;
+  return HP_OK;
+}
+
 hp_status hp_eval_costs(hp_ctx* ctx, const float* poses, int64_t n, float* costs, void* stream) {
   ARG(ctx, "hp_eval_costs: NULL ctx");
-  ARG(n >= 0 && n <= ctx->max_n, "hp_eval_costs: n < 0 or n > max_particles");
+  ARG(n >= 0 && n <= (int64_t)ctx->max_n * ctx->world,
+      "hp_eval_costs: n < 0 or n > max_particles (x world when sharded)");
   if (n == 0) return HP_OK;
   ARG(poses && costs, "hp_eval_costs: NULL buffer");
   cudaSetDevice(ctx->device);
+  if (ctx->comm) return eval_sharded(ctx, poses, n, costs, (cudaStream_t)stream);
   return eval_common(ctx, poses, n, costs, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 hp_status hp_eval_costs_host(hp_ctx* ctx, const float* poses, int64_t n, float* costs,
                              void* stream) {
   ARG(ctx, "hp_eval_costs_host: NULL ctx");
-  ARG(n >= 0 && n <= ctx->max_n, "hp_eval_costs_host: n < 0 or n > max_particles");
+  ARG(n >= 0 && n <= (int64_t)ctx->max_n * ctx->world,
+      "hp_eval_costs_host: n < 0 or n > max_particles (x world when sharded)");
   if (n == 0) return HP_OK;
   ARG(poses && costs, "hp_eval_costs_host: NULL buffer");
   cudaSetDevice(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
+  if (ctx->comm) {
+    // sharded: upload only this rank's slice, score it, allgather, download all costs
+    const int64_t chunk = (n + ctx->world - 1) / ctx->world;
+    int64_t b, e;
+    shard_range(n, ctx->rank, ctx->world, &b, &e);
+    memcpy(ctx->h_poses, poses + b * kNdof, (size_t)(e - b) * kNdof * sizeof(float));
+    if (e > b) {
+      CK(cudaMemcpyAsync(ctx->poses32, ctx->h_poses, (size_t)(e - b) * kNdof * sizeof(float),
+                         cudaMemcpyHostToDevice, s));
+      hp_status r = eval_common(ctx, ctx->poses32, e - b, ctx->gat32 + ctx->rank * chunk,
+                                nullptr, nullptr, s);
+      if (r != HP_OK) return r;
+    }
+    ncclResult_t nr = nccl_api()->allGather(ctx->gat32 + ctx->rank * chunk, ctx->gat32,
+                                            (size_t)chunk, kNcclFloat32, ctx->comm, s);
+    if (nr != 0) {
+      ctx->err = std::string("ncclAllGather: ") + nccl_api()->errorString(nr);
+      return HP_ERR_NCCL;
+    }
+    CK(cudaMemcpyAsync(ctx->h_costs, ctx->gat32, (size_t)n * sizeof(float),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    memcpy(costs, ctx->h_costs, (size_t)n * sizeof(float));
+    return HP_OK;
+  }
   // pinned staging so the copies are true async DMA
   memcpy(ctx->h_poses, poses, (size_t)n * kNdof * sizeof(float));
   CK(cudaMemcpyAsync(ctx->poses32, ctx->h_poses, (size_t)n * kNdof * sizeof(float),
@@ -527,6 +640,7 @@ hp_status hp_debug_fk(hp_ctx* ctx, const double* pose, float* records, int32_t* 
 static hp_status validate_pso(hp_ctx* ctx, const hp_pso_params* p) {
   ARG(p, "pso: NULL params");
   ARG(p->particles >= 1 && p->particles <= ctx->max_n, "pso: particles < 1 or > max_particles");
+  ARG(!ctx->comm || p->particles >= ctx->world, "pso: sharded fit needs particles >= world");
   ARG(p->generations >= 1, "pso: generations < 1");
   ARG(p->c1 + p->c2 > 4.0, "pso: c1 + c2 must exceed 4 (P:L150 constriction)");
   ARG(p->mutation_fraction >= 0.0 && p->mutation_fraction <= 1.0, "pso: mutation_fraction");
@@ -578,6 +692,37 @@ static hp_status enqueue_fit(hp_ctx* ctx, const PsoDev& d, bool sphere, cudaStre
       CK(launch_sphere_eval(d, ctx->centre, s));
       CK(launch_pso_book(d, k, s));
       n += 3;
+    }
+  } else if (ctx->comm) {
+    // sharded hand fit: every rank updates ALL particles (identical bits everywhere),
+    // scores its slice, allgathers the costs, and runs the identical bookkeeping
+    const int64_t chunk = (d.N + ctx->world - 1) / ctx->world;
+    int64_t b, e;
+    shard_range(d.N, ctx->rank, ctx->world, &b, &e);
+    EvalArgs a = base_args(ctx);
+    a.persist_grid = 0;
+    a.n = (int)(e - b);
+    a.S = hp_splits_for(ctx, e - b);
+    a.poses = d.X + b * d.D;
+    a.costs64 = ctx->gat64 + ctx->rank * chunk;
+    a.done = d.done;
+    for (int k = 0; k < d.K; k++) {
+      if (k >= 1) {
+        CK(launch_pso_update(d, k, s));
+        n++;
+      }
+      if (e > b) {
+        CK(launch_eval(a, true, kModeCost, &ctx->tmap, s));
+        n++;
+      }
+      ncclResult_t nr = nccl_api()->allGather(ctx->gat64 + ctx->rank * chunk, ctx->gat64,
+                                              (size_t)chunk, kNcclFloat64, ctx->comm, s);
+      if (nr != 0) {
+        ctx->err = std::string("ncclAllGather: ") + nccl_api()->errorString(nr);
+        return HP_ERR_NCCL;
+      }
+      CK(launch_pso_book(d, k, s));
+      n++;
     }
   } else {
     // the hand: ONE kernel per generation — PSO update (k >= 1) fused before FK in every
@@ -646,10 +791,17 @@ static hp_status run_fit(hp_ctx* ctx, const hp_pso_params* p, int D, const doubl
   CK(cudaMemcpyAsync(ctx->bnd, hbv.data(), 256 * sizeof(double), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(ctx->dyn, &dyn, sizeof dyn, cudaMemcpyHostToDevice, s));
   PsoDev d = pso_dev(ctx, N, D, p, mut_lo, mut_hi);
+  if (ctx->comm && !sphere) {
+    if ((N + ctx->world - 1) / ctx->world > ctx->gat_cap) {
+      ctx->err = "sharded fit: particles exceed max_particles * world";
+      return HP_ERR_INVALID_ARG;
+    }
+    d.E = ctx->gat64;  // costs arrive through the allgather
+  }
   Graph& g = ctx->graph;
   const bool same = g.exec && g.N == N && g.D == D && g.K == K && g.period == d.period &&
                     g.per_dim_r == d.per_dim_r && g.nmut == d.nmut && g.mut_lo == mut_lo &&
-                    g.mut_hi == mut_hi && g.sphere == (int)sphere;
+                    g.mut_hi == mut_hi && g.sphere == (int)sphere && g.world == ctx->world;
   int64_t launches = 0;
   if (!same) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -661,6 +813,7 @@ static hp_status run_fit(hp_ctx* ctx, const hp_pso_params* p, int D, const doubl
     if (r != HP_OK) return r;
     CK(ce);
     CK(cudaGraphInstantiate(&g.exec, graph, 0));
+    ctx->last_fit_launches = launches;
     cudaGraphDestroy(graph);
     g.N = N;
     g.D = D;
@@ -671,8 +824,9 @@ static hp_status run_fit(hp_ctx* ctx, const hp_pso_params* p, int D, const doubl
     g.mut_lo = mut_lo;
     g.mut_hi = mut_hi;
     g.sphere = sphere;
+    g.world = ctx->world;
   } else {
-    launches = sphere ? 3 * (int64_t)K : 1 + (int64_t)K;
+    launches = ctx->last_fit_launches;
   }
   CK(cudaGraphLaunch(g.exec, s));
   double* ho = ctx->h_out;
@@ -690,7 +844,7 @@ static hp_status run_fit(hp_ctx* ctx, const hp_pso_params* p, int D, const doubl
   memcpy(&gr, ho + 65, sizeof(int));
   if (gens_run) *gens_run = gr;
   ctx->last_gens = gr;
-  ctx->last_fused = !sphere;
+  ctx->last_fused = !sphere && !ctx->comm;
   if (trace) {
     for (int k = 0; k < K; k++) trace[k] = k < gr ? ho[72 + k] : ho[72 + gr - 1];
   }
@@ -749,6 +903,76 @@ hp_status hp_pso_state(hp_ctx* ctx, double* X, double* V, double* P, double* Pco
   if (V) CK(cudaMemcpy(V, second ? ctx->V2 : ctx->V, nd, cudaMemcpyDeviceToHost));
   if (P) CK(cudaMemcpy(P, ctx->P, nd, cudaMemcpyDeviceToHost));
   if (Pcost) CK(cudaMemcpy(Pcost, ctx->Pc, ctx->last_N * sizeof(double), cudaMemcpyDeviceToHost));
+  return HP_OK;
+}
+
+hp_status hp_shard_range(int64_t n, int32_t rank, int32_t world, int64_t* begin, int64_t* end) {
+  hp_ctx* ctx = nullptr;
+  ARG(begin && end && n >= 0 && world >= 1 && rank >= 0 && rank < world,
+      "hp_shard_range: bad argument");
+  shard_range(n, rank, world, begin, end);
+  return HP_OK;
+}
+
+hp_status hp_nccl_available(int32_t* available) {
+  if (!available) return HP_ERR_INVALID_ARG;
+  *available = nccl_api() != nullptr;
+  return HP_OK;
+}
+
+hp_status hp_get_nccl_id(uint8_t* id) {
+  hp_ctx* ctx = nullptr;
+  ARG(id, "hp_get_nccl_id: NULL id");
+  NcclApi* api = nccl_api();
+  if (!api) {
+    g_err = "hp_get_nccl_id: libnccl.so.2 not found (set HP_NCCL_LIB)";
+    return HP_ERR_NCCL;
+  }
+  ncclUniqueId u;
+  const ncclResult_t r = api->getUniqueId(&u);
+  if (r != 0) {
+    g_err = std::string("ncclGetUniqueId: ") + api->errorString(r);
+    return HP_ERR_NCCL;
+  }
+  memcpy(id, u.internal, 128);
+  return HP_OK;
+}
+
+hp_status hp_shard(hp_ctx* ctx, const uint8_t* id, int32_t rank, int32_t world) {
+  ARG(ctx && id, "hp_shard: NULL argument");
+  ARG(world >= 1 && rank >= 0 && rank < world, "hp_shard: bad rank/world");
+  if (ctx->comm) {
+    ctx->err = "hp_shard: context is already sharded";
+    return HP_ERR_STATE;
+  }
+  NcclApi* api = nccl_api();
+  if (!api) {
+    ctx->err = "hp_shard: libnccl.so.2 not found (set HP_NCCL_LIB)";
+    return HP_ERR_NCCL;
+  }
+  cudaSetDevice(ctx->device);
+  ncclUniqueId u;
+  memcpy(u.internal, id, 128);
+  const ncclResult_t r = api->commInitRank(&ctx->comm, world, u, rank);
+  if (r != 0) {
+    ctx->comm = nullptr;
+    ctx->err = std::string("ncclCommInitRank: ") + api->errorString(r);
+    return HP_ERR_NCCL;
+  }
+  ctx->rank = rank;
+  ctx->world = world;
+  ctx->gat_cap = ctx->max_n;  // chunk <= max_particles
+  const size_t cap = (size_t)ctx->gat_cap * world;
+  CK(cudaMalloc(&ctx->gat32, cap * sizeof(float)));
+  CK(cudaMalloc(&ctx->gat64, cap * sizeof(double)));
+  // host staging for the full gathered cost vector of hp_eval_costs_host
+  cudaFreeHost(ctx->h_costs);
+  ctx->h_costs = nullptr;
+  CK(cudaMallocHost(&ctx->h_costs, cap * sizeof(float)));
+  if (ctx->graph.exec) {
+    cudaGraphExecDestroy(ctx->graph.exec);
+    ctx->graph.exec = nullptr;
+  }
   return HP_OK;
 }
 

@@ -89,6 +89,11 @@ def lib() -> C.CDLL:
             "hp_debug_render": [_VP, _VP, _VP, _VP],
             "hp_debug_pso_sphere": [_VP, C.c_int32, _VP, _VP, _VP, _VP, C.c_int32, C.c_int32, _VP,
                                     C.POINTER(PsoParams), _VP, _VP, _VP, _VP, _VP],
+            "hp_shard_range": [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64),
+                               C.POINTER(C.c_int64)],
+            "hp_nccl_available": [C.POINTER(C.c_int32)],
+            "hp_get_nccl_id": [_VP],
+            "hp_shard": [_VP, _VP, C.c_int32, C.c_int32],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -112,7 +117,8 @@ def exported_symbols():
             "hp_bounds", "hp_create", "hp_set_observation", "hp_render_observation",
             "hp_eval_costs", "hp_eval_costs_host", "hp_eval_sums", "hp_pso_fit", "hp_pso_state",
             "hp_debug_fk", "hp_debug_render", "hp_debug_pso_sphere", "hp_last_launch_count",
-            "hp_splits_for", "hp_last_error", "hp_destroy"]
+            "hp_splits_for", "hp_last_error", "hp_destroy", "hp_shard_range",
+            "hp_nccl_available", "hp_get_nccl_id", "hp_shard"]
 
 
 def _check(status: int, ctx=None):
@@ -151,6 +157,59 @@ def bounds():
     hi = np.zeros(NDOF)
     _check(lib().hp_bounds(lo.ctypes.data, hi.ctypes.data))
     return lo, hi
+
+
+def shard_range(n: int, rank: int, world: int):
+    """[begin, end) of the poses rank `rank` of `world` scores (hp_shard_range)."""
+    b, e = C.c_int64(), C.c_int64()
+    _check(lib().hp_shard_range(n, rank, world, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+def nccl_available() -> bool:
+    v = C.c_int32()
+    _check(lib().hp_nccl_available(C.byref(v)))
+    return bool(v.value)
+
+
+def _nccl_lib_hint():
+    """Point HP_NCCL_LIB at the NCCL torch ships (the same library torch.distributed uses)."""
+    if os.environ.get("HP_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl  # noqa: F401
+
+        cand = os.path.join(os.path.dirname(nvidia.nccl.__file__), "lib", "libnccl.so.2")
+    except Exception:
+        return
+    if os.path.exists(cand):
+        os.environ["HP_NCCL_LIB"] = cand
+
+
+def nccl_unique_id() -> bytes:
+    _nccl_lib_hint()
+    buf = (C.c_uint8 * 128)()
+    _check(lib().hp_get_nccl_id(buf))
+    return bytes(buf)
+
+
+def broadcast_bytes(payload: bytes | None, rank: int, nbytes: int = 128, group=None) -> bytes:
+    """Broadcast `nbytes` from rank 0 over torch.distributed (any backend)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.zeros(nbytes, dtype=torch.uint8)
+    if rank == 0:
+        t.copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8))
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    dist.broadcast(t, src=0, group=group)
+    return bytes(t.cpu().numpy().tobytes())
+
+
+def exchange_nccl_id(rank: int, group=None) -> bytes:
+    """Rank 0 creates the NCCL unique id; torch.distributed broadcasts the 128 bytes."""
+    return broadcast_bytes(nccl_unique_id() if rank == 0 else None, rank, 128, group)
 
 
 def _dptr(t) -> int:
@@ -271,6 +330,15 @@ class Context:
         _check(self._L.hp_eval_sums(self._h, _dptr(poses), n, _dptr(sums), _dptr(costs),
                                     _stream(stream)), self._h)
         return sums, costs
+
+    def shard(self, rank: int, world: int, nccl_id: bytes | None = None, group=None):
+        """Particle-sharded mode (hp_shard): collective over the `world` ranks."""
+        _nccl_lib_hint()
+        if nccl_id is None:
+            nccl_id = exchange_nccl_id(rank, group)
+        buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        _check(self._L.hp_shard(self._h, buf, rank, world), self._h)
+        self.rank, self.world = rank, world
 
     def splits_for(self, n: int) -> int:
         return self._L.hp_splits_for(self._h, n)
