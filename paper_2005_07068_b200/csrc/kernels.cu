@@ -70,11 +70,46 @@ __global__ void k_depth_to_mask(const float* __restrict__ depth, uint8_t* __rest
 // and fp32 does not cancel (a camera-origin quadratic has |c|^2 ~ 1e6 mm^2 against
 // r^2 ~ 1e2).  Depth = t (d_z = 1).
 // ---------------------------------------------------------------------------------------
+// Pixel pairs use Blackwell's packed fp32 instructions (FFMA2 / FMUL2 / FADD2: two lanes
+// of fp32 per instruction, PTX .f32x2): the lane's pixels q = (0,1) and (2,3) are processed
+// as pairs, halving the issued FP instructions of the hot loop.  Scalars broadcast into a
+// pair fold into the instruction's .F32 operand modifier (no extra moves).
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ f2 bc(float v) { return pk(v, v); }
+__device__ __forceinline__ void unpk(f2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 struct Lane4 {
-  float dx;
-  float dy[kPxPerLane];
-  float inv_dd[kPxPerLane];
-  float zb[kPxPerLane];
+  float dx;                           // shared by the lane's pixels (one column)
+  f2 dy[kPxPerLane / 2];              // pairs of rows
+  f2 idd[kPxPerLane / 2];             // 1 / |d|^2 per pixel, paired
+  float zb[kPxPerLane];               // min depth so far
 };
 
 // Single-MUFU approximations (flush-to-zero: denormals never occur in these quantities).
@@ -88,7 +123,17 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-__device__ __forceinline__ float fast_sqrt(float x) { return x * rsqrt_approx(x); }  // NaN if x < 0
+// sqrt of both halves (NaN where negative) and 1/x of both halves
+__device__ __forceinline__ f2 sqrt2(f2 x) {
+  float a, b;
+  unpk(x, a, b);
+  return mul2(x, pk(rsqrt_approx(a), rsqrt_approx(b)));
+}
+__device__ __forceinline__ f2 rcp2(f2 x) {
+  float a, b;
+  unpk(x, a, b);
+  return pk(rcp_approx(a), rcp_approx(b));
+}
 
 // Branch-free min-depth update.  zb starts just above z_far, so z < zb also enforces
 // z <= z_far; a NaN z (no real root / axial range miss) never wins.
@@ -99,17 +144,26 @@ __device__ __forceinline__ void keep(float z, float& zb, float znear) {
   if (CHK) zb = (z >= znear) & (z < zb) ? z : zb;
   else zb = fminf(zb, z);
 }
+template <bool CHK>
+__device__ __forceinline__ void keep2(f2 z, float& zb0, float& zb1, float znear) {
+  float a, b;
+  unpk(z, a, b);
+  keep<CHK>(a, zb0, znear);
+  keep<CHK>(b, zb1, znear);
+}
 
 template <bool CHK>
 __device__ __forceinline__ void isect_sphere(const float* __restrict__ r, Lane4& L, float znear) {
   const float4 q = *reinterpret_cast<const float4*>(r);  // c, r^2
   const float bx = fmaf(L.dx, q.x, q.z);
 #pragma unroll
-  for (int j = 0; j < kPxPerLane; j++) {
-    const float tc = fmaf(L.dy[j], q.y, bx) * L.inv_dd[j];
-    const float ox = fmaf(tc, L.dx, -q.x), oy = fmaf(tc, L.dy[j], -q.y), oz = tc - q.z;
-    const float disc = q.w - fmaf(ox, ox, fmaf(oy, oy, oz * oz));
-    keep<CHK>(tc - fast_sqrt(disc * L.inv_dd[j]), L.zb[j], znear);
+  for (int j = 0; j < kPxPerLane / 2; j++) {
+    const f2 dy = L.dy[j], idd = L.idd[j];
+    const f2 tc = mul2(fma2(dy, bc(q.y), bc(bx)), idd);
+    const f2 ox = fma2(tc, bc(L.dx), bc(-q.x)), oy = fma2(tc, dy, bc(-q.y));
+    const f2 oz = add2(tc, bc(-q.z));
+    const f2 disc = sub2(bc(q.w), fma2(ox, ox, fma2(oy, oy, mul2(oz, oz))));
+    keep2<CHK>(sub2(tc, sqrt2(mul2(disc, idd))), L.zb[2 * j], L.zb[2 * j + 1], znear);
   }
 }
 
@@ -125,19 +179,21 @@ __device__ __forceinline__ void isect_ellipsoid(const float* __restrict__ r, Lan
               pz = fmaf(r2.z, L.dx, r3.x);
   const float bx = fmaf(L.dx, r0.x, r0.z);
 #pragma unroll
-  for (int j = 0; j < kPxPerLane; j++) {
-    const float dy = L.dy[j];
-    const float tc = fmaf(dy, r0.y, bx) * L.inv_dd[j];
-    const float lx = fmaf(r1.y, dy, px), ly = fmaf(r2.x, dy, py), lz = fmaf(r2.w, dy, pz);
-    const float ox = fmaf(tc, lx, -r3.y), oy = fmaf(tc, ly, -r3.z), oz = fmaf(tc, lz, -r3.w);
-    const float A = fmaf(lx, lx, fmaf(ly, ly, lz * lz));
-    const float B = fmaf(ox, lx, fmaf(oy, ly, oz * lz));
-    const float C = fmaf(ox, ox, fmaf(oy, oy, fmaf(oz, oz, -1.f)));
-    const float disc = fmaf(B, B, -A * C);
+  for (int j = 0; j < kPxPerLane / 2; j++) {
+    const f2 dy = L.dy[j];
+    const f2 tc = mul2(fma2(dy, bc(r0.y), bc(bx)), L.idd[j]);
+    const f2 lx = fma2(bc(r1.y), dy, bc(px)), ly = fma2(bc(r2.x), dy, bc(py)),
+             lz = fma2(bc(r2.w), dy, bc(pz));
+    const f2 ox = fma2(tc, lx, bc(-r3.y)), oy = fma2(tc, ly, bc(-r3.z)),
+             oz = fma2(tc, lz, bc(-r3.w));
+    const f2 A = fma2(lx, lx, fma2(ly, ly, mul2(lz, lz)));
+    const f2 B = fma2(ox, lx, fma2(oy, ly, mul2(oz, lz)));
+    const f2 C = fma2(ox, ox, fma2(oy, oy, fma2(oz, oz, bc(-1.f))));
+    const f2 disc = sub2(mul2(B, B), mul2(A, C));
     // A > 0: the smaller root; only the absolute error of s matters (z = t_c + s), so the
     // plain form is accurate to ~1e-6 mm here
-    const float s = (-B - fast_sqrt(disc)) * rcp_approx(A);
-    keep<CHK>(tc + s, L.zb[j], znear);
+    const f2 s = mul2(sub2(bc(0.f), add2(B, sqrt2(disc))), rcp2(A));
+    keep2<CHK>(add2(tc, s), L.zb[2 * j], L.zb[2 * j + 1], znear);
   }
 }
 
@@ -160,19 +216,25 @@ __device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L
   const float bx = fmaf(L.dx, r0.x, r0.z);
   const float rm = r4.x, k = r4.y, hl = r4.z;
 #pragma unroll
-  for (int j = 0; j < kPxPerLane; j++) {
-    const float dy = L.dy[j];
-    const float tc = fmaf(dy, r0.y, bx) * L.inv_dd[j];
-    const float lx = fmaf(r1.y, dy, px), ly = fmaf(r2.x, dy, py), lz = fmaf(r2.w, dy, pz);
-    const float ox = fmaf(tc, lx, -r3.y), oy = fmaf(tc, ly, -r3.z), oz = fmaf(tc, lz, -r3.w);
-    const float g = fmaf(k, oz, rm), kd = k * lz;
-    const float A = fmaf(lx, lx, fmaf(ly, ly, -kd * kd));
-    const float B = fmaf(ox, lx, fmaf(oy, ly, -kd * g));
-    const float C = fmaf(ox, ox, fmaf(oy, oy, -g * g));
-    const float disc = fmaf(B, B, -A * C);
-    const float s = (-B - fast_sqrt(disc)) * rcp_approx(A);  // NaN when disc < 0
-    const float z = fabsf(fmaf(s, lz, oz)) <= hl ? tc + s : __int_as_float(0x7fc00000);
-    keep<CHK>(z, L.zb[j], znear);
+  for (int j = 0; j < kPxPerLane / 2; j++) {
+    const f2 dy = L.dy[j];
+    const f2 tc = mul2(fma2(dy, bc(r0.y), bc(bx)), L.idd[j]);
+    const f2 lx = fma2(bc(r1.y), dy, bc(px)), ly = fma2(bc(r2.x), dy, bc(py)),
+             lz = fma2(bc(r2.w), dy, bc(pz));
+    const f2 ox = fma2(tc, lx, bc(-r3.y)), oy = fma2(tc, ly, bc(-r3.z)),
+             oz = fma2(tc, lz, bc(-r3.w));
+    const f2 g = fma2(bc(k), oz, bc(rm)), kd = mul2(bc(k), lz);
+    const f2 A = fma2(lx, lx, fma2(ly, ly, sub2(bc(0.f), mul2(kd, kd))));
+    const f2 B = fma2(ox, lx, fma2(oy, ly, sub2(bc(0.f), mul2(kd, g))));
+    const f2 C = fma2(ox, ox, fma2(oy, oy, sub2(bc(0.f), mul2(g, g))));
+    const f2 disc = sub2(mul2(B, B), mul2(A, C));
+    const f2 s = mul2(sub2(bc(0.f), add2(B, sqrt2(disc))), rcp2(A));  // NaN when disc < 0
+    float za0, za1, z0, z1;
+    unpk(fma2(s, lz, oz), za0, za1);
+    unpk(add2(tc, s), z0, z1);
+    const float nan = __int_as_float(0x7fc00000);
+    keep<CHK>(fabsf(za0) <= hl ? z0 : nan, L.zb[2 * j], znear);
+    keep<CHK>(fabsf(za1) <= hl ? z1 : nan, L.zb[2 * j + 1], znear);
   }
 }
 
@@ -238,11 +300,14 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
   Lane4 L;
   const int x = X0 + col;
   L.dx = s_dx[x];
+  const float ddx = fmaf(L.dx, L.dx, 1.f);
 #pragma unroll
-  for (int q = 0; q < kPxPerLane; q++) {
-    L.dy[q] = s_dy[Y0 + rowb + 2 * q];
-    L.inv_dd[q] = rcp_approx(fmaf(L.dx, L.dx, fmaf(L.dy[q], L.dy[q], 1.f)));
+  for (int q = 0; q < kPxPerLane; q += 2) {
+    const float dy0 = s_dy[Y0 + rowb + 2 * q], dy1 = s_dy[Y0 + rowb + 2 * q + 2];
+    L.dy[q / 2] = pk(dy0, dy1);
+    L.idd[q / 2] = pk(rcp_approx(fmaf(dy0, dy0, ddx)), rcp_approx(fmaf(dy1, dy1, ddx)));
     L.zb[q] = zinit;
+    L.zb[q + 1] = zinit;
   }
   if (fo.near_ok) {
     for (uint64_t m = mask & kSphereMask; m; m &= m - 1)
