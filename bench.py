@@ -65,6 +65,17 @@ def rank_swarm(rank, world):
     return np.ascontiguousarray(sw[rank * PER_RANK:(rank + 1) * PER_RANK], dtype=np.float32)
 
 
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the fused kernel, from the
+    committed ncu --set full capture (profiles/ncu_k_eval.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_k_eval.json")) as f:
+            d = json.load(f)
+        return d["dram_bytes_read_per_launch"] + d["dram_bytes_write_per_launch"]
+    except Exception:
+        return None
+
+
 def walg_per_hyp():
     with open(os.path.join(ROOT, "profiles", "walg.json")) as f:
         return json.load(f)["c4_640x480"]["flops_per_hyp"]
@@ -320,7 +331,7 @@ def run_ours(args):
                        "parallelism": f"particle-sharded x{world}, cost allgather",
                        "l2": "flushed between steps (256 MiB write, outside the events)"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": ncu_traffic(),
                          "kernel": "k_eval (fused FK+render+score+cost)",
                          "kernel_ms": kernel_s * 1e3,
                          "peak_note": f"FP32 FMA pipe: {sms} SMs x 128 lanes x 2 x "
