@@ -151,6 +151,18 @@ hp_status hp_eval_sums(hp_ctx* ctx, const float* poses_dev, int64_t n, uint64_t*
 hp_status hp_pso_fit(hp_ctx* ctx, const hp_pso_params* params, double* best_pose,
                      double* best_cost, double* trace, int32_t* gens_run, void* stream);
 
+/* Temporal tracking over a frame sequence (SPEC S:L568-576 warm
+ * start): frame f's observation (depth_seq / mask_seq [frames][H][W], host or device as
+ * on_device says) is fitted with hp_pso_fit, seed = params->seed + f; frame 0 uses the
+ * params' init box, frame f > 0 the box previous best pose +- track_radius[26] (host)
+ * intersected with Tables 1-2.  Outputs (host): poses_out [frames][26], costs_out
+ * [frames] and traces_out [frames][generations] (both may be NULL).  Synchronous.
+ * Errors: as hp_set_observation and hp_pso_fit. */
+hp_status hp_track(hp_ctx* ctx, const float* depth_seq, const uint8_t* mask_seq,
+                   int32_t frames, int32_t on_device, const hp_pso_params* params,
+                   const double* track_radius, double* poses_out, double* costs_out,
+                   double* traces_out, void* stream);
+
 /* Final swarm state of the last hp_pso_fit / hp_debug_pso_sphere (host, synchronous):
  * X, V, P [particles][D] and Pcost [particles]; any pointer may be NULL. */
 hp_status hp_pso_state(hp_ctx* ctx, double* X, double* V, double* P, double* Pcost);

@@ -872,6 +872,37 @@ hp_status hp_pso_fit(hp_ctx* ctx, const hp_pso_params* p, double* best_pose, dou
                  gens_run, (cudaStream_t)stream);
 }
 
+hp_status hp_track(hp_ctx* ctx, const float* depth_seq, const uint8_t* mask_seq,
+                   int32_t frames, int32_t on_device, const hp_pso_params* p,
+                   const double* track_radius, double* poses_out, double* costs_out,
+                   double* traces_out, void* stream) {
+  ARG(ctx && depth_seq && mask_seq && p && track_radius && poses_out,
+      "hp_track: NULL argument");
+  ARG(frames >= 0, "hp_track: frames < 0");
+  hp_status r = validate_pso(ctx, p);
+  if (r != HP_OK) return r;
+  const size_t npx = (size_t)ctx->cam.width * ctx->cam.height;
+  hp_pso_params q = *p;
+  double centre[26];
+  for (int32_t f = 0; f < frames; f++) {
+    r = hp_set_observation(ctx, depth_seq + f * npx, mask_seq + f * npx, on_device, stream);
+    if (r != HP_OK) return r;
+    q.seed = p->seed + (uint64_t)f;  // one independent Philox stream per frame
+    if (f > 0) {  // warm start: the previous frame's best pose +- track_radius
+      q.init_center = centre;
+      q.init_radius = track_radius;
+    }
+    double cost;
+    r = hp_pso_fit(ctx, &q, poses_out + 26 * (size_t)f, &cost,
+                   traces_out ? traces_out + (size_t)f * p->generations : nullptr, nullptr,
+                   stream);
+    if (r != HP_OK) return r;
+    if (costs_out) costs_out[f] = cost;
+    memcpy(centre, poses_out + 26 * (size_t)f, sizeof centre);
+  }
+  return HP_OK;
+}
+
 hp_status hp_debug_pso_sphere(hp_ctx* ctx, int32_t D, const double* lo, const double* hi,
                               const double* init_lo, const double* init_hi, int32_t mut_lo,
                               int32_t mut_hi, const double* centre, const hp_pso_params* p,

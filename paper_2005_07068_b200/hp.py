@@ -89,6 +89,8 @@ def lib() -> C.CDLL:
             "hp_debug_render": [_VP, _VP, _VP, _VP],
             "hp_debug_pso_sphere": [_VP, C.c_int32, _VP, _VP, _VP, _VP, C.c_int32, C.c_int32, _VP,
                                     C.POINTER(PsoParams), _VP, _VP, _VP, _VP, _VP],
+            "hp_track": [_VP, _VP, _VP, C.c_int32, C.c_int32, C.POINTER(PsoParams), _VP, _VP,
+                         _VP, _VP, _VP],
             "hp_shard_range": [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64),
                                C.POINTER(C.c_int64)],
             "hp_nccl_available": [C.POINTER(C.c_int32)],
@@ -118,7 +120,7 @@ def exported_symbols():
             "hp_eval_costs", "hp_eval_costs_host", "hp_eval_sums", "hp_pso_fit", "hp_pso_state",
             "hp_debug_fk", "hp_debug_render", "hp_debug_pso_sphere", "hp_last_launch_count",
             "hp_splits_for", "hp_last_error", "hp_destroy", "hp_shard_range",
-            "hp_nccl_available", "hp_get_nccl_id", "hp_shard"]
+            "hp_nccl_available", "hp_get_nccl_id", "hp_shard", "hp_track"]
 
 
 def _check(status: int, ctx=None):
@@ -373,6 +375,40 @@ class Context:
         _check(self._L.hp_pso_fit(self._h, C.byref(p), best.ctypes.data, C.byref(cost),
                                   trace.ctypes.data, C.byref(gr), _stream(stream)), self._h)
         return FitResult(best, cost.value, trace, gr.value)
+
+    def track(self, depth_seq, mask_seq, track_radius, seed: int = 0, particles: int = 64,
+              generations: int = 30, mutation_period: int = 3, init_center=None,
+              init_radius=None, stream=None):
+        """Temporal tracking (hp_track): per-frame fit warm-started at the previous best
+        pose +- track_radius.  depth_seq / mask_seq: [F][H][W] numpy (host) or CUDA
+        tensors.  Returns (poses [F][26], costs [F], traces [F][generations])."""
+        p = PsoParams()
+        _check(self._L.hp_default_pso(C.byref(p)))
+        p.seed, p.particles, p.generations, p.mutation_period = (seed, particles, generations,
+                                                                 mutation_period)
+        keep = []
+        if init_center is not None:
+            ic = np.ascontiguousarray(init_center, dtype=np.float64)
+            ir = np.ascontiguousarray(init_radius, dtype=np.float64)
+            keep += [ic, ir]
+            p.init_center = ic.ctypes.data_as(C.POINTER(C.c_double))
+            p.init_radius = ir.ctypes.data_as(C.POINTER(C.c_double))
+        tr = np.ascontiguousarray(track_radius, dtype=np.float64)
+        if isinstance(depth_seq, np.ndarray):
+            d = np.ascontiguousarray(depth_seq, dtype=np.float32)
+            m = np.ascontiguousarray(mask_seq, dtype=np.uint8)
+            F = d.shape[0]
+            dp, mp_, dev = d.ctypes.data, m.ctypes.data, 0
+        else:
+            F = depth_seq.shape[0]
+            dp, mp_, dev = _dptr(depth_seq), _dptr(mask_seq), 1
+        poses = np.zeros((F, NDOF))
+        costs = np.zeros(F)
+        traces = np.zeros((F, generations))
+        _check(self._L.hp_track(self._h, dp, mp_, F, dev, C.byref(p), tr.ctypes.data,
+                                poses.ctypes.data, costs.ctypes.data, traces.ctypes.data,
+                                _stream(stream)), self._h)
+        return poses, costs, traces
 
     def pso_state(self, particles: int, D: int = NDOF):
         X = np.zeros((particles, D))
