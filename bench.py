@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--fit-seeds", type=int, default=10)
     ap.add_argument("--no-fit", action="store_true")
+    ap.add_argument("--track-frames", type=int, default=100)
     ap.add_argument("--clock-ramp", type=float, default=1.0,
                     help="seconds of untimed load before the timed region (clock sampling)")
     return ap.parse_args()
@@ -308,6 +309,31 @@ def run_ours(args):
                "launches_per_fit": ctx.last_launch_count(),
                "paper_context": "0.8 s/frame on AMD HD5870M + i7-740QM, 64 x 30 (P:L197)"}
 
+    # ---- C5 tracking (next row f1): 100-frame synthetic motion at 640x480, warm start ----
+    track = None
+    if not args.no_fit and rank == 0:
+        seq = W.motion_sequence(frames=args.track_frames)
+        dseq = torch.empty((len(seq), HEIGHT, WIDTH), dtype=torch.float32, device=dev)
+        mseq = torch.empty((len(seq), HEIGHT, WIDTH), dtype=torch.uint8, device=dev)
+        for f, hf in enumerate(seq):
+            d, m = ctx.render_observation(hf)
+            dseq[f].copy_(d)
+            mseq[f].copy_(m)
+        radius = np.array([20.0] * 3 + [math.radians(10)] * 3 + [math.radians(25)] * 20)
+        r0 = np.array([50.0] * 3 + [math.radians(20)] * 3 + [math.pi] * 20)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        poses, tcosts, _ = ctx.track(dseq, mseq, radius, seed=1, particles=64, generations=40,
+                                     init_center=seq[0], init_radius=r0)
+        dt = time.perf_counter() - t0
+        err = np.abs(poses[:, :3] - seq[:, :3]).max(axis=1)
+        track = {"ms_per_frame": 1e3 * dt / len(seq), "frames": len(seq),
+                 "config": "C5: 640x480 synthetic motion (workloads.motion_sequence), 64 x 40 "
+                           "per frame, warm start at the previous best +- (20 mm, 10 deg, "
+                           "25 deg); includes the per-frame observation upload",
+                 "median_best_cost": float(np.median(tcosts)),
+                 "median_wrist_pos_err_mm": float(np.median(err))}
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.cpu_seconds, swarm)
@@ -345,6 +371,8 @@ def run_ours(args):
         }
         if fit:
             line["pso_fit"] = fit
+        if track:
+            line["tracking"] = track
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line))
