@@ -250,7 +250,7 @@ struct TileSums {
 // must start 16-byte aligned in global memory (an unaligned start faults on sm_100a).
 struct TileGrid {
   int x0, y0, tx, ntiles;
-  float inv_tx;
+  unsigned int magic;  // floor(2^32 / tx): t / tx = umulhi(t, magic) + {0, 1}
   __device__ __forceinline__ explicit TileGrid(int4 ub) {
     x0 = ub.x & ~3;
     y0 = ub.y;
@@ -258,13 +258,15 @@ struct TileGrid {
     tx = bw > 0 ? (bw + kTileW - 1) / kTileW : 0;
     const int ty = bh > 0 ? (bh + kTileH - 1) / kTileH : 0;
     ntiles = tx * ty;
-    inv_tx = 1.0f / (float)(tx > 0 ? tx : 1);
+    magic = tx > 1 ? 0xFFFFFFFFu / (unsigned)tx : 0u;
   }
   __device__ __forceinline__ void origin(int t, int& X0, int& Y0) const {
-    int qy = (int)((float)t * inv_tx);  // t / tx, corrected below
+    int qy = tx > 1 ? (int)__umulhi((unsigned)t, magic) : t;
     int qx = t - qy * tx;
-    if (qx < 0) { qy--; qx += tx; }
-    if (qx >= tx) { qy++; qx -= tx; }
+    if (qx >= tx) {  // the estimate is low by at most one
+      qy++;
+      qx -= tx;
+    }
     X0 = x0 + qx * kTileW;
     Y0 = y0 + qy * kTileH;
   }
@@ -280,12 +282,14 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
   const float znear = a.cam.znear, zfar = a.cam.zfar;
   const float zinit = __uint_as_float(__float_as_uint(zfar) + 1u);  // next float above z_far
   if (MODE == kModeCost && a.use_tma && lane == 0) {
-    fence_proxy_async();
+    // no proxy fence needed: the warp's reads of the previous tile in this buffer were
+    // consumed before the __syncwarp that ended it (WAR across proxies is ordered)
     mbar_expect_tx(bar, kTileW * kTileH * 4);
     tma_load_2d(obs_buf, a.use_tma == 2 ? a.tmap_g : tmap, X0, Y0, bar);
   }
-  // cull the 38 conservative boxes against the tile: two ballots -> 64-bit mask
-  uint64_t mask;
+  // cull the 38 conservative boxes against the tile: two ballots, split into 32-bit masks
+  // per kind (spheres = prims 0..19, cones + cylinder = 20..34, ellipsoids = 35..37)
+  unsigned int msph, mcone, mell;
   {
     const int4 b = fo.box[lane];
     const bool ov = b.x <= X0 + kTileW - 1 && b.z >= X0 && b.y <= Y0 + kTileH - 1 && b.w >= Y0;
@@ -294,8 +298,10 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
       const int4 c = fo.box[32 + lane];
       ov2 = c.x <= X0 + kTileW - 1 && c.z >= X0 && c.y <= Y0 + kTileH - 1 && c.w >= Y0;
     }
-    mask = (uint64_t)__ballot_sync(0xffffffffu, ov) |
-           ((uint64_t)__ballot_sync(0xffffffffu, ov2) << 32);
+    const unsigned int lo = __ballot_sync(0xffffffffu, ov), hi = __ballot_sync(0xffffffffu, ov2);
+    msph = lo & 0xFFFFFu;
+    mcone = (lo >> 20) | ((hi & 0x7u) << 12);
+    mell = hi >> 3;
   }
   Lane4 L;
   const int x = X0 + col;
@@ -310,19 +316,17 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
     L.zb[q + 1] = zinit;
   }
   if (fo.near_ok) {
-    for (uint64_t m = mask & kSphereMask; m; m &= m - 1)
-      isect_sphere<false>(fo.rec[__ffsll((long long)m) - 1], L, znear);
-    for (uint64_t m = mask & kConeMask; m; m &= m - 1)
-      isect_cone<false>(fo.rec[__ffsll((long long)m) - 1], L, znear);
-    for (uint64_t m = mask & kEllMask; m; m &= m - 1)
-      isect_ellipsoid<false>(fo.rec[__ffsll((long long)m) - 1], L, znear);
+    for (unsigned int m = msph; m; m &= m - 1) isect_sphere<false>(fo.rec[__ffs(m) - 1], L, znear);
+    for (unsigned int m = mcone; m; m &= m - 1)
+      isect_cone<false>(fo.rec[kCone0 + __ffs(m) - 1], L, znear);
+    for (unsigned int m = mell; m; m &= m - 1)
+      isect_ellipsoid<false>(fo.rec[kEll0 + __ffs(m) - 1], L, znear);
   } else {
-    for (uint64_t m = mask & kSphereMask; m; m &= m - 1)
-      isect_sphere<true>(fo.rec[__ffsll((long long)m) - 1], L, znear);
-    for (uint64_t m = mask & kConeMask; m; m &= m - 1)
-      isect_cone<true>(fo.rec[__ffsll((long long)m) - 1], L, znear);
-    for (uint64_t m = mask & kEllMask; m; m &= m - 1)
-      isect_ellipsoid<true>(fo.rec[__ffsll((long long)m) - 1], L, znear);
+    for (unsigned int m = msph; m; m &= m - 1) isect_sphere<true>(fo.rec[__ffs(m) - 1], L, znear);
+    for (unsigned int m = mcone; m; m &= m - 1)
+      isect_cone<true>(fo.rec[kCone0 + __ffs(m) - 1], L, znear);
+    for (unsigned int m = mell; m; m &= m - 1)
+      isect_ellipsoid<true>(fo.rec[kEll0 + __ffs(m) - 1], L, znear);
   }
 
   if (MODE == kModeDepth) {
@@ -348,6 +352,10 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
     const float d_m = a.cost.d_m, clampv = a.cost.clampv;
     const bool xin = x < a.cam.W;
     unsigned int num = 0;  // <= 4 px x 40 mm x 2^20 < 2^32
+    bool any = false;
+#pragma unroll
+    for (int q = 0; q < kPxPerLane; q++) any |= L.zb[q] <= zfar;
+    if (__any_sync(0xffffffffu, any))  // nothing rendered in this tile: nothing to score
 #pragma unroll
     for (int q = 0; q < kPxPerLane; q++) {
       const int y = Y0 + rowb + 2 * q;
