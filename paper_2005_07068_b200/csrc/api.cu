@@ -119,6 +119,7 @@ struct hp_ctx {
   int64_t gat_cap = 0;       // chunk capacity of the buffers
   int use_tma = 1;   // HP_NO_TMA=1 in the environment selects plain loads (A/B, debugging)
   int sync_debug = 0;  // HP_SYNC_DEBUG=1: synchronise after every launch
+  int use_pdl = 1;     // programmatic dependent launch between PSO generations (HP_NO_PDL=1)
   std::string err;
 };
 
@@ -321,6 +322,7 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   if (const char* e = getenv("HP_NO_TMA")) ctx->use_tma = atoi(e) ? 0 : 1;
   if (const char* e = getenv("HP_TMA_MODE")) ctx->use_tma = atoi(e);
   if (const char* e = getenv("HP_SYNC_DEBUG")) ctx->sync_debug = atoi(e);
+  if (const char* e = getenv("HP_NO_PDL")) ctx->use_pdl = atoi(e) ? 0 : 1;
   hp_status st = HP_OK;
 #define CKC(call)                                 \
   do {                                            \
@@ -736,6 +738,7 @@ static hp_status enqueue_fit(hp_ctx* ctx, const PsoDev& d, bool sphere, cudaStre
     a.pso_on = 1;
     a.pso = d;
     a.gcount = ctx->gcount;
+    a.pdl = ctx->use_pdl;
     double* Xb[2] = {ctx->X, ctx->X2};
     double* Vb[2] = {ctx->V, ctx->V2};
     for (int k = 0; k < d.K; k++) {

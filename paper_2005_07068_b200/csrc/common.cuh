@@ -102,6 +102,7 @@ struct EvalArgs {
   const double *x_in, *v_in;      // generation k-1 positions / velocities
   double *x_out, *v_out;          // generation k (evaluated)
   unsigned int* gcount;           // grid arrival counter (zero between launches)
+  int pdl;                        // launched with programmatic dependent launch
 };
 
 // --------------------------------------------------------------------------------------

@@ -18,6 +18,10 @@
 #include "fk.cuh"
 #include "pso.cuh"
 
+#ifndef HP_MINB_WARPS
+#define HP_MINB_WARPS 24  // resident warps per SM the register budget is sized for
+#endif
+
 namespace hp {
 
 // ---------------------------------------------------------------------------------------
@@ -409,7 +413,7 @@ __device__ __forceinline__ void finalize_cost(const EvalArgs& a, int p, const un
 // (S > 1 splits per particle keep every SM busy) and for the depth-image hooks.
 // ---------------------------------------------------------------------------------------
 template <int NW, typename PoseT, int MODE>
-__global__ void __launch_bounds__(NW * 32, 24 / NW)
+__global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     k_eval(const EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
   __shared__ FkScratch s_fk;
   __shared__ __align__(16) FkOut s_out;
@@ -419,6 +423,12 @@ __global__ void __launch_bounds__(NW * 32, 24 / NW)
   __shared__ int s_next;
   extern __shared__ float s_ray[];  // dx per column [W + pad], dy per row [H + pad]
 
+  if (a.pdl) {
+    // programmatic dependent launch (PSO generations): let the next generation's CTAs be
+    // scheduled now, then wait until the previous generation's results are visible
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   if (a.done && *a.done) return;  // PSO stop rule reached (grid-uniform)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.x / a.S, sidx = blockIdx.x % a.S;
@@ -523,7 +533,7 @@ __global__ void __launch_bounds__(NW * 32, 24 / NW)
 // accumulate in shared memory; the last warp to finish computes Eq. (4)-(5).
 // ---------------------------------------------------------------------------------------
 template <int NW, typename PoseT>
-__global__ void __launch_bounds__(NW * 32, 24 / NW)
+__global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     k_eval_persist(const EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
   __shared__ FkScratch s_fk;
   __shared__ __align__(16) FkOut s_out[2];
@@ -707,6 +717,18 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
       k_eval_persist<kEvalWarps, double><<<pgrid, block, dyn, st>>>(a, *map);
     else
       k_eval_persist<kEvalWarps, float><<<pgrid, block, dyn, st>>>(a, *map);
+  } else if (mode == kModeCost && a.pdl && pose_double) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_eval<kEvalWarps, double, kModeCost>, a, *map);
   } else if (mode == kModeCost) {
     if (pose_double)
       k_eval<kEvalWarps, double, kModeCost><<<grid, block, dyn, st>>>(a, *map);
