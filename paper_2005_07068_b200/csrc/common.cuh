@@ -18,6 +18,7 @@ constexpr int kRec = 24;   // floats per primitive record (96 B)
 constexpr int kPxPerLane = HP_PX;       // pixels per lane (one column, every other row)
 constexpr int kTileW = 16;              // warp tile: 16 x (2 * kPxPerLane) pixels
 constexpr int kTileH = 2 * kPxPerLane;
+constexpr int kMaxTiles = 512;          // producer tile list capacity per particle
 constexpr int kRayPad = 16;             // ray-table slack for tiles overhanging the image
                                         // (W + H + 2 kRayPad is a multiple of 4 when W, H are)
 

@@ -276,11 +276,27 @@ struct TileGrid {
   }
 };
 
+// Cull the 38 conservative boxes against the tile [X0, X0+16) x [Y0, Y0+8): two ballots,
+// split into 32-bit masks per kind (spheres = prims 0..19, cones + cylinder = 20..34,
+// ellipsoids = 35..37).  Warp-collective.
+__device__ __forceinline__ uint3 cull_tile(const FkOut& fo, int X0, int Y0) {
+  const int lane = threadIdx.x & 31;
+  const int4 b = fo.box[lane];
+  const bool ov = b.x <= X0 + kTileW - 1 && b.z >= X0 && b.y <= Y0 + kTileH - 1 && b.w >= Y0;
+  bool ov2 = false;
+  if (lane < kNprim - 32) {
+    const int4 c = fo.box[32 + lane];
+    ov2 = c.x <= X0 + kTileW - 1 && c.z >= X0 && c.y <= Y0 + kTileH - 1 && c.w >= Y0;
+  }
+  const unsigned int lo = __ballot_sync(0xffffffffu, ov), hi = __ballot_sync(0xffffffffu, ov2);
+  return make_uint3(lo & 0xFFFFFu, (lo >> 20) | ((hi & 0x7u) << 12), hi >> 3);
+}
+
 template <int MODE>
 __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tmap,
-                                        const FkOut& fo, int X0, int Y0, uint32_t* obs_buf,
-                                        uint64_t* bar, uint32_t& phase, const float* s_dx,
-                                        const float* s_dy, TileSums& acc) {
+                                        const FkOut& fo, int X0, int Y0, uint3 km,
+                                        uint32_t* obs_buf, uint64_t* bar, uint32_t& phase,
+                                        const float* s_dx, const float* s_dy, TileSums& acc) {
   const int lane = threadIdx.x & 31;
   const int col = lane & 15, rowb = lane >> 4;
   const float znear = a.cam.znear, zfar = a.cam.zfar;
@@ -291,22 +307,7 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
     mbar_expect_tx(bar, kTileW * kTileH * 4);
     tma_load_2d(obs_buf, a.use_tma == 2 ? a.tmap_g : tmap, X0, Y0, bar);
   }
-  // cull the 38 conservative boxes against the tile: two ballots, split into 32-bit masks
-  // per kind (spheres = prims 0..19, cones + cylinder = 20..34, ellipsoids = 35..37)
-  unsigned int msph, mcone, mell;
-  {
-    const int4 b = fo.box[lane];
-    const bool ov = b.x <= X0 + kTileW - 1 && b.z >= X0 && b.y <= Y0 + kTileH - 1 && b.w >= Y0;
-    bool ov2 = false;
-    if (lane < kNprim - 32) {
-      const int4 c = fo.box[32 + lane];
-      ov2 = c.x <= X0 + kTileW - 1 && c.z >= X0 && c.y <= Y0 + kTileH - 1 && c.w >= Y0;
-    }
-    const unsigned int lo = __ballot_sync(0xffffffffu, ov), hi = __ballot_sync(0xffffffffu, ov2);
-    msph = lo & 0xFFFFFu;
-    mcone = (lo >> 20) | ((hi & 0x7u) << 12);
-    mell = hi >> 3;
-  }
+  const unsigned int msph = km.x, mcone = km.y, mell = km.z;
   Lane4 L;
   const int x = X0 + col;
   L.dx = s_dx[x];
@@ -474,7 +475,10 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     if (lane == 0) jn = atomicAdd(&s_next, 1);  // next tile, fetched early
     int X0, Y0;
     g.origin(sidx + j * a.S, X0, Y0);
-    do_tile<MODE>(a, &tmap, s_out, X0, Y0, s_obs[warp], &s_bar[warp], phase, s_dx, s_dy, acc);
+    const uint3 km = cull_tile(s_out, X0, Y0);
+    if (km.x | km.y | km.z)  // no primitive box touches the tile: nothing to render or score
+      do_tile<MODE>(a, &tmap, s_out, X0, Y0, km, s_obs[warp], &s_bar[warp], phase, s_dx, s_dy,
+                    acc);
     j = __shfl_sync(0xffffffffu, jn, 0);
   }
 
@@ -541,7 +545,8 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   __shared__ __align__(8) uint64_t s_bar[NW];
   __shared__ __align__(8) uint64_t s_full[2], s_empty[2];
   __shared__ unsigned long long s_acc[2][4];
-  __shared__ int s_next[2], s_done[2], s_pid[2];
+  __shared__ int s_next[2], s_done[2], s_pid[2], s_ntl[2];
+  __shared__ uint4 s_tiles[2][kMaxTiles];  // (X0 | Y0 << 16, sphere, cone, ellipsoid masks)
   extern __shared__ float s_ray[];
 
   if (a.done && *a.done) return;
@@ -573,17 +578,29 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   auto consume = [&](int p, int b) {
     const FkOut& fo = s_out[b];
     const TileGrid g(fo.ubox);
+    const int nlist = s_ntl[b];  // >= 0: the producer's list of non-empty tiles + masks
+    const int nt = nlist >= 0 ? nlist : g.ntiles;
     TileSums acc;
     int t = 0;
     if (lane == 0) t = atomicAdd(&s_next[b], 1);
     t = __shfl_sync(0xffffffffu, t, 0);
-    while (t < g.ntiles) {
+    while (t < nt) {
       int tn = 0;
       if (lane == 0) tn = atomicAdd(&s_next[b], 1);
       int X0, Y0;
-      g.origin(t, X0, Y0);
-      do_tile<kModeCost>(a, &tmap, fo, X0, Y0, s_obs[warp], &s_bar[warp], phase, s_dx, s_dy,
-                         acc);
+      uint3 km;
+      if (nlist >= 0) {
+        const uint4 it = s_tiles[b][t];
+        X0 = (int)(it.x & 0xFFFFu);
+        Y0 = (int)(it.x >> 16);
+        km = make_uint3(it.y, it.z, it.w);
+      } else {
+        g.origin(t, X0, Y0);
+        km = cull_tile(fo, X0, Y0);
+      }
+      if (km.x | km.y | km.z)
+        do_tile<kModeCost>(a, &tmap, fo, X0, Y0, km, s_obs[warp], &s_bar[warp], phase, s_dx,
+                           s_dy, acc);
       t = __shfl_sync(0xffffffffu, tn, 0);
     }
     warp_reduce(acc);
@@ -619,6 +636,39 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
       if (p < a.n) {
         const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
         fk_warp<PoseT>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out[b]);
+        // the particle's non-empty tiles with their cull masks, row-major (saves the
+        // renderers the culling and the empty tiles; a box too large for the list falls
+        // back to culling on the fly)
+        const FkOut& fo = s_out[b];
+        const TileGrid g(fo.ubox);
+        int cnt = -1;
+        if (g.ntiles <= kMaxTiles) {
+          cnt = 0;
+          for (int base = 0; base < g.ntiles; base += 32) {  // one tile per lane
+            const int t = base + lane;
+            unsigned int m0 = 0, m1 = 0, m2 = 0;
+            int X0 = 0, Y0 = 0;
+            if (t < g.ntiles) {
+              g.origin(t, X0, Y0);
+#pragma unroll
+              for (int j = 0; j < kNprim; j++) {
+                const int4 bb = fo.box[j];
+                const unsigned int ov = bb.x <= X0 + kTileW - 1 && bb.z >= X0 &&
+                                        bb.y <= Y0 + kTileH - 1 && bb.w >= Y0;
+                if (j < kCone0) m0 |= ov << j;
+                else if (j < kEll0) m1 |= ov << (j - kCone0);
+                else m2 |= ov << (j - kEll0);
+              }
+            }
+            const bool ne = (m0 | m1 | m2) != 0;
+            const unsigned int bal = __ballot_sync(0xffffffffu, ne);
+            if (ne)
+              s_tiles[b][cnt + __popc(bal & ((1u << lane) - 1u))] =
+                  make_uint4((unsigned)X0 | ((unsigned)Y0 << 16), m0, m1, m2);
+            cnt += __popc(bal);
+          }
+        }
+        if (lane == 0) s_ntl[b] = cnt;
       }
       mbar_arrive(&s_full[b]);
       return p;
@@ -682,7 +732,29 @@ __global__ void k_fk_debug(const double* pose, const DimsD dims, const CamParams
 constexpr int kEvalWarps = HP_NW;
 int eval_warps_per_cta() { return kEvalWarps; }
 
+// Prefer the maximum shared-memory carveout (the default 64 KB split would cap the
+// persistent kernel, 37 KB of shared memory per CTA, at one CTA per SM).
+static void set_carveouts() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  const int pct = cudaSharedmemCarveoutMaxShared;
+  cudaFuncSetAttribute(k_eval_persist<kEvalWarps, float>,
+                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  cudaFuncSetAttribute(k_eval_persist<kEvalWarps, double>,
+                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  cudaFuncSetAttribute(k_eval<kEvalWarps, float, kModeCost>,
+                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  cudaFuncSetAttribute(k_eval<kEvalWarps, double, kModeCost>,
+                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  cudaFuncSetAttribute(k_eval<kEvalWarps, float, kModeDepth>,
+                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  cudaFuncSetAttribute(k_eval<kEvalWarps, double, kModeDepth>,
+                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 int persist_blocks_per_sm(const CamParams& cam) {
+  set_carveouts();
   int nb = 0;
   const size_t dyn = (size_t)((cam.W + cam.H + 2 * kRayPad + 3) & ~3) * sizeof(float);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_persist<kEvalWarps, float>,
