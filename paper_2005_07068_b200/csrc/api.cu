@@ -109,7 +109,11 @@ struct hp_ctx {
   CUtensorMap* tmap_g = nullptr;
   float* ray = nullptr;  // per-column / per-row ray directions (k_ray_table)
   unsigned int* pcount = nullptr;  // persistent-kernel counters (zero between launches)
-  int persist_grid = 0;            // CTAs of k_eval_persist (0 = never use it)
+  int persist_grid = 0;            // CTAs of the persistent kernels (0 = never use them)
+  int two_kernel = 1;              // k_fk_batch + k_render_persist (HP_PERSIST_PRODUCER=1: 0)
+  void* fk_g = nullptr;            // FkOut [max_n]
+  uint4* tiles_g = nullptr;        // [max_n][kMaxTiles]
+  int* ntl_g = nullptr;            // [max_n]
   int blocks_per_sm = 0;           // resident k_eval CTAs per SM
   // particle-sharded mode (hp_shard): rank r owns poses [r chunk, (r + 1) chunk)
   ncclComm_t comm = nullptr;
@@ -252,7 +256,7 @@ void hp_destroy(hp_ctx* ctx) {
                  ctx->poses32, ctx->costs32, ctx->scratch, ctx->X, ctx->V, ctx->P, ctx->Pc,
                  ctx->E, ctx->G, ctx->Gc, ctx->trace, ctx->bnd, ctx->centre, ctx->mark,
                  ctx->flags, ctx->dyn, ctx->tmap_g, ctx->ray, ctx->pcount, ctx->X2,
-                 ctx->V2, ctx->gcount};
+                 ctx->V2, ctx->gcount, ctx->fk_g, ctx->tiles_g, ctx->ntl_g};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_poses) cudaFreeHost(ctx->h_poses);
@@ -384,6 +388,10 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   // ray table, padded to a multiple of 4 floats for the float4 staging copy
   CKC(cudaMalloc(&ctx->ray, (size_t)((W + H + 2 * kRayPad + 3) & ~3) * sizeof(float)));
   CKC(launch_ray_table(ctx->camp, ctx->ray, ctx->st));
+  CKC(cudaMalloc(&ctx->fk_g, (size_t)max_particles * fk_record_bytes()));
+  CKC(cudaMalloc(&ctx->tiles_g, (size_t)max_particles * kMaxTiles * sizeof(uint4)));
+  CKC(cudaMalloc(&ctx->ntl_g, (size_t)max_particles * sizeof(int)));
+  if (const char* e = getenv("HP_PERSIST_PRODUCER")) ctx->two_kernel = atoi(e) ? 0 : 1;
   CKC(cudaMalloc(&ctx->pcount, 2 * sizeof(unsigned int)));
   CKC(cudaMemset(ctx->pcount, 0, 2 * sizeof(unsigned int)));
   ctx->blocks_per_sm = persist_blocks_per_sm(ctx->camp);
@@ -463,6 +471,10 @@ static EvalArgs base_args(hp_ctx* ctx) {
   a.ray = ctx->ray;
   a.pcount = ctx->pcount;
   a.persist_grid = ctx->persist_grid;
+  a.fk_g = ctx->fk_g;
+  a.tiles_g = ctx->tiles_g;
+  a.ntl_g = ctx->ntl_g;
+  a.two_kernel = ctx->two_kernel;
   return a;
 }
 
@@ -509,7 +521,8 @@ static hp_status eval_common(hp_ctx* ctx, const float* poses, int64_t n, float* 
   a.sums_out = reinterpret_cast<unsigned long long*>(sums);
   CK(launch_eval(a, false, kModeCost, &ctx->tmap, s));
   if (ctx->sync_debug) CK(cudaStreamSynchronize(s));
-  ctx->last_launches = 1;
+  // the batch path is two kernels (FK, then the persistent renderer)
+  ctx->last_launches = (a.S == 1 && a.persist_grid > 0 && a.two_kernel) ? 2 : 1;
   return HP_OK;
 }
 

@@ -104,6 +104,12 @@ struct EvalArgs {
   double *x_out, *v_out;          // generation k (evaluated)
   unsigned int* gcount;           // grid arrival counter (zero between launches)
   int pdl;                        // launched with programmatic dependent launch
+  // two-kernel batch path: k_fk_batch writes each particle's FK output and tile list here,
+  // k_render_persist bulk-copies them into shared memory
+  void* fk_g;                     // FkOut [n] (16-byte aligned records)
+  uint4* tiles_g;                 // [n][kMaxTiles] (X0 | Y0 << 16, sphere, cone, ell masks)
+  int* ntl_g;                     // [n] tile-list length (-1: box too large, cull on the fly)
+  int two_kernel;                 // 1: k_fk_batch + k_render_persist, 0: k_eval_persist
 };
 
 // --------------------------------------------------------------------------------------
@@ -161,6 +167,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+// 1-D bulk copy global -> shared (TMA unit), completing `bytes` on the mbarrier.
+// Addresses 16-byte aligned, size a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -179,6 +194,7 @@ cudaError_t launch_ray_table(const CamParams& cam, float* ray, cudaStream_t st);
 cudaError_t launch_depth_to_mask(const float* depth, uint8_t* mask, int npx, cudaStream_t st);
 int eval_warps_per_cta();
 int persist_blocks_per_sm(const CamParams& cam);
+size_t fk_record_bytes();
 
 // PSO (pso.cu)
 cudaError_t launch_pso_init(const PsoDev& p, cudaStream_t st);

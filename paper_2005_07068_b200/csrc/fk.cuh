@@ -19,7 +19,7 @@ struct FkScratch {
   int nearf[kNprim];        // primitive lies entirely beyond z_near
 };
 
-struct FkOut {
+struct __align__(16) FkOut {
   float rec[kNprim][kRec];
   int4 box[kNprim];  // x0, y0, x1, y1 inclusive; x0 > x1 = empty
   int4 ubox;
@@ -259,7 +259,7 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
 template <typename PoseT, int TEAM>
 __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam,
                         double kc_rest, FkScratch& s, FkOut& out) {
-  const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 1;
+  const int lane = threadIdx.x & 31, w = TEAM == 2 ? (threadIdx.x >> 5) & 1 : 0;
   if (w == 0) {
     if (lane < kNdof) {
       const double v = (double)pose[lane];

@@ -18,6 +18,12 @@
 #include "fk.cuh"
 #include "pso.cuh"
 
+#ifndef HP_NSLOT
+#define HP_NSLOT 2
+#endif
+#ifndef HP_PTEAM
+#define HP_PTEAM 1
+#endif
 #ifndef HP_MINB_WARPS
 #define HP_MINB_WARPS 24  // resident warps per SM the register budget is sized for
 #endif
@@ -539,14 +545,16 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
 template <int NW, typename PoseT>
 __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     k_eval_persist(const EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
+  constexpr int NS = HP_NSLOT;   // particle slots: the producers run up to NS - 1 ahead
+  constexpr int PT = HP_PTEAM;   // producer team: 1 or 2 warps
   __shared__ FkScratch s_fk;
-  __shared__ __align__(16) FkOut s_out[2];
+  __shared__ __align__(16) FkOut s_out[NS];
   __shared__ __align__(128) uint32_t s_obs[NW][kTileW * kTileH];
   __shared__ __align__(8) uint64_t s_bar[NW];
-  __shared__ __align__(8) uint64_t s_full[2], s_empty[2];
-  __shared__ unsigned long long s_acc[2][4];
-  __shared__ int s_next[2], s_done[2], s_pid[2], s_ntl[2];
-  __shared__ uint4 s_tiles[2][kMaxTiles];  // (X0 | Y0 << 16, sphere, cone, ellipsoid masks)
+  __shared__ __align__(8) uint64_t s_full[NS], s_empty[NS];
+  __shared__ unsigned long long s_acc[NS][4];
+  __shared__ int s_next[NS], s_done[NS], s_pid[NS], s_ntl[NS], s_fetch;
+  __shared__ uint4 s_tiles[NS][kMaxTiles];  // (X0 | Y0 << 16, sphere, cone, ellipsoid masks)
   extern __shared__ float s_ray[];
 
   if (a.done && *a.done) return;
@@ -555,8 +563,8 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   const float* s_dy = s_ray + a.cam.W + kRayPad;
   if (threadIdx.x == 0) {
     for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);
-    for (int b = 0; b < 2; b++) {
-      mbar_init(&s_full[b], 32);       // every producer lane arrives (releases its writes)
+    for (int b = 0; b < NS; b++) {
+      mbar_init(&s_full[b], PT * 32);  // every producer lane releases its writes
       mbar_init(&s_empty[b], NW * 32); // every lane arrives once its reads are done
       s_next[b] = 0;
       s_done[b] = 0;
@@ -626,66 +634,79 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     mbar_arrive(&s_empty[b]);
   };
 
-  if (warp == 0) {
-    // ---- producer: fetch + FK one particle ahead, then help render the current one ----
-    auto produce = [&](int b) {
-      int p = 0;
-      if (lane == 0) p = (int)atomicAdd(a.pcount, 1u);
-      p = __shfl_sync(0xffffffffu, p, 0);
-      if (lane == 0) s_pid[b] = p;
+  if (warp < PT) {
+    // ---- producer team (warps 0..PT-1): fetch + FK + tile list for particle
+    // j = i + 1 while the other warps render particle i, then help render particle i ----
+    auto produce = [&](int j) {
+      const int b = j % NS;
+      if (j >= NS) mbar_wait(&s_empty[b], ((j / NS) - 1) & 1);  // particle j - NS released
+      int p;
+      if (PT == 2) {
+        if (threadIdx.x == 0) s_fetch = (int)atomicAdd(a.pcount, 1u);
+        asm volatile("bar.sync 3, 64;" ::: "memory");
+        p = s_fetch;
+        asm volatile("bar.sync 3, 64;" ::: "memory");  // s_fetch may be overwritten next time
+      } else {
+        p = lane == 0 ? (int)atomicAdd(a.pcount, 1u) : 0;
+        p = __shfl_sync(0xffffffffu, p, 0);
+      }
+      if (threadIdx.x == 0) s_pid[b] = p;
       if (p < a.n) {
         const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
-        fk_warp<PoseT>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out[b]);
-        // the particle's non-empty tiles with their cull masks, row-major (saves the
-        // renderers the culling and the empty tiles; a box too large for the list falls
-        // back to culling on the fly)
-        const FkOut& fo = s_out[b];
-        const TileGrid g(fo.ubox);
-        int cnt = -1;
-        if (g.ntiles <= kMaxTiles) {
-          cnt = 0;
-          for (int base = 0; base < g.ntiles; base += 32) {  // one tile per lane
-            const int t = base + lane;
-            unsigned int m0 = 0, m1 = 0, m2 = 0;
-            int X0 = 0, Y0 = 0;
-            if (t < g.ntiles) {
-              g.origin(t, X0, Y0);
+        fk_team<PoseT, PT>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out[b]);
+        if (PT == 2) asm volatile("bar.sync 3, 64;" ::: "memory");  // warp 1's records done
+        // the particle's non-empty tiles with their cull masks, row-major, one tile per
+        // lane of warp 0 (a box too large for the list falls back to culling on the fly)
+        if (warp == 0) {
+          const FkOut& fo = s_out[b];
+          const TileGrid g(fo.ubox);
+          int cnt = -1;
+          if (g.ntiles <= kMaxTiles) {
+            cnt = 0;
+            for (int base = 0; base < g.ntiles; base += 32) {
+              const int t = base + lane;
+              unsigned int m0 = 0, m1 = 0, m2 = 0;
+              int X0 = 0, Y0 = 0;
+              if (t < g.ntiles) {
+                g.origin(t, X0, Y0);
 #pragma unroll
-              for (int j = 0; j < kNprim; j++) {
-                const int4 bb = fo.box[j];
-                const unsigned int ov = bb.x <= X0 + kTileW - 1 && bb.z >= X0 &&
-                                        bb.y <= Y0 + kTileH - 1 && bb.w >= Y0;
-                if (j < kCone0) m0 |= ov << j;
-                else if (j < kEll0) m1 |= ov << (j - kCone0);
-                else m2 |= ov << (j - kEll0);
+                for (int jj = 0; jj < kNprim; jj++) {
+                  const int4 bb = fo.box[jj];
+                  const unsigned int ov = bb.x <= X0 + kTileW - 1 && bb.z >= X0 &&
+                                          bb.y <= Y0 + kTileH - 1 && bb.w >= Y0;
+                  if (jj < kCone0) m0 |= ov << jj;
+                  else if (jj < kEll0) m1 |= ov << (jj - kCone0);
+                  else m2 |= ov << (jj - kEll0);
+                }
               }
+              const bool ne = (m0 | m1 | m2) != 0;
+              const unsigned int bal = __ballot_sync(0xffffffffu, ne);
+              if (ne)
+                s_tiles[b][cnt + __popc(bal & ((1u << lane) - 1u))] =
+                    make_uint4((unsigned)X0 | ((unsigned)Y0 << 16), m0, m1, m2);
+              cnt += __popc(bal);
             }
-            const bool ne = (m0 | m1 | m2) != 0;
-            const unsigned int bal = __ballot_sync(0xffffffffu, ne);
-            if (ne)
-              s_tiles[b][cnt + __popc(bal & ((1u << lane) - 1u))] =
-                  make_uint4((unsigned)X0 | ((unsigned)Y0 << 16), m0, m1, m2);
-            cnt += __popc(bal);
           }
+          if (lane == 0) s_ntl[b] = cnt;
         }
-        if (lane == 0) s_ntl[b] = cnt;
       }
+      __syncwarp();
       mbar_arrive(&s_full[b]);
       return p;
     };
     int pcur = produce(0);
     for (int i = 0; pcur < a.n; i++) {
-      const int b = i & 1;
-      if (i >= 1) mbar_wait(&s_empty[b ^ 1], ((i - 1) >> 1) & 1);  // particle i-1 released
-      const int pnext = produce(b ^ 1);
-      consume(pcur, b);
+      const int pnext = produce(i + 1);
+      // wait until particle i's slot is published (both producer warps contribute)
+      mbar_wait(&s_full[i % NS], (i / NS) & 1);
+      consume(pcur, i % NS);
       pcur = pnext;
     }
   } else {
-    // ---- consumers ----
+    // ---- renderers ----
     for (int i = 0;; i++) {
-      const int b = i & 1;
-      mbar_wait(&s_full[b], (i >> 1) & 1);
+      const int b = i % NS;
+      mbar_wait(&s_full[b], (i / NS) & 1);
       const int p = s_pid[b];
       if (p >= a.n) break;
       consume(p, b);
@@ -724,6 +745,182 @@ __global__ void k_fk_debug(const double* pose, const DimsD dims, const CamParams
 }
 
 // ---------------------------------------------------------------------------------------
+// Two-kernel batch path for large swarms.
+//   k_fk_batch      : one warp per particle — FK (fp64) and the particle's non-empty tile
+//                     list with cull masks, written to global memory (L2-resident).
+//   k_render_persist: persistent CTAs, ALL warps render.  Per particle one thread pulls the
+//                     FK record and tile list into shared memory with 1-D TMA bulk copies
+//                     (double-buffered: particle i + 2 is fetched as soon as particle i is
+//                     finished, while i + 1 renders), so no warp ever waits on FK latency.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out) {
+  const int lane = threadIdx.x & 31;
+  const TileGrid g(fo.ubox);
+  if (g.ntiles > kMaxTiles) return -1;
+  int cnt = 0;
+  for (int base = 0; base < g.ntiles; base += 32) {  // one tile per lane
+    const int t = base + lane;
+    unsigned int m0 = 0, m1 = 0, m2 = 0;
+    int X0 = 0, Y0 = 0;
+    if (t < g.ntiles) {
+      g.origin(t, X0, Y0);
+#pragma unroll
+      for (int jj = 0; jj < kNprim; jj++) {
+        const int4 bb = fo.box[jj];
+        const unsigned int ov = bb.x <= X0 + kTileW - 1 && bb.z >= X0 &&
+                                bb.y <= Y0 + kTileH - 1 && bb.w >= Y0;
+        if (jj < kCone0) m0 |= ov << jj;
+        else if (jj < kEll0) m1 |= ov << (jj - kCone0);
+        else m2 |= ov << (jj - kEll0);
+      }
+    }
+    const bool ne = (m0 | m1 | m2) != 0;
+    const unsigned int bal = __ballot_sync(0xffffffffu, ne);
+    if (ne)
+      out[cnt + __popc(bal & ((1u << lane) - 1u))] =
+          make_uint4((unsigned)X0 | ((unsigned)Y0 << 16), m0, m1, m2);
+    cnt += __popc(bal);
+  }
+  return cnt;
+}
+
+constexpr int kFkWarps = 4;
+template <typename PoseT>
+__global__ void __launch_bounds__(kFkWarps * 32) k_fk_batch(const EvalArgs a) {
+  __shared__ FkScratch s_fk[kFkWarps];
+  __shared__ FkOut s_out[kFkWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = blockIdx.x * kFkWarps + warp;
+  if (p >= a.n) return;  // warp-uniform; no block-wide barrier below
+  const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
+  fk_warp<PoseT>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk[warp], s_out[warp]);
+  const int cnt = build_tile_list(s_out[warp], a.tiles_g + (size_t)p * kMaxTiles);
+  const float4* src = reinterpret_cast<const float4*>(&s_out[warp]);
+  float4* dst = reinterpret_cast<float4*>(static_cast<FkOut*>(a.fk_g) + p);
+  for (int i = lane; i < (int)(sizeof(FkOut) / 16); i += 32) dst[i] = src[i];
+  if (lane == 0) a.ntl_g[p] = cnt;
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
+    k_render_persist(const EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
+  __shared__ __align__(16) FkOut s_out[2];
+  __shared__ __align__(16) uint4 s_tiles[2][kMaxTiles];
+  __shared__ __align__(128) uint32_t s_obs[NW][kTileW * kTileH];
+  __shared__ __align__(8) uint64_t s_bar[NW];
+  __shared__ __align__(8) uint64_t s_full[2];
+  __shared__ unsigned long long s_acc[2][4];
+  __shared__ int s_next[2], s_done[2], s_pid[2], s_ntl[2];
+  extern __shared__ float s_ray[];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* s_dx = s_ray;
+  const float* s_dy = s_ray + a.cam.W + kRayPad;
+  // one thread: take the next particle and pull its FK record + tile list into slot b
+  auto issue = [&](int b) {
+    const int p = (int)atomicAdd(a.pcount, 1u);
+    s_pid[b] = p;
+    if (p < a.n) {
+      const int ntl = __ldcg(a.ntl_g + p);
+      s_ntl[b] = ntl;
+      const uint32_t lb = ntl > 0 ? (uint32_t)ntl * 16u : 0u;
+      mbar_expect_tx(&s_full[b], (uint32_t)sizeof(FkOut) + lb);
+      bulk_g2s(&s_out[b], static_cast<const FkOut*>(a.fk_g) + p, (uint32_t)sizeof(FkOut),
+               &s_full[b]);
+      if (lb) bulk_g2s(s_tiles[b], a.tiles_g + (size_t)p * kMaxTiles, lb, &s_full[b]);
+    } else {
+      mbar_arrive(&s_full[b]);  // terminator: complete the phase without data
+    }
+  };
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&s_full[b], 1);
+      s_next[b] = 0;
+      s_done[b] = 0;
+      for (int k = 0; k < 4; k++) s_acc[b][k] = 0;
+    }
+    fence_mbar_init();
+    if (a.use_tma == 1) prefetch_tmap(&tmap);
+    issue(0);
+    issue(1);
+  }
+  {
+    const int n4 = (a.cam.W + a.cam.H + 2 * kRayPad + 3) / 4;
+    for (int i = threadIdx.x; i < n4; i += NW * 32)
+      reinterpret_cast<float4*>(s_ray)[i] = __ldg(reinterpret_cast<const float4*>(a.ray) + i);
+  }
+  __syncthreads();
+
+  uint32_t phase = 0;
+  for (int i = 0;; i++) {
+    const int b = i & 1;
+    mbar_wait(&s_full[b], (i >> 1) & 1);
+    const int p = s_pid[b];
+    if (p >= a.n) break;
+    const FkOut& fo = s_out[b];
+    const int nlist = s_ntl[b];
+    const TileGrid g(fo.ubox);
+    const int nt = nlist >= 0 ? nlist : g.ntiles;
+    TileSums acc;
+    int t = 0;
+    if (lane == 0) t = atomicAdd(&s_next[b], 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    while (t < nt) {
+      int tn = 0;
+      if (lane == 0) tn = atomicAdd(&s_next[b], 1);
+      int X0, Y0;
+      uint3 km;
+      if (nlist >= 0) {
+        const uint4 it = s_tiles[b][t];
+        X0 = (int)(it.x & 0xFFFFu);
+        Y0 = (int)(it.x >> 16);
+        km = make_uint3(it.y, it.z, it.w);
+      } else {
+        g.origin(t, X0, Y0);
+        km = cull_tile(fo, X0, Y0);
+      }
+      if (km.x | km.y | km.z)
+        do_tile<kModeCost>(a, &tmap, fo, X0, Y0, km, s_obs[warp], &s_bar[warp], phase, s_dx,
+                           s_dy, acc);
+      t = __shfl_sync(0xffffffffu, tn, 0);
+    }
+    warp_reduce(acc);
+    if (lane == 0) {
+      if (acc.rm) atomicAdd(&s_acc[b][0], (unsigned long long)acc.rm);
+      if (acc.and_) atomicAdd(&s_acc[b][1], (unsigned long long)acc.and_);
+      if (acc.num) atomicAdd(&s_acc[b][2], acc.num);
+      if (acc.both) atomicAdd(&s_acc[b][3], (unsigned long long)acc.both);
+      __threadfence_block();
+      if (atomicAdd(&s_done[b], 1) == NW - 1) {  // last warp for this particle
+        __threadfence_block();
+        unsigned long long v[4];
+        for (int k = 0; k < 4; k++) {
+          v[k] = s_acc[b][k];
+          s_acc[b][k] = 0;
+        }
+        finalize_cost(a, p, v, fo.kc);
+        s_next[b] = 0;
+        s_done[b] = 0;
+        fence_proxy_async();  // every warp's generic reads of slot b precede the refill
+        issue(b);             // particle i + 2 into the freed slot
+      }
+    }
+    __syncwarp();
+  }
+  // the last CTA to leave resets the particle counter for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(a.pcount + 1, 1u) == gridDim.x - 1) {
+      a.pcount[0] = 0;
+      a.pcount[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // Launchers
 // ---------------------------------------------------------------------------------------
 #ifndef HP_NW
@@ -741,6 +938,8 @@ static void set_carveouts() {
   const int pct = cudaSharedmemCarveoutMaxShared;
   cudaFuncSetAttribute(k_eval_persist<kEvalWarps, float>,
                        cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  cudaFuncSetAttribute(k_render_persist<kEvalWarps>,
+                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
   cudaFuncSetAttribute(k_eval_persist<kEvalWarps, double>,
                        cudaFuncAttributePreferredSharedMemoryCarveout, pct);
   cudaFuncSetAttribute(k_eval<kEvalWarps, float, kModeCost>,
@@ -753,11 +952,13 @@ static void set_carveouts() {
                        cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
+size_t fk_record_bytes() { return sizeof(FkOut); }
+
 int persist_blocks_per_sm(const CamParams& cam) {
   set_carveouts();
   int nb = 0;
   const size_t dyn = (size_t)((cam.W + cam.H + 2 * kRayPad + 3) & ~3) * sizeof(float);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval_persist<kEvalWarps, float>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_render_persist<kEvalWarps>,
                                                     kEvalWarps * 32, dyn) != cudaSuccess)
     return 0;
   return nb;
@@ -783,7 +984,15 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
   if (blocks == 0) return cudaSuccess;
   const dim3 grid((unsigned)blocks), block(kEvalWarps * 32);
   const size_t dyn = (size_t)((a.cam.W + a.cam.H + 2 * kRayPad + 3) & ~3) * sizeof(float);
-  if (mode == kModeCost && a.S == 1 && a.persist_grid > 0) {
+  if (mode == kModeCost && a.S == 1 && a.persist_grid > 0 && a.two_kernel) {
+    const dim3 fgrid((unsigned)((a.n + kFkWarps - 1) / kFkWarps));
+    if (pose_double) k_fk_batch<double><<<fgrid, kFkWarps * 32, 0, st>>>(a);
+    else k_fk_batch<float><<<fgrid, kFkWarps * 32, 0, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const dim3 pgrid((unsigned)(a.persist_grid < a.n ? a.persist_grid : a.n));
+    k_render_persist<kEvalWarps><<<pgrid, block, dyn, st>>>(a, *map);
+  } else if (mode == kModeCost && a.S == 1 && a.persist_grid > 0) {
     const dim3 pgrid((unsigned)(a.persist_grid < a.n ? a.persist_grid : a.n));
     if (pose_double)
       k_eval_persist<kEvalWarps, double><<<pgrid, block, dyn, st>>>(a, *map);
