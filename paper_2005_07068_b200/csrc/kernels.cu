@@ -784,18 +784,28 @@ __device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out) {
   return cnt;
 }
 
-constexpr int kFkWarps = 4;
+#ifndef HP_FK_TEAM
+#define HP_FK_TEAM 1
+#endif
+// HP_FK_TEAM = 1: 4 particles per CTA, one warp each; 2: one particle per 2-warp CTA (the
+// record build runs on both warps, halving the latency of the longest FK phase)
+constexpr int kFkTeam = HP_FK_TEAM;
+constexpr int kFkWarps = kFkTeam == 2 ? 2 : 4;
+constexpr int kFkPerCta = kFkTeam == 2 ? 1 : 4;
 template <typename PoseT>
-__global__ void __launch_bounds__(kFkWarps * 32) k_fk_batch(const EvalArgs a) {
-  __shared__ FkScratch s_fk[kFkWarps];
-  __shared__ FkOut s_out[kFkWarps];
+__global__ void __launch_bounds__(kFkWarps * 32, kFkTeam == 2 ? 16 : 8)
+    k_fk_batch(const EvalArgs a) {
+  __shared__ FkScratch s_fk[kFkPerCta];
+  __shared__ FkOut s_out[kFkPerCta];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int p = blockIdx.x * kFkWarps + warp;
-  if (p >= a.n) return;  // warp-uniform; no block-wide barrier below
+  const int slot = kFkTeam == 2 ? 0 : warp;
+  const int p = blockIdx.x * kFkPerCta + slot;
+  if (p >= a.n) return;  // uniform per team; only team-local barriers below
   const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
-  fk_warp<PoseT>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk[warp], s_out[warp]);
-  const int cnt = build_tile_list(s_out[warp], a.tiles_g + (size_t)p * kMaxTiles);
-  const float4* src = reinterpret_cast<const float4*>(&s_out[warp]);
+  fk_team<PoseT, kFkTeam>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk[slot], s_out[slot]);
+  if (kFkTeam == 2 && warp == 1) return;  // warp 0 finishes (fk_team synced the team)
+  const int cnt = build_tile_list(s_out[slot], a.tiles_g + (size_t)p * kMaxTiles);
+  const float4* src = reinterpret_cast<const float4*>(&s_out[slot]);
   float4* dst = reinterpret_cast<float4*>(static_cast<FkOut*>(a.fk_g) + p);
   for (int i = lane; i < (int)(sizeof(FkOut) / 16); i += 32) dst[i] = src[i];
   if (lane == 0) a.ntl_g[p] = cnt;
@@ -985,7 +995,7 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
   const dim3 grid((unsigned)blocks), block(kEvalWarps * 32);
   const size_t dyn = (size_t)((a.cam.W + a.cam.H + 2 * kRayPad + 3) & ~3) * sizeof(float);
   if (mode == kModeCost && a.S == 1 && a.persist_grid > 0 && a.two_kernel) {
-    const dim3 fgrid((unsigned)((a.n + kFkWarps - 1) / kFkWarps));
+    const dim3 fgrid((unsigned)((a.n + kFkPerCta - 1) / kFkPerCta));
     if (pose_double) k_fk_batch<double><<<fgrid, kFkWarps * 32, 0, st>>>(a);
     else k_fk_batch<float><<<fgrid, kFkWarps * 32, 0, st>>>(a);
     cudaError_t e = cudaGetLastError();
