@@ -167,6 +167,23 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+// Whole-warp call (uniform control flow, warp-uniform operands): one elected lane arms
+// the mbarrier with `bytes` and issues the 2-D TMA tile load.  Keeping the issue in
+// uniform control flow spares the compiler its lane-election loop around UTMALDG.
+__device__ __forceinline__ void tma_load_2d_elect(void* dst, const CUtensorMap* map, int x,
+                                                  int y, uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "elect.sync _|p, 0xffffffff;\n"
+      "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%4], %5;\n"
+      "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];\n"
+      "}\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "r"(bytes)
+      : "memory");
+}
+
 // 1-D bulk copy global -> shared (TMA unit), completing `bytes` on the mbarrier.
 // Addresses 16-byte aligned, size a multiple of 16.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,

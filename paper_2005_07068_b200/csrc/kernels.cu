@@ -307,11 +307,11 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
   const int col = lane & 15, rowb = lane >> 4;
   const float znear = a.cam.znear, zfar = a.cam.zfar;
   const float zinit = __uint_as_float(__float_as_uint(zfar) + 1u);  // next float above z_far
-  if (MODE == kModeCost && a.use_tma && lane == 0) {
+  if (MODE == kModeCost && a.use_tma) {
     // no proxy fence needed: the warp's reads of the previous tile in this buffer were
     // consumed before the __syncwarp that ended it (WAR across proxies is ordered)
-    mbar_expect_tx(bar, kTileW * kTileH * 4);
-    tma_load_2d(obs_buf, a.use_tma == 2 ? a.tmap_g : tmap, X0, Y0, bar);
+    tma_load_2d_elect(obs_buf, a.use_tma == 2 ? a.tmap_g : tmap, X0, Y0, bar,
+                      kTileW * kTileH * 4);
   }
   const unsigned int msph = km.x, mcone = km.y, mell = km.z;
   Lane4 L;
