@@ -209,6 +209,17 @@ hp_status hp_shard(hp_ctx* ctx, const uint8_t* id, int32_t rank, int32_t world);
 
 /* Number of kernel launches the last hp_eval_costs / hp_pso_fit enqueued (bench). */
 int64_t hp_last_launch_count(const hp_ctx* ctx);
+/* Per-launch device timing of the evaluation (bench.py's roofline leg).
+   hp_set_timing(ctx, 1) makes every later hp_eval_costs / hp_eval_costs_host / hp_eval_sums
+   record three CUDA events on the stream the kernels run on: before the first launch,
+   between the two launches of the batch path (k_fk_batch | k_render_persist), after the
+   last. hp_last_kernel_ms waits for the last event and returns ms[0] = first launch
+   (k_fk_batch; 0 on single-launch paths) and ms[1] = the renderer / fused kernel.
+   HP_ERR_STATE if no timed evaluation was enqueued since timing was switched on.
+   Timing adds two event records per call; leave it off outside measurement. */
+hp_status hp_set_timing(hp_ctx* ctx, int32_t on);
+hp_status hp_last_kernel_ms(hp_ctx* ctx, float ms[2]);
+
 /* Split factor S (CTAs per particle) used for n poses. */
 int32_t hp_splits_for(const hp_ctx* ctx, int64_t n);
 

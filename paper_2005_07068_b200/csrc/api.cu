@@ -124,6 +124,9 @@ struct hp_ctx {
   int use_tma = 1;   // HP_NO_TMA=1 in the environment selects plain loads (A/B, debugging)
   int sync_debug = 0;  // HP_SYNC_DEBUG=1: synchronise after every launch
   int use_pdl = 1;     // programmatic dependent launch between PSO generations (HP_NO_PDL=1)
+  cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};  // hp_set_timing: per-launch events
+  int timing = 0;
+  int timed = 0;  // the last hp_eval_costs / hp_eval_sums recorded tev
   std::string err;
 };
 
@@ -234,6 +237,29 @@ const char* hp_last_error(const hp_ctx* ctx) { return ctx ? ctx->err.c_str() : g
 
 int64_t hp_last_launch_count(const hp_ctx* ctx) { return ctx ? ctx->last_launches : -1; }
 
+hp_status hp_set_timing(hp_ctx* ctx, int32_t on) {
+  ARG(ctx, "hp_set_timing: NULL context");
+  cudaSetDevice(ctx->device);
+  if (on && !ctx->tev[0])
+    for (auto& e : ctx->tev) CK(cudaEventCreate(&e));
+  ctx->timing = on ? 1 : 0;
+  ctx->timed = 0;
+  return HP_OK;
+}
+
+hp_status hp_last_kernel_ms(hp_ctx* ctx, float ms[2]) {
+  ARG(ctx && ms, "hp_last_kernel_ms: NULL argument");
+  if (!ctx->timed) {
+    ctx->err = "hp_last_kernel_ms: no timed evaluation (hp_set_timing(ctx, 1) first)";
+    return HP_ERR_STATE;
+  }
+  cudaSetDevice(ctx->device);
+  CK(cudaEventSynchronize(ctx->tev[2]));
+  CK(cudaEventElapsedTime(&ms[0], ctx->tev[0], ctx->tev[1]));
+  CK(cudaEventElapsedTime(&ms[1], ctx->tev[1], ctx->tev[2]));
+  return HP_OK;
+}
+
 int32_t hp_splits_for(const hp_ctx* ctx, int64_t n) {
   if (!ctx || n <= 0) return 1;
   // as many CTAs per pose as fit in ONE wave of resident CTAs (a second partial wave
@@ -263,6 +289,8 @@ void hp_destroy(hp_ctx* ctx) {
   if (ctx->h_costs) cudaFreeHost(ctx->h_costs);
   if (ctx->h_out) cudaFreeHost(ctx->h_out);
   if (ctx->ev) cudaEventDestroy(ctx->ev);
+  for (auto e : ctx->tev)
+    if (e) cudaEventDestroy(e);
   if (ctx->st) cudaStreamDestroy(ctx->st);
   delete ctx;
 }
@@ -519,7 +547,8 @@ static hp_status eval_common(hp_ctx* ctx, const float* poses, int64_t n, float* 
   a.costs32 = costs32;
   a.costs64 = costs64;
   a.sums_out = reinterpret_cast<unsigned long long*>(sums);
-  CK(launch_eval(a, false, kModeCost, &ctx->tmap, s));
+  CK(launch_eval(a, false, kModeCost, &ctx->tmap, s, ctx->timing ? ctx->tev : nullptr));
+  ctx->timed = ctx->timing;
   if (ctx->sync_debug) CK(cudaStreamSynchronize(s));
   // the batch path is two kernels (FK, then the persistent renderer)
   ctx->last_launches = (a.S == 1 && a.persist_grid > 0 && a.two_kernel) ? 2 : 1;

@@ -202,8 +202,10 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 // --------------------------------------------------------------------------------------
 cudaError_t launch_pack_obs(const float* depth, const uint8_t* mask, uint32_t* obs, int W,
                             int H, int pitch_words, unsigned long long* S_o, cudaStream_t st);
+// tev (optional, 3 events): recorded before the first launch, between the two launches of
+// the batch path, and after the last (hp_set_timing); null when timing is off
 cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUtensorMap* map,
-                        cudaStream_t st);
+                        cudaStream_t st, cudaEvent_t* tev = nullptr);
 cudaError_t launch_fk_debug(const double* pose_dev, const DimsD& dims, const CamParams& cam,
                             float* rec, int* boxes, double* joints, double* kc,
                             cudaStream_t st);

@@ -989,19 +989,27 @@ cudaError_t launch_depth_to_mask(const float* depth, uint8_t* mask, int npx, cud
 }
 
 cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUtensorMap* map,
-                        cudaStream_t st) {
+                        cudaStream_t st, cudaEvent_t* tev) {
   const long long blocks = (long long)a.n * a.S;
   if (blocks == 0) return cudaSuccess;
+  const bool two = mode == kModeCost && a.S == 1 && a.persist_grid > 0 && a.two_kernel;
+  if (tev) {
+    cudaEventRecord(tev[0], st);
+    if (!two) cudaEventRecord(tev[1], st);  // single-launch paths: empty first interval
+  }
   const dim3 grid((unsigned)blocks), block(kEvalWarps * 32);
   const size_t dyn = (size_t)((a.cam.W + a.cam.H + 2 * kRayPad + 3) & ~3) * sizeof(float);
-  if (mode == kModeCost && a.S == 1 && a.persist_grid > 0 && a.two_kernel) {
+  if (two) {
     const dim3 fgrid((unsigned)((a.n + kFkPerCta - 1) / kFkPerCta));
     if (pose_double) k_fk_batch<double><<<fgrid, kFkWarps * 32, 0, st>>>(a);
     else k_fk_batch<float><<<fgrid, kFkWarps * 32, 0, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (tev) cudaEventRecord(tev[1], st);
     const dim3 pgrid((unsigned)(a.persist_grid < a.n ? a.persist_grid : a.n));
     k_render_persist<kEvalWarps><<<pgrid, block, dyn, st>>>(a, *map);
+    if (tev) cudaEventRecord(tev[2], st);
+    return cudaGetLastError();
   } else if (mode == kModeCost && a.S == 1 && a.persist_grid > 0) {
     const dim3 pgrid((unsigned)(a.persist_grid < a.n ? a.persist_grid : a.n));
     if (pose_double)
@@ -1019,7 +1027,9 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_eval<kEvalWarps, double, kModeCost>, a, *map);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_eval<kEvalWarps, double, kModeCost>, a, *map);
+    if (tev) cudaEventRecord(tev[2], st);
+    return e;
   } else if (mode == kModeCost) {
     if (pose_double)
       k_eval<kEvalWarps, double, kModeCost><<<grid, block, dyn, st>>>(a, *map);
@@ -1031,6 +1041,7 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     else
       k_eval<kEvalWarps, float, kModeDepth><<<grid, block, dyn, st>>>(a, *map);
   }
+  if (tev) cudaEventRecord(tev[2], st);
   return cudaGetLastError();
 }
 

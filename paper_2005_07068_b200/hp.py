@@ -96,6 +96,8 @@ def lib() -> C.CDLL:
             "hp_nccl_available": [C.POINTER(C.c_int32)],
             "hp_get_nccl_id": [_VP],
             "hp_shard": [_VP, _VP, C.c_int32, C.c_int32],
+            "hp_set_timing": [_VP, C.c_int32],
+            "hp_last_kernel_ms": [_VP, _VP],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -120,7 +122,8 @@ def exported_symbols():
             "hp_eval_costs", "hp_eval_costs_host", "hp_eval_sums", "hp_pso_fit", "hp_pso_state",
             "hp_debug_fk", "hp_debug_render", "hp_debug_pso_sphere", "hp_last_launch_count",
             "hp_splits_for", "hp_last_error", "hp_destroy", "hp_shard_range",
-            "hp_nccl_available", "hp_get_nccl_id", "hp_shard", "hp_track"]
+            "hp_nccl_available", "hp_get_nccl_id", "hp_shard", "hp_track",
+            "hp_set_timing", "hp_last_kernel_ms"]
 
 
 def _check(status: int, ctx=None):
@@ -347,6 +350,16 @@ class Context:
 
     def last_launch_count(self) -> int:
         return self._L.hp_last_launch_count(self._h)
+
+    def set_timing(self, on: bool = True):
+        """Record per-launch CUDA events around every later evaluation (hp_set_timing)."""
+        _check(self._L.hp_set_timing(self._h, 1 if on else 0), self._h)
+
+    def last_kernel_ms(self) -> tuple[float, float]:
+        """(first launch, renderer) device ms of the last timed evaluation."""
+        ms = (C.c_float * 2)()
+        _check(self._L.hp_last_kernel_ms(self._h, ms), self._h)
+        return float(ms[0]), float(ms[1])
 
     # -- PSO
     def pso_fit(self, seed: int = 0, particles: int = 64, generations: int = 30,
