@@ -137,7 +137,9 @@ hp_status hp_eval_costs_host(hp_ctx* ctx, const float* poses_host, int64_t n,
 
 /* Per-pose integer sums behind Eq. (4) (test hook, async): sums_dev [n][4] u64 =
  * (sum r_m, sum (o_s AND r_m), sum over both-defined pixels of rint(min(|o_d - r_d|,
- * clamp) * 2^20), number of both-defined pixels); costs64_dev [n] fp64 may be NULL. */
+ * clamp) * 2^q) * 2^(20 - q), number of both-defined pixels), i.e. the numerator in
+ * 2^-20 mm units quantised per pixel to 2^-q mm, q = the largest integer <= 20 with
+ * clamp * 2^q <= 2^22 (16 for the default 40 mm clamp); costs64_dev [n] fp64 may be NULL. */
 hp_status hp_eval_sums(hp_ctx* ctx, const float* poses_dev, int64_t n, uint64_t* sums_dev,
                        double* costs64_dev, void* stream);
 

@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -396,8 +397,22 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
         dd.RT0[i][j] = Rz[i][0] * Ry[0][j] + Rz[i][1] * Ry[1][j] + Rz[i][2] * Ry[2][j];
   }
   const hp_cost_params& c = ctx->cost;
-  ctx->costd = CostD{(float)c.d_m, (float)(c.clamp_at_dm ? c.d_m : c.d_M), c.lambda, c.lambda_k,
-                     c.depth_scale, c.kc_rest};
+  {
+    CostD& cd = ctx->costd;
+    cd.d_m = (float)c.d_m;
+    cd.clampv = (float)(c.clamp_at_dm ? c.d_m : c.d_M);
+    cd.lambda = c.lambda;
+    cd.lambda_k = c.lambda_k;
+    cd.depth_scale = c.depth_scale;
+    cd.kc_rest = c.kc_rest;
+    // numerator fixed point 2^-qbits mm: clamp * 2^qbits <= 2^22 (clamp <= 512 by the
+    // validation above, so qbits >= 13: 1.2e-4 mm; 16 for the default 40 mm)
+    int qb = 20;
+    while (qb > 0 && std::ldexp((double)cd.clampv, qb) > 4194304.0) qb--;
+    cd.qbits = qb;
+    cd.qscale = std::ldexp(1.0f, qb);
+    cd.qmagic = 12582912.0f;  // 1.5 * 2^23
+  }
   // observation buffers
   const int W = cam->width, H = cam->height;
   ctx->pitch_words = (W + 3) & ~3;  // 16-byte row pitch for TMA
@@ -413,8 +428,8 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
     hp_destroy(ctx);
     return st;
   }
-  // ray table, padded to a multiple of 4 floats for the float4 staging copy
-  CKC(cudaMalloc(&ctx->ray, (size_t)((W + H + 2 * kRayPad + 3) & ~3) * sizeof(float)));
+  // ray table (common.cuh layout; a multiple of 4 floats for the float4 staging copy)
+  CKC(cudaMalloc(&ctx->ray, (size_t)ray_floats(W, H) * sizeof(float)));
   CKC(launch_ray_table(ctx->camp, ctx->ray, ctx->st));
   CKC(cudaMalloc(&ctx->fk_g, (size_t)max_particles * fk_record_bytes()));
   CKC(cudaMalloc(&ctx->tiles_g, (size_t)max_particles * kMaxTiles * sizeof(uint4)));

@@ -20,7 +20,17 @@ constexpr int kTileW = 16;              // warp tile: 16 x (2 * kPxPerLane) pixe
 constexpr int kTileH = 2 * kPxPerLane;
 constexpr int kMaxTiles = 512;          // producer tile list capacity per particle
 constexpr int kRayPad = 16;             // ray-table slack for tiles overhanging the image
-                                        // (W + H + 2 kRayPad is a multiple of 4 when W, H are)
+static_assert(kPxPerLane == 4, "the row table packs a lane's 4 rows into one float4");
+// Ray table (k_ray_table), staged in shared memory by the evaluation kernels:
+//   dx[x]  for x in [0, ray_dx_len(W)): (x + 1/2 - c_x) / f_x, NaN for x >= W
+//   dy4[y] for y in [0, H + kRayPad):   float4 (dy(y), dy(y+2), dy(y+4), dy(y+6)) — the
+//          rows of a lane whose first row is y — with dy(y) = (y + 1/2 - c_y) / f_y, NaN
+//          for y >= H.  A NaN ray never hits (every intersection is NaN), so pixels off
+//          the image need no bounds test in the scoring loop.
+__host__ __device__ constexpr int ray_dx_len(int W) { return (W + kRayPad + 3) & ~3; }
+__host__ __device__ constexpr int ray_floats(int W, int H) {
+  return ray_dx_len(W) + 4 * (H + kRayPad);
+}
 
 // Primitive order on the device (sorted by kind so a cull mask splits by bit range):
 //   0..19  spheres   (finger f, joint k) -> 4 f + k
@@ -57,6 +67,10 @@ struct DimsD {
 
 struct CostD {
   float d_m, clampv;  // per-pixel fp32 compare / clamp
+  // numerator fixed point: round(min(|dd|, clamp) * 2^qbits) with qbits = the largest
+  // integer <= 20 with clamp * 2^qbits <= 2^22 (so fp32 magic-number rounding is exact)
+  float qscale, qmagic;  // 2^qbits, 1.5 * 2^23
+  int qbits;
   double lambda, lambda_k, depth_scale, kc_rest;
 };
 

@@ -8,7 +8,7 @@
 //                screen box: TMA-loads the observation tile, culls the 38 primitive boxes
 //                with two ballots, ray-casts the surviving primitives analytically (fp32,
 //                re-centred at the closest approach), resolves the min depth and scores the
-//                pixel.  Sums are integers (fixed point 2^-20 mm for the numerator): warp
+//                pixel.  Sums are integers (fixed point 2^-16 mm for the numerator): warp
 //                shuffles, one atomic per sum per CTA, and the last CTA of each particle
 //                computes Eq. (4)-(5) in fp64 and resets the accumulators.
 //   k_fk_debug : the same FK for the hp_debug_fk test hook.
@@ -55,14 +55,19 @@ __global__ void k_pack_obs(const float* __restrict__ depth, const uint8_t* __res
 // d = ((u + 0.5 - cx)/fx, (v + 0.5 - cy)/fy, 1)  (P:L114 camera C).
 // Layout: dx[W + kRayPad] then dy[H + kRayPad] (the pad covers tiles overhanging the image).
 __global__ void k_ray_table(const CamParams cam, float* ray) {
-  const int nx = cam.W + kRayPad, ny = cam.H + kRayPad;
+  const int nx = ray_dx_len(cam.W), ny = cam.H + kRayPad;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nx) ray[i] = __fdiv_rn((float)i + 0.5f - cam.cx, cam.fx);
-  else if (i < nx + ny) ray[i] = __fdiv_rn((float)(i - nx) + 0.5f - cam.cy, cam.fy);
+  const float nan = __int_as_float(0x7fc00000);
+  if (i < nx) {
+    ray[i] = i < cam.W ? __fdiv_rn((float)i + 0.5f - cam.cx, cam.fx) : nan;
+  } else if (i < nx + 4 * ny) {
+    const int y = (i - nx) / 4 + 2 * ((i - nx) % 4);  // dy4[y].q = dy(y + 2 q)
+    ray[i] = y < cam.H ? __fdiv_rn((float)y + 0.5f - cam.cy, cam.fy) : nan;
+  }
 }
 
 cudaError_t launch_ray_table(const CamParams& cam, float* ray, cudaStream_t st) {
-  const int n = cam.W + cam.H + 2 * kRayPad;
+  const int n = ray_floats(cam.W, cam.H);
   k_ray_table<<<(n + 255) / 256, 256, 0, st>>>(cam, ray);
   return cudaGetLastError();
 }
@@ -318,9 +323,11 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
   const int x = X0 + col;
   L.dx = s_dx[x];
   const float ddx = fmaf(L.dx, L.dx, 1.f);
+  const float4 dy4 = reinterpret_cast<const float4*>(s_dy)[Y0 + rowb];  // rows y, y+2, y+4, y+6
+  const float dyv[4] = {dy4.x, dy4.y, dy4.z, dy4.w};
 #pragma unroll
   for (int q = 0; q < kPxPerLane; q += 2) {
-    const float dy0 = s_dy[Y0 + rowb + 2 * q], dy1 = s_dy[Y0 + rowb + 2 * q + 2];
+    const float dy0 = dyv[q], dy1 = dyv[q + 1];
     L.dy[q / 2] = pk(dy0, dy1);
     L.idd[q / 2] = pk(rcp_approx(fmaf(dy0, dy0, ddx)), rcp_approx(fmaf(dy1, dy1, ddx)));
     L.zb[q] = zinit;
@@ -361,28 +368,32 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
       __syncwarp();
     }
     const float d_m = a.cost.d_m, clampv = a.cost.clampv;
-    const bool xin = x < a.cam.W;
-    unsigned int num = 0;  // <= 4 px x 40 mm x 2^20 < 2^32
+    const float qscale = a.cost.qscale, qmagic = a.cost.qmagic;
     bool any = false;
 #pragma unroll
     for (int q = 0; q < kPxPerLane; q++) any |= L.zb[q] <= zfar;
-    if (__any_sync(0xffffffffu, any))  // nothing rendered in this tile: nothing to score
+    if (__any_sync(0xffffffffu, any)) {  // nothing rendered in this tile: nothing to score
+      // numerator: round(min(|dd|, clamp) 2^qbits) from the bits of an fp32 magic-number
+      // FFMA (exact: the sum lies in [2^23, 2^24], ulp 1), summed mod 2^32 and un-biased
+      // once (the true per-lane sum is < 4 * 2^22); no float-to-int conversion on the XU
+      unsigned int num = 0u - (unsigned)kPxPerLane * __float_as_uint(qmagic);
 #pragma unroll
-    for (int q = 0; q < kPxPerLane; q++) {
-      const int y = Y0 + rowb + 2 * q;
-      const uint32_t w = obs_buf[(rowb + 2 * q) * kTileW + col];
-      const float od = __uint_as_float(w & 0x7fffffffu);
-      const float diff = fabsf(od - L.zb[q]);
-      const bool hit = xin & (y < a.cam.H) & (L.zb[q] <= zfar);
-      // r_m = 1 where |r_d - o_d| < d_m or o_d undefined (AMB-4, AMB-5)
-      const unsigned int rm = hit & ((od == 0.f) | (diff < d_m));
-      const bool both = hit & (od > 0.f);
-      acc.rm += rm;
-      acc.and_ += rm & (w >> 31);
-      acc.both += both;
-      num += both ? __float2uint_rn(fminf(diff, clampv) * 1048576.f) : 0u;  // 2^-20 mm
+      for (int q = 0; q < kPxPerLane; q++) {
+        const uint32_t w = obs_buf[(rowb + 2 * q) * kTileW + col];
+        const float od = __uint_as_float(w & 0x7fffffffu);
+        const float diff = fabsf(od - L.zb[q]);
+        // off-image pixels have NaN rays and never hit (k_ray_table)
+        const bool hit = L.zb[q] <= zfar;
+        // r_m = 1 where |r_d - o_d| < d_m or o_d undefined (AMB-4, AMB-5)
+        const unsigned int rm = hit & ((od == 0.f) | (diff < d_m));
+        const bool both = hit & (od > 0.f);
+        acc.rm += rm;
+        acc.and_ += rm & (w >> 31);
+        acc.both += both;
+        num += __float_as_uint(fmaf(both ? fminf(diff, clampv) : 0.f, qscale, qmagic));
+      }
+      acc.num += num;
     }
-    acc.num += num;
   }
   __syncwarp();
 }
@@ -396,22 +407,23 @@ __device__ __forceinline__ void warp_reduce(TileSums& s) {
 }
 
 // Eq. (4)-(5) in fp64 from the integer sums v = (sum r_m, sum o_s AND r_m, numerator in
-// 2^-20 mm, both-defined count)  (AMB-1, -2, -3, -6).
+// 2^-qbits mm, both-defined count)  (AMB-1, -2, -3, -6).
 __device__ __forceinline__ void finalize_cost(const EvalArgs& a, int p, const unsigned long long v[4],
                                               double kc) {
   const long long s_rm = (long long)v[0], s_and = (long long)v[1];
   const long long s_or = (long long)*a.S_o + s_rm - s_and;
   double D = 0.0;
   if (s_or > 0) {
-    const double num = (double)v[2] * (1.0 / 1048576.0);
+    const double num = ldexp((double)v[2], -a.cost.qbits);
     const double sor = (double)s_or, sand = (double)s_and;
     D = a.cost.depth_scale * num / sor + a.cost.lambda * (1.0 - 2.0 * sand / (sand + sor));
   }
   const double E = D + a.cost.lambda_k * kc;
   if (a.costs32) a.costs32[p] = (float)E;
   if (a.costs64) a.costs64[p] = E;
-  if (a.sums_out)
-    for (int k = 0; k < 4; k++) a.sums_out[(size_t)p * 4 + k] = v[k];
+  if (a.sums_out)  // the ABI reports the numerator in 2^-20 mm (qbits <= 20)
+    for (int k = 0; k < 4; k++)
+      a.sums_out[(size_t)p * 4 + k] = k == 2 ? v[k] << (20 - a.cost.qbits) : v[k];
 }
 
 // ---------------------------------------------------------------------------------------
@@ -440,7 +452,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.x / a.S, sidx = blockIdx.x % a.S;
   const float* s_dx = s_ray;
-  const float* s_dy = s_ray + a.cam.W + kRayPad;
+  const float* s_dy = s_ray + ray_dx_len(a.cam.W);
 
   if (warp <= 1) {
     // FK on warps 0 and 1 (warp 1 builds the non-sphere records in parallel)
@@ -458,7 +470,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     }
   } else {
     // while warps 0-1 run FK: stage the per-column / per-row ray directions (k_ray_table)
-    const int n4 = (a.cam.W + a.cam.H + 2 * kRayPad + 3) / 4;
+    const int n4 = ray_floats(a.cam.W, a.cam.H) / 4;
     for (int i = threadIdx.x - 64; i < n4; i += (NW - 2) * 32)
       reinterpret_cast<float4*>(s_ray)[i] = __ldg(reinterpret_cast<const float4*>(a.ray) + i);
     if (MODE == kModeCost && warp == NW - 1 && lane == 0) {
@@ -560,7 +572,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   if (a.done && *a.done) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* s_dx = s_ray;
-  const float* s_dy = s_ray + a.cam.W + kRayPad;
+  const float* s_dy = s_ray + ray_dx_len(a.cam.W);
   if (threadIdx.x == 0) {
     for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);
     for (int b = 0; b < NS; b++) {
@@ -574,7 +586,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     if (a.use_tma == 1) prefetch_tmap(&tmap);
   }
   {
-    const int n4 = (a.cam.W + a.cam.H + 2 * kRayPad + 3) / 4;
+    const int n4 = ray_floats(a.cam.W, a.cam.H) / 4;
     for (int i = threadIdx.x; i < n4; i += NW * 32)
       reinterpret_cast<float4*>(s_ray)[i] = __ldg(reinterpret_cast<const float4*>(a.ray) + i);
   }
@@ -825,7 +837,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* s_dx = s_ray;
-  const float* s_dy = s_ray + a.cam.W + kRayPad;
+  const float* s_dy = s_ray + ray_dx_len(a.cam.W);
   // one thread: take the next particle and pull its FK record + tile list into slot b
   auto issue = [&](int b) {
     const int p = (int)atomicAdd(a.pcount, 1u);
@@ -856,7 +868,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     issue(1);
   }
   {
-    const int n4 = (a.cam.W + a.cam.H + 2 * kRayPad + 3) / 4;
+    const int n4 = ray_floats(a.cam.W, a.cam.H) / 4;
     for (int i = threadIdx.x; i < n4; i += NW * 32)
       reinterpret_cast<float4*>(s_ray)[i] = __ldg(reinterpret_cast<const float4*>(a.ray) + i);
   }
@@ -967,7 +979,7 @@ size_t fk_record_bytes() { return sizeof(FkOut); }
 int persist_blocks_per_sm(const CamParams& cam) {
   set_carveouts();
   int nb = 0;
-  const size_t dyn = (size_t)((cam.W + cam.H + 2 * kRayPad + 3) & ~3) * sizeof(float);
+  const size_t dyn = (size_t)ray_floats(cam.W, cam.H) * sizeof(float);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_render_persist<kEvalWarps>,
                                                     kEvalWarps * 32, dyn) != cudaSuccess)
     return 0;
@@ -998,7 +1010,7 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     if (!two) cudaEventRecord(tev[1], st);  // single-launch paths: empty first interval
   }
   const dim3 grid((unsigned)blocks), block(kEvalWarps * 32);
-  const size_t dyn = (size_t)((a.cam.W + a.cam.H + 2 * kRayPad + 3) & ~3) * sizeof(float);
+  const size_t dyn = (size_t)ray_floats(a.cam.W, a.cam.H) * sizeof(float);
   if (two) {
     const dim3 fgrid((unsigned)((a.n + kFkPerCta - 1) / kFkPerCta));
     if (pose_double) k_fk_batch<double><<<fgrid, kFkWarps * 32, 0, st>>>(a);
