@@ -144,10 +144,11 @@ __device__ __forceinline__ f2 sqrt2(f2 x) {
   unpk(x, a, b);
   return mul2(x, pk(rsqrt_approx(a), rsqrt_approx(b)));
 }
-__device__ __forceinline__ f2 rcp2(f2 x) {
+// -1/x of both halves (the negation folds into the MUFU operand)
+__device__ __forceinline__ f2 nrcp2(f2 x) {
   float a, b;
   unpk(x, a, b);
-  return pk(rcp_approx(a), rcp_approx(b));
+  return pk(rcp_approx(-a), rcp_approx(-b));
 }
 
 // Branch-free min-depth update.  zb starts just above z_far, so z < zb also enforces
@@ -177,8 +178,13 @@ __device__ __forceinline__ void isect_sphere(const float* __restrict__ r, Lane4&
     const f2 tc = mul2(fma2(dy, bc(q.y), bc(bx)), idd);
     const f2 ox = fma2(tc, bc(L.dx), bc(-q.x)), oy = fma2(tc, dy, bc(-q.y));
     const f2 oz = add2(tc, bc(-q.z));
-    const f2 disc = sub2(bc(q.w), fma2(ox, ox, fma2(oy, oy, mul2(oz, oz))));
-    keep2<CHK>(sub2(tc, sqrt2(mul2(disc, idd))), L.zb[2 * j], L.zb[2 * j + 1], znear);
+    // m = -disc / |d|^2 with disc = r^2 - |o|^2;  z = t_c - sqrt(-m) = t_c + m rsqrt(-m)
+    // (NaN when disc < 0: no hit)
+    const f2 m = mul2(fma2(ox, ox, fma2(oy, oy, fma2(oz, oz, bc(-q.w)))), idd);
+    float m0, m1;
+    unpk(m, m0, m1);
+    keep2<CHK>(fma2(m, pk(rsqrt_approx(-m0), rsqrt_approx(-m1)), tc), L.zb[2 * j],
+               L.zb[2 * j + 1], znear);
   }
 }
 
@@ -207,7 +213,7 @@ __device__ __forceinline__ void isect_ellipsoid(const float* __restrict__ r, Lan
     const f2 disc = sub2(mul2(B, B), mul2(A, C));
     // A > 0: the smaller root; only the absolute error of s matters (z = t_c + s), so the
     // plain form is accurate to ~1e-6 mm here
-    const f2 s = mul2(sub2(bc(0.f), add2(B, sqrt2(disc))), rcp2(A));
+    const f2 s = mul2(add2(B, sqrt2(disc)), nrcp2(A));
     keep2<CHK>(add2(tc, s), L.zb[2 * j], L.zb[2 * j + 1], znear);
   }
 }
@@ -243,7 +249,7 @@ __device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L
     const f2 B = fma2(ox, lx, fma2(oy, ly, sub2(bc(0.f), mul2(kd, g))));
     const f2 C = fma2(ox, ox, fma2(oy, oy, sub2(bc(0.f), mul2(g, g))));
     const f2 disc = sub2(mul2(B, B), mul2(A, C));
-    const f2 s = mul2(sub2(bc(0.f), add2(B, sqrt2(disc))), rcp2(A));  // NaN when disc < 0
+    const f2 s = mul2(add2(B, sqrt2(disc)), nrcp2(A));  // NaN when disc < 0
     float za0, za1, z0, z1;
     unpk(fma2(s, lz, oz), za0, za1);
     unpk(add2(tc, s), z0, z1);
