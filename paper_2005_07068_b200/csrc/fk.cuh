@@ -190,9 +190,10 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
     }
     put3(rec, kC, m);
     double rows[3][3];
+    const double iw = 1.0 / dm.palm_half_w, it = 1.0 / dm.palm_half_t;
     for (int i = 0; i < 3; i++) {
-      rows[0][i] = cx[i] / dm.palm_half_w;
-      rows[1][i] = cz[i] / dm.palm_half_t;
+      rows[0][i] = cx[i] * iw;
+      rows[1][i] = cz[i] * it;
       rows[2][i] = cy[i];
     }
     for (int a = 0; a < 3; a++) {
@@ -234,7 +235,8 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
     }
     put3(rec, kC, c);
     for (int a = 0; a < 3; a++) {
-      double row[3] = {cols[a][0] / sd[a], cols[a][1] / sd[a], cols[a][2] / sd[a]};
+      const double is = 1.0 / sd[a];
+      double row[3] = {cols[a][0] * is, cols[a][1] * is, cols[a][2] * is};
       put3(rec, kM + 3 * a, row);
       rec[kCl + a] = (float)(row[0] * c[0] + row[1] * c[1] + row[2] * c[2]);
     }

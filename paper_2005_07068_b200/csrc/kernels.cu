@@ -771,28 +771,47 @@ __global__ void k_fk_debug(const double* pose, const DimsD dims, const CamParams
 //                     (double-buffered: particle i + 2 is fetched as soon as particle i is
 //                     finished, while i + 1 renders), so no warp ever waits on FK latency.
 // ---------------------------------------------------------------------------------------
-__device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out) {
+// A tile (qx, qy) overlaps primitive j iff column qx's x-range and row qy's y-range both
+// overlap box j — the same four compares as cull_tile — so the tile masks are the AND of
+// per-column and per-row 38-bit masks (tx + ty sets of 38 tests instead of tx * ty).
+constexpr int kMaxBand = 64;  // columns / rows of the per-warp band masks
+__device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out, uint2* s_cm,
+                                               uint2* s_rm) {
   const int lane = threadIdx.x & 31;
   const TileGrid g(fo.ubox);
-  if (g.ntiles > kMaxTiles) return -1;
+  if (g.ntiles > kMaxTiles || g.tx > kMaxBand) return -1;  // the renderer culls per tile
+  const int ty = g.tx > 0 ? g.ntiles / g.tx : 0;
+  if (ty > kMaxBand) return -1;
+  for (int q = lane; q < g.tx + ty; q += 32) {
+    const bool col = q < g.tx;
+    const int lo = col ? g.x0 + q * kTileW : g.y0 + (q - g.tx) * kTileH;
+    const int hi = lo + (col ? kTileW : kTileH) - 1;
+    // box j as (lo, hi) pairs along this axis: ints 0, 2 (x) or 1, 3 (y) of fo.box[j]
+    const int* bx = reinterpret_cast<const int*>(fo.box) + (col ? 0 : 1);
+    unsigned int m0 = 0, m1 = 0;
+#pragma unroll 8
+    for (int jj = 0; jj < 32; jj++)
+      m0 |= (unsigned)(bx[4 * jj] <= hi && bx[4 * jj + 2] >= lo) << jj;
+#pragma unroll
+    for (int jj = 32; jj < kNprim; jj++)
+      m1 |= (unsigned)(bx[4 * jj] <= hi && bx[4 * jj + 2] >= lo) << (jj - 32);
+    if (col) s_cm[q] = make_uint2(m0, m1);
+    else s_rm[q - g.tx] = make_uint2(m0, m1);
+  }
+  __syncwarp();
   int cnt = 0;
   for (int base = 0; base < g.ntiles; base += 32) {  // one tile per lane
     const int t = base + lane;
-    unsigned int m0 = 0, m1 = 0, m2 = 0;
+    unsigned int lo = 0, hi = 0;
     int X0 = 0, Y0 = 0;
     if (t < g.ntiles) {
       g.origin(t, X0, Y0);
-#pragma unroll
-      for (int jj = 0; jj < kNprim; jj++) {
-        const int4 bb = fo.box[jj];
-        const unsigned int ov = bb.x <= X0 + kTileW - 1 && bb.z >= X0 &&
-                                bb.y <= Y0 + kTileH - 1 && bb.w >= Y0;
-        if (jj < kCone0) m0 |= ov << jj;
-        else if (jj < kEll0) m1 |= ov << (jj - kCone0);
-        else m2 |= ov << (jj - kEll0);
-      }
+      const uint2 c = s_cm[(X0 - g.x0) / kTileW], r = s_rm[(Y0 - g.y0) / kTileH];
+      lo = c.x & r.x;
+      hi = c.y & r.y;
     }
-    const bool ne = (m0 | m1 | m2) != 0;
+    const unsigned int m0 = lo & 0xFFFFFu, m1 = (lo >> 20) | ((hi & 0x7u) << 12), m2 = hi >> 3;
+    const bool ne = (lo | hi) != 0;
     const unsigned int bal = __ballot_sync(0xffffffffu, ne);
     if (ne)
       out[cnt + __popc(bal & ((1u << lane) - 1u))] =
@@ -814,7 +833,8 @@ template <typename PoseT>
 __global__ void __launch_bounds__(kFkWarps * 32, kFkTeam == 2 ? 16 : 8)
     k_fk_batch(const EvalArgs a) {
   __shared__ FkScratch s_fk[kFkPerCta];
-  __shared__ FkOut s_out[kFkPerCta];
+  __shared__ __align__(16) FkOut s_out[kFkPerCta];
+  static_assert(sizeof(FkScratch) >= 2 * kMaxBand * sizeof(uint2), "band masks alias s_fk");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = kFkTeam == 2 ? 0 : warp;
   const int p = blockIdx.x * kFkPerCta + slot;
@@ -822,11 +842,25 @@ __global__ void __launch_bounds__(kFkWarps * 32, kFkTeam == 2 ? 16 : 8)
   const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
   fk_team<PoseT, kFkTeam>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk[slot], s_out[slot]);
   if (kFkTeam == 2 && warp == 1) return;  // warp 0 finishes (fk_team synced the team)
-  const int cnt = build_tile_list(s_out[slot], a.tiles_g + (size_t)p * kMaxTiles);
-  const float4* src = reinterpret_cast<const float4*>(&s_out[slot]);
-  float4* dst = reinterpret_cast<float4*>(static_cast<FkOut*>(a.fk_g) + p);
-  for (int i = lane; i < (int)(sizeof(FkOut) / 16); i += 32) dst[i] = src[i];
-  if (lane == 0) a.ntl_g[p] = cnt;
+  if (kFkTeam == 1) {
+    // the record leaves by one bulk copy while the warp builds the tile list: every lane
+    // orders its record writes before the async proxy, then lane 0 issues the copy
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0)
+      bulk_s2g(static_cast<FkOut*>(a.fk_g) + p, &s_out[slot], (uint32_t)sizeof(FkOut));
+  } else {
+    const float4* src = reinterpret_cast<const float4*>(&s_out[slot]);
+    float4* dst = reinterpret_cast<float4*>(static_cast<FkOut*>(a.fk_g) + p);
+    for (int i = lane; i < (int)(sizeof(FkOut) / 16); i += 32) dst[i] = src[i];
+  }
+  uint2* band = reinterpret_cast<uint2*>(&s_fk[slot]);  // FK scratch is dead by now
+  const int cnt = build_tile_list(s_out[slot], a.tiles_g + (size_t)p * kMaxTiles, band,
+                                  band + kMaxBand);
+  if (lane == 0) {
+    a.ntl_g[p] = cnt;
+    if (kFkTeam == 1) bulk_wait_all();  // complete before the CTA's shared memory retires
+  }
 }
 
 template <int NW>
