@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--fit-seeds", type=int, default=10)
     ap.add_argument("--no-fit", action="store_true")
     ap.add_argument("--track-frames", type=int, default=100)
+    ap.add_argument("--frames", type=int, default=8,
+                    help="row f2: observation frames per frame-batched call (0 = skip)")
     ap.add_argument("--clock-ramp", type=float, default=1.0,
                     help="seconds of untimed load before the timed region (clock sampling)")
     return ap.parse_args()
@@ -338,6 +340,47 @@ def run_ours(args):
                  "median_best_cost": float(np.median(tcosts)),
                  "median_wrist_pos_err_mm": float(np.median(err))}
 
+    # ---- row f2: frame-batched scoring, M frames x (4096 / M) poses per call on each GPU ----
+    frames = None
+    if args.frames > 0:
+        M = args.frames
+        npf = PER_RANK // M
+        seq = W.motion_sequence(frames=M, seed=100 + rank)
+        fctx = hp.Context(WIDTH, HEIGHT, max_particles=PER_RANK)
+        fd = torch.empty((M, HEIGHT, WIDTH), dtype=torch.float32, device=dev)
+        fm = torch.empty((M, HEIGHT, WIDTH), dtype=torch.uint8, device=dev)
+        for f in range(M):
+            d, m = fctx.render_observation(seq[f])
+            fd[f].copy_(d)
+            fm[f].copy_(m)
+        fctx.set_observations(fd, fm)
+        FP = torch.tensor(np.stack([W.swarm_around(seq[f], npf, 7068 + f) for f in range(M)])
+                          .astype(np.float32), device=dev)
+        fout = torch.empty((M, npf), dtype=torch.float32, device=dev)
+        for _ in range(args.warmup):
+            fctx.eval_costs_frames(FP, out=fout)
+        fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush.zero_()
+            fev[k][0].record(stream)
+            fctx.eval_costs_frames(FP, out=fout)
+            fev[k][1].record(stream)
+        torch.cuda.synchronize()
+        tf = torch.tensor([sum(a.elapsed_time(b) for a, b in fev)], dtype=torch.float64,
+                          device=dev)
+        if world > 1:
+            dist.all_reduce(tf, op=dist.ReduceOp.MAX)
+        fms = float(tf[0]) / args.steps
+        frames = {"value": M * npf * world / (fms * 1e-3), "unit": "hyp/s",
+                  "ms_per_call": fms, "frames_per_call": M, "poses_per_frame": npf,
+                  "config": f"row f2: {M} frames of a 640x480 synthetic motion sequence "
+                            f"(motion_sequence seed 100 + rank) x {npf} poses each (C4 recipe "
+                            f"around each frame's truth) per GPU, one hp_eval_costs_frames call, "
+                            "L2 flushed between calls; frames shard by rank, no collective"}
+        del fctx
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.cpu_seconds, swarm)
@@ -380,6 +423,8 @@ def run_ours(args):
             line["pso_fit"] = fit
         if track:
             line["tracking"] = track
+        if frames:
+            line["frames"] = frames
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line))

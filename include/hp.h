@@ -117,6 +117,16 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims,
 hp_status hp_set_observation(hp_ctx* ctx, const float* depth_mm, const uint8_t* mask,
                              int32_t on_device, void* stream);
 
+/* Frame-batched observations (M frames x N particles per call, the
+ * per-particle parallelism of P:L162 extended over a batch of observations): depth
+ * [frames][H][W] fp32 and mask [frames][H][W] u8, same conventions as hp_set_observation,
+ * which is this call with frames = 1.  Replaces the current observation(s); buffers grow
+ * on demand (growing synchronises the device and rebuilds the cached fit graph).  Plain
+ * hp_eval_costs / hp_pso_fit / hp_track score frame 0.
+ * Errors: INVALID_ARG (NULL pointers, frames < 1), OOM, CUDA. */
+hp_status hp_set_observations(hp_ctx* ctx, const float* depth_mm, const uint8_t* mask,
+                              int32_t frames, int32_t on_device, void* stream);
+
 /* Simulation protocol: render pose h_ref (host fp64 [26]) with this context's
  * camera and model into depth_dev [H][W] fp32 (0 = no hit) and mask_dev [H][W] u8
  * (silhouette), both device buffers (mask_dev may be NULL).  Async on `stream`. */
@@ -129,6 +139,18 @@ hp_status hp_render_observation(hp_ctx* ctx, const double* h_ref, float* depth_d
  * Errors: INVALID_ARG (NULL ctx/pointers with n > 0, n < 0 or n > max_particles). */
 hp_status hp_eval_costs(hp_ctx* ctx, const float* poses_dev, int64_t n, float* costs_dev,
                         void* stream);
+
+/* Frame-batched objective: poses_dev [frames][n_per_frame][26] fp32, pose i of block f
+ * scored against observation frame f (hp_set_observations); costs_dev [frames][n_per_frame]
+ * fp32.  Bitwise equal to scoring each block with hp_eval_costs against that frame alone.
+ * Local to this context even when sharded (frames shard across ranks with no collective).
+ * n_per_frame = 0 is a no-op.  Async on `stream`.
+ * Errors: INVALID_ARG (n_per_frame < 0, frames * n_per_frame > max_particles, NULL). */
+hp_status hp_eval_costs_frames(hp_ctx* ctx, const float* poses_dev, int64_t n_per_frame,
+                               float* costs_dev, void* stream);
+/* Its test hook: the sums and fp64 costs of hp_eval_sums, frame-batched. */
+hp_status hp_eval_sums_frames(hp_ctx* ctx, const float* poses_dev, int64_t n_per_frame,
+                              uint64_t* sums_dev, double* costs64_dev, void* stream);
 
 /* Same with HOST buffers: copies poses in, scores, copies costs out, then synchronises
  * `stream` (the end-to-end path a host application calls). */

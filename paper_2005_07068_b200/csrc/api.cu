@@ -83,6 +83,8 @@ struct hp_ctx {
   CUtensorMap tmap{};
   float* up_depth = nullptr;  // staging for host uploads
   uint8_t* up_mask = nullptr;
+  int frames = 1;      // observation frames currently set (hp_set_observations)
+  int frames_cap = 1;  // frames the buffers above hold
   // evaluation workspace
   unsigned long long* acc = nullptr;
   unsigned int* counters = nullptr;
@@ -308,7 +310,9 @@ static hp_status make_tmap(hp_ctx* ctx) {
     }
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  cuuint64_t gdim[2] = {(cuuint64_t)ctx->cam.width, (cuuint64_t)ctx->cam.height};
+  // frames stack vertically: frame f is rows [f H, (f + 1) H)
+  cuuint64_t gdim[2] = {(cuuint64_t)ctx->cam.width,
+                        (cuuint64_t)ctx->cam.height * (cuuint64_t)ctx->frames_cap};
   cuuint64_t gstride[1] = {(cuuint64_t)ctx->pitch_words * 4};
   cuuint32_t box[2] = {(cuuint32_t)kTileW, (cuuint32_t)kTileH};
   cuuint32_t es[2] = {1, 1};
@@ -479,24 +483,70 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   return HP_OK;
 }
 
-hp_status hp_set_observation(hp_ctx* ctx, const float* depth, const uint8_t* mask,
-                             int32_t on_device, void* stream) {
-  ARG(ctx && depth && mask, "hp_set_observation: NULL argument");
+// Grow the observation buffers to M frames: re-encode the tensor map and drop captured
+// graphs (they hold the old map by value).
+static hp_status ensure_frames(hp_ctx* ctx, int M) {
+  if (M <= ctx->frames_cap) return HP_OK;
+  const int W = ctx->cam.width, H = ctx->cam.height;
+  CK(cudaDeviceSynchronize());
+  cudaFree(ctx->obs);
+  cudaFree(ctx->S_o);
+  cudaFree(ctx->up_depth);
+  cudaFree(ctx->up_mask);
+  ctx->obs = nullptr;
+  ctx->S_o = nullptr;
+  ctx->up_depth = nullptr;
+  ctx->up_mask = nullptr;
+  ctx->frames_cap = 0;
+  const size_t px = (size_t)W * H * M;
+  CK(cudaMalloc(&ctx->obs, (size_t)ctx->pitch_words * H * M * 4));
+  CK(cudaMemset(ctx->obs, 0, (size_t)ctx->pitch_words * H * M * 4));
+  CK(cudaMalloc(&ctx->S_o, (size_t)M * sizeof(unsigned long long)));
+  CK(cudaMemset(ctx->S_o, 0, (size_t)M * sizeof(unsigned long long)));
+  CK(cudaMalloc(&ctx->up_depth, px * 4));
+  CK(cudaMalloc(&ctx->up_mask, px));
+  ctx->frames_cap = M;
+  hp_status st = make_tmap(ctx);
+  if (st != HP_OK) return st;
+  CK(cudaMemcpy(ctx->tmap_g, &ctx->tmap, sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  if (ctx->graph.exec) {
+    cudaGraphExecDestroy(ctx->graph.exec);
+    ctx->graph.exec = nullptr;
+  }
+  return HP_OK;
+}
+
+hp_status hp_set_observations(hp_ctx* ctx, const float* depth, const uint8_t* mask,
+                              int32_t frames, int32_t on_device, void* stream) {
+  ARG(ctx && depth && mask, "hp_set_observations: NULL argument");
+  ARG(frames >= 1, "hp_set_observations: frames must be >= 1");
   cudaSetDevice(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
+  hp_status st = ensure_frames(ctx, frames);
+  if (st != HP_OK) return st;
   const int W = ctx->cam.width, H = ctx->cam.height;
+  const size_t npx = (size_t)W * H;
   const float* dd = depth;
   const uint8_t* dm = mask;
   if (!on_device) {
-    CK(cudaMemcpyAsync(ctx->up_depth, depth, (size_t)W * H * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(ctx->up_mask, mask, (size_t)W * H, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->up_depth, depth, npx * frames * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->up_mask, mask, npx * frames, cudaMemcpyHostToDevice, s));
     dd = ctx->up_depth;
     dm = ctx->up_mask;
   }
-  CK(cudaMemsetAsync(ctx->S_o, 0, sizeof(unsigned long long), s));
-  CK(launch_pack_obs(dd, dm, ctx->obs, W, H, ctx->pitch_words, ctx->S_o, s));
+  CK(cudaMemsetAsync(ctx->S_o, 0, (size_t)frames * sizeof(unsigned long long), s));
+  for (int f = 0; f < frames; f++)
+    CK(launch_pack_obs(dd + f * npx, dm + f * npx, ctx->obs + (size_t)f * H * ctx->pitch_words,
+                       W, H, ctx->pitch_words, ctx->S_o + f, s));
   CK(cudaStreamSynchronize(s));
+  ctx->frames = frames;
   return HP_OK;
+}
+
+hp_status hp_set_observation(hp_ctx* ctx, const float* depth, const uint8_t* mask,
+                             int32_t on_device, void* stream) {
+  ARG(ctx && depth && mask, "hp_set_observation: NULL argument");
+  return hp_set_observations(ctx, depth, mask, 1, on_device, stream);
 }
 
 static EvalArgs base_args(hp_ctx* ctx) {
@@ -554,10 +604,12 @@ hp_status hp_debug_render(hp_ctx* ctx, const float* pose_dev, float* depth_dev, 
 }
 
 static hp_status eval_common(hp_ctx* ctx, const float* poses, int64_t n, float* costs32,
-                             double* costs64, uint64_t* sums, cudaStream_t s) {
+                             double* costs64, uint64_t* sums, cudaStream_t s,
+                             int64_t frame_n = 0) {
   EvalArgs a = base_args(ctx);
   a.poses = poses;
   a.n = (int)n;
+  a.frame_n = (int)frame_n;
   a.S = hp_splits_for(ctx, n);
   a.costs32 = costs32;
   a.costs64 = costs64;
@@ -614,6 +666,33 @@ hp_status hp_eval_costs(hp_ctx* ctx, const float* poses, int64_t n, float* costs
   cudaSetDevice(ctx->device);
   if (ctx->comm) return eval_sharded(ctx, poses, n, costs, (cudaStream_t)stream);
   return eval_common(ctx, poses, n, costs, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+hp_status hp_eval_costs_frames(hp_ctx* ctx, const float* poses, int64_t n_per_frame,
+                               float* costs, void* stream) {
+  ARG(ctx, "hp_eval_costs_frames: NULL context");
+  const int64_t total = n_per_frame * ctx->frames;
+  ARG(n_per_frame >= 0 && total <= ctx->max_n,
+      "hp_eval_costs_frames: n_per_frame * frames must be in [0, max_particles]");
+  if (total == 0) return HP_OK;
+  ARG(poses && costs, "hp_eval_costs_frames: NULL argument");
+  cudaSetDevice(ctx->device);
+  // frames are this rank's own: no collective even in sharded mode (frames shard by rank)
+  return eval_common(ctx, poses, total, costs, nullptr, nullptr, (cudaStream_t)stream,
+                     n_per_frame);
+}
+
+hp_status hp_eval_sums_frames(hp_ctx* ctx, const float* poses, int64_t n_per_frame,
+                              uint64_t* sums, double* costs64, void* stream) {
+  ARG(ctx, "hp_eval_sums_frames: NULL context");
+  const int64_t total = n_per_frame * ctx->frames;
+  ARG(n_per_frame >= 0 && total <= ctx->max_n,
+      "hp_eval_sums_frames: n_per_frame * frames must be in [0, max_particles]");
+  if (total == 0) return HP_OK;
+  ARG(poses && sums, "hp_eval_sums_frames: NULL argument");
+  cudaSetDevice(ctx->device);
+  return eval_common(ctx, poses, total, nullptr, costs64, sums, (cudaStream_t)stream,
+                     n_per_frame);
 }
 
 hp_status hp_eval_costs_host(hp_ctx* ctx, const float* poses, int64_t n, float* costs,

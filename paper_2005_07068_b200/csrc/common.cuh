@@ -96,7 +96,9 @@ struct EvalArgs {
   CamParams cam;
   DimsD dims;
   CostD cost;
-  const unsigned long long* S_o;  // device scalar: sum o_s
+  const unsigned long long* S_o;  // [frames] sum o_s per observation frame
+  int frame_n;                    // frame-batched scoring: pose p scores frame p / frame_n
+                                  // (0: every pose scores frame 0)
   unsigned long long* acc;        // [n][4] accumulators (zero between launches)
   unsigned int* counters;         // [n] CTA arrival counters (zero between launches)
   float* costs32;                 // optional [n]
@@ -125,6 +127,11 @@ struct EvalArgs {
   int* ntl_g;                     // [n] tile-list length (-1: box too large, cull on the fly)
   int two_kernel;                 // 1: k_fk_batch + k_render_persist, 0: k_eval_persist
 };
+
+// Observation frame of pose p; frame f occupies rows [f H, (f + 1) H) of the packed buffer
+__device__ __forceinline__ int frame_of(const EvalArgs& a, int p) {
+  return a.frame_n ? p / a.frame_n : 0;
+}
 
 // --------------------------------------------------------------------------------------
 // PTX helpers: mbarrier + TMA (cp.async.bulk.tensor), sm_90+ / sm_100a

@@ -313,7 +313,8 @@ template <int MODE>
 __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tmap,
                                         const FkOut& fo, int X0, int Y0, uint3 km,
                                         uint32_t* obs_buf, uint64_t* bar, uint32_t& phase,
-                                        const float* s_dx, const float* s_dy, TileSums& acc) {
+                                        const float* s_dx, const float* s_dy, TileSums& acc,
+                                        int yoff = 0) {
   const int lane = threadIdx.x & 31;
   const int col = lane & 15, rowb = lane >> 4;
   const float znear = a.cam.znear, zfar = a.cam.zfar;
@@ -321,7 +322,9 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
   if (MODE == kModeCost && a.use_tma) {
     // no proxy fence needed: the warp's reads of the previous tile in this buffer were
     // consumed before the __syncwarp that ended it (WAR across proxies is ordered)
-    tma_load_2d_elect(obs_buf, a.use_tma == 2 ? a.tmap_g : tmap, X0, Y0, bar,
+    // rows past this frame's bottom come from the next frame (or TMA zero fill): they are
+    // off-image, their rays are NaN and they are never scored
+    tma_load_2d_elect(obs_buf, a.use_tma == 2 ? a.tmap_g : tmap, X0, Y0 + yoff, bar,
                       kTileW * kTileH * 4);
   }
   const unsigned int msph = km.x, mcone = km.y, mell = km.z;
@@ -369,7 +372,7 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
       for (int q = 0; q < kPxPerLane; q++) {
         const int y = Y0 + rowb + 2 * q;
         obs_buf[(rowb + 2 * q) * kTileW + col] =
-            (x < a.cam.W && y < a.cam.H) ? a.obs[(size_t)y * a.obs_pitch + x] : 0u;
+            (x < a.cam.W && y < a.cam.H) ? a.obs[(size_t)(y + yoff) * a.obs_pitch + x] : 0u;
       }
       __syncwarp();
     }
@@ -417,7 +420,7 @@ __device__ __forceinline__ void warp_reduce(TileSums& s) {
 __device__ __forceinline__ void finalize_cost(const EvalArgs& a, int p, const unsigned long long v[4],
                                               double kc) {
   const long long s_rm = (long long)v[0], s_and = (long long)v[1];
-  const long long s_or = (long long)*a.S_o + s_rm - s_and;
+  const long long s_or = (long long)a.S_o[frame_of(a, p)] + s_rm - s_and;
   double D = 0.0;
   if (s_or > 0) {
     const double num = ldexp((double)v[2], -a.cost.qbits);
@@ -502,7 +505,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     const uint3 km = cull_tile(s_out, X0, Y0);
     if (km.x | km.y | km.z)  // no primitive box touches the tile: nothing to render or score
       do_tile<MODE>(a, &tmap, s_out, X0, Y0, km, s_obs[warp], &s_bar[warp], phase, s_dx, s_dy,
-                    acc);
+                    acc, frame_of(a, p) * a.cam.H);
     j = __shfl_sync(0xffffffffu, jn, 0);
   }
 
@@ -603,6 +606,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   uint32_t phase = 0;
   auto consume = [&](int p, int b) {
     const FkOut& fo = s_out[b];
+    const int yoff = frame_of(a, p) * a.cam.H;
     const TileGrid g(fo.ubox);
     const int nlist = s_ntl[b];  // >= 0: the producer's list of non-empty tiles + masks
     const int nt = nlist >= 0 ? nlist : g.ntiles;
@@ -626,7 +630,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
       }
       if (km.x | km.y | km.z)
         do_tile<kModeCost>(a, &tmap, fo, X0, Y0, km, s_obs[warp], &s_bar[warp], phase, s_dx,
-                           s_dy, acc);
+                           s_dy, acc, yoff);
       t = __shfl_sync(0xffffffffu, tn, 0);
     }
     warp_reduce(acc);
@@ -922,6 +926,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     if (p >= a.n) break;
     const FkOut& fo = s_out[b];
     const int nlist = s_ntl[b];
+    const int yoff = frame_of(a, p) * a.cam.H;
     const TileGrid g(fo.ubox);
     const int nt = nlist >= 0 ? nlist : g.ntiles;
     TileSums acc;
@@ -944,7 +949,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
       }
       if (km.x | km.y | km.z)
         do_tile<kModeCost>(a, &tmap, fo, X0, Y0, km, s_obs[warp], &s_bar[warp], phase, s_dx,
-                           s_dy, acc);
+                           s_dy, acc, yoff);
       t = __shfl_sync(0xffffffffu, tn, 0);
     }
     warp_reduce(acc);

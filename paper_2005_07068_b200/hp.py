@@ -97,6 +97,9 @@ def lib() -> C.CDLL:
             "hp_get_nccl_id": [_VP],
             "hp_shard": [_VP, _VP, C.c_int32, C.c_int32],
             "hp_set_timing": [_VP, C.c_int32],
+            "hp_set_observations": [_VP, _VP, _VP, C.c_int32, C.c_int32, _VP],
+            "hp_eval_costs_frames": [_VP, _VP, C.c_int64, _VP, _VP],
+            "hp_eval_sums_frames": [_VP, _VP, C.c_int64, _VP, _VP, _VP],
             "hp_last_kernel_ms": [_VP, _VP],
         }
         for name, args in sig.items():
@@ -123,7 +126,8 @@ def exported_symbols():
             "hp_debug_fk", "hp_debug_render", "hp_debug_pso_sphere", "hp_last_launch_count",
             "hp_splits_for", "hp_last_error", "hp_destroy", "hp_shard_range",
             "hp_nccl_available", "hp_get_nccl_id", "hp_shard", "hp_track",
-            "hp_set_timing", "hp_last_kernel_ms"]
+            "hp_set_timing", "hp_last_kernel_ms", "hp_set_observations",
+            "hp_eval_costs_frames", "hp_eval_sums_frames"]
 
 
 def _check(status: int, ctx=None):
@@ -292,6 +296,22 @@ class Context:
             assert tuple(depth.shape) == (self.height, self.width)
             _check(self._L.hp_set_observation(self._h, _dptr(depth), _dptr(mask), 1,
                                               _stream(stream)), self._h)
+        self.frames = 1
+
+    def set_observations(self, depth, mask, stream=None):
+        """Frame batch (row f2): depth fp32 [M][H][W], mask u8 [M][H][W]; host or device."""
+        if isinstance(depth, np.ndarray):
+            d = np.ascontiguousarray(depth, dtype=np.float32)
+            m = np.ascontiguousarray(mask, dtype=np.uint8)
+            assert d.ndim == 3 and d.shape[1:] == (self.height, self.width) and m.shape == d.shape
+            _check(self._L.hp_set_observations(self._h, d.ctypes.data, m.ctypes.data, d.shape[0],
+                                               0, _stream(stream)), self._h)
+        else:
+            assert depth.dim() == 3 and tuple(depth.shape[1:]) == (self.height, self.width)
+            assert depth.is_contiguous() and mask.is_contiguous()
+            _check(self._L.hp_set_observations(self._h, _dptr(depth), _dptr(mask),
+                                               depth.shape[0], 1, _stream(stream)), self._h)
+        self.frames = int(depth.shape[0])
 
     def render_observation(self, h_ref, stream=None):
         """Simulation protocol: render h_ref on the GPU -> (depth, mask) tensors."""
@@ -316,6 +336,30 @@ class Context:
         _check(self._L.hp_eval_costs(self._h, _dptr(poses), n, _dptr(out), _stream(stream)),
                self._h)
         return out
+
+    def eval_costs_frames(self, poses, out=None, stream=None):
+        """Frame-batched E: poses [M][n][26] fp32 CUDA tensor (M = frames set) -> [M][n]."""
+        import torch
+
+        assert poses.dtype == torch.float32 and poses.dim() == 3 and poses.shape[-1] == NDOF
+        assert poses.is_contiguous()
+        m, n = poses.shape[0], poses.shape[1]
+        if out is None:
+            out = torch.empty((m, n), dtype=torch.float32, device=poses.device)
+        _check(self._L.hp_eval_costs_frames(self._h, _dptr(poses), n, _dptr(out),
+                                            _stream(stream)), self._h)
+        return out
+
+    def eval_sums_frames(self, poses, stream=None):
+        """(sums [M][n][4] int64, costs fp64 [M][n]) of the frame-batched evaluation."""
+        import torch
+
+        m, n = poses.shape[0], poses.shape[1]
+        sums = torch.zeros((m, n, 4), dtype=torch.int64, device=poses.device)
+        costs = torch.empty((m, n), dtype=torch.float64, device=poses.device)
+        _check(self._L.hp_eval_sums_frames(self._h, _dptr(poses), n, _dptr(sums), _dptr(costs),
+                                           _stream(stream)), self._h)
+        return sums, costs
 
     def eval_costs_host(self, poses: np.ndarray, stream=None) -> np.ndarray:
         """Host-buffer variant: copies in, scores, copies out, synchronises."""

@@ -100,10 +100,16 @@ def random_poses(seed: int, n: int) -> np.ndarray:
 def swarm_c4(n: int = 4096, seed: int = 7068) -> np.ndarray:
     """C4 mid-fit swarm: clip(h_A + sigma * N(0,1)), sigma = 20 mm on position,
     10 deg on wrist angles, 15 deg on finger angles."""
+    return swarm_around(H_A, n, seed)
+
+
+def swarm_around(centre, n: int, seed: int) -> np.ndarray:
+    """The C4 swarm recipe around an arbitrary pose (row f2: one swarm per frame)."""
     rng = np.random.default_rng(seed)
     sigma = np.array([20.0] * 3 + [math.radians(10.0)] * 3 + [math.radians(15.0)] * 20)
     lo, hi = input_bounds()
-    return np.clip(H_A[None, :] + sigma[None, :] * rng.standard_normal((n, NDOF)), lo, hi)
+    c = np.asarray(centre, np.float64)
+    return np.clip(c[None, :] + sigma[None, :] * rng.standard_normal((n, NDOF)), lo, hi)
 
 
 def local_init_box():
