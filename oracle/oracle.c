@@ -924,3 +924,37 @@ int32_t or_pso_fit_hand(const float* obs_depth, const uint8_t* obs_mask, const o
   return or_pso_run(26, lo, hi, ilo, ihi, 6, 26, pp, hand_batch, &c, best_x, best_cost, trace,
                     gens_run, X_out, V_out, P_out, Pcost_out);
 }
+
+/* ---- observation front end (row f3; definitions in oracle.h, DESIGN.md AMB-33..36) */
+void or_segment(const uint16_t* depth_u16, const uint8_t* skin, int64_t npx,
+                const or_segment_params* sp, float* o_d, uint8_t* o_s, int32_t band_out[2]) {
+  int64_t lo = sp->lo, hi = sp->hi;
+  if (sp->mode == 1) {
+    int64_t m = -1;  /* nearest candidate depth */
+    for (int64_t i = 0; i < npx; i++) {
+      int64_t d = depth_u16[i];
+      int cand = d > 0 && (skin == NULL || skin[i] != 0);
+      if (cand && (m < 0 || d < m)) m = d;
+    }
+    if (m < 0) {
+      lo = 1;
+      hi = 0;  /* empty band */
+    } else {
+      lo = m;
+      hi = m + sp->width;
+    }
+  }
+  for (int64_t i = 0; i < npx; i++) {
+    int64_t d = depth_u16[i];
+    int valid = d > 0;
+    int in_band = valid && lo <= d && d <= hi;
+    int s = skin ? (skin[i] != 0 && (!valid || in_band)) : in_band;
+    o_s[i] = (uint8_t)s;
+    if (sp->keep_background) o_d[i] = valid ? (float)d : 0.0f;
+    else o_d[i] = in_band ? (float)d : 0.0f;
+  }
+  if (band_out) {
+    band_out[0] = (int32_t)lo;
+    band_out[1] = (int32_t)hi;
+  }
+}

@@ -21,6 +21,8 @@
  *   or_kc .................... pinned (closed-form pair examples)
  *   or_pso_run ............... pinned (w closed form, fixed point, sphere convergence)
  *   or_pso_fit_hand .......... parity unpinned: the paper prints no trajectory (Figs. 6-9 absent)
+ *   or_segment ............... pinned (recovers a rendered hand in front of a background
+ *                              plane exactly; dropout / skin / empty-frame special cases)
  */
 #ifndef HP_ORACLE_H
 #define HP_ORACLE_H
@@ -130,6 +132,27 @@ void or_edge_mask(const double h[26], const or_dims* d, const or_camera* cam, do
 /* conservative pixel box [x0,x1]x[y0,y1] of one primitive (inclusive), margin in px;
  * returns 0 if empty. */
 int32_t or_prim_box(const or_prim* p, const or_camera* cam, int32_t margin, int32_t box[4]);
+
+/* ---- observation front end ("skin colour detection and depth
+ * segmentation extract the hand region of the colour and depth images; the result of this
+ * preprocessing is O = (O_s, O_d)").  DESIGN.md §3 AMB-33..36 fix the reading:
+ *   valid    = d > 0                       (Kinect: 0 = no reading)
+ *   band     = [lo, hi] (mode 0) or [m, m + width], m = min d over valid pixels that are
+ *              skin (or all valid pixels without a skin image): the hand is the nearest
+ *              object (mode 1; no candidate: empty band)
+ *   in_band  = valid and lo <= d <= hi
+ *   O_s      = skin ? skin and (not valid or in_band) : in_band
+ *   O_d      = keep_background ? (valid ? d : 0) : (in_band ? d : 0)
+ * All band limits are integer mm, so every decision is exact in any precision. */
+typedef struct {
+  int32_t mode;            /* 0 fixed band, 1 nearest-object band */
+  int32_t lo, hi, width;   /* mm */
+  int32_t keep_background; /* 1: O_d keeps all valid depth (o_d defined where o_s = 0, AMB-30) */
+} or_segment_params;
+/* depth_u16 [npx] mm, skin [npx] u8 or NULL -> o_d [npx] fp32 mm, o_s [npx] u8 0/1;
+ * band_out (may be NULL) receives the band used {lo, hi} (mode 1 without candidates: {1, 0}). */
+void or_segment(const uint16_t* depth_u16, const uint8_t* skin, int64_t npx,
+                const or_segment_params* sp, float* o_d, uint8_t* o_s, int32_t band_out[2]);
 
 /* ---- cost (Eq. 4-5) ---- */
 void or_score(const float* obs_depth, const uint8_t* obs_mask, const float* r_d, int64_t npx,

@@ -223,6 +223,28 @@ def synthesize(h_ref, cam: Camera, dims: Dims | None = None) -> Observation:
     return Observation(d, (d > 0).astype(np.uint8), cam)
 
 
+class SegmentParams(C.Structure):
+    """or_segment_params (oracle.h): mode 0 fixed band [lo, hi], 1 nearest-object band."""
+    _fields_ = [("mode", C.c_int32), ("lo", C.c_int32), ("hi", C.c_int32),
+                ("width", C.c_int32), ("keep_background", C.c_int32)]
+
+
+def segment(depth_u16, skin=None, mode: int = 1, lo: int = 0, hi: int = 0, width: int = 150,
+            keep_background: bool = False, cam: Camera | None = None):
+    """Row f3 front end: raw u16 depth (+ optional skin mask) -> Observation
+    (O_d, O_s) and the band used."""
+    d = np.ascontiguousarray(depth_u16, dtype=np.uint16)
+    sk = None if skin is None else np.ascontiguousarray(skin, dtype=np.uint8)
+    assert sk is None or sk.shape == d.shape
+    od = np.zeros(d.shape, np.float32)
+    os_ = np.zeros(d.shape, np.uint8)
+    band = (C.c_int32 * 2)()
+    sp = SegmentParams(mode, lo, hi, width, int(keep_background))
+    lib().or_segment(_p(d, C.c_uint16), None if sk is None else _p(sk, C.c_uint8),
+                     C.c_int64(d.size), C.byref(sp), _p(od, C.c_float), _p(os_, C.c_uint8), band)
+    return Observation(od, os_, cam), (int(band[0]), int(band[1]))
+
+
 def eval_batch(poses, obs: Observation, dims: Dims | None = None, cp: CostParams | None = None,
                culled: bool = True, threads: int = 0, with_sums: bool = False):
     poses = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, NDOF)

@@ -528,3 +528,65 @@ def test_pso_hand_fit_recovers_from_local_init():
     assert np.all((r.X >= lo) & (r.X <= hi))
     r2 = O.pso_fit_hand(obs, pp, c, rad, threads=3)
     assert np.array_equal(r.best_x, r2.best_x) and np.array_equal(r.trace, r2.trace)
+
+
+# ------------------------------------------------------------------ observation front end
+# Row f3: the depth-band segmentation is pinned by what it must recover, not by its
+# own formula: a rendered hand in front of a background plane comes back exactly.
+def _hand_scene(background=1500.0, **noise):
+    cam = O.camera(160, 120)
+    clean = O.render(W.H_A, cam)
+    depth, skin = W.kinect_frame(clean, seed=3, background_mm=background, **noise)
+    return cam, clean, depth, skin
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_segment_recovers_rendered_hand(mode):
+    cam, clean, depth, _ = _hand_scene()
+    hand = clean > 0
+    obs, band = O.segment(depth, None, mode=mode, lo=500, hi=1100, width=250, cam=cam)
+    assert np.array_equal(obs.mask, hand.astype(np.uint8))
+    assert np.array_equal(obs.depth, np.where(hand, np.rint(clean), 0).astype(np.float32))
+    if mode == 1:  # the nearest object is the hand: the band starts at its nearest depth
+        assert band == (int(np.rint(clean[hand]).min()), int(np.rint(clean[hand]).min()) + 250)
+    # the same scene without a background: identical result
+    _, _, d2, _ = _hand_scene(background=None)
+    obs2, _ = O.segment(d2, None, mode=mode, lo=500, hi=1100, width=250)
+    assert np.array_equal(obs2.mask, obs.mask) and np.array_equal(obs2.depth, obs.depth)
+
+
+def test_segment_keep_background_and_cost_ordering():
+    cam, clean, depth, skin = _hand_scene()
+    obs, _ = O.segment(depth, skin, mode=1, width=250, keep_background=True, cam=cam)
+    assert np.array_equal(obs.depth, depth.astype(np.float32))   # every valid depth kept
+    assert np.array_equal(obs.mask, (clean > 0).astype(np.uint8))
+    # the truth still scores best against the segmented frame (background depth only
+    # enters where the model renders: AMB-3/AMB-30)
+    poses = np.stack([W.H_A] + list(W.random_poses(4, 6)))
+    costs, _, _, _ = O.eval_batch(poses, obs, with_sums=True)
+    assert costs[0] < 0.1 and np.all(costs[1:] > costs[0])
+
+
+def test_segment_skin_dropout_and_flips():
+    cam, clean, depth, skin = _hand_scene(dropout=0.2, mask_flip=0.05)
+    hand = clean > 0
+    obs, band = O.segment(depth, skin, mode=1, width=250)
+    valid = depth > 0
+    # skin pixels with no depth reading stay in O_s (missing depth is legal)
+    assert np.all(obs.mask[(skin == 1) & ~valid] == 1)
+    assert np.all(obs.depth[~valid] == 0)
+    # skin flipped onto the far background (valid, outside the band) is rejected
+    assert np.all(obs.mask[(skin == 1) & valid & ~hand] == 0)
+    # non-skin pixels never enter O_s, and O_d is defined only inside the band
+    assert np.all(obs.mask[skin == 0] == 0)
+    assert np.all((obs.depth == 0) | ((obs.depth >= band[0]) & (obs.depth <= band[1])))
+
+
+def test_segment_band_limits_inclusive_and_empty_frame():
+    d = np.array([[699, 700, 850, 1000, 1001, 0]], np.uint16)
+    obs, band = O.segment(d, None, mode=0, lo=700, hi=1000)
+    assert obs.mask.tolist() == [[0, 1, 1, 1, 0, 0]] and band == (700, 1000)
+    obs, band = O.segment(d, None, mode=1, width=301)
+    assert obs.mask.tolist() == [[1, 1, 1, 1, 0, 0]] and band == (699, 1000)
+    empty, band = O.segment(np.zeros((3, 4), np.uint16), None, mode=1, width=100)
+    assert empty.mask.sum() == 0 and empty.depth.sum() == 0 and band == (1, 0)

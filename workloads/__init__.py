@@ -132,3 +132,34 @@ def motion_sequence(frames: int = 100, seed: int = 5) -> np.ndarray:
     centre[:6] = H_A[:6]
     seq = centre[None, :] + amp[None, :] * np.sin(freq[None, :] * t + phase[None, :])
     return np.clip(seq, lo, hi)
+
+
+def kinect_frame(clean_depth, seed: int, depth_sigma: float = 0.0, dropout: float = 0.0,
+                 mask_flip: float = 0.0, background_mm: float | None = None,
+                 background_slope=(0.0, 0.0)):
+    """Row f3 input: a Kinect-like raw frame from a clean hand render (SPEC S:L219-244
+    NoiseSpec; the paper's sensor is a Kinect).  Returns (depth u16 mm, skin u8).
+
+    Scene: the hand render in front of an optional background plane whose depth is
+    background_mm + sx (u - W/2) + sy (v - H/2).  Sensor: additive Gaussian noise of
+    depth_sigma mm on every valid depth, rounding to integer mm, then each valid pixel
+    drops to 0 with probability `dropout`.  Skin image (the colour detector's output): the
+    hand silhouette with each pixel flipped with probability `mask_flip`.  Seeded numpy
+    draws; no method arithmetic."""
+    rng = np.random.default_rng(seed)
+    clean = np.asarray(clean_depth, np.float64)
+    H, W = clean.shape
+    hand = clean > 0
+    scene = clean.copy()
+    if background_mm is not None:
+        v, u = np.mgrid[0:H, 0:W]
+        plane = background_mm + background_slope[0] * (u - W / 2) + background_slope[1] * (v - H / 2)
+        scene = np.where(hand, clean, plane)
+    valid = scene > 0
+    noisy = scene + depth_sigma * rng.standard_normal(scene.shape)
+    depth = np.where(valid, np.clip(np.rint(noisy), 1, 65535), 0)
+    drop = rng.random(scene.shape) < dropout
+    depth = np.where(drop, 0, depth).astype(np.uint16)
+    flip = rng.random(scene.shape) < mask_flip
+    skin = (hand ^ flip).astype(np.uint8)
+    return depth, skin
