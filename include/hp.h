@@ -127,6 +127,34 @@ hp_status hp_set_observation(hp_ctx* ctx, const float* depth_mm, const uint8_t* 
 hp_status hp_set_observations(hp_ctx* ctx, const float* depth_mm, const uint8_t* mask,
                               int32_t frames, int32_t on_device, void* stream);
 
+/* Kinect-like observation front end.  P:L92: "skin colour detection
+ * and depth segmentation extract the hand region ... O = (O_s, O_d)".  Readings DESIGN.md
+ * AMB-33..36: with valid = d > 0 and band = [lo_mm, hi_mm] (mode 0) or [m, m + width_mm]
+ * (mode 1, m = the nearest valid depth among skin pixels, or among all pixels without a skin
+ * image; no candidate = empty band), in_band = valid && lo <= d <= hi:
+ *   O_s = skin ? skin && (!valid || in_band) : in_band
+ *   O_d = keep_background ? (valid ? d : 0) : (in_band ? d : 0)
+ * Integer mm limits, inclusive: bit-exact with the oracle's or_segment. */
+typedef struct {
+  int32_t mode;            /* 0 fixed band, 1 nearest-object band (default) */
+  int32_t lo_mm, hi_mm;    /* mode 0 */
+  int32_t width_mm;        /* mode 1 (default 250) */
+  int32_t keep_background; /* 1: O_d keeps every valid depth (default 0) */
+} hp_segment_params;
+hp_status hp_default_segment(hp_segment_params* out);
+/* depth_mm [frames][H][W] u16 (Kinect mm, 0 = no reading), skin [frames][H][W] u8 or NULL,
+ * host (on_device = 0) or device pointers; seg NULL = defaults.  Segments, packs and sets
+ * `frames` observation frames (as hp_set_observations).  band_out (host [frames][2], may be
+ * NULL) receives each frame's band.  Synchronises `stream`.
+ * Errors: INVALID_ARG (NULL ctx/depth, frames < 1, mode not 0/1, width_mm < 0), OOM, CUDA. */
+hp_status hp_set_observation_kinect(hp_ctx* ctx, const uint16_t* depth_mm, const uint8_t* skin,
+                                    int32_t frames, const hp_segment_params* seg,
+                                    int32_t on_device, int32_t* band_out, void* stream);
+/* Unpack observation frame `frame` into device buffers depth [H][W] fp32 (0 = undefined) and
+ * mask [H][W] u8 (either may be NULL).  Async.  Errors: INVALID_ARG (frame out of range). */
+hp_status hp_get_observation(hp_ctx* ctx, int32_t frame, float* depth_dev, uint8_t* mask_dev,
+                             void* stream);
+
 /* Simulation protocol: render pose h_ref (host fp64 [26]) with this context's
  * camera and model into depth_dev [H][W] fp32 (0 = no hit) and mask_dev [H][W] u8
  * (silhouette), both device buffers (mask_dev may be NULL).  Async on `stream`. */

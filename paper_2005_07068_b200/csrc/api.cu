@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -85,6 +86,7 @@ struct hp_ctx {
   uint8_t* up_mask = nullptr;
   int frames = 1;      // observation frames currently set (hp_set_observations)
   int frames_cap = 1;  // frames the buffers above hold
+  unsigned int* band_m = nullptr;  // [frames_cap] nearest-depth reduction (row f3)
   // evaluation workspace
   unsigned long long* acc = nullptr;
   unsigned int* counters = nullptr;
@@ -281,7 +283,8 @@ void hp_destroy(hp_ctx* ctx) {
   if (ctx->gat32) cudaFree(ctx->gat32);
   if (ctx->gat64) cudaFree(ctx->gat64);
   if (ctx->graph.exec) cudaGraphExecDestroy(ctx->graph.exec);
-  void* dev[] = {ctx->obs, ctx->S_o, ctx->up_depth, ctx->up_mask, ctx->acc, ctx->counters,
+  void* dev[] = {ctx->obs, ctx->S_o, ctx->band_m, ctx->up_depth, ctx->up_mask, ctx->acc,
+                 ctx->counters,
                  ctx->poses32, ctx->costs32, ctx->scratch, ctx->X, ctx->V, ctx->P, ctx->Pc,
                  ctx->E, ctx->G, ctx->Gc, ctx->trace, ctx->bnd, ctx->centre, ctx->mark,
                  ctx->flags, ctx->dyn, ctx->tmap_g, ctx->ray, ctx->pcount, ctx->X2,
@@ -424,6 +427,7 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   CKC(cudaMemset(ctx->obs, 0, (size_t)ctx->pitch_words * H * 4));
   CKC(cudaMalloc(&ctx->S_o, sizeof(unsigned long long)));
   CKC(cudaMemset(ctx->S_o, 0, sizeof(unsigned long long)));
+  CKC(cudaMalloc(&ctx->band_m, sizeof(unsigned int)));
   CKC(cudaMalloc(&ctx->up_depth, (size_t)W * H * 4));
   CKC(cudaMalloc(&ctx->up_mask, (size_t)W * H));
   st = make_tmap(ctx);
@@ -491,10 +495,12 @@ static hp_status ensure_frames(hp_ctx* ctx, int M) {
   CK(cudaDeviceSynchronize());
   cudaFree(ctx->obs);
   cudaFree(ctx->S_o);
+  cudaFree(ctx->band_m);
   cudaFree(ctx->up_depth);
   cudaFree(ctx->up_mask);
   ctx->obs = nullptr;
   ctx->S_o = nullptr;
+  ctx->band_m = nullptr;
   ctx->up_depth = nullptr;
   ctx->up_mask = nullptr;
   ctx->frames_cap = 0;
@@ -503,6 +509,7 @@ static hp_status ensure_frames(hp_ctx* ctx, int M) {
   CK(cudaMemset(ctx->obs, 0, (size_t)ctx->pitch_words * H * M * 4));
   CK(cudaMalloc(&ctx->S_o, (size_t)M * sizeof(unsigned long long)));
   CK(cudaMemset(ctx->S_o, 0, (size_t)M * sizeof(unsigned long long)));
+  CK(cudaMalloc(&ctx->band_m, (size_t)M * sizeof(unsigned int)));
   CK(cudaMalloc(&ctx->up_depth, px * 4));
   CK(cudaMalloc(&ctx->up_mask, px));
   ctx->frames_cap = M;
@@ -540,6 +547,84 @@ hp_status hp_set_observations(hp_ctx* ctx, const float* depth, const uint8_t* ma
                        W, H, ctx->pitch_words, ctx->S_o + f, s));
   CK(cudaStreamSynchronize(s));
   ctx->frames = frames;
+  return HP_OK;
+}
+
+hp_status hp_default_segment(hp_segment_params* out) {
+  if (!out) return HP_ERR_INVALID_ARG;
+  *out = hp_segment_params{1, 0, 0, 250, 0};  // nearest-object band, 25 cm deep (AMB-34)
+  return HP_OK;
+}
+
+hp_status hp_set_observation_kinect(hp_ctx* ctx, const uint16_t* depth_mm, const uint8_t* skin,
+                                    int32_t frames, const hp_segment_params* seg,
+                                    int32_t on_device, int32_t* band_out, void* stream) {
+  ARG(ctx && depth_mm, "hp_set_observation_kinect: NULL argument");
+  ARG(frames >= 1, "hp_set_observation_kinect: frames must be >= 1");
+  hp_segment_params sp;
+  hp_default_segment(&sp);
+  if (seg) sp = *seg;
+  ARG((sp.mode == 0 || sp.mode == 1) && sp.width_mm >= 0,
+      "hp_set_observation_kinect: mode must be 0 or 1 and width_mm >= 0");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  hp_status st = ensure_frames(ctx, frames);
+  if (st != HP_OK) return st;
+  const int W = ctx->cam.width, H = ctx->cam.height;
+  const size_t npx = (size_t)W * H;
+  const uint16_t* dd = depth_mm;
+  const uint8_t* sk = skin;
+  if (!on_device) {  // staging: up_depth holds 4 bytes per pixel, u16 needs 2
+    CK(cudaMemcpyAsync(ctx->up_depth, depth_mm, npx * frames * 2, cudaMemcpyHostToDevice, s));
+    dd = reinterpret_cast<const uint16_t*>(ctx->up_depth);
+    if (skin) {
+      CK(cudaMemcpyAsync(ctx->up_mask, skin, npx * frames, cudaMemcpyHostToDevice, s));
+      sk = ctx->up_mask;
+    }
+  }
+  const SegD sd{sp.mode, sp.lo_mm, sp.hi_mm, sp.width_mm, sp.keep_background};
+  CK(cudaMemsetAsync(ctx->S_o, 0, (size_t)frames * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(ctx->band_m, 0xFF, (size_t)frames * sizeof(unsigned int), s));
+  for (int f = 0; f < frames; f++) {
+    const uint16_t* df = dd + f * npx;
+    const uint8_t* sf = sk ? sk + f * npx : nullptr;
+    if (sp.mode == 1) CK(launch_band_min(df, sf, (int)npx, ctx->band_m + f, s));
+    CK(launch_ingest(df, sf, W, H, ctx->pitch_words, sd, ctx->band_m + f,
+                     ctx->obs + (size_t)f * H * ctx->pitch_words, ctx->S_o + f, s));
+  }
+  if (band_out) {
+    std::vector<unsigned int> m(frames);
+    CK(cudaMemcpyAsync(m.data(), ctx->band_m, frames * sizeof(unsigned int),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int f = 0; f < frames; f++) {
+      long long lo = sp.lo_mm, hi = sp.hi_mm;
+      if (sp.mode == 1) {
+        if (m[f] == 0xFFFFFFFFu) {
+          lo = 1;
+          hi = 0;
+        } else {
+          lo = m[f];
+          hi = (long long)m[f] + sp.width_mm;
+        }
+      }
+      band_out[2 * f] = (int32_t)lo;
+      band_out[2 * f + 1] = (int32_t)std::min<long long>(hi, INT32_MAX);
+    }
+  }
+  CK(cudaStreamSynchronize(s));
+  ctx->frames = frames;
+  return HP_OK;
+}
+
+hp_status hp_get_observation(hp_ctx* ctx, int32_t frame, float* depth_dev, uint8_t* mask_dev,
+                             void* stream) {
+  ARG(ctx, "hp_get_observation: NULL context");
+  ARG(frame >= 0 && frame < ctx->frames, "hp_get_observation: frame out of range");
+  cudaSetDevice(ctx->device);
+  const int W = ctx->cam.width, H = ctx->cam.height;
+  CK(launch_unpack_obs(ctx->obs + (size_t)frame * H * ctx->pitch_words, W, H, ctx->pitch_words,
+                       depth_dev, mask_dev, (cudaStream_t)stream));
   return HP_OK;
 }
 

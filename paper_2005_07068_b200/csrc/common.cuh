@@ -233,6 +233,18 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 // --------------------------------------------------------------------------------------
 cudaError_t launch_pack_obs(const float* depth, const uint8_t* mask, uint32_t* obs, int W,
                             int H, int pitch_words, unsigned long long* S_o, cudaStream_t st);
+// Row f3 front end: Kinect u16 depth (+ optional skin image) -> segmented packed observation.
+struct SegD {
+  int mode, lo, hi, width, keep_background;
+};
+// band_min (mode 1 only; *m preset to 0xFFFFFFFF): nearest valid (skin) depth of the frame
+cudaError_t launch_band_min(const uint16_t* depth, const uint8_t* skin, int npx, unsigned int* m,
+                            cudaStream_t st);
+cudaError_t launch_ingest(const uint16_t* depth, const uint8_t* skin, int W, int H,
+                          int pitch_words, const SegD& seg, const unsigned int* m, uint32_t* obs,
+                          unsigned long long* S_o, cudaStream_t st);
+cudaError_t launch_unpack_obs(const uint32_t* obs, int W, int H, int pitch_words, float* depth,
+                              uint8_t* mask, cudaStream_t st);
 // tev (optional, 3 events): recorded before the first launch, between the two launches of
 // the batch path, and after the last (hp_set_timing); null when timing is off
 cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUtensorMap* map,

@@ -14,6 +14,8 @@
 //   k_fk_debug : the same FK for the hp_debug_fk test hook.
 #include <math.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "fk.cuh"
 #include "pso.cuh"
@@ -49,6 +51,64 @@ __global__ void k_pack_obs(const float* __restrict__ depth, const uint8_t* __res
   }
   cnt = __reduce_add_sync(0xffffffffu, cnt);
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(S_o, (unsigned long long)cnt);
+}
+
+// ---------------------------------------------------------------------------------------
+// Row f3 observation front end ("skin colour detection and depth segmentation";
+// DESIGN AMB-33..36).  Integer mm throughout, so every decision is exact.
+//   valid = d > 0;  band = [lo, hi] (mode 0) or [m, m + width] with m the nearest valid
+//   (skin) depth (mode 1; none: empty band);  in_band = valid && lo <= d <= hi;
+//   o_s = skin ? skin && (!valid || in_band) : in_band;
+//   o_d = keep_background ? (valid ? d : 0) : (in_band ? d : 0).
+// ---------------------------------------------------------------------------------------
+__global__ void k_band_min(const uint16_t* __restrict__ depth, const uint8_t* __restrict__ skin,
+                           int npx, unsigned int* m) {
+  unsigned int best = 0xFFFFFFFFu;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npx; i += gridDim.x * blockDim.x) {
+    const unsigned int d = depth[i];
+    if (d > 0u && (skin == nullptr || skin[i] != 0)) best = min(best, d);
+  }
+  best = __reduce_min_sync(0xffffffffu, best);
+  if ((threadIdx.x & 31) == 0 && best != 0xFFFFFFFFu) atomicMin(m, best);
+}
+
+__global__ void k_ingest(const uint16_t* __restrict__ depth, const uint8_t* __restrict__ skin,
+                         int W, int H, int pitch, const SegD seg, const unsigned int* m,
+                         uint32_t* __restrict__ obs, unsigned long long* S_o) {
+  long long lo = seg.lo, hi = seg.hi;
+  if (seg.mode == 1) {
+    const unsigned int mm = *m;
+    if (mm == 0xFFFFFFFFu) {
+      lo = 1;
+      hi = 0;
+    } else {
+      lo = mm;
+      hi = (long long)mm + seg.width;
+    }
+  }
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned int cnt = 0;
+  if (i < (long long)W * H) {
+    const long long d = depth[i];
+    const bool valid = d > 0, in_band = valid && lo <= d && d <= hi;
+    const bool s = skin ? (skin[i] != 0 && (!valid || in_band)) : in_band;
+    const bool def = seg.keep_background ? valid : in_band;
+    const uint32_t bits = def ? __float_as_uint((float)d) : 0u;
+    const int y = (int)(i / W), x = (int)(i % W);
+    obs[(long long)y * pitch + x] = bits | ((uint32_t)s << 31);
+    cnt = s;
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(S_o, (unsigned long long)cnt);
+}
+
+__global__ void k_unpack_obs(const uint32_t* __restrict__ obs, int W, int H, int pitch,
+                             float* __restrict__ depth, uint8_t* __restrict__ mask) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)W * H) return;
+  const uint32_t w = obs[(i / W) * pitch + i % W];
+  if (depth) depth[i] = __uint_as_float(w & 0x7fffffffu);
+  if (mask) mask[i] = (uint8_t)(w >> 31);
 }
 
 // Per-column / per-row ray directions, correctly rounded:
@@ -1037,6 +1097,30 @@ cudaError_t launch_pack_obs(const float* depth, const uint8_t* mask, uint32_t* o
   const int threads = 256;
   const long long blocks = (npx + threads - 1) / threads;
   k_pack_obs<<<(unsigned)blocks, threads, 0, st>>>(depth, mask, obs, W, H, pitch_words, S_o);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_band_min(const uint16_t* depth, const uint8_t* skin, int npx, unsigned int* m,
+                            cudaStream_t st) {
+  const int threads = 256, blocks = std::min((npx + threads - 1) / threads, 1184);
+  if (blocks > 0) k_band_min<<<blocks, threads, 0, st>>>(depth, skin, npx, m);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ingest(const uint16_t* depth, const uint8_t* skin, int W, int H,
+                          int pitch_words, const SegD& seg, const unsigned int* m, uint32_t* obs,
+                          unsigned long long* S_o, cudaStream_t st) {
+  const long long npx = (long long)W * H;
+  k_ingest<<<(unsigned)((npx + 255) / 256), 256, 0, st>>>(depth, skin, W, H, pitch_words, seg,
+                                                           m, obs, S_o);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_obs(const uint32_t* obs, int W, int H, int pitch_words, float* depth,
+                              uint8_t* mask, cudaStream_t st) {
+  const long long npx = (long long)W * H;
+  k_unpack_obs<<<(unsigned)((npx + 255) / 256), 256, 0, st>>>(obs, W, H, pitch_words, depth,
+                                                               mask);
   return cudaGetLastError();
 }
 

@@ -62,6 +62,12 @@ _lib = None
 _VP = C.c_void_p
 
 
+class SegmentParams(C.Structure):
+    """hp_segment_params (include/hp.h, row f3)."""
+    _fields_ = [("mode", C.c_int32), ("lo_mm", C.c_int32), ("hi_mm", C.c_int32),
+                ("width_mm", C.c_int32), ("keep_background", C.c_int32)]
+
+
 def lib() -> C.CDLL:
     """Load libhp.so (raises if it was not built: run ``python -m paper_2005_07068_b200.build``)."""
     global _lib
@@ -98,6 +104,10 @@ def lib() -> C.CDLL:
             "hp_shard": [_VP, _VP, C.c_int32, C.c_int32],
             "hp_set_timing": [_VP, C.c_int32],
             "hp_set_observations": [_VP, _VP, _VP, C.c_int32, C.c_int32, _VP],
+            "hp_default_segment": [C.POINTER(SegmentParams)],
+            "hp_set_observation_kinect": [_VP, _VP, _VP, C.c_int32, C.POINTER(SegmentParams),
+                                          C.c_int32, _VP, _VP],
+            "hp_get_observation": [_VP, C.c_int32, _VP, _VP, _VP],
             "hp_eval_costs_frames": [_VP, _VP, C.c_int64, _VP, _VP],
             "hp_eval_sums_frames": [_VP, _VP, C.c_int64, _VP, _VP, _VP],
             "hp_last_kernel_ms": [_VP, _VP],
@@ -127,7 +137,8 @@ def exported_symbols():
             "hp_splits_for", "hp_last_error", "hp_destroy", "hp_shard_range",
             "hp_nccl_available", "hp_get_nccl_id", "hp_shard", "hp_track",
             "hp_set_timing", "hp_last_kernel_ms", "hp_set_observations",
-            "hp_eval_costs_frames", "hp_eval_sums_frames"]
+            "hp_eval_costs_frames", "hp_eval_sums_frames", "hp_default_segment",
+            "hp_set_observation_kinect", "hp_get_observation"]
 
 
 def _check(status: int, ctx=None):
@@ -312,6 +323,41 @@ class Context:
             _check(self._L.hp_set_observations(self._h, _dptr(depth), _dptr(mask),
                                                depth.shape[0], 1, _stream(stream)), self._h)
         self.frames = int(depth.shape[0])
+
+    def set_observation_kinect(self, depth_u16, skin=None, mode: int = 1, lo_mm: int = 0,
+                               hi_mm: int = 0, width_mm: int = 250,
+                               keep_background: bool = False, stream=None):
+        """Row f3 front end: Kinect u16 depth [H][W] or [M][H][W] (+ optional u8 skin image),
+        numpy (host) or CUDA tensors (device) -> segmented observation frames.  Returns the
+        band used per frame as an int array [M][2]."""
+        seg = SegmentParams(mode, lo_mm, hi_mm, width_mm, int(keep_background))
+        if isinstance(depth_u16, np.ndarray):
+            d = np.ascontiguousarray(depth_u16, dtype=np.uint16)
+            sk = None if skin is None else np.ascontiguousarray(skin, dtype=np.uint8)
+            shape, dp, sp, dev = d.shape, d.ctypes.data, (None if sk is None else sk.ctypes.data), 0
+        else:
+            import torch
+
+            assert depth_u16.dtype in (torch.uint16, torch.int16) and depth_u16.is_contiguous()
+            shape, dp, dev = tuple(depth_u16.shape), _dptr(depth_u16), 1
+            sp = None if skin is None else _dptr(skin)
+        frames = 1 if len(shape) == 2 else shape[0]
+        assert tuple(shape[-2:]) == (self.height, self.width)
+        band = np.zeros((frames, 2), np.int32)
+        _check(self._L.hp_set_observation_kinect(self._h, dp, sp, frames, C.byref(seg), dev,
+                                                 band.ctypes.data, _stream(stream)), self._h)
+        self.frames = frames
+        return band
+
+    def get_observation(self, frame: int = 0, stream=None):
+        """(O_d fp32 [H][W], O_s u8 [H][W]) CUDA tensors of observation frame `frame`."""
+        import torch
+
+        d = torch.empty((self.height, self.width), dtype=torch.float32, device="cuda")
+        m = torch.empty((self.height, self.width), dtype=torch.uint8, device="cuda")
+        _check(self._L.hp_get_observation(self._h, frame, _dptr(d), _dptr(m), _stream(stream)),
+               self._h)
+        return d, m
 
     def render_observation(self, h_ref, stream=None):
         """Simulation protocol: render h_ref on the GPU -> (depth, mask) tensors."""
