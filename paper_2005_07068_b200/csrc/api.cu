@@ -115,7 +115,6 @@ struct hp_ctx {
   float* ray = nullptr;  // per-column / per-row ray directions (k_ray_table)
   unsigned int* pcount = nullptr;  // persistent-kernel counters (zero between launches)
   int persist_grid = 0;            // CTAs of the persistent kernels (0 = never use them)
-  int two_kernel = 1;              // k_fk_batch + k_render_persist (HP_PERSIST_PRODUCER=1: 0)
   void* fk_g = nullptr;            // FkOut [max_n]
   uint4* tiles_g = nullptr;        // [max_n][kMaxTiles]
   int* ntl_g = nullptr;            // [max_n]
@@ -442,7 +441,6 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   CKC(cudaMalloc(&ctx->fk_g, (size_t)max_particles * fk_record_bytes()));
   CKC(cudaMalloc(&ctx->tiles_g, (size_t)max_particles * kMaxTiles * sizeof(uint4)));
   CKC(cudaMalloc(&ctx->ntl_g, (size_t)max_particles * sizeof(int)));
-  if (const char* e = getenv("HP_PERSIST_PRODUCER")) ctx->two_kernel = atoi(e) ? 0 : 1;
   CKC(cudaMalloc(&ctx->pcount, 2 * sizeof(unsigned int)));
   CKC(cudaMemset(ctx->pcount, 0, 2 * sizeof(unsigned int)));
   ctx->blocks_per_sm = persist_blocks_per_sm(ctx->camp);
@@ -652,7 +650,6 @@ static EvalArgs base_args(hp_ctx* ctx) {
   a.fk_g = ctx->fk_g;
   a.tiles_g = ctx->tiles_g;
   a.ntl_g = ctx->ntl_g;
-  a.two_kernel = ctx->two_kernel;
   return a;
 }
 
@@ -703,7 +700,7 @@ static hp_status eval_common(hp_ctx* ctx, const float* poses, int64_t n, float* 
   ctx->timed = ctx->timing;
   if (ctx->sync_debug) CK(cudaStreamSynchronize(s));
   // the batch path is two kernels (FK, then the persistent renderer)
-  ctx->last_launches = (a.S == 1 && a.persist_grid > 0 && a.two_kernel) ? 2 : 1;
+  ctx->last_launches = (a.S == 1 && a.persist_grid > 0) ? 2 : 1;
   return HP_OK;
 }
 

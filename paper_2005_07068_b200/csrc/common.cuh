@@ -112,7 +112,8 @@ struct EvalArgs {
   const CUtensorMap* tmap_g;      // the same descriptor in global memory (use_tma = 2)
   const float* ray;               // k_ray_table output: dx[W + pad], dy[H + pad]
   unsigned int* pcount;           // [2] persistent kernel: particle counter, CTA exit counter
-  int persist_grid;               // > 0: use k_eval_persist with this many CTAs
+  int persist_grid;               // > 0: batch path (k_fk_batch + k_render_persist) with
+                                  // this many renderer CTAs
   // PSO generation mode (hp_pso_fit): fused update before FK, fused bookkeeping at the end
   int pso_on, pso_k;
   PsoDev pso;
@@ -125,7 +126,6 @@ struct EvalArgs {
   void* fk_g;                     // FkOut [n] (16-byte aligned records)
   uint4* tiles_g;                 // [n][kMaxTiles] (X0 | Y0 << 16, sphere, cone, ell masks)
   int* ntl_g;                     // [n] tile-list length (-1: box too large, cull on the fly)
-  int two_kernel;                 // 1: k_fk_batch + k_render_persist, 0: k_eval_persist
 };
 
 // Observation frame of pose p; frame f occupies rows [f H, (f + 1) H) of the packed buffer

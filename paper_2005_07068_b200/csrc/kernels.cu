@@ -20,12 +20,6 @@
 #include "fk.cuh"
 #include "pso.cuh"
 
-#ifndef HP_NSLOT
-#define HP_NSLOT 2
-#endif
-#ifndef HP_PTEAM
-#define HP_PTEAM 1
-#endif
 #ifndef HP_MINB_WARPS
 #define HP_MINB_WARPS 24  // resident warps per SM the register budget is sized for
 #endif
@@ -614,198 +608,6 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   if (s_lastcta) pso_book_block(a.pso, a.pso_k, a.pso_k >= 1 ? a.x_out : a.pso.X);
 }
 
-// ---------------------------------------------------------------------------------------
-// k_eval_persist: persistent, warp-specialised version for large swarms (one CTA per SM
-// slot, one particle at a time per CTA).  Warp 0 is the FK producer: it fetches the next
-// particle from a global counter and runs FK into one of two shared-memory slots while
-// warps 1..NW-1 render the particle in the other slot, so FK latency is hidden behind
-// rendering; once its FK is done, warp 0 joins the rendering.  Slots are handed over with
-// mbarriers (full: producer -> renderers, empty: all warps -> producer).  A particle's sums
-// accumulate in shared memory; the last warp to finish computes Eq. (4)-(5).
-// ---------------------------------------------------------------------------------------
-template <int NW, typename PoseT>
-__global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
-    k_eval_persist(const EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
-  constexpr int NS = HP_NSLOT;   // particle slots: the producers run up to NS - 1 ahead
-  constexpr int PT = HP_PTEAM;   // producer team: 1 or 2 warps
-  __shared__ FkScratch s_fk;
-  __shared__ __align__(16) FkOut s_out[NS];
-  __shared__ __align__(128) uint32_t s_obs[NW][kTileW * kTileH];
-  __shared__ __align__(8) uint64_t s_bar[NW];
-  __shared__ __align__(8) uint64_t s_full[NS], s_empty[NS];
-  __shared__ unsigned long long s_acc[NS][4];
-  __shared__ int s_next[NS], s_done[NS], s_pid[NS], s_ntl[NS], s_fetch;
-  __shared__ uint4 s_tiles[NS][kMaxTiles];  // (X0 | Y0 << 16, sphere, cone, ellipsoid masks)
-  extern __shared__ float s_ray[];
-
-  if (a.done && *a.done) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const float* s_dx = s_ray;
-  const float* s_dy = s_ray + ray_dx_len(a.cam.W);
-  if (threadIdx.x == 0) {
-    for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);
-    for (int b = 0; b < NS; b++) {
-      mbar_init(&s_full[b], PT * 32);  // every producer lane releases its writes
-      mbar_init(&s_empty[b], NW * 32); // every lane arrives once its reads are done
-      s_next[b] = 0;
-      s_done[b] = 0;
-      for (int k = 0; k < 4; k++) s_acc[b][k] = 0;
-    }
-    fence_mbar_init();
-    if (a.use_tma == 1) prefetch_tmap(&tmap);
-  }
-  {
-    const int n4 = ray_floats(a.cam.W, a.cam.H) / 4;
-    for (int i = threadIdx.x; i < n4; i += NW * 32)
-      reinterpret_cast<float4*>(s_ray)[i] = __ldg(reinterpret_cast<const float4*>(a.ray) + i);
-  }
-  __syncthreads();
-
-  // Render (this warp's share of) particle p in slot b; the last of the NW warps to finish
-  // computes Eq. (4)-(5) and resets the slot's shared accumulators.
-  uint32_t phase = 0;
-  auto consume = [&](int p, int b) {
-    const FkOut& fo = s_out[b];
-    const int yoff = frame_of(a, p) * a.cam.H;
-    const TileGrid g(fo.ubox);
-    const int nlist = s_ntl[b];  // >= 0: the producer's list of non-empty tiles + masks
-    const int nt = nlist >= 0 ? nlist : g.ntiles;
-    TileSums acc;
-    int t = 0;
-    if (lane == 0) t = atomicAdd(&s_next[b], 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    while (t < nt) {
-      int tn = 0;
-      if (lane == 0) tn = atomicAdd(&s_next[b], 1);
-      int X0, Y0;
-      uint3 km;
-      if (nlist >= 0) {
-        const uint4 it = s_tiles[b][t];
-        X0 = (int)(it.x & 0xFFFFu);
-        Y0 = (int)(it.x >> 16);
-        km = make_uint3(it.y, it.z, it.w);
-      } else {
-        g.origin(t, X0, Y0);
-        km = cull_tile(fo, X0, Y0);
-      }
-      if (km.x | km.y | km.z)
-        do_tile<kModeCost>(a, &tmap, fo, X0, Y0, km, s_obs[warp], &s_bar[warp], phase, s_dx,
-                           s_dy, acc, yoff);
-      t = __shfl_sync(0xffffffffu, tn, 0);
-    }
-    warp_reduce(acc);
-    if (lane == 0) {
-      if (acc.rm) atomicAdd(&s_acc[b][0], (unsigned long long)acc.rm);
-      if (acc.and_) atomicAdd(&s_acc[b][1], (unsigned long long)acc.and_);
-      if (acc.num) atomicAdd(&s_acc[b][2], acc.num);
-      if (acc.both) atomicAdd(&s_acc[b][3], (unsigned long long)acc.both);
-      __threadfence_block();
-      if (atomicAdd(&s_done[b], 1) == NW - 1) {  // last warp for this particle
-        __threadfence_block();
-        unsigned long long v[4];
-        for (int k = 0; k < 4; k++) {
-          v[k] = s_acc[b][k];
-          s_acc[b][k] = 0;
-        }
-        finalize_cost(a, p, v, fo.kc);
-        s_next[b] = 0;
-        s_done[b] = 0;
-      }
-    }
-    __syncwarp();
-    mbar_arrive(&s_empty[b]);
-  };
-
-  if (warp < PT) {
-    // ---- producer team (warps 0..PT-1): fetch + FK + tile list for particle
-    // j = i + 1 while the other warps render particle i, then help render particle i ----
-    auto produce = [&](int j) {
-      const int b = j % NS;
-      if (j >= NS) mbar_wait(&s_empty[b], ((j / NS) - 1) & 1);  // particle j - NS released
-      int p;
-      if (PT == 2) {
-        if (threadIdx.x == 0) s_fetch = (int)atomicAdd(a.pcount, 1u);
-        asm volatile("bar.sync 3, 64;" ::: "memory");
-        p = s_fetch;
-        asm volatile("bar.sync 3, 64;" ::: "memory");  // s_fetch may be overwritten next time
-      } else {
-        p = lane == 0 ? (int)atomicAdd(a.pcount, 1u) : 0;
-        p = __shfl_sync(0xffffffffu, p, 0);
-      }
-      if (threadIdx.x == 0) s_pid[b] = p;
-      if (p < a.n) {
-        const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
-        fk_team<PoseT, PT>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out[b]);
-        if (PT == 2) asm volatile("bar.sync 3, 64;" ::: "memory");  // warp 1's records done
-        // the particle's non-empty tiles with their cull masks, row-major, one tile per
-        // lane of warp 0 (a box too large for the list falls back to culling on the fly)
-        if (warp == 0) {
-          const FkOut& fo = s_out[b];
-          const TileGrid g(fo.ubox);
-          int cnt = -1;
-          if (g.ntiles <= kMaxTiles) {
-            cnt = 0;
-            for (int base = 0; base < g.ntiles; base += 32) {
-              const int t = base + lane;
-              unsigned int m0 = 0, m1 = 0, m2 = 0;
-              int X0 = 0, Y0 = 0;
-              if (t < g.ntiles) {
-                g.origin(t, X0, Y0);
-#pragma unroll
-                for (int jj = 0; jj < kNprim; jj++) {
-                  const int4 bb = fo.box[jj];
-                  const unsigned int ov = bb.x <= X0 + kTileW - 1 && bb.z >= X0 &&
-                                          bb.y <= Y0 + kTileH - 1 && bb.w >= Y0;
-                  if (jj < kCone0) m0 |= ov << jj;
-                  else if (jj < kEll0) m1 |= ov << (jj - kCone0);
-                  else m2 |= ov << (jj - kEll0);
-                }
-              }
-              const bool ne = (m0 | m1 | m2) != 0;
-              const unsigned int bal = __ballot_sync(0xffffffffu, ne);
-              if (ne)
-                s_tiles[b][cnt + __popc(bal & ((1u << lane) - 1u))] =
-                    make_uint4((unsigned)X0 | ((unsigned)Y0 << 16), m0, m1, m2);
-              cnt += __popc(bal);
-            }
-          }
-          if (lane == 0) s_ntl[b] = cnt;
-        }
-      }
-      __syncwarp();
-      mbar_arrive(&s_full[b]);
-      return p;
-    };
-    int pcur = produce(0);
-    for (int i = 0; pcur < a.n; i++) {
-      const int pnext = produce(i + 1);
-      // wait until particle i's slot is published (both producer warps contribute)
-      mbar_wait(&s_full[i % NS], (i / NS) & 1);
-      consume(pcur, i % NS);
-      pcur = pnext;
-    }
-  } else {
-    // ---- renderers ----
-    for (int i = 0;; i++) {
-      const int b = i % NS;
-      mbar_wait(&s_full[b], (i / NS) & 1);
-      const int p = s_pid[b];
-      if (p >= a.n) break;
-      consume(p, b);
-    }
-  }
-  // the last CTA to leave resets the particle counter for the next launch
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(a.pcount + 1, 1u) == gridDim.x - 1) {
-      a.pcount[0] = 0;
-      a.pcount[1] = 0;
-      __threadfence();
-    }
-  }
-}
-
 __global__ void k_fk_debug(const double* pose, const DimsD dims, const CamParams cam,
                            float* rec, int* boxes, double* joints, double* kc) {
   __shared__ FkScratch s;
@@ -1063,11 +865,7 @@ static void set_carveouts() {
   if (done) return;
   done = true;
   const int pct = cudaSharedmemCarveoutMaxShared;
-  cudaFuncSetAttribute(k_eval_persist<kEvalWarps, float>,
-                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
   cudaFuncSetAttribute(k_render_persist<kEvalWarps>,
-                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-  cudaFuncSetAttribute(k_eval_persist<kEvalWarps, double>,
                        cudaFuncAttributePreferredSharedMemoryCarveout, pct);
   cudaFuncSetAttribute(k_eval<kEvalWarps, float, kModeCost>,
                        cudaFuncAttributePreferredSharedMemoryCarveout, pct);
@@ -1133,7 +931,7 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
                         cudaStream_t st, cudaEvent_t* tev) {
   const long long blocks = (long long)a.n * a.S;
   if (blocks == 0) return cudaSuccess;
-  const bool two = mode == kModeCost && a.S == 1 && a.persist_grid > 0 && a.two_kernel;
+  const bool two = mode == kModeCost && a.S == 1 && a.persist_grid > 0;
   if (tev) {
     cudaEventRecord(tev[0], st);
     if (!two) cudaEventRecord(tev[1], st);  // single-launch paths: empty first interval
@@ -1151,12 +949,6 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     k_render_persist<kEvalWarps><<<pgrid, block, dyn, st>>>(a, *map);
     if (tev) cudaEventRecord(tev[2], st);
     return cudaGetLastError();
-  } else if (mode == kModeCost && a.S == 1 && a.persist_grid > 0) {
-    const dim3 pgrid((unsigned)(a.persist_grid < a.n ? a.persist_grid : a.n));
-    if (pose_double)
-      k_eval_persist<kEvalWarps, double><<<pgrid, block, dyn, st>>>(a, *map);
-    else
-      k_eval_persist<kEvalWarps, float><<<pgrid, block, dyn, st>>>(a, *map);
   } else if (mode == kModeCost && a.pdl && pose_double) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
