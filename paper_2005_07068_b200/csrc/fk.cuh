@@ -346,7 +346,13 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
     }
     asm volatile("bar.sync 1, 64;" ::: "memory");
   } else {
-    for (int j = lane; j < kNprim; j += 32) {
+    // 38 records on 32 lanes: lanes 0..9 build two spheres each (the cheapest records),
+    // lanes 10..27 one cone / cylinder / ellipsoid each, so no lane builds a sphere AND an
+    // expensive record (the critical path of j = lane, lane + 32)
+    static_assert(kCone0 == 20 && kNprim == 38, "lane map assumes 20 spheres + 18 others");
+    const int nj = lane < 10 ? 2 : (lane < 28 ? 1 : 0);
+    for (int k = 0; k < nj; k++) {
+      const int j = lane < 10 ? 2 * lane + k : lane + 10;
       float zmin;
       build_prim(j, s, dm, cam, out.rec[j], out.box[j], zmin);
       s.nearf[j] = zmin > cam.znear * 1.001f;
