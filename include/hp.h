@@ -181,7 +181,9 @@ hp_status hp_eval_sums_frames(hp_ctx* ctx, const float* poses_dev, int64_t n_per
                               uint64_t* sums_dev, double* costs64_dev, void* stream);
 
 /* Same with HOST buffers: copies poses in, scores, copies costs out, then synchronises
- * `stream` (the end-to-end path a host application calls). */
+ * `stream` (the end-to-end path a host application calls).  Page-locked buffers
+ * (cudaHostAlloc, cudaHostRegister, torch pin_memory) are DMA'd directly; pageable ones are
+ * staged through the context's pinned buffers (one extra host memcpy each way). */
 hp_status hp_eval_costs_host(hp_ctx* ctx, const float* poses_host, int64_t n,
                              float* costs_host, void* stream);
 

@@ -777,6 +777,15 @@ hp_status hp_eval_sums_frames(hp_ctx* ctx, const float* poses, int64_t n_per_fra
                      n_per_frame);
 }
 
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();  // clear the sticky-free error of an unknown pointer
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 hp_status hp_eval_costs_host(hp_ctx* ctx, const float* poses, int64_t n, float* costs,
                              void* stream) {
   ARG(ctx, "hp_eval_costs_host: NULL ctx");
@@ -791,9 +800,11 @@ hp_status hp_eval_costs_host(hp_ctx* ctx, const float* poses, int64_t n, float* 
     const int64_t chunk = (n + ctx->world - 1) / ctx->world;
     int64_t b, e;
     shard_range(n, ctx->rank, ctx->world, &b, &e);
-    memcpy(ctx->h_poses, poses + b * kNdof, (size_t)(e - b) * kNdof * sizeof(float));
+    const size_t in_bytes = (size_t)(e - b) * kNdof * sizeof(float);
+    const bool in_pinned = is_pinned(poses), out_pinned = is_pinned(costs);
+    if (!in_pinned) memcpy(ctx->h_poses, poses + b * kNdof, in_bytes);
     if (e > b) {
-      CK(cudaMemcpyAsync(ctx->poses32, ctx->h_poses, (size_t)(e - b) * kNdof * sizeof(float),
+      CK(cudaMemcpyAsync(ctx->poses32, in_pinned ? poses + b * kNdof : ctx->h_poses, in_bytes,
                          cudaMemcpyHostToDevice, s));
       hp_status r = eval_common(ctx, ctx->poses32, e - b, ctx->gat32 + ctx->rank * chunk,
                                 nullptr, nullptr, s);
@@ -805,22 +816,28 @@ hp_status hp_eval_costs_host(hp_ctx* ctx, const float* poses, int64_t n, float* 
       ctx->err = std::string("ncclAllGather: ") + nccl_api()->errorString(nr);
       return HP_ERR_NCCL;
     }
-    CK(cudaMemcpyAsync(ctx->h_costs, ctx->gat32, (size_t)n * sizeof(float),
+    CK(cudaMemcpyAsync(out_pinned ? costs : ctx->h_costs, ctx->gat32, (size_t)n * sizeof(float),
                        cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    memcpy(costs, ctx->h_costs, (size_t)n * sizeof(float));
+    if (!out_pinned) memcpy(costs, ctx->h_costs, (size_t)n * sizeof(float));
     return HP_OK;
   }
-  // pinned staging so the copies are true async DMA
-  memcpy(ctx->h_poses, poses, (size_t)n * kNdof * sizeof(float));
-  CK(cudaMemcpyAsync(ctx->poses32, ctx->h_poses, (size_t)n * kNdof * sizeof(float),
-                     cudaMemcpyHostToDevice, s));
+  // Page-locked caller buffers (cudaHostAlloc / cudaHostRegister / torch pin_memory) are
+  // DMA'd directly; pageable ones go through the context's pinned staging buffers.
+  const size_t in_bytes = (size_t)n * kNdof * sizeof(float), out_bytes = (size_t)n * 4;
+  const bool in_pinned = is_pinned(poses), out_pinned = is_pinned(costs);
+  const float* src = poses;
+  if (!in_pinned) {
+    memcpy(ctx->h_poses, poses, in_bytes);
+    src = ctx->h_poses;
+  }
+  CK(cudaMemcpyAsync(ctx->poses32, src, in_bytes, cudaMemcpyHostToDevice, s));
   hp_status r = eval_common(ctx, ctx->poses32, n, ctx->costs32, nullptr, nullptr, s);
   if (r != HP_OK) return r;
-  CK(cudaMemcpyAsync(ctx->h_costs, ctx->costs32, (size_t)n * sizeof(float),
+  CK(cudaMemcpyAsync(out_pinned ? costs : ctx->h_costs, ctx->costs32, out_bytes,
                      cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  memcpy(costs, ctx->h_costs, (size_t)n * sizeof(float));
+  if (!out_pinned) memcpy(costs, ctx->h_costs, out_bytes);
   return HP_OK;
 }
 

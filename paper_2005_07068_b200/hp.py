@@ -407,10 +407,14 @@ class Context:
                                            _stream(stream)), self._h)
         return sums, costs
 
-    def eval_costs_host(self, poses: np.ndarray, stream=None) -> np.ndarray:
-        """Host-buffer variant: copies in, scores, copies out, synchronises."""
+    def eval_costs_host(self, poses: np.ndarray, out: np.ndarray | None = None,
+                        stream=None) -> np.ndarray:
+        """Host-buffer variant: copies in, scores, copies out, synchronises.  Page-locked
+        arrays (e.g. numpy views of torch pin_memory tensors) are DMA'd directly."""
         p = np.ascontiguousarray(poses, dtype=np.float32).reshape(-1, NDOF)
-        out = np.empty(p.shape[0], dtype=np.float32)
+        if out is None:
+            out = np.empty(p.shape[0], dtype=np.float32)
+        assert out.dtype == np.float32 and out.flags.c_contiguous and out.size >= p.shape[0]
         _check(self._L.hp_eval_costs_host(self._h, p.ctypes.data, p.shape[0], out.ctypes.data,
                                           _stream(stream)), self._h)
         return out

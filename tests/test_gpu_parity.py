@@ -192,6 +192,11 @@ def test_determinism_permutation_and_host_path():
     assert np.array_equal(s_p, s_a[perm]) and np.array_equal(c_p, c_a[perm])
     host = ctx.eval_costs_host(P)
     assert np.array_equal(host, c_a.astype(np.float32))
+    # page-locked caller buffers take the direct-DMA path: same bits
+    pin_in = torch.from_numpy(P.copy()).pin_memory()
+    pin_out = torch.zeros(len(P), dtype=torch.float32).pin_memory()
+    ctx.eval_costs_host(pin_in.numpy(), out=pin_out.numpy())
+    assert np.array_equal(pin_out.numpy(), host)
 
 
 def test_edge_cases():
