@@ -443,8 +443,8 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   CKC(cudaMalloc(&ctx->ntl_g, (size_t)max_particles * sizeof(int)));
   CKC(cudaMalloc(&ctx->pcount, 2 * sizeof(unsigned int)));
   CKC(cudaMemset(ctx->pcount, 0, 2 * sizeof(unsigned int)));
-  ctx->blocks_per_sm = persist_blocks_per_sm(ctx->camp);
-  ctx->persist_grid = ctx->sm_count * ctx->blocks_per_sm;
+  ctx->blocks_per_sm = eval_blocks_per_sm(ctx->camp);
+  ctx->persist_grid = ctx->sm_count * persist_blocks_per_sm(ctx->camp);
   if (const char* e = getenv("HP_NO_PERSIST"))
     if (atoi(e)) ctx->persist_grid = 0;
   CKC(cudaMalloc(&ctx->tmap_g, sizeof(CUtensorMap)));

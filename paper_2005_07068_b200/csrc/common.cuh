@@ -256,6 +256,7 @@ cudaError_t launch_ray_table(const CamParams& cam, float* ray, cudaStream_t st);
 cudaError_t launch_depth_to_mask(const float* depth, uint8_t* mask, int npx, cudaStream_t st);
 int eval_warps_per_cta();
 int persist_blocks_per_sm(const CamParams& cam);
+int eval_blocks_per_sm(const CamParams& cam);  // resident k_eval CTAs per SM
 size_t fk_record_bytes();
 
 // PSO (pso.cu)

@@ -20,8 +20,13 @@
 #include "fk.cuh"
 #include "pso.cuh"
 
+// resident warps per SM the register budgets are sized for: 64 registers, 4 CTAs x 8 warps
+// per SM (the renderer has no spills; k_eval's cost path spills 8 bytes, harmless)
 #ifndef HP_MINB_WARPS
-#define HP_MINB_WARPS 24  // resident warps per SM the register budget is sized for
+#define HP_MINB_WARPS 32
+#endif
+#ifndef HP_MINB_WARPS_EVAL
+#define HP_MINB_WARPS_EVAL 32
 #endif
 
 namespace hp {
@@ -495,7 +500,7 @@ __device__ __forceinline__ void finalize_cost(const EvalArgs& a, int p, const un
 // (S > 1 splits per particle keep every SM busy) and for the depth-image hooks.
 // ---------------------------------------------------------------------------------------
 template <int NW, typename PoseT, int MODE>
-__global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
+__global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
     k_eval(const EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
   __shared__ FkScratch s_fk;
   __shared__ __align__(16) FkOut s_out;
@@ -878,6 +883,16 @@ static void set_carveouts() {
 }
 
 size_t fk_record_bytes() { return sizeof(FkOut); }
+
+int eval_blocks_per_sm(const CamParams& cam) {
+  set_carveouts();
+  int nb = 0;
+  const size_t dyn = (size_t)ray_floats(cam.W, cam.H) * sizeof(float);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &nb, k_eval<kEvalWarps, double, kModeCost>, kEvalWarps * 32, dyn) != cudaSuccess)
+    return 0;
+  return nb;
+}
 
 int persist_blocks_per_sm(const CamParams& cam) {
   set_carveouts();
