@@ -692,6 +692,9 @@ __device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out, uint
   return cnt;
 }
 
+#ifndef HP_FK_PDL
+#define HP_FK_PDL 1  // programmatic dependent launch of k_render_persist after k_fk_batch
+#endif
 #ifndef HP_FK_TEAM
 #define HP_FK_TEAM 1
 #endif
@@ -707,6 +710,11 @@ __global__ void __launch_bounds__(kFkWarps * 32, kFkTeam == 2 ? 16 : 8)
   __shared__ __align__(16) FkOut s_out[kFkPerCta];
   static_assert(sizeof(FkScratch) >= 2 * kMaxBand * sizeof(uint2), "band masks alias s_fk");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if HP_FK_PDL
+  // the renderer (launched with programmatic stream serialisation) may start its prologue
+  // on SMs this grid frees; it waits for this grid's completion before reading its output
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   const int slot = kFkTeam == 2 ? 0 : warp;
   const int p = blockIdx.x * kFkPerCta + slot;
   if (p >= a.n) return;  // uniform per team; only team-local barriers below
@@ -775,6 +783,9 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     }
     fence_mbar_init();
     if (a.use_tma == 1) prefetch_tmap(&tmap);
+#if HP_FK_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // k_fk_batch complete and visible
+#endif
     issue(0);
     issue(1);
   }
@@ -961,7 +972,22 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     if (e != cudaSuccess) return e;
     if (tev) cudaEventRecord(tev[1], st);
     const dim3 pgrid((unsigned)(a.persist_grid < a.n ? a.persist_grid : a.n));
+#if HP_FK_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = pgrid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k_render_persist<kEvalWarps>, a, *map);
+    if (e != cudaSuccess) return e;
+#else
     k_render_persist<kEvalWarps><<<pgrid, block, dyn, st>>>(a, *map);
+#endif
     if (tev) cudaEventRecord(tev[2], st);
     return cudaGetLastError();
   } else if (mode == kModeCost && a.pdl && pose_double) {
