@@ -118,6 +118,8 @@ struct hp_ctx {
   void* fk_g = nullptr;            // FkOut [max_n]
   uint4* tiles_g = nullptr;        // [max_n][kMaxTiles]
   int* ntl_g = nullptr;            // [max_n]
+  int* near_list = nullptr;        // [max_n] near-plane pass queue
+  unsigned int* near_count = nullptr;
   int blocks_per_sm = 0;           // resident k_eval CTAs per SM
   // particle-sharded mode (hp_shard): rank r owns poses [r chunk, (r + 1) chunk)
   ncclComm_t comm = nullptr;
@@ -287,7 +289,8 @@ void hp_destroy(hp_ctx* ctx) {
                  ctx->poses32, ctx->costs32, ctx->scratch, ctx->X, ctx->V, ctx->P, ctx->Pc,
                  ctx->E, ctx->G, ctx->Gc, ctx->trace, ctx->bnd, ctx->centre, ctx->mark,
                  ctx->flags, ctx->dyn, ctx->tmap_g, ctx->ray, ctx->pcount, ctx->X2,
-                 ctx->V2, ctx->gcount, ctx->fk_g, ctx->tiles_g, ctx->ntl_g};
+                 ctx->V2, ctx->gcount, ctx->fk_g, ctx->tiles_g, ctx->ntl_g, ctx->near_list,
+                 ctx->near_count};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_poses) cudaFreeHost(ctx->h_poses);
@@ -441,8 +444,11 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   CKC(cudaMalloc(&ctx->fk_g, (size_t)max_particles * fk_record_bytes()));
   CKC(cudaMalloc(&ctx->tiles_g, (size_t)max_particles * kMaxTiles * sizeof(uint4)));
   CKC(cudaMalloc(&ctx->ntl_g, (size_t)max_particles * sizeof(int)));
-  CKC(cudaMalloc(&ctx->pcount, 2 * sizeof(unsigned int)));
-  CKC(cudaMemset(ctx->pcount, 0, 2 * sizeof(unsigned int)));
+  CKC(cudaMalloc(&ctx->pcount, 4 * sizeof(unsigned int)));
+  CKC(cudaMemset(ctx->pcount, 0, 4 * sizeof(unsigned int)));
+  CKC(cudaMalloc(&ctx->near_list, (size_t)max_particles * sizeof(int)));
+  CKC(cudaMalloc(&ctx->near_count, sizeof(unsigned int)));
+  CKC(cudaMemset(ctx->near_count, 0, sizeof(unsigned int)));
   ctx->blocks_per_sm = eval_blocks_per_sm(ctx->camp);
   ctx->persist_grid = ctx->sm_count * persist_blocks_per_sm(ctx->camp);
   if (const char* e = getenv("HP_NO_PERSIST"))
@@ -650,6 +656,8 @@ static EvalArgs base_args(hp_ctx* ctx) {
   a.fk_g = ctx->fk_g;
   a.tiles_g = ctx->tiles_g;
   a.ntl_g = ctx->ntl_g;
+  a.near_list = ctx->near_list;
+  a.near_count = ctx->near_count;
   return a;
 }
 
@@ -699,8 +707,8 @@ static hp_status eval_common(hp_ctx* ctx, const float* poses, int64_t n, float* 
   CK(launch_eval(a, false, kModeCost, &ctx->tmap, s, ctx->timing ? ctx->tev : nullptr));
   ctx->timed = ctx->timing;
   if (ctx->sync_debug) CK(cudaStreamSynchronize(s));
-  // the batch path is two kernels (FK, then the persistent renderer)
-  ctx->last_launches = (a.S == 1 && a.persist_grid > 0) ? 2 : 1;
+  // the batch path is three kernels (FK, the persistent renderer, its near-plane pass)
+  ctx->last_launches = (a.S == 1 && a.persist_grid > 0) ? 3 : 1;
   return HP_OK;
 }
 

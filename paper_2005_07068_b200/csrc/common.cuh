@@ -111,7 +111,8 @@ struct EvalArgs {
   int use_tma;                    // 1: TMA tile loads (default), 0: plain loads
   const CUtensorMap* tmap_g;      // the same descriptor in global memory (use_tma = 2)
   const float* ray;               // k_ray_table output: dx[W + pad], dy[H + pad]
-  unsigned int* pcount;           // [2] persistent kernel: particle counter, CTA exit counter
+  unsigned int* pcount;           // [4] persistent kernels (batch pass, near-plane pass):
+                                  // particle counter, CTA exit counter
   int persist_grid;               // > 0: batch path (k_fk_batch + k_render_persist) with
                                   // this many renderer CTAs
   // PSO generation mode (hp_pso_fit): fused update before FK, fused bookkeeping at the end
@@ -125,7 +126,10 @@ struct EvalArgs {
   // k_render_persist bulk-copies them into shared memory
   void* fk_g;                     // FkOut [n] (16-byte aligned records)
   uint4* tiles_g;                 // [n][kMaxTiles] (X0 | Y0 << 16, sphere, cone, ell masks)
-  int* ntl_g;                     // [n] tile-list length (-1: box too large, cull on the fly)
+  int* ntl_g;                     // [n] tile-list length (-1: box too large, cull on the fly;
+                                  // -2: queued for the near-plane pass)
+  int* near_list;                 // [n] particles whose primitives may cross z_near
+  unsigned int* near_count;       // their number (reset by the near-plane pass)
 };
 
 // Observation frame of pose p; frame f occupies rows [f H, (f + 1) H) of the packed buffer

@@ -242,8 +242,19 @@ __device__ __forceinline__ void isect_sphere(const float* __restrict__ r, Lane4&
     const f2 m = mul2(fma2(ox, ox, fma2(oy, oy, fma2(oz, oz, bc(-q.w)))), idd);
     float m0, m1;
     unpk(m, m0, m1);
-    keep2<CHK>(fma2(m, pk(rsqrt_approx(-m0), rsqrt_approx(-m1)), tc), L.zb[2 * j],
-               L.zb[2 * j + 1], znear);
+    if (CHK) {
+      // exact solid semantics near the camera (DESIGN §2 render definition): the smallest
+      // t > 0 on the surface — the exit root when the camera is inside the sphere
+      const f2 h = mul2(m, pk(rsqrt_approx(-m0), rsqrt_approx(-m1)));  // -sqrt(-m)
+      float t10, t11, t20, t21;
+      unpk(add2(tc, h), t10, t11);
+      unpk(sub2(tc, h), t20, t21);
+      keep<true>(t10 > 0.f ? t10 : t20, L.zb[2 * j], znear);
+      keep<true>(t11 > 0.f ? t11 : t21, L.zb[2 * j + 1], znear);
+    } else {
+      keep2<false>(fma2(m, pk(rsqrt_approx(-m0), rsqrt_approx(-m1)), tc), L.zb[2 * j],
+                   L.zb[2 * j + 1], znear);
+    }
   }
 }
 
@@ -272,8 +283,17 @@ __device__ __forceinline__ void isect_ellipsoid(const float* __restrict__ r, Lan
     const f2 disc = sub2(mul2(B, B), mul2(A, C));
     // A > 0: the smaller root; only the absolute error of s matters (z = t_c + s), so the
     // plain form is accurate to ~1e-6 mm here
-    const f2 s = mul2(add2(B, sqrt2(disc)), nrcp2(A));
-    keep2<CHK>(add2(tc, s), L.zb[2 * j], L.zb[2 * j + 1], znear);
+    if (CHK) {  // smallest t > 0: the far root when the camera is inside
+      const f2 sq = sqrt2(disc), ia = nrcp2(A);
+      float t10, t11, t20, t21;
+      unpk(add2(tc, mul2(add2(B, sq), ia)), t10, t11);
+      unpk(add2(tc, mul2(sub2(B, sq), ia)), t20, t21);
+      keep<true>(t10 > 0.f ? t10 : t20, L.zb[2 * j], znear);
+      keep<true>(t11 > 0.f ? t11 : t21, L.zb[2 * j + 1], znear);
+    } else {
+      const f2 s = mul2(add2(B, sqrt2(disc)), nrcp2(A));
+      keep2<false>(add2(tc, s), L.zb[2 * j], L.zb[2 * j + 1], znear);
+    }
   }
 }
 
@@ -308,13 +328,50 @@ __device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L
     const f2 B = fma2(ox, lx, fma2(oy, ly, sub2(bc(0.f), mul2(kd, g))));
     const f2 C = fma2(ox, ox, fma2(oy, oy, sub2(bc(0.f), mul2(g, g))));
     const f2 disc = sub2(mul2(B, B), mul2(A, C));
-    const f2 s = mul2(add2(B, sqrt2(disc)), nrcp2(A));  // NaN when disc < 0
-    float za0, za1, z0, z1;
-    unpk(fma2(s, lz, oz), za0, za1);
-    unpk(add2(tc, s), z0, z1);
-    const float nan = __int_as_float(0x7fc00000);
-    keep<CHK>(fabsf(za0) <= hl ? z0 : nan, L.zb[2 * j], znear);
-    keep<CHK>(fabsf(za1) <= hl ? z1 : nan, L.zb[2 * j + 1], znear);
+    if (CHK) {
+      // Exact solid near the camera: with the near plane cutting a joint sphere, the caps
+      // are no longer covered, so take the smallest t > 0 over both lateral roots in the
+      // axial range and both cap discs (as the oracle's or_first_hit does).
+      float a_[2], b_[2], dsc[2], tcv[2], lxv[2], lyv[2], lzv[2], oxv[2], oyv[2], ozv[2];
+      unpk(A, a_[0], a_[1]);
+      unpk(B, b_[0], b_[1]);
+      unpk(disc, dsc[0], dsc[1]);
+      unpk(tc, tcv[0], tcv[1]);
+      unpk(lx, lxv[0], lxv[1]);
+      unpk(ly, lyv[0], lyv[1]);
+      unpk(lz, lzv[0], lzv[1]);
+      unpk(ox, oxv[0], oxv[1]);
+      unpk(oy, oyv[0], oyv[1]);
+      unpk(oz, ozv[0], ozv[1]);
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        float best = __int_as_float(0x7f800000);
+        const float sq = sqrtf(dsc[e]), ia = 1.f / a_[e];  // NaN roots when disc < 0
+        const float sr[2] = {-(b_[e] + sq) * ia, (sq - b_[e]) * ia};
+#pragma unroll
+        for (int i = 0; i < 2; i++) {
+          const float t = tcv[e] + sr[i];
+          if (fabsf(fmaf(sr[i], lzv[e], ozv[e])) <= hl && t > 0.f) best = fminf(best, t);
+        }
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+          const float zc = c == 0 ? -hl : hl, rc = fmaf(k, zc, rm);
+          const float sc = (zc - ozv[e]) / lzv[e];
+          const float x = fmaf(sc, lxv[e], oxv[e]), y = fmaf(sc, lyv[e], oyv[e]);
+          const float t = tcv[e] + sc;
+          if (fmaf(x, x, y * y) <= rc * rc && t > 0.f) best = fminf(best, t);
+        }
+        keep<true>(best, L.zb[2 * j + e], znear);
+      }
+    } else {
+      const f2 s = mul2(add2(B, sqrt2(disc)), nrcp2(A));  // NaN when disc < 0
+      float za0, za1, z0, z1;
+      unpk(fma2(s, lz, oz), za0, za1);
+      unpk(add2(tc, s), z0, z1);
+      const float nan = __int_as_float(0x7fc00000);
+      keep<false>(fabsf(za0) <= hl ? z0 : nan, L.zb[2 * j], znear);
+      keep<false>(fabsf(za1) <= hl ? z1 : nan, L.zb[2 * j + 1], znear);
+    }
   }
 }
 
@@ -368,7 +425,7 @@ __device__ __forceinline__ uint3 cull_tile(const FkOut& fo, int X0, int Y0) {
   return make_uint3(lo & 0xFFFFFu, (lo >> 20) | ((hi & 0x7u) << 12), hi >> 3);
 }
 
-template <int MODE>
+template <int MODE, bool CHK>
 __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tmap,
                                         const FkOut& fo, int X0, int Y0, uint3 km,
                                         uint32_t* obs_buf, uint64_t* bar, uint32_t& phase,
@@ -401,19 +458,13 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
     L.zb[q] = zinit;
     L.zb[q + 1] = zinit;
   }
-  if (fo.near_ok) {
-    for (unsigned int m = msph; m; m &= m - 1) isect_sphere<false>(fo.rec[__ffs(m) - 1], L, znear);
-    for (unsigned int m = mcone; m; m &= m - 1)
-      isect_cone<false>(fo.rec[kCone0 + __ffs(m) - 1], L, znear);
-    for (unsigned int m = mell; m; m &= m - 1)
-      isect_ellipsoid<false>(fo.rec[kEll0 + __ffs(m) - 1], L, znear);
-  } else {
-    for (unsigned int m = msph; m; m &= m - 1) isect_sphere<true>(fo.rec[__ffs(m) - 1], L, znear);
-    for (unsigned int m = mcone; m; m &= m - 1)
-      isect_cone<true>(fo.rec[kCone0 + __ffs(m) - 1], L, znear);
-    for (unsigned int m = mell; m; m &= m - 1)
-      isect_ellipsoid<true>(fo.rec[kEll0 + __ffs(m) - 1], L, znear);
-  }
+  // CHK = false (the hot path): FK proved every primitive lies beyond z_near; CHK = true:
+  // exact solid semantics near the camera (instantiated only out of line, see tiles_near)
+  for (unsigned int m = msph; m; m &= m - 1) isect_sphere<CHK>(fo.rec[__ffs(m) - 1], L, znear);
+  for (unsigned int m = mcone; m; m &= m - 1)
+    isect_cone<CHK>(fo.rec[kCone0 + __ffs(m) - 1], L, znear);
+  for (unsigned int m = mell; m; m &= m - 1)
+    isect_ellipsoid<CHK>(fo.rec[kEll0 + __ffs(m) - 1], L, znear);
 
   if (MODE == kModeDepth) {
 #pragma unroll
@@ -466,6 +517,79 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
   __syncwarp();
 }
 
+// A warp's share of one particle's tiles.  Tiles come from the FK kernel's list
+// (nlist >= 0) or, when there is none, from the union grid with per-tile culling; the
+// warps of a CTA take them through the shared counter *next.
+struct TileRun {
+  TileSums acc;
+  uint32_t phase;
+};
+template <int MODE, bool CHK>
+__device__ __forceinline__ TileRun tile_loop(const EvalArgs& a, const CUtensorMap* tmap,
+                                             const FkOut& fo, const uint4* list, int nlist,
+                                             int first, int stride, int count, int* next,
+                                             uint32_t* obs_buf, uint64_t* bar, uint32_t phase,
+                                             const float* s_dx, const float* s_dy, int yoff) {
+  const int lane = threadIdx.x & 31;
+  const TileGrid g(fo.ubox);
+  TileRun r;
+  r.phase = phase;
+  int j = 0;
+  if (lane == 0) j = atomicAdd(next, 1);
+  j = __shfl_sync(0xffffffffu, j, 0);
+  while (j < count) {
+    int jn = 0;
+    if (lane == 0) jn = atomicAdd(next, 1);  // the next tile, fetched early
+    int X0, Y0;
+    uint3 km;
+    if (nlist >= 0) {
+      const uint4 it = list[j];
+      X0 = (int)(it.x & 0xFFFFu);
+      Y0 = (int)(it.x >> 16);
+      km = make_uint3(it.y, it.z, it.w);
+    } else {
+      g.origin(first + j * stride, X0, Y0);
+      km = cull_tile(fo, X0, Y0);
+    }
+    if (km.x | km.y | km.z)  // no primitive box touches the tile: nothing to render or score
+      do_tile<MODE, CHK>(a, tmap, fo, X0, Y0, km, obs_buf, bar, r.phase, s_dx, s_dy, r.acc,
+                         yoff);
+    j = __shfl_sync(0xffffffffu, jn, 0);
+  }
+  return r;
+}
+
+// Particles with a primitive that may cross z_near (rare: a hand within ~25 cm of the near
+// plane) take the exact-solid path out of line, so its registers never weigh on the hot
+// loop's allocation.  The kernels' EvalArgs are __grid_constant__: no copy for the reference.
+template <int MODE>
+__device__ __noinline__ TileRun tiles_near(const EvalArgs& a, const CUtensorMap* tmap,
+                                           const FkOut& fo, const uint4* list, int nlist,
+                                           int first, int stride, int count, int* next,
+                                           uint32_t* obs_buf, uint64_t* bar, uint32_t phase,
+                                           const float* s_dx, const float* s_dy, int yoff) {
+  return tile_loop<MODE, true>(a, tmap, fo, list, nlist, first, stride, count, next, obs_buf,
+                               bar, phase, s_dx, s_dy, yoff);
+}
+
+template <int MODE>
+__device__ __forceinline__ TileRun run_tiles(const EvalArgs& a, const CUtensorMap* tmap,
+                                             const FkOut& fo, const uint4* list, int nlist,
+                                             int first, int stride, int count, int* next,
+                                             uint32_t* obs_buf, uint64_t* bar, uint32_t phase,
+                                             const float* s_dx, const float* s_dy, int yoff) {
+#if HP_NEAR_TEST
+  return tile_loop<MODE, false>(a, tmap, fo, list, nlist, first, stride, count, next,
+                                obs_buf, bar, phase, s_dx, s_dy, yoff);
+#else
+  if (fo.near_ok)
+    return tile_loop<MODE, false>(a, tmap, fo, list, nlist, first, stride, count, next,
+                                  obs_buf, bar, phase, s_dx, s_dy, yoff);
+  return tiles_near<MODE>(a, tmap, fo, list, nlist, first, stride, count, next, obs_buf, bar,
+                          phase, s_dx, s_dy, yoff);
+#endif
+}
+
 __device__ __forceinline__ void warp_reduce(TileSums& s) {
   s.rm = __reduce_add_sync(0xffffffffu, s.rm);
   s.and_ = __reduce_add_sync(0xffffffffu, s.and_);
@@ -501,7 +625,7 @@ __device__ __forceinline__ void finalize_cost(const EvalArgs& a, int p, const un
 // ---------------------------------------------------------------------------------------
 template <int NW, typename PoseT, int MODE>
 __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
-    k_eval(const EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
+    k_eval(const __grid_constant__ EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
   __shared__ FkScratch s_fk;
   __shared__ __align__(16) FkOut s_out;
   __shared__ __align__(128) uint32_t s_obs[NW][kTileW * kTileH];
@@ -546,27 +670,16 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
       fence_mbar_init();
       if (a.use_tma == 1) prefetch_tmap(&tmap);
     }
-    if (threadIdx.x == 64) s_next = NW;
+    if (threadIdx.x == 64) s_next = 0;
   }
   __syncthreads();
 
   const TileGrid g(s_out.ubox);
   // this CTA owns tiles sidx, sidx + S, ...; warps take them dynamically (load balance)
   const int nmine = g.ntiles > sidx ? (g.ntiles - sidx + a.S - 1) / a.S : 0;
-  TileSums acc;
-  uint32_t phase = 0;
-  int j = warp;
-  while (j < nmine) {
-    int jn = 0;
-    if (lane == 0) jn = atomicAdd(&s_next, 1);  // next tile, fetched early
-    int X0, Y0;
-    g.origin(sidx + j * a.S, X0, Y0);
-    const uint3 km = cull_tile(s_out, X0, Y0);
-    if (km.x | km.y | km.z)  // no primitive box touches the tile: nothing to render or score
-      do_tile<MODE>(a, &tmap, s_out, X0, Y0, km, s_obs[warp], &s_bar[warp], phase, s_dx, s_dy,
-                    acc, frame_of(a, p) * a.cam.H);
-    j = __shfl_sync(0xffffffffu, jn, 0);
-  }
+  TileSums acc = run_tiles<MODE>(a, &tmap, s_out, nullptr, -1, sidx, a.S, nmine, &s_next,
+                                 s_obs[warp], &s_bar[warp], 0u, s_dx, s_dy,
+                                 frame_of(a, p) * a.cam.H).acc;
 
   if (MODE != kModeCost) return;
   // ---- reduction: warp shuffles, one atomic per sum per CTA ----
@@ -737,16 +850,26 @@ __global__ void __launch_bounds__(kFkWarps * 32, kFkTeam == 2 ? 16 : 8)
   const int cnt = build_tile_list(s_out[slot], a.tiles_g + (size_t)p * kMaxTiles, band,
                                   band + kMaxBand);
   if (lane == 0) {
-    a.ntl_g[p] = cnt;
+    int ntl = cnt;
+    if (!s_out[slot].near_ok) {  // some primitive may cross z_near: the exact pass renders it
+      a.near_list[atomicAdd(a.near_count, 1u)] = p;
+      ntl = -2;
+    }
+    a.ntl_g[p] = ntl;
     if (kFkTeam == 1) bulk_wait_all();  // complete before the CTA's shared memory retires
   }
 }
 
-template <int NW>
+// NEAR = false: the batch renderer.  Particles whose FK found a primitive that may cross
+// z_near were queued by k_fk_batch (ntl = -2) and are skipped here; NEAR = true renders
+// exactly those (exact-solid path) in a second, normally empty launch, so the
+// near-plane code never shares a register allocation with the hot loop.
+template <int NW, bool NEAR>
 __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
-    k_render_persist(const EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
+    k_render_persist(const __grid_constant__ EvalArgs a,
+                     const __grid_constant__ CUtensorMap tmap) {
   __shared__ __align__(16) FkOut s_out[2];
-  __shared__ __align__(16) uint4 s_tiles[2][kMaxTiles];
+  __shared__ __align__(16) uint4 s_tiles[2][NEAR ? 1 : kMaxTiles];
   __shared__ __align__(128) uint32_t s_obs[NW][kTileW * kTileH];
   __shared__ __align__(8) uint64_t s_bar[NW];
   __shared__ __align__(8) uint64_t s_full[2];
@@ -757,13 +880,24 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* s_dx = s_ray;
   const float* s_dy = s_ray + ray_dx_len(a.cam.W);
+  unsigned int* const counter = a.pcount + (NEAR ? 2 : 0);  // [taken, CTAs exited]
   // one thread: take the next particle and pull its FK record + tile list into slot b
   auto issue = [&](int b) {
-    const int p = (int)atomicAdd(a.pcount, 1u);
+    int p = a.n;
+    if (NEAR) {
+      const unsigned k = atomicAdd(counter, 1u);
+      if (k < __ldcg(a.near_count)) p = __ldcg(a.near_list + k);
+    } else {
+      p = (int)atomicAdd(counter, 1u);
+    }
     s_pid[b] = p;
     if (p < a.n) {
-      const int ntl = __ldcg(a.ntl_g + p);
+      const int ntl = NEAR ? -1 : __ldcg(a.ntl_g + p);  // NEAR: cull every tile
       s_ntl[b] = ntl;
+      if (ntl == -2) {  // queued for the near-plane pass: nothing to fetch
+        mbar_arrive(&s_full[b]);
+        return;
+      }
       const uint32_t lb = ntl > 0 ? (uint32_t)ntl * 16u : 0u;
       mbar_expect_tx(&s_full[b], (uint32_t)sizeof(FkOut) + lb);
       bulk_g2s(&s_out[b], static_cast<const FkOut*>(a.fk_g) + p, (uint32_t)sizeof(FkOut),
@@ -773,6 +907,21 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
       mbar_arrive(&s_full[b]);  // terminator: complete the phase without data
     }
   };
+#if HP_FK_PDL
+  // the near-plane pass may start its prologue as this grid's CTAs retire
+  if (!NEAR) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+  if (NEAR) {  // usually nothing was queued: leave before any set-up work
+    __shared__ int s_any;
+    if (threadIdx.x == 0) {
+#if HP_FK_PDL
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+      s_any = __ldcg(a.near_count) > 0u;
+    }
+    __syncthreads();
+    if (!s_any) return;  // the same for every CTA: no counter to reset
+  }
   if (threadIdx.x == 0) {
     for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);
     for (int b = 0; b < 2; b++) {
@@ -784,7 +933,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     fence_mbar_init();
     if (a.use_tma == 1) prefetch_tmap(&tmap);
 #if HP_FK_PDL
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // k_fk_batch complete and visible
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous grid is complete
 #endif
     issue(0);
     issue(1);
@@ -805,30 +954,32 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     const FkOut& fo = s_out[b];
     const int nlist = s_ntl[b];
     const int yoff = frame_of(a, p) * a.cam.H;
-    const TileGrid g(fo.ubox);
-    const int nt = nlist >= 0 ? nlist : g.ntiles;
     TileSums acc;
-    int t = 0;
-    if (lane == 0) t = atomicAdd(&s_next[b], 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    while (t < nt) {
-      int tn = 0;
-      if (lane == 0) tn = atomicAdd(&s_next[b], 1);
-      int X0, Y0;
-      uint3 km;
-      if (nlist >= 0) {
-        const uint4 it = s_tiles[b][t];
-        X0 = (int)(it.x & 0xFFFFu);
-        Y0 = (int)(it.x >> 16);
-        km = make_uint3(it.y, it.z, it.w);
-      } else {
-        g.origin(t, X0, Y0);
-        km = cull_tile(fo, X0, Y0);
+    if (nlist != -2) {
+      const TileGrid g(fo.ubox);
+      const int nt = nlist >= 0 ? nlist : g.ntiles;
+      int t = 0;
+      if (lane == 0) t = atomicAdd(&s_next[b], 1);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      while (t < nt) {
+        int tn = 0;
+        if (lane == 0) tn = atomicAdd(&s_next[b], 1);
+        int X0, Y0;
+        uint3 km;
+        if (nlist >= 0) {
+          const uint4 it = s_tiles[b][t];
+          X0 = (int)(it.x & 0xFFFFu);
+          Y0 = (int)(it.x >> 16);
+          km = make_uint3(it.y, it.z, it.w);
+        } else {
+          g.origin(t, X0, Y0);
+          km = cull_tile(fo, X0, Y0);
+        }
+        if (km.x | km.y | km.z)
+          do_tile<kModeCost, NEAR>(a, &tmap, fo, X0, Y0, km, s_obs[warp], &s_bar[warp], phase,
+                                   s_dx, s_dy, acc, yoff);
+        t = __shfl_sync(0xffffffffu, tn, 0);
       }
-      if (km.x | km.y | km.z)
-        do_tile<kModeCost>(a, &tmap, fo, X0, Y0, km, s_obs[warp], &s_bar[warp], phase, s_dx,
-                           s_dy, acc, yoff);
-      t = __shfl_sync(0xffffffffu, tn, 0);
     }
     warp_reduce(acc);
     if (lane == 0) {
@@ -844,7 +995,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
           v[k] = s_acc[b][k];
           s_acc[b][k] = 0;
         }
-        finalize_cost(a, p, v, fo.kc);
+        if (nlist != -2) finalize_cost(a, p, v, fo.kc);  // queued ones: the near pass
         s_next[b] = 0;
         s_done[b] = 0;
         fence_proxy_async();  // every warp's generic reads of slot b precede the refill
@@ -853,13 +1004,14 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     }
     __syncwarp();
   }
-  // the last CTA to leave resets the particle counter for the next launch
+  // the last CTA to leave resets the counters for the next launch
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(a.pcount + 1, 1u) == gridDim.x - 1) {
-      a.pcount[0] = 0;
-      a.pcount[1] = 0;
+    if (atomicAdd(counter + 1, 1u) == gridDim.x - 1) {
+      counter[0] = 0;
+      counter[1] = 0;
+      if (NEAR) *a.near_count = 0;
       __threadfence();
     }
   }
@@ -881,7 +1033,9 @@ static void set_carveouts() {
   if (done) return;
   done = true;
   const int pct = cudaSharedmemCarveoutMaxShared;
-  cudaFuncSetAttribute(k_render_persist<kEvalWarps>,
+  cudaFuncSetAttribute(k_render_persist<kEvalWarps, false>,
+                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  cudaFuncSetAttribute(k_render_persist<kEvalWarps, true>,
                        cudaFuncAttributePreferredSharedMemoryCarveout, pct);
   cudaFuncSetAttribute(k_eval<kEvalWarps, float, kModeCost>,
                        cudaFuncAttributePreferredSharedMemoryCarveout, pct);
@@ -909,7 +1063,7 @@ int persist_blocks_per_sm(const CamParams& cam) {
   set_carveouts();
   int nb = 0;
   const size_t dyn = (size_t)ray_floats(cam.W, cam.H) * sizeof(float);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_render_persist<kEvalWarps>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_render_persist<kEvalWarps, false>,
                                                     kEvalWarps * 32, dyn) != cudaSuccess)
     return 0;
   return nb;
@@ -983,10 +1137,16 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, k_render_persist<kEvalWarps>, a, *map);
+    e = cudaLaunchKernelEx(&cfg, k_render_persist<kEvalWarps, false>, a, *map);
+    if (e != cudaSuccess) return e;
+    // the near-plane pass (exits at once when k_fk_batch queued nothing)
+    cfg.gridDim = dim3((unsigned)(pgrid.x < 148u ? pgrid.x : 148u));
+    e = cudaLaunchKernelEx(&cfg, k_render_persist<kEvalWarps, true>, a, *map);
     if (e != cudaSuccess) return e;
 #else
-    k_render_persist<kEvalWarps><<<pgrid, block, dyn, st>>>(a, *map);
+    k_render_persist<kEvalWarps, false><<<pgrid, block, dyn, st>>>(a, *map);
+    k_render_persist<kEvalWarps, true><<<dim3(pgrid.x < 148u ? pgrid.x : 148u), block, dyn,
+                                         st>>>(a, *map);
 #endif
     if (tev) cudaEventRecord(tev[2], st);
     return cudaGetLastError();

@@ -292,3 +292,44 @@ def test_pso_hand_fit_parity_c1():
         assert np.max(np.abs(g.best_pose - r.best_x)) <= 1e-4
         np.testing.assert_allclose(g.trace, r.trace, rtol=E_REL, atol=E_ABS)
         assert np.all(np.diff(g.trace) <= 0)
+
+
+def test_batch_path_close_up_poses_beyond_tile_list_capacity():
+    """Hands close to the camera have union boxes of more than kMaxTiles (512) 16x8 tiles;
+    the FK kernel then hands the renderer no tile list and it culls every tile itself.
+    Mixed into a batch large enough for the persistent path (S = 1)."""
+    ctx = ctx_for(640, 480)
+    obs = obs_for(W.H_A, 640, 480)
+    close = []
+    for z in (250.0, 300.0, 350.0, 420.0):
+        for dx in (-30.0, 0.0, 30.0):
+            h = W.H_A.copy()
+            h[0] += dx
+            h[2] = z
+            close.append(h)
+    close = np.asarray(close, np.float32)
+    # the union boxes really exceed the tile-list capacity
+    big = 0
+    for h in close:
+        _, boxes, _, _ = ctx.debug_fk(h.astype(np.float64))
+        b = boxes[boxes[:, 0] <= boxes[:, 2]]
+        x0 = int(b[:, 0].min()) & ~3
+        tiles = -(-(int(b[:, 2].max()) - x0 + 1) // 16) * -(-(int(b[:, 3].max()) - int(b[:, 1].min()) + 1) // 8)
+        big += tiles > 512
+    assert big >= 3
+    batch = np.concatenate([W.swarm_c4(1012).astype(np.float32), close])
+    assert ctx.splits_for(len(batch)) == 1
+    sums, c64, _ = gpu_costs(ctx, obs, batch)
+    off = 1012
+    for k in range(len(close)):  # split path (S > 1) gives the same bits
+        s1, c1, _ = gpu_costs(ctx, obs, close[k:k + 1])
+        assert np.array_equal(s1[0], sums[off + k]) and c1[0] == c64[off + k]
+    sample = [0, 4, 8, 11]
+    co, so, _, _ = oracle_eval(obs, close[sample])
+    for j, k in enumerate(sample):
+        if int(sums[off + k, 0]) == so[j].s_rm and int(sums[off + k, 1]) == so[j].s_and:
+            assert abs(c64[off + k] - co[j]) <= E_REL * abs(co[j]) + E_ABS
+        else:  # edge pixels only
+            ne = int(O.edge_mask(close[k].astype(np.float64), O.camera(640, 480),
+                                 obs_depth=obs.depth).sum())
+            assert abs(int(sums[off + k, 0]) - so[j].s_rm) <= ne
