@@ -426,7 +426,7 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   const int W = cam->width, H = cam->height;
   ctx->pitch_words = (W + 3) & ~3;  // 16-byte row pitch for TMA
   CKC(cudaMalloc(&ctx->obs, (size_t)ctx->pitch_words * H * 4));
-  CKC(cudaMemset(ctx->obs, 0, (size_t)ctx->pitch_words * H * 4));
+  CKC(launch_fill_undef(ctx->obs, (long long)ctx->pitch_words * H, ctx->st));
   CKC(cudaMalloc(&ctx->S_o, sizeof(unsigned long long)));
   CKC(cudaMemset(ctx->S_o, 0, sizeof(unsigned long long)));
   CKC(cudaMalloc(&ctx->band_m, sizeof(unsigned int)));
@@ -510,7 +510,8 @@ static hp_status ensure_frames(hp_ctx* ctx, int M) {
   ctx->frames_cap = 0;
   const size_t px = (size_t)W * H * M;
   CK(cudaMalloc(&ctx->obs, (size_t)ctx->pitch_words * H * M * 4));
-  CK(cudaMemset(ctx->obs, 0, (size_t)ctx->pitch_words * H * M * 4));
+  CK(launch_fill_undef(ctx->obs, (long long)ctx->pitch_words * H * M, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
   CK(cudaMalloc(&ctx->S_o, (size_t)M * sizeof(unsigned long long)));
   CK(cudaMemset(ctx->S_o, 0, (size_t)M * sizeof(unsigned long long)));
   CK(cudaMalloc(&ctx->band_m, (size_t)M * sizeof(unsigned int)));

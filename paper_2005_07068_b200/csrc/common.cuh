@@ -235,6 +235,10 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 // --------------------------------------------------------------------------------------
 // Launchers (kernels.cu)
 // --------------------------------------------------------------------------------------
+// Packed observation word: fp32 o_d bits (bit 31 = o_s); an undefined o_d is this quiet
+// NaN, so |o_d - r_d| is NaN exactly where o_d is undefined (one compare in the scoring)
+constexpr uint32_t kObsUndef = 0x7fc00000u;
+cudaError_t launch_fill_undef(uint32_t* obs, long long words, cudaStream_t st);
 cudaError_t launch_pack_obs(const float* depth, const uint8_t* mask, uint32_t* obs, int W,
                             int H, int pitch_words, unsigned long long* S_o, cudaStream_t st);
 // Row f3 front end: Kinect u16 depth (+ optional skin image) -> segmented packed observation.

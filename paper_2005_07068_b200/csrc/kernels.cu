@@ -43,7 +43,7 @@ __global__ void k_pack_obs(const float* __restrict__ depth, const uint8_t* __res
   if (i < npx) {
     const int y = (int)(i / W), x = (int)(i % W);
     const float d = depth[i];
-    const uint32_t bits = (d > 0.f && isfinite(d)) ? __float_as_uint(d) : 0u;
+    const uint32_t bits = (d > 0.f && isfinite(d)) ? __float_as_uint(d) : kObsUndef;
     const uint32_t s = mask[i] ? 1u : 0u;
     obs[(long long)y * pitch + x] = bits | (s << 31);
     cnt = s;
@@ -92,7 +92,7 @@ __global__ void k_ingest(const uint16_t* __restrict__ depth, const uint8_t* __re
     const bool valid = d > 0, in_band = valid && lo <= d && d <= hi;
     const bool s = skin ? (skin[i] != 0 && (!valid || in_band)) : in_band;
     const bool def = seg.keep_background ? valid : in_band;
-    const uint32_t bits = def ? __float_as_uint((float)d) : 0u;
+    const uint32_t bits = def ? __float_as_uint((float)d) : kObsUndef;
     const int y = (int)(i / W), x = (int)(i % W);
     obs[(long long)y * pitch + x] = bits | ((uint32_t)s << 31);
     cnt = s;
@@ -101,12 +101,17 @@ __global__ void k_ingest(const uint16_t* __restrict__ depth, const uint8_t* __re
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(S_o, (unsigned long long)cnt);
 }
 
+__global__ void k_fill_undef(uint32_t* __restrict__ obs, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) obs[i] = kObsUndef;
+}
+
 __global__ void k_unpack_obs(const uint32_t* __restrict__ obs, int W, int H, int pitch,
                              float* __restrict__ depth, uint8_t* __restrict__ mask) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)W * H) return;
   const uint32_t w = obs[(i / W) * pitch + i % W];
-  if (depth) depth[i] = __uint_as_float(w & 0x7fffffffu);
+  if (depth) depth[i] = (w & 0x7fffffffu) == kObsUndef ? 0.f : __uint_as_float(w & 0x7fffffffu);
   if (mask) mask[i] = (uint8_t)(w >> 31);
 }
 
@@ -499,13 +504,14 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
 #pragma unroll
       for (int q = 0; q < kPxPerLane; q++) {
         const uint32_t w = obs_buf[(rowb + 2 * q) * kTileW + col];
-        const float od = __uint_as_float(w & 0x7fffffffu);
-        const float diff = fabsf(od - L.zb[q]);
+        // o_d undefined is stored as NaN (kObsUndef), so diff is NaN exactly there
+        const float diff = fabsf(__uint_as_float(w & 0x7fffffffu) - L.zb[q]);
         // off-image pixels have NaN rays and never hit (k_ray_table)
         const bool hit = L.zb[q] <= zfar;
-        // r_m = 1 where |r_d - o_d| < d_m or o_d undefined (AMB-4, AMB-5)
-        const unsigned int rm = hit & ((od == 0.f) | (diff < d_m));
-        const bool both = hit & (od > 0.f);
+        // r_m = 1 where |r_d - o_d| < d_m or o_d undefined (AMB-4, AMB-5):
+        // !(diff >= d_m) is true for NaN
+        const unsigned int rm = hit & !(diff >= d_m);
+        const bool both = hit & (diff == diff);
         acc.rm += rm;
         acc.and_ += rm & (w >> 31);
         acc.both += both;
@@ -1091,6 +1097,11 @@ cudaError_t launch_ingest(const uint16_t* depth, const uint8_t* skin, int W, int
   const long long npx = (long long)W * H;
   k_ingest<<<(unsigned)((npx + 255) / 256), 256, 0, st>>>(depth, skin, W, H, pitch_words, seg,
                                                            m, obs, S_o);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_undef(uint32_t* obs, long long words, cudaStream_t st) {
+  if (words > 0) k_fill_undef<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(obs, words);
   return cudaGetLastError();
 }
 
