@@ -393,6 +393,8 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
       dd.len[f][i] = d.seg_len[f][i];
     }
     for (int i = 0; i < 4; i++) dd.rad[f][i] = d.radius[f][i];
+    for (int i = 0; i < 3; i++)
+      dd.cone_k[f][i] = (dd.rad[f][i + 1] - dd.rad[f][i]) / dd.len[f][i];
   }
   dd.th_x = d.thumb_ell_x;
   dd.th_z = d.thumb_ell_z;

@@ -63,6 +63,7 @@ struct DimsD {
   double base[5][3], len[5][3], rad[5][4];
   double th_x, th_z;
   double RT0[3][3];  // thumb base frame Rz(yaw) Ry(pitch), host fp64
+  double cone_k[5][3];  // (r_{k+1} - r_k) / L_k, the cone slopes (host fp64)
 };
 
 struct CostD {

@@ -43,20 +43,31 @@ __device__ __forceinline__ void mat3_mul(const double a[3][3], const double b[3]
 //   disc = Aaa cz^2 + Azz ca^2 - 2 Aaz ca cz + Aaz^2 - Aaa Azz.
 // Accumulates into [u0,u1]x[v0,v1] (normalised image coordinates); returns 0 behind the
 // camera, 2 if the body straddles z = 0.
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rcp_approx_fk(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ int gen_bounds(const float c[3], const float A[3][3], float& u0,
                                           float& u1, float& v0, float& v1, float& zmin) {
-  const float zext = sqrtf(fmaxf(A[2][2], 0.f));
+  const float zext = sqrt_approx(fmaxf(A[2][2], 0.f));
   zmin = fminf(zmin, c[2] - zext);
   if (c[2] + zext <= 0.f) return 0;
   if (c[2] - zext <= 0.f) return 2;
-  const float qa = fmaf(c[2], c[2], -A[2][2]), inv = 1.f / qa;
+  // approximate rcp / sqrt: ~1e-7 relative, far inside the boxes' 1 px margin
+  const float qa = fmaf(c[2], c[2], -A[2][2]), inv = rcp_approx_fk(qa);
 #pragma unroll
   for (int ax = 0; ax < 2; ax++) {
     const float ca = c[ax], Aaa = A[ax][ax], Aaz = A[ax][2], Azz = A[2][2];
     const float qb = fmaf(ca, c[2], -Aaz);
     const float disc = Aaa * c[2] * c[2] + Azz * ca * ca - 2.f * Aaz * ca * c[2] + Aaz * Aaz -
                        Aaa * Azz;
-    const float sq = sqrtf(fmaxf(disc, 0.f));
+    const float sq = sqrt_approx(fmaxf(disc, 0.f));
     const float lo = (qb - sq) * inv, hi = (qb + sq) * inv;
     if (ax == 0) {
       u0 = fminf(u0, lo);
@@ -170,7 +181,7 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
       rec[kCl + a] = (float)(rows[a][0] * m[0] + rows[a][1] * m[1] + rows[a][2] * m[2]);
     }
     rec[kRm] = (float)(0.5 * (r0 + r1));
-    rec[kK] = (float)((r1 - r0) / L);
+    rec[kK] = (float)dm.cone_k[f][k];
     rec[kHl] = (float)(0.5 * L);
     float axf[3] = {(float)ax[0], (float)ax[1], (float)ax[2]};
     for (int i = 0; i < 3; i++) {
@@ -258,9 +269,17 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
 //           columns 1, 2 (the segment runs along -B[:,1])
 //   phase C: the 38 records + fp32 screen boxes (TEAM 2: spheres on warp 0, the rest on
 //           warp 1, in parallel), then the union box, the near-plane flag and kc(h)
+#if HP_FK_PROF
+__device__ unsigned long long g_fkprof[16];
+#define FKPROF(i) \
+  if (blockIdx.x == 7 && threadIdx.x == 0) g_fkprof[i] = clock64();
+#else
+#define FKPROF(i)
+#endif
 template <typename PoseT, int TEAM>
 __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam,
                         double kc_rest, FkScratch& s, FkOut& out) {
+  FKPROF(0)
   const int lane = threadIdx.x & 31, w = TEAM == 2 ? (threadIdx.x >> 5) & 1 : 0;
   if (w == 0) {
     if (lane < kNdof) {
@@ -269,6 +288,7 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
       if (lane >= 3) sincos(v, &s.sn[lane], &s.cs[lane]);
     }
     __syncwarp();
+    FKPROF(1)
     int bad = 0;
     if (lane < kNdof) bad = !isfinite(s.h[lane]);
     bad = __any_sync(0xffffffffu, bad);
@@ -332,6 +352,7 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
   } else if (TEAM == 2) {
     asm volatile("bar.sync 2, 64;" ::: "memory");
   }
+  FKPROF(2)
   // ---- phase C: records + boxes ----
   if (TEAM == 2) {
     const int j = w == 0 ? lane : 20 + lane;
@@ -359,6 +380,7 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
     }
     __syncwarp();
   }
+  FKPROF(3)
   // ---- warp 0: union box, near-plane flag, kc ----
   // (the solid is the convex hull of its generators, so zmin bounds its nearest point; the
   // 1e-3 relative slack covers the fp32 evaluation)

@@ -852,9 +852,11 @@ __global__ void __launch_bounds__(kFkWarps * 32, kFkTeam == 2 ? 16 : 8)
     float4* dst = reinterpret_cast<float4*>(static_cast<FkOut*>(a.fk_g) + p);
     for (int i = lane; i < (int)(sizeof(FkOut) / 16); i += 32) dst[i] = src[i];
   }
+  FKPROF(4)
   uint2* band = reinterpret_cast<uint2*>(&s_fk[slot]);  // FK scratch is dead by now
   const int cnt = build_tile_list(s_out[slot], a.tiles_g + (size_t)p * kMaxTiles, band,
                                   band + kMaxBand);
+  FKPROF(5)
   if (lane == 0) {
     int ntl = cnt;
     if (!s_out[slot].near_ok) {  // some primitive may cross z_near: the exact pass renders it
@@ -864,6 +866,7 @@ __global__ void __launch_bounds__(kFkWarps * 32, kFkTeam == 2 ? 16 : 8)
     a.ntl_g[p] = ntl;
     if (kFkTeam == 1) bulk_wait_all();  // complete before the CTA's shared memory retires
   }
+  FKPROF(6)
 }
 
 // NEAR = false: the batch renderer.  Particles whose FK found a primitive that may cross
@@ -1189,6 +1192,12 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
   if (tev) cudaEventRecord(tev[2], st);
   return cudaGetLastError();
 }
+
+#if HP_FK_PROF
+extern "C" int hp_debug_fk_prof(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_fkprof, sizeof(g_fkprof));
+}
+#endif
 
 cudaError_t launch_fk_debug(const double* pose_dev, const DimsD& dims, const CamParams& cam,
                             float* rec, int* boxes, double* joints, double* kc,
