@@ -820,10 +820,13 @@ __device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out, uint
 // HP_FK_TEAM = 1: 4 particles per CTA, one warp each; 2: one particle per 2-warp CTA (the
 // record build runs on both warps, halving the latency of the longest FK phase)
 constexpr int kFkTeam = HP_FK_TEAM;
-constexpr int kFkWarps = kFkTeam == 2 ? 2 : 4;
-constexpr int kFkPerCta = kFkTeam == 2 ? 1 : 4;
+#ifndef HP_FK_WARPS
+#define HP_FK_WARPS 4  // particles (warps) per k_fk_batch CTA
+#endif
+constexpr int kFkWarps = kFkTeam == 2 ? 2 : HP_FK_WARPS;
+constexpr int kFkPerCta = kFkTeam == 2 ? 1 : HP_FK_WARPS;
 template <typename PoseT>
-__global__ void __launch_bounds__(kFkWarps * 32, kFkTeam == 2 ? 16 : 8)
+__global__ void __launch_bounds__(kFkWarps * 32, kFkTeam == 2 ? 16 : 32 / HP_FK_WARPS)
     k_fk_batch(const EvalArgs a) {
   __shared__ FkScratch s_fk[kFkPerCta];
   __shared__ __align__(16) FkOut s_out[kFkPerCta];
