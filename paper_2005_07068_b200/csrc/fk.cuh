@@ -268,6 +268,8 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
 //           sparse column updates: B <- B Rz(MPz) touches columns 0, 1, B <- B Rx(t)
 //           columns 1, 2 (the segment runs along -B[:,1])
 //   phase C: the 38 records + fp32 screen boxes (TEAM 2: spheres on warp 0, the rest on
+//           warp 1; TEAM 3: spheres | cones | cylinder + ellipsoids, one kind per warp, so no
+//           warp serialises the branches of several kinds;
 //           warp 1, in parallel), then the union box, the near-plane flag and kc(h)
 #if HP_FK_PROF
 __device__ unsigned long long g_fkprof[16];
@@ -280,7 +282,8 @@ template <typename PoseT, int TEAM>
 __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam,
                         double kc_rest, FkScratch& s, FkOut& out) {
   FKPROF(0)
-  const int lane = threadIdx.x & 31, w = TEAM == 2 ? (threadIdx.x >> 5) & 1 : 0;
+  static_assert(TEAM >= 1 && TEAM <= 3, "FK teams of 1..3 warps (warps 0..TEAM-1 of the CTA)");
+  const int lane = threadIdx.x & 31, w = TEAM >= 2 ? (int)(threadIdx.x >> 5) : 0;
   if (w == 0) {
     if (lane < kNdof) {
       const double v = (double)pose[lane];
@@ -348,24 +351,27 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
       }
     }
     __syncwarp();
-    if (TEAM == 2) asm volatile("bar.arrive 2, 64;" ::: "memory");
-  } else if (TEAM == 2) {
-    asm volatile("bar.sync 2, 64;" ::: "memory");
+    if (TEAM >= 2) asm volatile("bar.arrive 2, %0;" ::"n"(32 * TEAM) : "memory");
+  } else if (TEAM >= 2) {
+    asm volatile("bar.sync 2, %0;" ::"n"(32 * TEAM) : "memory");
   }
   FKPROF(2)
   // ---- phase C: records + boxes ----
-  if (TEAM == 2) {
-    const int j = w == 0 ? lane : 20 + lane;
-    if ((w == 0 && lane < 20) || (w == 1 && lane < kNprim - 20)) {
+  if (TEAM >= 2) {
+    // TEAM 2: warp 0 spheres, warp 1 the 18 others; TEAM 3: spheres | cones | the rest
+    const int j0 = w == 0 ? 0 : (w == 1 ? kCone0 : kCyl);
+    const int j1 = w == 0 ? kCone0 : (w == 1 ? (TEAM == 3 ? kCyl : kNprim) : kNprim);
+    const int j = j0 + lane;
+    if (j < j1) {
       float zmin;
       build_prim(j, s, dm, cam, out.rec[j], out.box[j], zmin);
       s.nearf[j] = zmin > cam.znear * 1.001f;
     }
-    if (w == 1) {
-      asm volatile("bar.arrive 1, 64;" ::: "memory");
+    if (w != 0) {
+      asm volatile("bar.arrive 1, %0;" ::"n"(32 * TEAM) : "memory");
       return;
     }
-    asm volatile("bar.sync 1, 64;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * TEAM) : "memory");
   } else {
     // 38 records on 32 lanes: lanes 0..9 build two spheres each (the cheapest records),
     // lanes 10..27 one cone / cylinder / ellipsoid each, so no lane builds a sphere AND an

@@ -629,6 +629,10 @@ __device__ __forceinline__ void finalize_cost(const EvalArgs& a, int p, const un
 // warps stage the ray table; then all warps take tiles dynamically.  Used for small swarms
 // (S > 1 splits per particle keep every SM busy) and for the depth-image hooks.
 // ---------------------------------------------------------------------------------------
+#ifndef HP_EVAL_FK_TEAM
+#define HP_EVAL_FK_TEAM 3  // k_eval's FK team: warps 0..2 (one primitive kind per warp)
+#endif
+constexpr int kEvalFkTeam = HP_EVAL_FK_TEAM;
 template <int NW, typename PoseT, int MODE>
 __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
     k_eval(const __grid_constant__ EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
@@ -652,8 +656,8 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
   const float* s_dx = s_ray;
   const float* s_dy = s_ray + ray_dx_len(a.cam.W);
 
-  if (warp <= 1) {
-    // FK on warps 0 and 1 (warp 1 builds the non-sphere records in parallel)
+  if (warp < kEvalFkTeam) {
+    // FK on warps 0..kEvalFkTeam-1 (the records of each primitive kind on their own warp)
     __shared__ double s_pose[32];
     if (a.pso_on && a.pso_k >= 1) {
       // fused PSO update (Eq. 6-7, row A8) of this particle; every CTA of the particle
@@ -661,22 +665,22 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
       if (warp == 0)
         pso_update_warp(a.pso, p, a.pso_k, a.x_in, a.v_in, a.x_out, a.v_out, sidx == 0, s_pose);
       __syncwarp();
-      fk_team<double, 2>(s_pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
+      fk_team<double, kEvalFkTeam>(s_pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
     } else {
       const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
-      fk_team<PoseT, 2>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
+      fk_team<PoseT, kEvalFkTeam>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
     }
   } else {
-    // while warps 0-1 run FK: stage the per-column / per-row ray directions (k_ray_table)
+    // while the FK team runs: stage the per-column / per-row ray directions (k_ray_table)
     const int n4 = ray_floats(a.cam.W, a.cam.H) / 4;
-    for (int i = threadIdx.x - 64; i < n4; i += (NW - 2) * 32)
+    for (int i = threadIdx.x - 32 * kEvalFkTeam; i < n4; i += (NW - kEvalFkTeam) * 32)
       reinterpret_cast<float4*>(s_ray)[i] = __ldg(reinterpret_cast<const float4*>(a.ray) + i);
     if (MODE == kModeCost && warp == NW - 1 && lane == 0) {
       for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);  // count 1: the expect_tx arrival
       fence_mbar_init();
       if (a.use_tma == 1) prefetch_tmap(&tmap);
     }
-    if (threadIdx.x == 64) s_next = 0;
+    if (threadIdx.x == 32 * kEvalFkTeam) s_next = 0;
   }
   __syncthreads();
 
