@@ -119,6 +119,7 @@ struct hp_ctx {
   uint4* tiles_g = nullptr;        // [max_n][kMaxTiles]
   int* ntl_g = nullptr;            // [max_n]
   int* near_list = nullptr;        // [max_n] near-plane pass queue
+  double* kc_g = nullptr;          // [max_n] kc per particle (fused PSO generations)
   unsigned int* near_count = nullptr;
   int blocks_per_sm = 0;           // resident k_eval CTAs per SM
   // particle-sharded mode (hp_shard): rank r owns poses [r chunk, (r + 1) chunk)
@@ -290,7 +291,7 @@ void hp_destroy(hp_ctx* ctx) {
                  ctx->E, ctx->G, ctx->Gc, ctx->trace, ctx->bnd, ctx->centre, ctx->mark,
                  ctx->flags, ctx->dyn, ctx->tmap_g, ctx->ray, ctx->pcount, ctx->X2,
                  ctx->V2, ctx->gcount, ctx->fk_g, ctx->tiles_g, ctx->ntl_g, ctx->near_list,
-                 ctx->near_count};
+                 ctx->near_count, ctx->kc_g};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_poses) cudaFreeHost(ctx->h_poses);
@@ -449,6 +450,7 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   CKC(cudaMalloc(&ctx->pcount, 4 * sizeof(unsigned int)));
   CKC(cudaMemset(ctx->pcount, 0, 4 * sizeof(unsigned int)));
   CKC(cudaMalloc(&ctx->near_list, (size_t)max_particles * sizeof(int)));
+  CKC(cudaMalloc(&ctx->kc_g, (size_t)max_particles * sizeof(double)));
   CKC(cudaMalloc(&ctx->near_count, sizeof(unsigned int)));
   CKC(cudaMemset(ctx->near_count, 0, sizeof(unsigned int)));
   ctx->blocks_per_sm = eval_blocks_per_sm(ctx->camp);
@@ -984,6 +986,7 @@ static hp_status enqueue_fit(hp_ctx* ctx, const PsoDev& d, bool sphere, cudaStre
     a.pso_on = 1;
     a.pso = d;
     a.gcount = ctx->gcount;
+    a.kc_g = ctx->kc_g;
     a.pdl = ctx->use_pdl;
     double* Xb[2] = {ctx->X, ctx->X2};
     double* Vb[2] = {ctx->V, ctx->V2};

@@ -606,8 +606,8 @@ __device__ __forceinline__ void warp_reduce(TileSums& s) {
 
 // Eq. (4)-(5) in fp64 from the integer sums v = (sum r_m, sum o_s AND r_m, numerator in
 // 2^-qbits mm, both-defined count)  (AMB-1, -2, -3, -6).
-__device__ __forceinline__ void finalize_cost(const EvalArgs& a, int p, const unsigned long long v[4],
-                                              double kc) {
+__device__ __forceinline__ double finalize_cost(const EvalArgs& a, int p,
+                                                const unsigned long long v[4], double kc) {
   const long long s_rm = (long long)v[0], s_and = (long long)v[1];
   const long long s_or = (long long)a.S_o[frame_of(a, p)] + s_rm - s_and;
   double D = 0.0;
@@ -622,6 +622,7 @@ __device__ __forceinline__ void finalize_cost(const EvalArgs& a, int p, const un
   if (a.sums_out)  // the ABI reports the numerator in 2^-20 mm (qbits <= 20)
     for (int k = 0; k < 4; k++)
       a.sums_out[(size_t)p * 4 + k] = k == 2 ? v[k] << (20 - a.cost.qbits) : v[k];
+  return E;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -629,6 +630,35 @@ __device__ __forceinline__ void finalize_cost(const EvalArgs& a, int p, const un
 // warps stage the ray table; then all warps take tiles dynamically.  Used for small swarms
 // (S > 1 splits per particle keep every SM busy) and for the depth-image hooks.
 // ---------------------------------------------------------------------------------------
+#if HP_GEN_PROF
+__device__ unsigned long long g_genprof[64][5];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define GENPROF_MIN(i) \
+  if (a.pso_on && threadIdx.x == 0 && a.pso_k < 64) atomicMin(&g_genprof[a.pso_k][i], gtime());
+#define GENPROF_MAX(i) \
+  if (a.pso_on && threadIdx.x == 0 && a.pso_k < 64) atomicMax(&g_genprof[a.pso_k][i], gtime());
+#define GENPROF_SET(i) \
+  if (a.pso_on && threadIdx.x == 0 && a.pso_k < 64) g_genprof[a.pso_k][i] = gtime();
+extern "C" int hp_debug_gen_prof(unsigned long long* out, int reset) {
+  if (reset) {
+    static unsigned long long init[64][5];
+    for (int k = 0; k < 64; k++) {
+      init[k][0] = ~0ull;
+      for (int i = 1; i < 5; i++) init[k][i] = 0;
+    }
+    return (int)cudaMemcpyToSymbol(g_genprof, init, sizeof(init));
+  }
+  return (int)cudaMemcpyFromSymbol(out, g_genprof, sizeof(g_genprof));
+}
+#else
+#define GENPROF_MIN(i)
+#define GENPROF_MAX(i)
+#define GENPROF_SET(i)
+#endif
 #ifndef HP_EVAL_FK_TEAM
 #define HP_EVAL_FK_TEAM 3  // k_eval's FK team: warps 0..2 (one primitive kind per warp)
 #endif
@@ -650,6 +680,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
   }
+  GENPROF_MIN(0)
   if (a.done && *a.done) return;  // PSO stop rule reached (grid-uniform)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.x / a.S, sidx = blockIdx.x % a.S;
@@ -684,6 +715,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
   }
   __syncthreads();
 
+  GENPROF_MAX(1)
   const TileGrid g(s_out.ubox);
   // this CTA owns tiles sidx, sidx + S, ...; warps take them dynamically (load balance)
   const int nmine = g.ntiles > sidx ? (g.ntiles - sidx + a.S - 1) / a.S : 0;
@@ -691,6 +723,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
                                  s_obs[warp], &s_bar[warp], 0u, s_dx, s_dy,
                                  frame_of(a, p) * a.cam.H).acc;
 
+  GENPROF_MAX(2)
   if (MODE != kModeCost) return;
   // ---- reduction: warp shuffles, one atomic per sum per CTA ----
   warp_reduce(acc);
@@ -702,6 +735,50 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
   }
   __syncthreads();
   unsigned long long* gacc = a.acc + (size_t)p * 4;
+  if (a.pso_on) {
+    // ---- fused PSO generation: the CTAs only add their sums; the grid's last CTA
+    // finalises every particle (Eq. 4-5) and runs the bookkeeping (row A7), so no CTA
+    // waits on a per-particle counter round trip ----
+    __shared__ int s_lastcta;
+    if (threadIdx.x == 0) {
+      unsigned long long v[4] = {0, 0, 0, 0};
+      for (int w = 0; w < NW; w++)
+        for (int k = 0; k < 4; k++) v[k] += s_red[w][k];
+      for (int k = 0; k < 4; k++)
+        if (v[k]) atomicAdd(gacc + k, v[k]);
+      if (sidx == 0) a.kc_g[p] = s_out.kc;
+      __threadfence();
+      const unsigned prev = atomicAdd(a.gcount, 1u);
+      s_lastcta = prev == gridDim.x - 1;
+      if (s_lastcta) {
+        __threadfence();
+        *a.gcount = 0;
+      }
+    }
+    __syncthreads();
+    if (!s_lastcta) return;
+    GENPROF_SET(3)
+    // the ray table is dead now: its shared memory holds E and the pbest costs when they fit
+    const int N = a.pso.N;
+    const bool in_smem = (size_t)2 * N * sizeof(double) <=
+                         (size_t)ray_floats(a.cam.W, a.cam.H) * sizeof(float);
+    double* e = in_smem ? reinterpret_cast<double*>(s_ray) : a.pso.E;
+    __syncthreads();  // every warp is past its last ray-table read
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      unsigned long long v[4];
+      for (int k = 0; k < 4; k++) {
+        v[k] = __ldcg(a.acc + (size_t)i * 4 + k);
+        a.acc[(size_t)i * 4 + k] = 0ull;  // zero for the next generation
+      }
+      e[i] = finalize_cost(a, i, v, __ldcg(a.kc_g + i));  // also stores costs64 = E
+    }
+    __syncthreads();
+    pso_book_block(a.pso, a.pso_k, a.pso_k >= 1 ? a.x_out : a.pso.X, e,
+                   in_smem ? e + N : nullptr);
+    __syncthreads();
+    GENPROF_SET(4)
+    return;
+  }
   if (threadIdx.x == 0) {
     unsigned long long v[4] = {0, 0, 0, 0};
     for (int w = 0; w < NW; w++)
@@ -720,20 +797,6 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
     }
     if (last) finalize_cost(a, p, v, s_out.kc);
   }
-  if (!a.pso_on) return;
-  // ---- fused PSO bookkeeping (row A7): the last CTA of the grid, after every cost ----
-  __shared__ int s_lastcta;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(a.gcount, 1u);
-    s_lastcta = prev == gridDim.x - 1;
-    if (s_lastcta) {
-      __threadfence();
-      *a.gcount = 0;
-    }
-  }
-  __syncthreads();
-  if (s_lastcta) pso_book_block(a.pso, a.pso_k, a.pso_k >= 1 ? a.x_out : a.pso.X);
 }
 
 __global__ void k_fk_debug(const double* pose, const DimsD dims, const CamParams cam,

@@ -98,28 +98,41 @@ __device__ __forceinline__ void pso_update_warp(const PsoDev& p, int i, int k, c
 // positions X — pbest (strict <), gbest (lowest index on ties, NaN = +inf), trace, stop
 // rule, and the mutation marks for generation k + 1 (worst floor(N frac) by Pcost, ties:
 // higher index worse).  Ends with __syncthreads.
-__device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const double* X) {
+// e: this generation's costs (global p.E, or a shared-memory copy); spc: optional
+// shared-memory scratch [N] for the personal-best costs (the global p.Pc is kept in step).
+__device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const double* X,
+                                               const double* e_in = nullptr,
+                                               double* spc = nullptr) {
   __shared__ double s_v[32];
   __shared__ int s_i[32];
   __shared__ int s_g;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int nw = nt >> 5;
+  const double* E = e_in ? e_in : p.E;
+  double* PC = spc ? spc : p.Pc;
+  if (spc) {
+    for (int i = tid; i < p.N; i += nt) spc[i] = p.Pc[i];
+    __syncthreads();
+  }
   // pbest: one warp per particle, lanes copy the dims
   for (int i = warp; i < p.N; i += nw) {
-    double e = p.E[i];
+    double e = E[i];
     if (isnan(e)) e = INFINITY;
-    const bool imp = k == 0 || e < p.Pc[i];
+    const bool imp = k == 0 || e < PC[i];
     if (imp) {
       for (int d = lane; d < p.D; d += 32)
         p.P[(long long)i * p.D + d] = X[(long long)i * p.D + d];
-      if (lane == 0) p.Pc[i] = e;
+      if (lane == 0) {
+        PC[i] = e;
+        if (spc) p.Pc[i] = e;
+      }
     }
   }
   __syncthreads();
   double bv = INFINITY;
   int bi = 0x7fffffff;
   for (int i = tid; i < p.N; i += nt) {
-    const double v = p.Pc[i];
+    const double v = PC[i];
     if (v < bv || (v == bv && i < bi)) {
       bv = v;
       bi = i;
@@ -149,10 +162,10 @@ __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const dou
       }
     if (g >= p.N) g = 0;  // all +inf (or NaN): lowest index
     s_g = g;
-    *p.Gc = p.Pc[g];
-    p.trace[k] = p.Pc[g];
+    *p.Gc = PC[g];
+    p.trace[k] = PC[g];
     *p.gens_run = k + 1;
-    if (p.dyn->stop > -INFINITY && p.Pc[g] < p.dyn->stop) *p.done = 1;  // P:L148 stop rule
+    if (p.dyn->stop > -INFINITY && PC[g] < p.dyn->stop) *p.done = 1;  // P:L148 stop rule
   }
   __syncthreads();
   const int g = s_g;
@@ -162,10 +175,10 @@ __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const dou
   for (int i = tid; i < p.N; i += nt) {
     int m = 0;
     if (mut) {
-      const double ci = p.Pc[i];
+      const double ci = PC[i];
       int rank = 0;
       for (int j = 0; j < p.N; j++) {
-        const double cj = p.Pc[j];
+        const double cj = PC[j];
         rank += (cj < ci) || (cj == ci && j < i);
       }
       m = rank >= p.N - p.nmut;
