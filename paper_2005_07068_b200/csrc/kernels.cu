@@ -18,6 +18,37 @@
 
 #include "common.cuh"
 #include "fk.cuh"
+#if HP_GEN_PROF
+__device__ unsigned long long g_genprof[64][8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define GENPROF_MIN(i) \
+  if (a.pso_on && threadIdx.x == 0 && a.pso_k < 64) atomicMin(&g_genprof[a.pso_k][i], gtime());
+#define GENPROF_MAX(i) \
+  if (a.pso_on && threadIdx.x == 0 && a.pso_k < 64) atomicMax(&g_genprof[a.pso_k][i], gtime());
+#define GENPROF_SET(i) \
+  if (a.pso_on && threadIdx.x == 0 && a.pso_k < 64) g_genprof[a.pso_k][i] = gtime();
+#define GENPROF_BOOK(i) \
+  if (threadIdx.x == 0 && k < 64) g_genprof[k][i] = gtime();
+extern "C" int hp_debug_gen_prof(unsigned long long* out, int reset) {
+  if (reset) {
+    static unsigned long long init[64][8];
+    for (int k = 0; k < 64; k++) {
+      init[k][0] = ~0ull;
+      for (int i = 1; i < 8; i++) init[k][i] = 0;
+    }
+    return (int)cudaMemcpyToSymbol(g_genprof, init, sizeof(init));
+  }
+  return (int)cudaMemcpyFromSymbol(out, g_genprof, sizeof(g_genprof));
+}
+#else
+#define GENPROF_MIN(i)
+#define GENPROF_MAX(i)
+#define GENPROF_SET(i)
+#endif
 #include "pso.cuh"
 
 // resident warps per SM the register budgets are sized for: 64 registers, 4 CTAs x 8 warps
@@ -630,35 +661,6 @@ __device__ __forceinline__ double finalize_cost(const EvalArgs& a, int p,
 // warps stage the ray table; then all warps take tiles dynamically.  Used for small swarms
 // (S > 1 splits per particle keep every SM busy) and for the depth-image hooks.
 // ---------------------------------------------------------------------------------------
-#if HP_GEN_PROF
-__device__ unsigned long long g_genprof[64][5];
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define GENPROF_MIN(i) \
-  if (a.pso_on && threadIdx.x == 0 && a.pso_k < 64) atomicMin(&g_genprof[a.pso_k][i], gtime());
-#define GENPROF_MAX(i) \
-  if (a.pso_on && threadIdx.x == 0 && a.pso_k < 64) atomicMax(&g_genprof[a.pso_k][i], gtime());
-#define GENPROF_SET(i) \
-  if (a.pso_on && threadIdx.x == 0 && a.pso_k < 64) g_genprof[a.pso_k][i] = gtime();
-extern "C" int hp_debug_gen_prof(unsigned long long* out, int reset) {
-  if (reset) {
-    static unsigned long long init[64][5];
-    for (int k = 0; k < 64; k++) {
-      init[k][0] = ~0ull;
-      for (int i = 1; i < 5; i++) init[k][i] = 0;
-    }
-    return (int)cudaMemcpyToSymbol(g_genprof, init, sizeof(init));
-  }
-  return (int)cudaMemcpyFromSymbol(out, g_genprof, sizeof(g_genprof));
-}
-#else
-#define GENPROF_MIN(i)
-#define GENPROF_MAX(i)
-#define GENPROF_SET(i)
-#endif
 #ifndef HP_EVAL_FK_TEAM
 #define HP_EVAL_FK_TEAM 3  // k_eval's FK team: warps 0..2 (one primitive kind per warp)
 #endif
@@ -747,13 +749,12 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
       for (int k = 0; k < 4; k++)
         if (v[k]) atomicAdd(gacc + k, v[k]);
       if (sidx == 0) a.kc_g[p] = s_out.kc;
-      __threadfence();
-      const unsigned prev = atomicAdd(a.gcount, 1u);
+      // one acq_rel arrival: releases this CTA's sums, and the last CTA acquires everyone's
+      unsigned prev;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                   : "=r"(prev) : "l"(a.gcount) : "memory");
       s_lastcta = prev == gridDim.x - 1;
-      if (s_lastcta) {
-        __threadfence();
-        *a.gcount = 0;
-      }
+      if (s_lastcta) *a.gcount = 0;
     }
     __syncthreads();
     if (!s_lastcta) return;
@@ -770,11 +771,13 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
         v[k] = __ldcg(a.acc + (size_t)i * 4 + k);
         a.acc[(size_t)i * 4 + k] = 0ull;  // zero for the next generation
       }
+      if (in_smem) e[N + i] = __ldcg(a.pso.Pc + i);  // the bookkeeping's pbest copy
       e[i] = finalize_cost(a, i, v, __ldcg(a.kc_g + i));  // also stores costs64 = E
     }
     __syncthreads();
+    GENPROF_SET(5)
     pso_book_block(a.pso, a.pso_k, a.pso_k >= 1 ? a.x_out : a.pso.X, e,
-                   in_smem ? e + N : nullptr);
+                   in_smem ? e + N : nullptr, /*spc_loaded=*/true);
     __syncthreads();
     GENPROF_SET(4)
     return;

@@ -98,11 +98,13 @@ __device__ __forceinline__ void pso_update_warp(const PsoDev& p, int i, int k, c
 // positions X — pbest (strict <), gbest (lowest index on ties, NaN = +inf), trace, stop
 // rule, and the mutation marks for generation k + 1 (worst floor(N frac) by Pcost, ties:
 // higher index worse).  Ends with __syncthreads.
+constexpr int kPsoMaxFlags = 1024;  // particles whose pbest flags fit the shared bitmask
 // e: this generation's costs (global p.E, or a shared-memory copy); spc: optional
 // shared-memory scratch [N] for the personal-best costs (the global p.Pc is kept in step).
 __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const double* X,
                                                const double* e_in = nullptr,
-                                               double* spc = nullptr) {
+                                               double* spc = nullptr,
+                                               bool spc_loaded = false) {
   __shared__ double s_v[32];
   __shared__ int s_i[32];
   __shared__ int s_g;
@@ -110,25 +112,42 @@ __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const dou
   const int nw = nt >> 5;
   const double* E = e_in ? e_in : p.E;
   double* PC = spc ? spc : p.Pc;
-  if (spc) {
+  const double stop = p.dyn->stop;  // loaded early: off the tail's critical path
+  if (spc && !spc_loaded) {
     for (int i = tid; i < p.N; i += nt) spc[i] = p.Pc[i];
     __syncthreads();
   }
-  // pbest: one warp per particle, lanes copy the dims
-  for (int i = warp; i < p.N; i += nw) {
+  // pbest: the improvement flags first (one thread per particle), then every (particle,
+  // dim) copy in parallel so the global loads overlap instead of queueing per particle
+  __shared__ unsigned s_imp[(kPsoMaxFlags + 31) / 32];
+  const bool flags_in_smem = p.N <= kPsoMaxFlags;
+  for (int i = tid; i < p.N; i += nt) {
     double e = E[i];
     if (isnan(e)) e = INFINITY;
     const bool imp = k == 0 || e < PC[i];
     if (imp) {
-      for (int d = lane; d < p.D; d += 32)
-        p.P[(long long)i * p.D + d] = X[(long long)i * p.D + d];
-      if (lane == 0) {
-        PC[i] = e;
-        if (spc) p.Pc[i] = e;
-      }
+      PC[i] = e;
+      if (spc) p.Pc[i] = e;
+    }
+    if (flags_in_smem) {
+      if (imp) atomicOr(&s_imp[i >> 5], 1u << (i & 31));
+      else atomicAnd(&s_imp[i >> 5], ~(1u << (i & 31)));
+    } else if (imp) {
+      for (int d = 0; d < p.D; d++) p.P[(long long)i * p.D + d] = X[(long long)i * p.D + d];
     }
   }
   __syncthreads();
+  if (flags_in_smem) {
+    const int nd = p.N * p.D;  // <= 1024 x 64
+    for (int idx = tid; idx < nd; idx += nt) {
+      const int i = idx / p.D;
+      if ((s_imp[i >> 5] >> (i & 31)) & 1u) p.P[idx] = X[idx];
+    }
+  }
+  __syncthreads();
+#ifdef GENPROF_BOOK
+  GENPROF_BOOK(6)
+#endif
   double bv = INFINITY;
   int bi = 0x7fffffff;
   for (int i = tid; i < p.N; i += nt) {
@@ -165,11 +184,14 @@ __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const dou
     *p.Gc = PC[g];
     p.trace[k] = PC[g];
     *p.gens_run = k + 1;
-    if (p.dyn->stop > -INFINITY && PC[g] < p.dyn->stop) *p.done = 1;  // P:L148 stop rule
+    if (stop > -INFINITY && PC[g] < stop) *p.done = 1;  // P:L148 stop rule
   }
   __syncthreads();
   const int g = s_g;
   for (int d = tid; d < p.D; d += nt) p.G[d] = p.P[(long long)g * p.D + d];
+#ifdef GENPROF_BOOK
+  GENPROF_BOOK(7)
+#endif
   const int kn = k + 1;
   const bool mut = p.period > 0 && kn < p.K && kn % p.period == 0 && p.nmut > 0;
   for (int i = tid; i < p.N; i += nt) {

@@ -18,16 +18,18 @@ ctx.set_observation(d, m)
 c, r = W.local_init_box()
 ctx.pso_fit(seed=0, particles=64, generations=40, init_center=c, init_radius=r)
 L = hp.hp.lib()
-out = (C.c_ulonglong * (64 * 5))()
+out = (C.c_ulonglong * (64 * 8))()
 L.hp_debug_gen_prof(out, 1)
 ctx.pso_fit(seed=1, particles=64, generations=40, init_center=c, init_radius=r)
 torch.cuda.synchronize()
 L.hp_debug_gen_prof(out, 0)
-t = np.array(out[:], dtype=np.float64).reshape(64, 5)
+t = np.array(out[:], dtype=np.float64).reshape(64, 8)
 prev_end = None
 for k in range(1, 40):
-    s0, fk, tiles, b0, b1 = t[k]
+    s0, fk, tiles, b0, b1, fin, pb, am = t[k]
     gap = (s0 - prev_end) / 1e3 if prev_end else float("nan")
     print(f"gen {k:2d}: gap {gap:5.2f}  fk {(fk - s0) / 1e3:5.2f}  tiles {(tiles - fk) / 1e3:5.2f}  "
-          f"->book {(b0 - tiles) / 1e3:5.2f}  book {(b1 - b0) / 1e3:5.2f}  total {(b1 - s0) / 1e3:6.2f} us")
+          f"->last {(b0 - tiles) / 1e3:5.2f}  finalize {(fin - b0) / 1e3:5.2f}  pbest "
+          f"{(pb - fin) / 1e3:5.2f}  argmin {(am - pb) / 1e3:5.2f}  marks {(b1 - am) / 1e3:5.2f}  "
+          f"total {(b1 - s0) / 1e3:6.2f} us")
     prev_end = b1
