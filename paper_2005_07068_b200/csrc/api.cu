@@ -99,6 +99,8 @@ struct hp_ctx {
   double *X = nullptr, *V = nullptr, *P = nullptr, *Pc = nullptr, *E = nullptr;
   double *G = nullptr, *Gc = nullptr, *trace = nullptr, *bnd = nullptr, *centre = nullptr;
   int* mark = nullptr;
+  int* pimp = nullptr;  // deferred pbest flags (fused generations)
+  int* gsel = nullptr;  // deferred gbest (index, from X)
   int* flags = nullptr;  // [0] done, [1] gens_run
   PsoDyn* dyn = nullptr;
   double* h_out = nullptr;  // pinned: G[64], Gc, trace[K], gens_run
@@ -291,7 +293,7 @@ void hp_destroy(hp_ctx* ctx) {
                  ctx->E, ctx->G, ctx->Gc, ctx->trace, ctx->bnd, ctx->centre, ctx->mark,
                  ctx->flags, ctx->dyn, ctx->tmap_g, ctx->ray, ctx->pcount, ctx->X2,
                  ctx->V2, ctx->gcount, ctx->fk_g, ctx->tiles_g, ctx->ntl_g, ctx->near_list,
-                 ctx->near_count, ctx->kc_g};
+                 ctx->near_count, ctx->kc_g, ctx->pimp, ctx->gsel};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_poses) cudaFreeHost(ctx->h_poses);
@@ -482,6 +484,8 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   CKC(cudaMalloc(&ctx->Pc, N * sizeof(double)));
   CKC(cudaMalloc(&ctx->E, N * sizeof(double)));
   CKC(cudaMalloc(&ctx->mark, N * sizeof(int)));
+  CKC(cudaMalloc(&ctx->pimp, N * sizeof(int)));
+  CKC(cudaMalloc(&ctx->gsel, 2 * sizeof(int)));
   CKC(cudaMalloc(&ctx->G, 64 * sizeof(double)));
   CKC(cudaMalloc(&ctx->Gc, sizeof(double)));
   CKC(cudaMalloc(&ctx->bnd, 4 * 64 * sizeof(double)));
@@ -922,6 +926,8 @@ static PsoDev pso_dev(hp_ctx* ctx, int N, int D, const hp_pso_params* p, int mut
   d.Gc = ctx->Gc;
   d.trace = ctx->trace;
   d.mark = ctx->mark;
+  d.pimp = ctx->pimp;
+  d.gsel = ctx->gsel;
   d.done = ctx->flags;
   d.gens_run = ctx->flags + 1;
   return d;

@@ -87,6 +87,8 @@ struct PsoDev {
   int* mark;
   int* done;
   int* gens_run;
+  int* pimp;  // [N] deferred pbest flags (fused generations)
+  int* gsel;  // [2] deferred gbest: index, taken from X (fused generations)
 };
 
 enum EvalMode { kModeCost = 0, kModeDepth = 1 };

@@ -696,7 +696,8 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
       // fused PSO update (Eq. 6-7, row A8) of this particle; every CTA of the particle
       // computes the same bits, split 0 stores them (double-buffered X, V)
       if (warp == 0)
-        pso_update_warp(a.pso, p, a.pso_k, a.x_in, a.v_in, a.x_out, a.v_out, sidx == 0, s_pose);
+        pso_update_warp(a.pso, p, a.pso_k, a.x_in, a.v_in, a.x_out, a.v_out, sidx == 0, s_pose,
+                        /*deferred=*/true);
       __syncwarp();
       fk_team<double, kEvalFkTeam>(s_pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
     } else {
@@ -777,7 +778,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
     __syncthreads();
     GENPROF_SET(5)
     pso_book_block(a.pso, a.pso_k, a.pso_k >= 1 ? a.x_out : a.pso.X, e,
-                   in_smem ? e + N : nullptr, /*spc_loaded=*/true);
+                   in_smem ? e + N : nullptr, /*spc_loaded=*/true, /*deferred=*/true);
     __syncthreads();
     GENPROF_SET(4)
     return;

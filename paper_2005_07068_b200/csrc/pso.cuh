@@ -48,11 +48,19 @@ __device__ __forceinline__ double lerp_rn(double lo, double hi, double u) {
 // One warp: Eq. (6)-(7) + clamp + mutation for particle i at generation k >= 1.  Reads
 // x, v from Xin/Vin; if `write` stores them to Xout/Vout (may alias Xin/Vin when no other
 // thread reads the old values); if pose != nullptr lane d also leaves x_d there.
+// deferred (the fused generation kernel): the previous bookkeeping left P and G stale and
+// recorded pimp[i] (particle i improved: its pbest is its evaluated position Xin[i]) and
+// gsel = (g, pimp[g]); the update reads the values they stand for, and the writer CTA
+// materialises P[i].  Same bits as the eager form.
 __device__ __forceinline__ void pso_update_warp(const PsoDev& p, int i, int k, const double* Xin,
                                                 const double* Vin, double* Xout, double* Vout,
-                                                bool write, double* pose) {
+                                                bool write, double* pose,
+                                                bool deferred = false) {
   const int lane = threadIdx.x & 31;
   const PsoDyn dyn = *p.dyn;
+  const bool imp_i = deferred && p.pimp[i] != 0;
+  const int gi = deferred ? p.gsel[0] : 0;
+  const bool g_from_x = deferred && p.gsel[1] != 0;
   double r1 = 0.0, r2 = 0.0;
   if (!p.per_dim_r) {
     const uint4 r = draw(dyn.seed, (uint32_t)i, 0u, (uint32_t)k, 1u);
@@ -68,10 +76,20 @@ __device__ __forceinline__ void pso_update_warp(const PsoDev& p, int i, int k, c
     }
     const long long id = (long long)i * p.D + d;
     const double x0 = Xin[id];
+    double pb, gb;
+    if (deferred) {
+      pb = imp_i ? x0 : p.P[id];
+      if (imp_i && write) p.P[id] = x0;
+      const long long gid = (long long)gi * p.D + d;  // P[g] is not written when g_from_x
+      gb = g_from_x ? Xin[gid] : p.P[gid];
+    } else {
+      pb = p.P[id];
+      gb = p.G[d];
+    }
     // Eq. (6): v = w (v + c1 r1 (P - x) + c2 r2 (G - x));  Eq. (7): x = x + v
-    const double t1 = __dmul_rn(__dmul_rn(dyn.c1, r1), __dsub_rn(p.P[id], x0));
+    const double t1 = __dmul_rn(__dmul_rn(dyn.c1, r1), __dsub_rn(pb, x0));
     const double t2 = __dadd_rn(Vin[id], t1);
-    const double t3 = __dmul_rn(__dmul_rn(dyn.c2, r2), __dsub_rn(p.G[d], x0));
+    const double t3 = __dmul_rn(__dmul_rn(dyn.c2, r2), __dsub_rn(gb, x0));
     double v = __dmul_rn(dyn.w, __dadd_rn(t2, t3));
     double x = __dadd_rn(x0, v);
     if (x < p.lo[d]) {  // AMB-16: clamp, zero that velocity component
@@ -104,7 +122,8 @@ constexpr int kPsoMaxFlags = 1024;  // particles whose pbest flags fit the share
 __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const double* X,
                                                const double* e_in = nullptr,
                                                double* spc = nullptr,
-                                               bool spc_loaded = false) {
+                                               bool spc_loaded = false,
+                                               bool deferred = false) {
   __shared__ double s_v[32];
   __shared__ int s_i[32];
   __shared__ int s_g;
@@ -129,7 +148,9 @@ __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const dou
       PC[i] = e;
       if (spc) p.Pc[i] = e;
     }
-    if (flags_in_smem) {
+    if (deferred) {
+      p.pimp[i] = imp;
+    } else if (flags_in_smem) {
       if (imp) atomicOr(&s_imp[i >> 5], 1u << (i & 31));
       else atomicAnd(&s_imp[i >> 5], ~(1u << (i & 31)));
     } else if (imp) {
@@ -137,7 +158,7 @@ __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const dou
     }
   }
   __syncthreads();
-  if (flags_in_smem) {
+  if (!deferred && flags_in_smem) {
     const int nd = p.N * p.D;  // <= 1024 x 64
     for (int idx = tid; idx < nd; idx += nt) {
       const int i = idx / p.D;
@@ -188,7 +209,19 @@ __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const dou
   }
   __syncthreads();
   const int g = s_g;
-  for (int d = tid; d < p.D; d += nt) p.G[d] = p.P[(long long)g * p.D + d];
+  if (!deferred) {
+    for (int d = tid; d < p.D; d += nt) p.G[d] = p.P[(long long)g * p.D + d];
+  } else if (k + 1 >= p.K || *p.done) {
+    // last generation (or the stop rule fired): materialise P and G for the host
+    const int nd = p.N * p.D;
+    for (int idx = tid; idx < nd; idx += nt)
+      if (p.pimp[idx / p.D]) p.P[idx] = X[idx];
+    for (int d = tid; d < p.D; d += nt)
+      p.G[d] = p.pimp[g] ? X[(long long)g * p.D + d] : p.P[(long long)g * p.D + d];
+  } else if (tid == 0) {
+    p.gsel[0] = g;
+    p.gsel[1] = p.pimp[g];
+  }
 #ifdef GENPROF_BOOK
   GENPROF_BOOK(7)
 #endif
