@@ -31,8 +31,6 @@ __device__ __forceinline__ unsigned long long gtime() {
   if (a.pso_on && threadIdx.x == 0 && a.pso_k < 64) atomicMax(&g_genprof[a.pso_k][i], gtime());
 #define GENPROF_SET(i) \
   if (a.pso_on && threadIdx.x == 0 && a.pso_k < 64) g_genprof[a.pso_k][i] = gtime();
-#define GENPROF_BOOK(i) \
-  if (threadIdx.x == 0 && k < 64) g_genprof[k][i] = gtime();
 extern "C" int hp_debug_gen_prof(unsigned long long* out, int reset) {
   if (reset) {
     static unsigned long long init[64][8];
@@ -760,26 +758,38 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
     __syncthreads();
     if (!s_lastcta) return;
     GENPROF_SET(3)
-    // the ray table is dead now: its shared memory holds E and the pbest costs when they fit
-    const int N = a.pso.N;
-    const bool in_smem = (size_t)2 * N * sizeof(double) <=
+    // one pass per particle: Eq. (4)-(5), pbest (strict <, NaN = +inf) and the argmin;
+    // pbest / gbest positions are left to the next generation's update (deferred)
+    const PsoDev& ps = a.pso;
+    const int N = ps.N, k = a.pso_k;
+    const double stop = ps.dyn->stop;
+    // the ray table is dead now: its shared memory holds the pbest costs when they fit
+    const bool in_smem = (size_t)N * sizeof(double) <=
                          (size_t)ray_floats(a.cam.W, a.cam.H) * sizeof(float);
-    double* e = in_smem ? reinterpret_cast<double*>(s_ray) : a.pso.E;
+    double* pcs = in_smem ? reinterpret_cast<double*>(s_ray) : ps.Pc;
     __syncthreads();  // every warp is past its last ray-table read
+    double bv = INFINITY;
+    int bi = 0x7fffffff;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
       unsigned long long v[4];
-      for (int k = 0; k < 4; k++) {
-        v[k] = __ldcg(a.acc + (size_t)i * 4 + k);
-        a.acc[(size_t)i * 4 + k] = 0ull;  // zero for the next generation
+      for (int q = 0; q < 4; q++) {
+        v[q] = __ldcg(a.acc + (size_t)i * 4 + q);
+        a.acc[(size_t)i * 4 + q] = 0ull;  // zero for the next generation
       }
-      if (in_smem) e[N + i] = __ldcg(a.pso.Pc + i);  // the bookkeeping's pbest copy
-      e[i] = finalize_cost(a, i, v, __ldcg(a.kc_g + i));  // also stores costs64 = E
+      const double pc_old = __ldcg(ps.Pc + i);
+      double e = finalize_cost(a, i, v, __ldcg(a.kc_g + i));  // also stores costs64 = E
+      if (isnan(e)) e = INFINITY;
+      const bool imp = k == 0 || e < pc_old;
+      const double pc = imp ? e : pc_old;
+      if (imp) ps.Pc[i] = e;
+      if (in_smem) pcs[i] = pc;
+      ps.pimp[i] = imp;
+      if (pc < bv) {  // i ascending per thread: the lowest index wins ties
+        bv = pc;
+        bi = i;
+      }
     }
-    __syncthreads();
-    GENPROF_SET(5)
-    pso_book_block(a.pso, a.pso_k, a.pso_k >= 1 ? a.x_out : a.pso.X, e,
-                   in_smem ? e + N : nullptr, /*spc_loaded=*/true, /*deferred=*/true);
-    __syncthreads();
+    pso_book_tail(ps, k, a.pso_k >= 1 ? a.x_out : ps.X, pcs, bv, bi, stop);
     GENPROF_SET(4)
     return;
   }

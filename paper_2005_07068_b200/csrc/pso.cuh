@@ -122,8 +122,7 @@ constexpr int kPsoMaxFlags = 1024;  // particles whose pbest flags fit the share
 __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const double* X,
                                                const double* e_in = nullptr,
                                                double* spc = nullptr,
-                                               bool spc_loaded = false,
-                                               bool deferred = false) {
+                                               bool spc_loaded = false) {
   __shared__ double s_v[32];
   __shared__ int s_i[32];
   __shared__ int s_g;
@@ -148,9 +147,7 @@ __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const dou
       PC[i] = e;
       if (spc) p.Pc[i] = e;
     }
-    if (deferred) {
-      p.pimp[i] = imp;
-    } else if (flags_in_smem) {
+    if (flags_in_smem) {
       if (imp) atomicOr(&s_imp[i >> 5], 1u << (i & 31));
       else atomicAnd(&s_imp[i >> 5], ~(1u << (i & 31)));
     } else if (imp) {
@@ -158,7 +155,7 @@ __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const dou
     }
   }
   __syncthreads();
-  if (!deferred && flags_in_smem) {
+  if (flags_in_smem) {
     const int nd = p.N * p.D;  // <= 1024 x 64
     for (int idx = tid; idx < nd; idx += nt) {
       const int i = idx / p.D;
@@ -166,9 +163,6 @@ __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const dou
     }
   }
   __syncthreads();
-#ifdef GENPROF_BOOK
-  GENPROF_BOOK(6)
-#endif
   double bv = INFINITY;
   int bi = 0x7fffffff;
   for (int i = tid; i < p.N; i += nt) {
@@ -209,22 +203,7 @@ __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const dou
   }
   __syncthreads();
   const int g = s_g;
-  if (!deferred) {
-    for (int d = tid; d < p.D; d += nt) p.G[d] = p.P[(long long)g * p.D + d];
-  } else if (k + 1 >= p.K || *p.done) {
-    // last generation (or the stop rule fired): materialise P and G for the host
-    const int nd = p.N * p.D;
-    for (int idx = tid; idx < nd; idx += nt)
-      if (p.pimp[idx / p.D]) p.P[idx] = X[idx];
-    for (int d = tid; d < p.D; d += nt)
-      p.G[d] = p.pimp[g] ? X[(long long)g * p.D + d] : p.P[(long long)g * p.D + d];
-  } else if (tid == 0) {
-    p.gsel[0] = g;
-    p.gsel[1] = p.pimp[g];
-  }
-#ifdef GENPROF_BOOK
-  GENPROF_BOOK(7)
-#endif
+  for (int d = tid; d < p.D; d += nt) p.G[d] = p.P[(long long)g * p.D + d];
   const int kn = k + 1;
   const bool mut = p.period > 0 && kn < p.K && kn % p.period == 0 && p.nmut > 0;
   for (int i = tid; i < p.N; i += nt) {
@@ -234,6 +213,81 @@ __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const dou
       int rank = 0;
       for (int j = 0; j < p.N; j++) {
         const double cj = PC[j];
+        rank += (cj < ci) || (cj == ci && j < i);
+      }
+      m = rank >= p.N - p.nmut;
+    }
+    p.mark[i] = m;
+  }
+  __syncthreads();
+}
+
+// The fused generation kernel's bookkeeping tail (deferred form, see pso_update_warp): the
+// caller has finalised E, updated Pc / pimp and left each thread's (best pcost, index) in
+// (bv, bi); pcs = the pbest costs (shared memory, or the global Pc).  Reduces the argmin,
+// writes Gc / trace / stop, the deferred gbest (or, after the last generation or the stop,
+// materialises P and G for the host), then the mutation marks.  Ends with __syncthreads.
+__device__ __forceinline__ void pso_book_tail(const PsoDev& p, int k, const double* X,
+                                              const double* pcs, double bv, int bi,
+                                              double stop) {
+  __shared__ double s_v[32];
+  __shared__ int s_i[32];
+  __shared__ int s_g, s_final;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = nt >> 5;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+    if (ov < bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    s_v[warp] = bv;
+    s_i[warp] = bi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double v = INFINITY;
+    int g = 0x7fffffff;
+    for (int w = 0; w < nw; w++)
+      if (s_v[w] < v || (s_v[w] == v && s_i[w] < g)) {
+        v = s_v[w];
+        g = s_i[w];
+      }
+    if (g >= p.N) g = 0;  // all +inf (or NaN): lowest index
+    s_g = g;
+    const double gc = pcs[g];
+    *p.Gc = gc;
+    p.trace[k] = gc;
+    *p.gens_run = k + 1;
+    const bool stopped = stop > -INFINITY && gc < stop;  // P:L148 stop rule
+    if (stopped) *p.done = 1;
+    s_final = stopped || k + 1 >= p.K;
+  }
+  __syncthreads();
+  const int g = s_g;
+  if (s_final) {  // materialise P and G for the host
+    const int nd = p.N * p.D;
+    for (int idx = tid; idx < nd; idx += nt)
+      if (p.pimp[idx / p.D]) p.P[idx] = X[idx];
+    for (int d = tid; d < p.D; d += nt)
+      p.G[d] = p.pimp[g] ? X[(long long)g * p.D + d] : p.P[(long long)g * p.D + d];
+  } else if (tid == 0) {
+    p.gsel[0] = g;
+    p.gsel[1] = p.pimp[g];
+  }
+  const int kn = k + 1;
+  const bool mut = p.period > 0 && kn < p.K && kn % p.period == 0 && p.nmut > 0;
+  for (int i = tid; i < p.N; i += nt) {
+    int m = 0;
+    if (mut) {
+      const double ci = pcs[i];
+      int rank = 0;
+      for (int j = 0; j < p.N; j++) {
+        const double cj = pcs[j];
         rank += (cj < ci) || (cj == ci && j < i);
       }
       m = rank >= p.N - p.nmut;

@@ -26,10 +26,9 @@ L.hp_debug_gen_prof(out, 0)
 t = np.array(out[:], dtype=np.float64).reshape(64, 8)
 prev_end = None
 for k in range(1, 40):
-    s0, fk, tiles, b0, b1, fin, pb, am = t[k]
+    s0, fk, tiles, b0, b1 = t[k][:5]
     gap = (s0 - prev_end) / 1e3 if prev_end else float("nan")
-    print(f"gen {k:2d}: gap {gap:5.2f}  fk {(fk - s0) / 1e3:5.2f}  tiles {(tiles - fk) / 1e3:5.2f}  "
-          f"->last {(b0 - tiles) / 1e3:5.2f}  finalize {(fin - b0) / 1e3:5.2f}  pbest "
-          f"{(pb - fin) / 1e3:5.2f}  argmin {(am - pb) / 1e3:5.2f}  marks {(b1 - am) / 1e3:5.2f}  "
-          f"total {(b1 - s0) / 1e3:6.2f} us")
+    print(f"gen {k:2d}: gap {gap:5.2f}  update+fk {(fk - s0) / 1e3:5.2f}  tiles "
+          f"{(tiles - fk) / 1e3:5.2f}  ->last CTA {(b0 - tiles) / 1e3:5.2f}  finalize+book "
+          f"{(b1 - b0) / 1e3:5.2f}  total {(b1 - s0) / 1e3:6.2f} us")
     prev_end = b1
