@@ -279,6 +279,38 @@ def run_ours(args):
     value = PER_RANK * world / (ms_per_step * 1e-3)
     launches = args.steps * ctx.last_launch_count()
 
+    # ---- pipelined (SURVEY §8(d) M1's second mode): two contexts on two streams, calls
+    #      k and k + 1 overlapped (one call's FK under the other's render tail); inputs
+    #      resident, no flush between the overlapped calls ----
+    pipelined = None
+    if world == 1 and args.steps >= 4:
+        ctx2 = hp.Context(WIDTH, HEIGHT, max_particles=PER_RANK)
+        ctx2.set_observation(depth, mask)
+        costs2 = torch.empty_like(costs)
+        sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+        pairs = [(ctx, costs, sa), (ctx2, costs2, sb)]
+        for k in range(4):
+            c_, o_, st_ = pairs[k & 1]
+            c_.eval_costs(P, out=o_, stream=st_)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sa.wait_event(e0)
+        sb.wait_event(e0)
+        for k in range(args.steps):
+            c_, o_, st_ = pairs[k & 1]
+            c_.eval_costs(P, out=o_, stream=st_)
+        ea.record(sa)
+        eb.record(sb)
+        torch.cuda.synchronize()
+        pms = max(e0.elapsed_time(ea), e0.elapsed_time(eb)) / args.steps
+        pipelined = {"value": PER_RANK / (pms * 1e-3), "unit": "hyp/s", "ms_per_call": pms,
+                     "config": "two contexts on two streams, alternating calls on the C4 "
+                               "batch; inputs resident in HBM, no L2 flush between the "
+                               "overlapped calls"}
+        del ctx2
+
     # ---- end to end through the public host API (pinned host <-> device inside) ----
     # inputs and outputs in page-locked host memory (the contract's e2e setup)
     pin_in = torch.from_numpy(np.ascontiguousarray(
@@ -461,6 +493,8 @@ def run_ours(args):
             line["pso_fit"] = fit
         if track:
             line["tracking"] = track
+        if pipelined:
+            line["pipelined"] = pipelined
         if frames:
             line["frames"] = frames
         if kinect:
