@@ -97,3 +97,30 @@ def test_tracking_sequence_matches_oracle():
         centre, rad = r.best_x, radius
     # frame 0 starts from the motion truth's neighbourhood: the fit beats a cold start
     assert costs[0] < 25.0
+
+
+def test_timing_hooks_and_two_contexts_on_two_streams():
+    """hp_set_timing / hp_last_kernel_ms (bench's roofline leg) and the pipelined mode: two
+    contexts driven on two streams concurrently give the single-context results."""
+    import paper_2005_07068_b200 as hp
+
+    ctx = hp.Context(320, 240, max_particles=2048)
+    obs = O.synthesize(W.H_A, O.camera(320, 240))
+    ctx.set_observation(obs.depth, obs.mask)
+    P = torch.tensor(W.swarm_c4(1500).astype(np.float32), device="cuda")
+    with pytest.raises(hp.HPError):
+        ctx.last_kernel_ms()  # nothing timed yet
+    ctx.set_timing(True)
+    ref = ctx.eval_costs(P).cpu().numpy()
+    fk_ms, render_ms = ctx.last_kernel_ms()
+    assert ctx.last_launch_count() == 3 and fk_ms > 0 and render_ms > 0
+    ctx.set_timing(False)
+    ctx2 = hp.Context(320, 240, max_particles=2048)
+    ctx2.set_observation(obs.depth, obs.mask)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = [torch.empty(1500, device="cuda") for _ in range(6)]
+    for k in range(6):
+        (ctx if k % 2 == 0 else ctx2).eval_costs(P, out=outs[k], stream=sa if k % 2 == 0 else sb)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert np.array_equal(o.cpu().numpy(), ref)
