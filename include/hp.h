@@ -180,10 +180,13 @@ hp_status hp_eval_costs_frames(hp_ctx* ctx, const float* poses_dev, int64_t n_pe
 hp_status hp_eval_sums_frames(hp_ctx* ctx, const float* poses_dev, int64_t n_per_frame,
                               uint64_t* sums_dev, double* costs64_dev, void* stream);
 
-/* Same with HOST buffers: copies poses in, scores, copies costs out, then synchronises
- * `stream` (the end-to-end path a host application calls).  Page-locked buffers
- * (cudaHostAlloc, cudaHostRegister, torch pin_memory) are DMA'd directly; pageable ones are
- * staged through the context's pinned buffers (one extra host memcpy each way). */
+/* Same with HOST buffers: moves poses in, scores, moves costs out, then synchronises
+ * `stream` (the end-to-end path a host application calls).  Mapped page-locked buffers
+ * (cudaHostAlloc / torch pin_memory under unified addressing) are accessed by the kernels
+ * directly — the FK kernel loads the poses and the cost finalisation stores the costs over
+ * the host link, no separate copies (HP_NO_ZEROCOPY=1 in the environment: DMA copies
+ * instead); other page-locked buffers are DMA'd directly; pageable ones are staged through
+ * the context's pinned buffers (one extra host memcpy each way). */
 hp_status hp_eval_costs_host(hp_ctx* ctx, const float* poses_host, int64_t n,
                              float* costs_host, void* stream);
 

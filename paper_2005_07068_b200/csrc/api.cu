@@ -133,6 +133,7 @@ struct hp_ctx {
   int use_tma = 1;   // HP_NO_TMA=1 in the environment selects plain loads (A/B, debugging)
   int sync_debug = 0;  // HP_SYNC_DEBUG=1: synchronise after every launch
   int use_pdl = 1;     // programmatic dependent launch between PSO generations (HP_NO_PDL=1)
+  int zero_copy = 1;   // host path: kernels access mapped pinned buffers (HP_NO_ZEROCOPY=1)
   cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};  // hp_set_timing: per-launch events
   int timing = 0;
   int timed = 0;  // the last hp_eval_costs / hp_eval_sums recorded tev
@@ -457,6 +458,8 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   CKC(cudaMemset(ctx->near_count, 0, sizeof(unsigned int)));
   ctx->blocks_per_sm = eval_blocks_per_sm(ctx->camp);
   ctx->persist_grid = ctx->sm_count * persist_blocks_per_sm(ctx->camp);
+  if (const char* e = getenv("HP_NO_ZEROCOPY"))
+    if (atoi(e)) ctx->zero_copy = 0;
   if (const char* e = getenv("HP_NO_PERSIST"))
     if (atoi(e)) ctx->persist_grid = 0;
   CKC(cudaMalloc(&ctx->tmap_g, sizeof(CUtensorMap)));
@@ -794,13 +797,16 @@ hp_status hp_eval_sums_frames(hp_ctx* ctx, const float* poses, int64_t n_per_fra
                      n_per_frame);
 }
 
-static bool is_pinned(const void* p) {
+static bool is_pinned(const void* p, void** dev = nullptr) {
   cudaPointerAttributes at{};
+  if (dev) *dev = nullptr;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     cudaGetLastError();  // clear the sticky-free error of an unknown pointer
     return false;
   }
-  return at.type == cudaMemoryTypeHost;
+  if (at.type != cudaMemoryTypeHost) return false;
+  if (dev) *dev = at.devicePointer;  // mapped page-locked memory: the kernels' address
+  return true;
 }
 
 hp_status hp_eval_costs_host(hp_ctx* ctx, const float* poses, int64_t n, float* costs,
@@ -841,18 +847,29 @@ hp_status hp_eval_costs_host(hp_ctx* ctx, const float* poses, int64_t n, float* 
   }
   // Page-locked caller buffers (cudaHostAlloc / cudaHostRegister / torch pin_memory) are
   // DMA'd directly; pageable ones go through the context's pinned staging buffers.
+  // Mapped page-locked buffers are read / written by the kernels over the host link
+  // (zero-copy: the FK kernel's pose loads are the host->device transfer, the cost
+  // finalisation's stores the device->host one), unless HP_NO_ZEROCOPY=1.
   const size_t in_bytes = (size_t)n * kNdof * sizeof(float), out_bytes = (size_t)n * 4;
-  const bool in_pinned = is_pinned(poses), out_pinned = is_pinned(costs);
+  void *in_dev = nullptr, *out_dev = nullptr;
+  const bool in_pinned = is_pinned(poses, &in_dev), out_pinned = is_pinned(costs, &out_dev);
+  if (!ctx->zero_copy) in_dev = out_dev = nullptr;
   const float* src = poses;
   if (!in_pinned) {
     memcpy(ctx->h_poses, poses, in_bytes);
     src = ctx->h_poses;
   }
-  CK(cudaMemcpyAsync(ctx->poses32, src, in_bytes, cudaMemcpyHostToDevice, s));
-  hp_status r = eval_common(ctx, ctx->poses32, n, ctx->costs32, nullptr, nullptr, s);
+  const float* dposes = static_cast<const float*>(in_dev);
+  if (!dposes) {
+    CK(cudaMemcpyAsync(ctx->poses32, src, in_bytes, cudaMemcpyHostToDevice, s));
+    dposes = ctx->poses32;
+  }
+  float* dcosts = out_dev ? static_cast<float*>(out_dev) : ctx->costs32;
+  hp_status r = eval_common(ctx, dposes, n, dcosts, nullptr, nullptr, s);
   if (r != HP_OK) return r;
-  CK(cudaMemcpyAsync(out_pinned ? costs : ctx->h_costs, ctx->costs32, out_bytes,
-                     cudaMemcpyDeviceToHost, s));
+  if (!out_dev)
+    CK(cudaMemcpyAsync(out_pinned ? costs : ctx->h_costs, ctx->costs32, out_bytes,
+                       cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (!out_pinned) memcpy(costs, ctx->h_costs, out_bytes);
   return HP_OK;
