@@ -266,7 +266,6 @@ cudaError_t launch_fk_debug(const double* pose_dev, const DimsD& dims, const Cam
                             cudaStream_t st);
 cudaError_t launch_ray_table(const CamParams& cam, float* ray, cudaStream_t st);
 cudaError_t launch_depth_to_mask(const float* depth, uint8_t* mask, int npx, cudaStream_t st);
-int eval_warps_per_cta();
 int persist_blocks_per_sm(const CamParams& cam);
 int eval_blocks_per_sm(const CamParams& cam);  // resident k_eval CTAs per SM
 size_t fk_record_bytes();

@@ -895,22 +895,15 @@ __device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out, uint
 #ifndef HP_FK_PDL
 #define HP_FK_PDL 1  // programmatic dependent launch of k_render_persist after k_fk_batch
 #endif
-#ifndef HP_FK_TEAM
-#define HP_FK_TEAM 1
-#endif
-// HP_FK_TEAM = 1: 4 particles per CTA, one warp each; 2: one particle per 2-warp CTA (the
-// record build runs on both warps, halving the latency of the longest FK phase)
-constexpr int kFkTeam = HP_FK_TEAM;
 #ifndef HP_FK_WARPS
 #define HP_FK_WARPS 4  // particles (warps) per k_fk_batch CTA
 #endif
-constexpr int kFkWarps = kFkTeam == 2 ? 2 : HP_FK_WARPS;
-constexpr int kFkPerCta = kFkTeam == 2 ? 1 : HP_FK_WARPS;
+constexpr int kFkWarps = HP_FK_WARPS;
 template <typename PoseT>
-__global__ void __launch_bounds__(kFkWarps * 32, kFkTeam == 2 ? 16 : 32 / HP_FK_WARPS)
+__global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
     k_fk_batch(const EvalArgs a) {
-  __shared__ FkScratch s_fk[kFkPerCta];
-  __shared__ __align__(16) FkOut s_out[kFkPerCta];
+  __shared__ FkScratch s_fk[kFkWarps];
+  __shared__ __align__(16) FkOut s_out[kFkWarps];
   static_assert(sizeof(FkScratch) >= 2 * kMaxBand * sizeof(uint2), "band masks alias s_fk");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #if HP_FK_PDL
@@ -918,37 +911,29 @@ __global__ void __launch_bounds__(kFkWarps * 32, kFkTeam == 2 ? 16 : 32 / HP_FK_
   // on SMs this grid frees; it waits for this grid's completion before reading its output
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
-  const int slot = kFkTeam == 2 ? 0 : warp;
-  const int p = blockIdx.x * kFkPerCta + slot;
-  if (p >= a.n) return;  // uniform per team; only team-local barriers below
+  const int p = blockIdx.x * kFkWarps + warp;  // one warp per particle
+  if (p >= a.n) return;  // warp-uniform; only warp-local synchronisation below
   const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
-  fk_team<PoseT, kFkTeam>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk[slot], s_out[slot]);
-  if (kFkTeam == 2 && warp == 1) return;  // warp 0 finishes (fk_team synced the team)
-  if (kFkTeam == 1) {
-    // the record leaves by one bulk copy while the warp builds the tile list: every lane
-    // orders its record writes before the async proxy, then lane 0 issues the copy
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0)
-      bulk_s2g(static_cast<FkOut*>(a.fk_g) + p, &s_out[slot], (uint32_t)sizeof(FkOut));
-  } else {
-    const float4* src = reinterpret_cast<const float4*>(&s_out[slot]);
-    float4* dst = reinterpret_cast<float4*>(static_cast<FkOut*>(a.fk_g) + p);
-    for (int i = lane; i < (int)(sizeof(FkOut) / 16); i += 32) dst[i] = src[i];
-  }
+  fk_team<PoseT, 1>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk[warp], s_out[warp]);
+  // the record leaves by one bulk copy while the warp builds the tile list: every lane
+  // orders its record writes before the async proxy, then lane 0 issues the copy
+  fence_proxy_async();
+  __syncwarp();
+  if (lane == 0)
+    bulk_s2g(static_cast<FkOut*>(a.fk_g) + p, &s_out[warp], (uint32_t)sizeof(FkOut));
   FKPROF(4)
-  uint2* band = reinterpret_cast<uint2*>(&s_fk[slot]);  // FK scratch is dead by now
-  const int cnt = build_tile_list(s_out[slot], a.tiles_g + (size_t)p * kMaxTiles, band,
+  uint2* band = reinterpret_cast<uint2*>(&s_fk[warp]);  // FK scratch is dead by now
+  const int cnt = build_tile_list(s_out[warp], a.tiles_g + (size_t)p * kMaxTiles, band,
                                   band + kMaxBand);
   FKPROF(5)
   if (lane == 0) {
     int ntl = cnt;
-    if (!s_out[slot].near_ok) {  // some primitive may cross z_near: the exact pass renders it
+    if (!s_out[warp].near_ok) {  // some primitive may cross z_near: the exact pass renders it
       a.near_list[atomicAdd(a.near_count, 1u)] = p;
       ntl = -2;
     }
     a.ntl_g[p] = ntl;
-    if (kFkTeam == 1) bulk_wait_all();  // complete before the CTA's shared memory retires
+    bulk_wait_all();  // the record copy completes before the CTA's shared memory retires
   }
   FKPROF(6)
 }
@@ -1117,7 +1102,6 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
 #define HP_NW 8
 #endif
 constexpr int kEvalWarps = HP_NW;
-int eval_warps_per_cta() { return kEvalWarps; }
 
 // Prefer the maximum shared-memory carveout (the default 64 KB split would cap the
 // persistent kernel, 37 KB of shared memory per CTA, at one CTA per SM).
@@ -1217,7 +1201,7 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
   const dim3 grid((unsigned)blocks), block(kEvalWarps * 32);
   const size_t dyn = (size_t)ray_floats(a.cam.W, a.cam.H) * sizeof(float);
   if (two) {
-    const dim3 fgrid((unsigned)((a.n + kFkPerCta - 1) / kFkPerCta));
+    const dim3 fgrid((unsigned)((a.n + kFkWarps - 1) / kFkWarps));
     if (pose_double) k_fk_batch<double><<<fgrid, kFkWarps * 32, 0, st>>>(a);
     else k_fk_batch<float><<<fgrid, kFkWarps * 32, 0, st>>>(a);
     cudaError_t e = cudaGetLastError();
