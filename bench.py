@@ -348,6 +348,21 @@ def run_ours(args):
                          f"{args.fit_seeds} seeds", "last_best_cost": r.best_cost,
                "launches_per_fit": ctx.last_launch_count(),
                "paper_context": "0.8 s/frame on AMD HD5870M + i7-740QM, 64 x 30 (P:L197)"}
+        # M2's smaller configurations: C1 160x120 16 x 10, C2 320x240 64 x 40
+        for name, (fw, fh, fn, fk) in (("C1", (160, 120, 16, 10)), ("C2", (320, 240, 64, 40))):
+            cctx = hp.Context(fw, fh, max_particles=fn)
+            cd, cm = cctx.render_observation(W.H_A)
+            cctx.set_observation(cd, cm)
+            cctx.pso_fit(seed=0, particles=fn, generations=fk, init_center=c, init_radius=rad)
+            cms = []
+            for sd in range(args.fit_seeds):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                cctx.pso_fit(seed=sd + 1, particles=fn, generations=fk, init_center=c,
+                             init_radius=rad)
+                cms.append(1e3 * (time.perf_counter() - t0))
+            fit[f"{name}_ms_per_frame"] = statistics.median(cms)
+            del cctx
 
     # ---- C5 tracking (next row f1): 100-frame synthetic motion at 640x480, warm start ----
     track = None
