@@ -157,7 +157,15 @@ def cpu_baseline(seconds: float, swarm: np.ndarray):
         O.eval_batch(batch, obs, culled=True, threads=cores)
         done += len(batch)
     dt = time.perf_counter() - t0
+    # the same sample on one core, a short bounded run
+    one, t1 = 0, time.perf_counter()
+    while time.perf_counter() - t1 < min(4.0, seconds / 3):
+        O.eval_batch(np.asarray(swarm[one % len(swarm):][:4], np.float64), obs, culled=True,
+                     threads=1)
+        one += 4
+    one_rate = one / (time.perf_counter() - t1)
     return {"value": done / dt, "unit": "hyp/s", "cores": cores, "kind": "oracle",
+            "value_1core": one_rate,
             "sample": f"{done} poses of the C4 swarm in order (cycling after {len(swarm)}) at "
                       f"640x480, oracle culled mode (fp64, bitwise equal to brute force), "
                       f"{dt:.1f} s"}
