@@ -333,3 +333,24 @@ def test_batch_path_close_up_poses_beyond_tile_list_capacity():
             ne = int(O.edge_mask(close[k].astype(np.float64), O.camera(640, 480),
                                  obs_depth=obs.depth).sum())
             assert abs(int(sums[off + k, 0]) - so[j].s_rm) <= ne
+
+
+def test_max_batch_16384_sampled_parity():
+    """The largest batch a context is sized for (max_particles = 16384 at 640x480): the
+    persistent path's outputs sampled against the oracle and against single-pose calls."""
+    ctx = hp.Context(640, 480, max_particles=16384)
+    obs = obs_for(W.H_A, 640, 480)
+    swarm = np.concatenate([W.swarm_c4(12288, seed=1), W.random_poses(77, 4096)]).astype(np.float32)
+    sums, c64, c32 = gpu_costs(ctx, obs, swarm)
+    assert ctx.last_launch_count() == 3 and np.all(np.isfinite(c32))
+    for i in (0, 9999, 16383):
+        s1, c1, _ = gpu_costs(ctx, obs, swarm[i:i + 1])
+        assert np.array_equal(s1[0], sums[i]) and c1[0] == c64[i]
+    sample = [5, 6000, 12287, 12288, 16000]
+    co, so, _, _ = oracle_eval(obs, swarm[sample])
+    for k, i in enumerate(sample):
+        if int(sums[i, 0]) == so[k].s_rm and int(sums[i, 1]) == so[k].s_and:
+            assert abs(c64[i] - co[k]) <= E_REL * abs(co[k]) + E_ABS
+    with pytest.raises(hp.HPError):
+        ctx.eval_costs(torch.zeros((16385, 26), device="cuda"))
+    ctx.close()
