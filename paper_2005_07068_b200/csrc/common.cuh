@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+
 namespace hp {
 
 constexpr int kNdof = 26;
@@ -135,6 +137,23 @@ struct EvalArgs {
   int* near_list;                 // [n] particles whose primitives may cross z_near
   unsigned int* near_count;       // their number (reset by the near-plane pass)
 };
+
+// Debug builds (-DHP_DEBUG_CHECKS=1): device-side bounds checks that trap (the GPU test
+// suite is run once against such a build; compute-sanitizer is not available on the pool).
+#if HP_DEBUG_CHECKS
+#define HP_CHECK(cond)                                                              \
+  do {                                                                              \
+    if (!(cond)) {                                                                  \
+      printf("HP_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__,   \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                          \
+      __trap();                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define HP_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
 
 // Observation frame of pose p; frame f occupies rows [f H, (f + 1) H) of the packed buffer
 __device__ __forceinline__ int frame_of(const EvalArgs& a, int p) {

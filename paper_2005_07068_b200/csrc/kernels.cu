@@ -474,12 +474,15 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
     // consumed before the __syncwarp that ended it (WAR across proxies is ordered)
     // rows past this frame's bottom come from the next frame (or TMA zero fill): they are
     // off-image, their rays are NaN and they are never scored
+    HP_CHECK(yoff >= 0 && Y0 < a.cam.H);
     tma_load_2d_elect(obs_buf, a.use_tma == 2 ? a.tmap_g : tmap, X0, Y0 + yoff, bar,
                       kTileW * kTileH * 4);
   }
   const unsigned int msph = km.x, mcone = km.y, mell = km.z;
   Lane4 L;
   const int x = X0 + col;
+  HP_CHECK(X0 >= 0 && x < ray_dx_len(a.cam.W) && Y0 >= 0 && Y0 + rowb < a.cam.H + kRayPad);
+  HP_CHECK((X0 & 3) == 0);  // TMA boxes start 16-byte aligned
   L.dx = s_dx[x];
   const float ddx = fmaf(L.dx, L.dx, 1.f);
   const float4 dy4 = reinterpret_cast<const float4*>(s_dy)[Y0 + rowb];  // rows y, y+2, y+4, y+6
@@ -866,6 +869,7 @@ __device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out, uint
 #pragma unroll
     for (int jj = 32; jj < kNprim; jj++)
       m1 |= (unsigned)(bx[4 * jj] <= hi && bx[4 * jj + 2] >= lo) << (jj - 32);
+    HP_CHECK(q < g.tx + ty && q < 2 * kMaxBand);
     if (col) s_cm[q] = make_uint2(m0, m1);
     else s_rm[q - g.tx] = make_uint2(m0, m1);
   }
@@ -877,6 +881,7 @@ __device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out, uint
     int X0 = 0, Y0 = 0;
     if (t < g.ntiles) {
       g.origin(t, X0, Y0);
+      HP_CHECK((X0 - g.x0) / kTileW < kMaxBand && (Y0 - g.y0) / kTileH < kMaxBand);
       const uint2 c = s_cm[(X0 - g.x0) / kTileW], r = s_rm[(Y0 - g.y0) / kTileH];
       lo = c.x & r.x;
       hi = c.y & r.y;
@@ -884,9 +889,11 @@ __device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out, uint
     const unsigned int m0 = lo & 0xFFFFFu, m1 = (lo >> 20) | ((hi & 0x7u) << 12), m2 = hi >> 3;
     const bool ne = (lo | hi) != 0;
     const unsigned int bal = __ballot_sync(0xffffffffu, ne);
-    if (ne)
+    if (ne) {
+      HP_CHECK(cnt + __popc(bal & ((1u << lane) - 1u)) < kMaxTiles);
       out[cnt + __popc(bal & ((1u << lane) - 1u))] =
           make_uint4((unsigned)X0 | ((unsigned)Y0 << 16), m0, m1, m2);
+    }
     cnt += __popc(bal);
   }
   return cnt;
@@ -929,7 +936,9 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
   if (lane == 0) {
     int ntl = cnt;
     if (!s_out[warp].near_ok) {  // some primitive may cross z_near: the exact pass renders it
-      a.near_list[atomicAdd(a.near_count, 1u)] = p;
+      const unsigned slot_ = atomicAdd(a.near_count, 1u);
+      HP_CHECK(slot_ < (unsigned)a.n);
+      a.near_list[slot_] = p;
       ntl = -2;
     }
     a.ntl_g[p] = ntl;
@@ -1045,6 +1054,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
         int X0, Y0;
         uint3 km;
         if (nlist >= 0) {
+          HP_CHECK(t >= 0 && t < kMaxTiles);
           const uint4 it = s_tiles[b][t];
           X0 = (int)(it.x & 0xFFFFu);
           Y0 = (int)(it.x >> 16);
