@@ -103,7 +103,8 @@ hp_status hp_bounds(double lo[26], double hi[26]);
 /* Create a context on `device` (the current CUDA device if < 0) with a workspace for up
  * to max_particles poses per call.  dims/cost may be NULL (defaults).  The observation
  * starts empty (all undefined); set it with hp_set_observation.
- * Errors: INVALID_ARG (NULL out/cam, bad intrinsics, max_particles < 1), NO_DEVICE, OOM. */
+ * Errors: INVALID_ARG (NULL out/cam, bad intrinsics, max_particles < 1, an image whose
+ * ray table (width + 4 height + 80 floats) exceeds 64 KB of shared memory), NO_DEVICE, OOM. */
 hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims,
                     const hp_cost_params* cost, int32_t max_particles, int32_t device,
                     hp_ctx** out);

@@ -341,6 +341,9 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   ARG(out && cam, "hp_create: NULL argument");
   *out = nullptr;
   ARG(cam->width >= 1 && cam->height >= 1, "hp_create: width/height < 1");
+  ARG((size_t)ray_floats(cam->width, cam->height) * sizeof(float) <= kMaxRayBytes,
+      "hp_create: image too large (width + 4 height must stay below ~16k: the per-column / "
+      "per-row ray table lives in shared memory)");
   ARG(cam->fx > 0 && cam->fy > 0, "hp_create: fx/fy <= 0");
   ARG(cam->z_near_mm > 0 && cam->z_far_mm > cam->z_near_mm, "hp_create: need 0 < z_near < z_far");
   ARG(max_particles >= 1, "hp_create: max_particles < 1");

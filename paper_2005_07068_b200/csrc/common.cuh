@@ -30,6 +30,7 @@ static_assert(kPxPerLane == 4, "the row table packs a lane's 4 rows into one flo
 //          for y >= H.  A NaN ray never hits (every intersection is NaN), so pixels off
 //          the image need no bounds test in the scoring loop.
 __host__ __device__ constexpr int ray_dx_len(int W) { return (W + kRayPad + 3) & ~3; }
+constexpr size_t kMaxRayBytes = 64 * 1024;  // dynamic shared memory the kernels may use
 __host__ __device__ constexpr int ray_floats(int W, int H) {
   return ray_dx_len(W) + 4 * (H + kRayPad);
 }

@@ -1115,23 +1115,23 @@ constexpr int kEvalWarps = HP_NW;
 
 // Prefer the maximum shared-memory carveout (the default 64 KB split would cap the
 // persistent kernel, 37 KB of shared memory per CTA, at one CTA per SM).
+// Prefer the maximum shared-memory carveout and allow dynamic shared memory (the ray
+// table) beyond the default 48 KB for large images (hp_create caps it at kMaxRayBytes).
 static void set_carveouts() {
   static bool done = false;
   if (done) return;
   done = true;
   const int pct = cudaSharedmemCarveoutMaxShared;
-  cudaFuncSetAttribute(k_render_persist<kEvalWarps, false>,
-                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-  cudaFuncSetAttribute(k_render_persist<kEvalWarps, true>,
-                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-  cudaFuncSetAttribute(k_eval<kEvalWarps, float, kModeCost>,
-                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-  cudaFuncSetAttribute(k_eval<kEvalWarps, double, kModeCost>,
-                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-  cudaFuncSetAttribute(k_eval<kEvalWarps, float, kModeDepth>,
-                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-  cudaFuncSetAttribute(k_eval<kEvalWarps, double, kModeDepth>,
-                       cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  auto cfg = [&](auto f) {
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxRayBytes);
+  };
+  cfg(k_render_persist<kEvalWarps, false>);
+  cfg(k_render_persist<kEvalWarps, true>);
+  cfg(k_eval<kEvalWarps, float, kModeCost>);
+  cfg(k_eval<kEvalWarps, double, kModeCost>);
+  cfg(k_eval<kEvalWarps, float, kModeDepth>);
+  cfg(k_eval<kEvalWarps, double, kModeDepth>);
 }
 
 size_t fk_record_bytes() { return sizeof(FkOut); }

@@ -74,6 +74,9 @@ def test_create_validates_and_reports_no_device():
     assert L.hp_create(C.byref(bad), None, None, 16, -1, C.byref(h)) == hp.hp.HP_ERR_INVALID_ARG
     ok = hp.default_intrinsics(160, 120)
     assert L.hp_create(C.byref(ok), None, None, 0, -1, C.byref(h)) == hp.hp.HP_ERR_INVALID_ARG
+    huge = hp.default_intrinsics(8192, 4096)  # the ray table would not fit shared memory
+    assert L.hp_create(C.byref(huge), None, None, 16, -1, C.byref(h)) == hp.hp.HP_ERR_INVALID_ARG
+    assert b"too large" in L.hp_last_error(None)
     import torch
 
     if not torch.cuda.is_available():

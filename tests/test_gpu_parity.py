@@ -354,3 +354,21 @@ def test_max_batch_16384_sampled_parity():
     with pytest.raises(hp.HPError):
         ctx.eval_costs(torch.zeros((16385, 26), device="cuda"))
     ctx.close()
+
+
+def test_large_image_ray_table_beyond_48kb():
+    """4096x2160: the shared-memory ray table exceeds the default 48 KB dynamic limit."""
+    w, h = 4096, 2160
+    ctx = hp.Context(w, h, max_particles=64)
+    obs = obs_for(W.H_A, w, h)
+    poses = np.stack([W.H_A, W.NAMED["fist"]]).astype(np.float32)
+    sums, c64, _ = gpu_costs(ctx, obs, poses)
+    co, so, _, _ = oracle_eval(obs, poses)
+    for i in range(2):
+        if int(sums[i, 0]) == so[i].s_rm and int(sums[i, 1]) == so[i].s_and:
+            assert abs(c64[i] - co[i]) <= E_REL * abs(co[i]) + E_ABS
+        else:
+            ne = int(O.edge_mask(poses[i].astype(np.float64), O.camera(w, h),
+                                 obs_depth=obs.depth).sum())
+            assert abs(int(sums[i, 0]) - so[i].s_rm) <= ne
+    ctx.close()
