@@ -459,7 +459,9 @@ __device__ __forceinline__ uint3 cull_tile(const FkOut& fo, int X0, int Y0) {
   return make_uint3(lo & 0xFFFFFu, (lo >> 20) | ((hi & 0x7u) << 12), hi >> 3);
 }
 
-template <int MODE, bool CHK>
+// BOTH: count the both-defined pixels (only the hp_eval_sums test hook reports them; the
+// cost needs just the r_m and o_s AND r_m counts and the numerator)
+template <int MODE, bool CHK, bool BOTH = true>
 __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tmap,
                                         const FkOut& fo, int X0, int Y0, uint3 km,
                                         uint32_t* obs_buf, uint64_t* bar, uint32_t& phase,
@@ -546,7 +548,7 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
         const bool both = hit & (diff == diff);
         acc.rm += rm;
         acc.and_ += rm & (w >> 31);
-        acc.both += both;
+        if (BOTH) acc.both += both;
         num += __float_as_uint(fmaf(both ? fminf(diff, clampv) : 0.f, qscale, qmagic));
       }
       acc.num += num;
@@ -951,7 +953,7 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
 // z_near were queued by k_fk_batch (ntl = -2) and are skipped here; NEAR = true renders
 // exactly those (exact-solid path) in a second, normally empty launch, so the
 // near-plane code never shares a register allocation with the hot loop.
-template <int NW, bool NEAR>
+template <int NW, bool NEAR, bool SUMS>
 __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     k_render_persist(const __grid_constant__ EvalArgs a,
                      const __grid_constant__ CUtensorMap tmap) {
@@ -1064,8 +1066,8 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
           km = cull_tile(fo, X0, Y0);
         }
         if (km.x | km.y | km.z)
-          do_tile<kModeCost, NEAR>(a, &tmap, fo, X0, Y0, km, s_obs[warp], &s_bar[warp], phase,
-                                   s_dx, s_dy, acc, yoff);
+          do_tile<kModeCost, NEAR, SUMS>(a, &tmap, fo, X0, Y0, km, s_obs[warp], &s_bar[warp],
+                                         phase, s_dx, s_dy, acc, yoff);
         t = __shfl_sync(0xffffffffu, tn, 0);
       }
     }
@@ -1126,8 +1128,10 @@ static void set_carveouts() {
     cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxRayBytes);
   };
-  cfg(k_render_persist<kEvalWarps, false>);
-  cfg(k_render_persist<kEvalWarps, true>);
+  cfg(k_render_persist<kEvalWarps, false, false>);
+  cfg(k_render_persist<kEvalWarps, true, false>);
+  cfg(k_render_persist<kEvalWarps, false, true>);
+  cfg(k_render_persist<kEvalWarps, true, true>);
   cfg(k_eval<kEvalWarps, float, kModeCost>);
   cfg(k_eval<kEvalWarps, double, kModeCost>);
   cfg(k_eval<kEvalWarps, float, kModeDepth>);
@@ -1150,7 +1154,8 @@ int persist_blocks_per_sm(const CamParams& cam) {
   set_carveouts();
   int nb = 0;
   const size_t dyn = (size_t)ray_floats(cam.W, cam.H) * sizeof(float);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_render_persist<kEvalWarps, false>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb,
+                                                    k_render_persist<kEvalWarps, false, false>,
                                                     kEvalWarps * 32, dyn) != cudaSuccess)
     return 0;
   return nb;
@@ -1229,16 +1234,25 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, k_render_persist<kEvalWarps, false>, a, *map);
+    const bool sums = a.sums_out != nullptr;
+    e = sums ? cudaLaunchKernelEx(&cfg, k_render_persist<kEvalWarps, false, true>, a, *map)
+             : cudaLaunchKernelEx(&cfg, k_render_persist<kEvalWarps, false, false>, a, *map);
     if (e != cudaSuccess) return e;
     // the near-plane pass (exits at once when k_fk_batch queued nothing)
     cfg.gridDim = dim3((unsigned)(pgrid.x < 148u ? pgrid.x : 148u));
-    e = cudaLaunchKernelEx(&cfg, k_render_persist<kEvalWarps, true>, a, *map);
+    e = sums ? cudaLaunchKernelEx(&cfg, k_render_persist<kEvalWarps, true, true>, a, *map)
+             : cudaLaunchKernelEx(&cfg, k_render_persist<kEvalWarps, true, false>, a, *map);
     if (e != cudaSuccess) return e;
 #else
-    k_render_persist<kEvalWarps, false><<<pgrid, block, dyn, st>>>(a, *map);
-    k_render_persist<kEvalWarps, true><<<dim3(pgrid.x < 148u ? pgrid.x : 148u), block, dyn,
-                                         st>>>(a, *map);
+    if (a.sums_out) {
+      k_render_persist<kEvalWarps, false, true><<<pgrid, block, dyn, st>>>(a, *map);
+      k_render_persist<kEvalWarps, true, true><<<dim3(pgrid.x < 148u ? pgrid.x : 148u), block,
+                                                 dyn, st>>>(a, *map);
+    } else {
+      k_render_persist<kEvalWarps, false, false><<<pgrid, block, dyn, st>>>(a, *map);
+      k_render_persist<kEvalWarps, true, false><<<dim3(pgrid.x < 148u ? pgrid.x : 148u), block,
+                                                  dyn, st>>>(a, *map);
+    }
 #endif
     if (tev) cudaEventRecord(tev[2], st);
     return cudaGetLastError();
