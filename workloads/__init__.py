@@ -112,6 +112,14 @@ def swarm_around(centre, n: int, seed: int) -> np.ndarray:
     return np.clip(c[None, :] + sigma[None, :] * rng.standard_normal((n, NDOF)), lo, hi)
 
 
+def cold_box(n: int = 4096, seed: int = 7069) -> np.ndarray:
+    """C4's cold-box variant: poses uniform in the full Tables 1-2 box —
+    a first-generation swarm; most hands are small, partly or wholly off-screen."""
+    rng = np.random.default_rng(seed)
+    lo, hi = input_bounds()
+    return rng.uniform(lo[None, :], hi[None, :], size=(n, NDOF))
+
+
 def local_init_box():
     """C2/C3 local PSO init: centre h_A, +-50 mm, +-20 deg on the wrist angles,
     full Table 1 on the fingers (radius large enough to cover the whole range)."""
