@@ -372,3 +372,26 @@ def test_large_image_ray_table_beyond_48kb():
                                  obs_depth=obs.depth).sum())
             assert abs(int(sums[i, 0]) - so[i].s_rm) <= ne
     ctx.close()
+
+
+def test_cold_box_batch_sampled_parity():
+    """A first-generation swarm uniform in Tables 1-2 (off-screen, tiny and near-plane hands
+    mixed) through the batch path: sampled oracle parity, split-path bitwise equality."""
+    ctx = ctx_for(640, 480)
+    obs = obs_for(W.H_A, 640, 480)
+    swarm = W.cold_box(2048, seed=3).astype(np.float32)
+    sums, c64, c32 = gpu_costs(ctx, obs, swarm)
+    assert ctx.splits_for(len(swarm)) == 1
+    rng = np.random.default_rng(4)
+    sample = rng.choice(len(swarm), 12, replace=False)
+    for i in sample[:4]:
+        s1, c1, _ = gpu_costs(ctx, obs, swarm[i:i + 1])
+        assert np.array_equal(s1[0], sums[i]) and c1[0] == c64[i]
+    co, so, _, _ = oracle_eval(obs, swarm[sample])
+    for k, i in enumerate(sample):
+        if int(sums[i, 0]) == so[k].s_rm and int(sums[i, 1]) == so[k].s_and:
+            assert abs(c64[i] - co[k]) <= E_REL * abs(co[k]) + E_ABS, (i, c64[i], co[k])
+        else:
+            ne = int(O.edge_mask(swarm[i].astype(np.float64), O.camera(640, 480),
+                                 obs_depth=obs.depth).sum())
+            assert abs(int(sums[i, 0]) - so[k].s_rm) <= ne
