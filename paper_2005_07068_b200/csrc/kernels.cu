@@ -1,16 +1,23 @@
-// kernels.cu — the hot path of libhp on sm_100a.
+// kernels.cu — the hot path of libhp on sm_100a (DESIGN §9).
 //
-//   k_pack_obs : observation O = (O_s, O_d) -> one u32 per pixel (fp32 depth bits, bit 31 =
-//                o_s) and S_o = sum o_s                     (DESIGN §1 row A0)
-//   k_eval     : fused FK + render + score + cost finalize   (rows A2-A5; P:L114-130,
-//                P:L162-171).  One CTA per (particle, split); warp 0 runs FK in fp64 into
-//                shared memory, then every warp walks 16x8-pixel tiles of the particle's
-//                screen box: TMA-loads the observation tile, culls the 38 primitive boxes
-//                with two ballots, ray-casts the surviving primitives analytically (fp32,
-//                re-centred at the closest approach), resolves the min depth and scores the
-//                pixel.  Sums are integers (fixed point 2^-16 mm for the numerator): warp
-//                shuffles, one atomic per sum per CTA, and the last CTA of each particle
-//                computes Eq. (4)-(5) in fp64 and resets the accumulators.
+//   k_pack_obs, k_band_min, k_ingest : observation O = (O_s, O_d) -> one u32 per pixel
+//                (fp32 depth bits, undefined depth = a quiet NaN, bit 31 = o_s) and
+//                S_o = sum o_s; k_band_min / k_ingest segment a Kinect-like u16 frame first
+//                (rows A0, f3)
+//   k_ray_table: per-column dx, per-lane-row dy4 (NaN off the image)
+//   k_fk_batch : batch path, one warp per pose — FK in fp64 (rows A2), the record out by a
+//                bulk TMA store, the pose's list of non-empty 16x8 tiles with per-kind cull
+//                masks (row A3); near-plane poses are queued for the exact pass
+//   k_render_persist<NEAR, SUMS> : batch path renderer, persistent, PDL after k_fk_batch —
+//                records + tile lists pulled into shared memory by 1-D TMA bulk copies,
+//                per tile a TMA load of the observation, analytic ray casting of the tile's
+//                primitives in packed fp32x2 (FFMA2), min depth, scoring, integer sums,
+//                Eq. (4)-(5) per pose (rows A4, A5).  NEAR = true:
+//                the second, normally empty launch for the queued poses (exact solids)
+//   k_eval     : one CTA per (pose, split): FK on a 3-warp team, tiles culled on the fly,
+//                split sums in global integer atomics; with pso_on it is the fused PSO
+//                generation (update before FK, finalisation and bookkeeping in the grid's
+//                last CTA; rows A7, A8).  Also the depth-image hooks (MODE = kModeDepth)
 //   k_fk_debug : the same FK for the hp_debug_fk test hook.
 #include <math.h>
 
