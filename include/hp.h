@@ -265,7 +265,9 @@ hp_status hp_get_nccl_id(uint8_t* id);
  * INVALID_ARG, STATE (already sharded), NCCL, OOM. */
 hp_status hp_shard(hp_ctx* ctx, const uint8_t* id, int32_t rank, int32_t world);
 
-/* Number of kernel launches the last hp_eval_costs / hp_pso_fit enqueued (bench). */
+/* Number of kernel launches the last hp_eval_costs / hp_pso_fit enqueued (bench).  A hand
+ * fit first runs generation kernels without the near-plane code; if a particle needed it
+ * the fit is repeated with the exact kernels and both passes are counted. */
 int64_t hp_last_launch_count(const hp_ctx* ctx);
 /* Per-launch device timing of the evaluation (bench.py's roofline leg).
    hp_set_timing(ctx, 1) makes every later hp_eval_costs / hp_eval_costs_host / hp_eval_sums

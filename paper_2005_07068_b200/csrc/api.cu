@@ -64,6 +64,7 @@ struct Graph {
   int N = -1, D = -1, K = -1, period = -1, per_dim_r = -1, nmut = -1, mut_lo = -1, mut_hi = -1;
   int sphere = -1;
   int world = -1;
+  int exact = -1;  // 1: generation kernels with the near-plane code (after a speculative miss)
 };
 
 }  // namespace
@@ -101,7 +102,7 @@ struct hp_ctx {
   int* mark = nullptr;
   int* pimp = nullptr;  // deferred pbest flags (fused generations)
   int* gsel = nullptr;  // deferred gbest (index, from X)
-  int* flags = nullptr;  // [0] done, [1] gens_run
+  int* flags = nullptr;  // [0] done, [1] gens_run, [2] near-plane particle seen (speculative fit)
   PsoDyn* dyn = nullptr;
   double* h_out = nullptr;  // pinned: G[64], Gc, trace[K], gens_run
   int trace_cap = 0;
@@ -496,7 +497,8 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   CKC(cudaMalloc(&ctx->Gc, sizeof(double)));
   CKC(cudaMalloc(&ctx->bnd, 4 * 64 * sizeof(double)));
   CKC(cudaMalloc(&ctx->centre, 64 * sizeof(double)));
-  CKC(cudaMalloc(&ctx->flags, 2 * sizeof(int)));
+  CKC(cudaMalloc(&ctx->flags, 4 * sizeof(int)));
+  CKC(cudaMemset(ctx->flags, 0, 4 * sizeof(int)));
   CKC(cudaMalloc(&ctx->dyn, sizeof(PsoDyn)));
   ctx->trace_cap = 0;
   CKC(cudaDeviceSynchronize());
@@ -955,7 +957,7 @@ static PsoDev pso_dev(hp_ctx* ctx, int N, int D, const hp_pso_params* p, int mut
 
 // Enqueue the whole fit on `s` (captured into a graph by the caller).
 static hp_status enqueue_fit(hp_ctx* ctx, const PsoDev& d, bool sphere, cudaStream_t s,
-                             int64_t* launches) {
+                             int64_t* launches, bool exact) {
   int64_t n = 0;
   CK(launch_pso_init(d, s));
   n++;
@@ -1013,6 +1015,9 @@ static hp_status enqueue_fit(hp_ctx* ctx, const PsoDev& d, bool sphere, cudaStre
     a.pso = d;
     a.gcount = ctx->gcount;
     a.kc_g = ctx->kc_g;
+    // speculative: generation kernels without the near-plane code; a particle that needs it
+    // sets flags[2] and run_fit repeats the fit with the exact kernels
+    a.near_seen = exact ? nullptr : ctx->flags + 2;
     a.pdl = ctx->use_pdl;
     double* Xb[2] = {ctx->X, ctx->X2};
     double* Vb[2] = {ctx->V, ctx->V2};
@@ -1077,42 +1082,56 @@ static hp_status run_fit(hp_ctx* ctx, const hp_pso_params* p, int D, const doubl
     d.E = ctx->gat64;  // costs arrive through the allgather
   }
   Graph& g = ctx->graph;
-  const bool same = g.exec && g.N == N && g.D == D && g.K == K && g.period == d.period &&
-                    g.per_dim_r == d.per_dim_r && g.nmut == d.nmut && g.mut_lo == mut_lo &&
-                    g.mut_hi == mut_hi && g.sphere == (int)sphere && g.world == ctx->world;
-  int64_t launches = 0;
-  if (!same) {
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-    g.exec = nullptr;
-    cudaGraph_t graph;
-    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    hp_status r = enqueue_fit(ctx, d, sphere, s, &launches);
-    cudaError_t ce = cudaStreamEndCapture(s, &graph);
-    if (r != HP_OK) return r;
-    CK(ce);
-    CK(cudaGraphInstantiate(&g.exec, graph, 0));
-    ctx->last_fit_launches = launches;
-    cudaGraphDestroy(graph);
-    g.N = N;
-    g.D = D;
-    g.K = K;
-    g.period = d.period;
-    g.per_dim_r = d.per_dim_r;
-    g.nmut = d.nmut;
-    g.mut_lo = mut_lo;
-    g.mut_hi = mut_hi;
-    g.sphere = sphere;
-    g.world = ctx->world;
-  } else {
-    launches = ctx->last_fit_launches;
-  }
-  CK(cudaGraphLaunch(g.exec, s));
+  // the fused hand fit runs speculatively without the near-plane code first (exact = 0);
+  // only if some particle needed it is the whole fit repeated with the exact kernels
+  // (same seed: the same trajectory, now exact).  Sphere / sharded fits never use it.
+  const bool fused = !sphere && !ctx->comm;
   double* ho = ctx->h_out;
-  CK(cudaMemcpyAsync(ho, ctx->G, D * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(ho + 64, ctx->Gc, sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(ho + 65, ctx->flags + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(ho + 72, ctx->trace, K * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  int64_t launches = 0, total_launches = 0;
+  for (int exact = fused ? 0 : 1;; exact++) {
+    const bool same = g.exec && g.N == N && g.D == D && g.K == K && g.period == d.period &&
+                      g.per_dim_r == d.per_dim_r && g.nmut == d.nmut &&
+                      g.mut_lo == mut_lo && g.mut_hi == mut_hi && g.sphere == (int)sphere &&
+                      g.world == ctx->world && g.exact == exact;
+    if (!same) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+      cudaGraph_t graph;
+      CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      hp_status r = enqueue_fit(ctx, d, sphere, s, &launches, exact != 0);
+      cudaError_t ce = cudaStreamEndCapture(s, &graph);
+      if (r != HP_OK) return r;
+      CK(ce);
+      CK(cudaGraphInstantiate(&g.exec, graph, 0));
+      ctx->last_fit_launches = launches;
+      cudaGraphDestroy(graph);
+      g.N = N;
+      g.D = D;
+      g.K = K;
+      g.period = d.period;
+      g.per_dim_r = d.per_dim_r;
+      g.nmut = d.nmut;
+      g.mut_lo = mut_lo;
+      g.mut_hi = mut_hi;
+      g.sphere = sphere;
+      g.world = ctx->world;
+      g.exact = exact;
+    } else {
+      launches = ctx->last_fit_launches;
+    }
+    if (!exact) CK(cudaMemsetAsync(ctx->flags + 2, 0, sizeof(int), s));
+    CK(cudaGraphLaunch(g.exec, s));
+    CK(cudaMemcpyAsync(ho, ctx->G, D * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ho + 64, ctx->Gc, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ho + 65, ctx->flags + 1, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ho + 72, ctx->trace, K * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    total_launches += launches;
+    int seen = 0;
+    memcpy(&seen, reinterpret_cast<int*>(ho + 65) + 1, sizeof(int));
+    if (exact || !seen) break;
+  }
+  launches = total_launches;  // both passes when the speculative one had to be repeated
   ctx->last_launches = launches;
   ctx->last_N = N;
   ctx->last_D = D;

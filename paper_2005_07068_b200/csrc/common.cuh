@@ -128,6 +128,8 @@ struct EvalArgs {
   double *x_out, *v_out;          // generation k (evaluated)
   unsigned int* gcount;           // grid arrival counter (zero between launches)
   double* kc_g;                   // [n] kc(h) of each particle (fused generation epilogue)
+  int* near_seen;                 // non-null: speculative fit kernel (no near-plane code);
+                                  // set when a particle needed it
   int pdl;                        // launched with programmatic dependent launch
   // two-kernel batch path: k_fk_batch writes each particle's FK output and tile list here,
   // k_render_persist bulk-copies them into shared memory

@@ -619,7 +619,9 @@ __device__ __noinline__ TileRun tiles_near(const EvalArgs& a, const CUtensorMap*
                                bar, phase, s_dx, s_dy, yoff);
 }
 
-template <int MODE>
+// NEARCODE = false (the speculative fit kernels): no near-plane code at all; a particle
+// that would need it raises a_.near_seen and the host re-runs the fit with NEARCODE = true.
+template <int MODE, bool NEARCODE = true>
 __device__ __forceinline__ TileRun run_tiles(const EvalArgs& a, const CUtensorMap* tmap,
                                              const FkOut& fo, const uint4* list, int nlist,
                                              int first, int stride, int count, int* next,
@@ -629,6 +631,11 @@ __device__ __forceinline__ TileRun run_tiles(const EvalArgs& a, const CUtensorMa
   return tile_loop<MODE, false>(a, tmap, fo, list, nlist, first, stride, count, next,
                                 obs_buf, bar, phase, s_dx, s_dy, yoff);
 #else
+  if (!NEARCODE) {
+    if (!fo.near_ok && threadIdx.x == 0 && a.near_seen) atomicOr(a.near_seen, 1);
+    return tile_loop<MODE, false>(a, tmap, fo, list, nlist, first, stride, count, next,
+                                  obs_buf, bar, phase, s_dx, s_dy, yoff);
+  }
   if (fo.near_ok)
     return tile_loop<MODE, false>(a, tmap, fo, list, nlist, first, stride, count, next,
                                   obs_buf, bar, phase, s_dx, s_dy, yoff);
@@ -675,7 +682,7 @@ __device__ __forceinline__ double finalize_cost(const EvalArgs& a, int p,
 #define HP_EVAL_FK_TEAM 3  // k_eval's FK team: warps 0..2 (one primitive kind per warp)
 #endif
 constexpr int kEvalFkTeam = HP_EVAL_FK_TEAM;
-template <int NW, typename PoseT, int MODE>
+template <int NW, typename PoseT, int MODE, bool NEARCODE = true>
 __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
     k_eval(const __grid_constant__ EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
   __shared__ FkScratch s_fk;
@@ -732,9 +739,10 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
   const TileGrid g(s_out.ubox);
   // this CTA owns tiles sidx, sidx + S, ...; warps take them dynamically (load balance)
   const int nmine = g.ntiles > sidx ? (g.ntiles - sidx + a.S - 1) / a.S : 0;
-  TileSums acc = run_tiles<MODE>(a, &tmap, s_out, nullptr, -1, sidx, a.S, nmine, &s_next,
-                                 s_obs[warp], &s_bar[warp], 0u, s_dx, s_dy,
-                                 frame_of(a, p) * a.cam.H).acc;
+  TileSums acc = run_tiles<MODE, NEARCODE>(a, &tmap, s_out, nullptr, -1, sidx, a.S, nmine,
+                                           &s_next, s_obs[warp], &s_bar[warp], 0u, s_dx, s_dy,
+                                           frame_of(a, p) * a.cam.H)
+                     .acc;
 
   GENPROF_MAX(2)
   if (MODE != kModeCost) return;
@@ -1141,6 +1149,7 @@ static void set_carveouts() {
   cfg(k_render_persist<kEvalWarps, true, true>);
   cfg(k_eval<kEvalWarps, float, kModeCost>);
   cfg(k_eval<kEvalWarps, double, kModeCost>);
+  cfg(k_eval<kEvalWarps, double, kModeCost, false>);
   cfg(k_eval<kEvalWarps, float, kModeDepth>);
   cfg(k_eval<kEvalWarps, double, kModeDepth>);
 }
@@ -1274,11 +1283,16 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_eval<kEvalWarps, double, kModeCost>, a, *map);
+    cudaError_t e =
+        a.near_seen ? cudaLaunchKernelEx(&cfg, k_eval<kEvalWarps, double, kModeCost, false>, a,
+                                         *map)
+                    : cudaLaunchKernelEx(&cfg, k_eval<kEvalWarps, double, kModeCost>, a, *map);
     if (tev) cudaEventRecord(tev[2], st);
     return e;
   } else if (mode == kModeCost) {
-    if (pose_double)
+    if (pose_double && a.near_seen)
+      k_eval<kEvalWarps, double, kModeCost, false><<<grid, block, dyn, st>>>(a, *map);
+    else if (pose_double)
       k_eval<kEvalWarps, double, kModeCost><<<grid, block, dyn, st>>>(a, *map);
     else
       k_eval<kEvalWarps, float, kModeCost><<<grid, block, dyn, st>>>(a, *map);

@@ -395,3 +395,34 @@ def test_cold_box_batch_sampled_parity():
             ne = int(O.edge_mask(swarm[i].astype(np.float64), O.camera(640, 480),
                                  obs_depth=obs.depth).sum())
             assert abs(int(sums[i, 0]) - so[k].s_rm) <= ne
+
+
+def test_speculative_fit_reruns_exactly_when_a_particle_crosses_the_near_plane():
+    """Fits run first with generation kernels that carry no near-plane code; a near-plane
+    particle makes the library repeat the fit with the exact kernels.  With z_near = 790 mm
+    every hand (wrist at ~800 mm) crosses the near plane: the result must still match the
+    oracle's fit, and a normal fit must be unaffected."""
+    w, h = 160, 120
+    cam = O.camera(w, h)
+    cam.z_near = 790.0
+    intr = hp.default_intrinsics(w, h)
+    intr.z_near_mm = 790.0
+    ctx = hp.Context(w, h, max_particles=64, intrinsics=intr)
+    d = O.render(W.H_A, cam)
+    obs = O.Observation(d, (d > 0).astype(np.uint8), cam)
+    assert obs.mask.sum() > 0  # the hand is cut, not gone
+    ctx.set_observation(obs.depth, obs.mask)
+    c, rad = W.local_init_box()
+    g = ctx.pso_fit(seed=3, particles=16, generations=6, init_center=c, init_radius=rad)
+    assert ctx.last_launch_count() == 2 * (1 + 6)  # speculative pass + exact repeat
+    r = O.pso_fit_hand(obs, O.default_pso(seed=3, particles=16, generations=6), c, rad)
+    assert np.max(np.abs(g.best_pose - r.best_x)) <= 1e-4
+    np.testing.assert_allclose(g.trace, r.trace, rtol=E_REL, atol=E_ABS)
+    # the default camera: no particle near the plane, one pass
+    ctx2 = hp.Context(w, h, max_particles=64)
+    obs2 = obs_for(W.H_A, w, h)
+    ctx2.set_observation(obs2.depth, obs2.mask)
+    ctx2.pso_fit(seed=3, particles=16, generations=6, init_center=c, init_radius=rad)
+    assert ctx2.last_launch_count() == 1 + 6
+    ctx.close()
+    ctx2.close()
