@@ -426,3 +426,17 @@ def test_speculative_fit_reruns_exactly_when_a_particle_crosses_the_near_plane()
     assert ctx2.last_launch_count() == 1 + 6
     ctx.close()
     ctx2.close()
+
+
+def test_identical_poses_identical_costs_and_gpu_render_self_match():
+    """identical poses in a batch score identically (both paths); a pose scored
+    against its own GPU render (hp_render_observation) costs ~0."""
+    ctx = ctx_for(320, 240)
+    d, m = ctx.render_observation(W.H_A)
+    ctx.set_observation(d, m)
+    h32 = np.asarray(W.H_A, np.float32)
+    for n in (5, 1200):  # split path and batch path
+        P = torch.tensor(np.repeat(h32[None], n, axis=0), device="cuda")
+        c = ctx.eval_costs(P).cpu().numpy()
+        assert np.all(c == c[0])
+        assert 0.0 <= c[0] <= E_ABS
