@@ -124,3 +124,25 @@ def test_timing_hooks_and_two_contexts_on_two_streams():
     torch.cuda.synchronize()
     for o in outs:
         assert np.array_equal(o.cpu().numpy(), ref)
+
+
+def test_context_create_destroy_releases_device_memory():
+    """hp_destroy frees everything hp_create and the calls allocated (frames, fit graphs)."""
+    import paper_2005_07068_b200 as hp
+
+    def cycle():
+        ctx = hp.Context(320, 240, max_particles=1024)
+        obs = O.synthesize(W.H_A, O.camera(320, 240))
+        ctx.set_observations(np.stack([obs.depth] * 3), np.stack([obs.mask] * 3))
+        ctx.eval_costs(torch.tensor(W.swarm_c4(600).astype(np.float32), device="cuda"))
+        c, r = W.local_init_box()
+        ctx.pso_fit(seed=1, particles=16, generations=3, init_center=c, init_radius=r)
+        torch.cuda.synchronize()
+        ctx.close()
+
+    cycle()  # first use: lazy module / driver allocations
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(5):
+        cycle()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < 16 << 20, (free0, free1)  # no per-context leak
