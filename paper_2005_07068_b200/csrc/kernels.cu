@@ -1129,6 +1129,10 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
 #define HP_NW 8
 #endif
 constexpr int kEvalWarps = HP_NW;
+#ifndef HP_RENDER_NW
+#define HP_RENDER_NW 16  // warps per k_render_persist CTA (2 CTAs per SM at 64 registers)
+#endif
+constexpr int kRenderWarps = HP_RENDER_NW;
 
 // Prefer the maximum shared-memory carveout (the default 64 KB split would cap the
 // persistent kernel, 37 KB of shared memory per CTA, at one CTA per SM).
@@ -1143,10 +1147,10 @@ static void set_carveouts() {
     cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxRayBytes);
   };
-  cfg(k_render_persist<kEvalWarps, false, false>);
-  cfg(k_render_persist<kEvalWarps, true, false>);
-  cfg(k_render_persist<kEvalWarps, false, true>);
-  cfg(k_render_persist<kEvalWarps, true, true>);
+  cfg(k_render_persist<kRenderWarps, false, false>);
+  cfg(k_render_persist<kRenderWarps, true, false>);
+  cfg(k_render_persist<kRenderWarps, false, true>);
+  cfg(k_render_persist<kRenderWarps, true, true>);
   cfg(k_eval<kEvalWarps, float, kModeCost>);
   cfg(k_eval<kEvalWarps, double, kModeCost>);
   cfg(k_eval<kEvalWarps, double, kModeCost, false>);
@@ -1171,8 +1175,8 @@ int persist_blocks_per_sm(const CamParams& cam) {
   int nb = 0;
   const size_t dyn = (size_t)ray_floats(cam.W, cam.H) * sizeof(float);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb,
-                                                    k_render_persist<kEvalWarps, false, false>,
-                                                    kEvalWarps * 32, dyn) != cudaSuccess)
+                                                    k_render_persist<kRenderWarps, false, false>,
+                                                    kRenderWarps * 32, dyn) != cudaSuccess)
     return 0;
   return nb;
 }
@@ -1232,6 +1236,7 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
   const dim3 grid((unsigned)blocks), block(kEvalWarps * 32);
   const size_t dyn = (size_t)ray_floats(a.cam.W, a.cam.H) * sizeof(float);
   if (two) {
+    const dim3 rblock(kRenderWarps * 32);
     const dim3 fgrid((unsigned)((a.n + kFkWarps - 1) / kFkWarps));
     if (pose_double) k_fk_batch<double><<<fgrid, kFkWarps * 32, 0, st>>>(a);
     else k_fk_batch<float><<<fgrid, kFkWarps * 32, 0, st>>>(a);
@@ -1242,7 +1247,7 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
 #if HP_FK_PDL
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = pgrid;
-    cfg.blockDim = block;
+    cfg.blockDim = rblock;
     cfg.dynamicSmemBytes = dyn;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -1251,22 +1256,22 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const bool sums = a.sums_out != nullptr;
-    e = sums ? cudaLaunchKernelEx(&cfg, k_render_persist<kEvalWarps, false, true>, a, *map)
-             : cudaLaunchKernelEx(&cfg, k_render_persist<kEvalWarps, false, false>, a, *map);
+    e = sums ? cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, false, true>, a, *map)
+             : cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, false, false>, a, *map);
     if (e != cudaSuccess) return e;
     // the near-plane pass (exits at once when k_fk_batch queued nothing)
     cfg.gridDim = dim3((unsigned)(pgrid.x < 148u ? pgrid.x : 148u));
-    e = sums ? cudaLaunchKernelEx(&cfg, k_render_persist<kEvalWarps, true, true>, a, *map)
-             : cudaLaunchKernelEx(&cfg, k_render_persist<kEvalWarps, true, false>, a, *map);
+    e = sums ? cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, true, true>, a, *map)
+             : cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, true, false>, a, *map);
     if (e != cudaSuccess) return e;
 #else
     if (a.sums_out) {
-      k_render_persist<kEvalWarps, false, true><<<pgrid, block, dyn, st>>>(a, *map);
-      k_render_persist<kEvalWarps, true, true><<<dim3(pgrid.x < 148u ? pgrid.x : 148u), block,
+      k_render_persist<kRenderWarps, false, true><<<pgrid, rblock, dyn, st>>>(a, *map);
+      k_render_persist<kRenderWarps, true, true><<<dim3(pgrid.x < 148u ? pgrid.x : 148u), rblock,
                                                  dyn, st>>>(a, *map);
     } else {
-      k_render_persist<kEvalWarps, false, false><<<pgrid, block, dyn, st>>>(a, *map);
-      k_render_persist<kEvalWarps, true, false><<<dim3(pgrid.x < 148u ? pgrid.x : 148u), block,
+      k_render_persist<kRenderWarps, false, false><<<pgrid, rblock, dyn, st>>>(a, *map);
+      k_render_persist<kRenderWarps, true, false><<<dim3(pgrid.x < 148u ? pgrid.x : 148u), rblock,
                                                   dyn, st>>>(a, *map);
     }
 #endif
