@@ -1,0 +1,278 @@
+// batch.cuh — the batch path: k_fk_batch (FK + tile lists) and the persistent renderer k_render_persist (rows A2-A5)
+// Part of the single translation unit kernels.cu (included after the observation kernels;
+// shares its macros and helpers).
+#pragma once
+
+namespace hp {
+
+// ---------------------------------------------------------------------------------------
+// Two-kernel batch path for large swarms.
+//   k_fk_batch      : one warp per particle — FK (fp64) and the particle's non-empty tile
+//                     list with cull masks, written to global memory (L2-resident).
+//   k_render_persist: persistent CTAs, ALL warps render.  Per particle one thread pulls the
+//                     FK record and tile list into shared memory with 1-D TMA bulk copies
+//                     (double-buffered: particle i + 2 is fetched as soon as particle i is
+//                     finished, while i + 1 renders), so no warp ever waits on FK latency.
+// ---------------------------------------------------------------------------------------
+// A tile (qx, qy) overlaps primitive j iff column qx's x-range and row qy's y-range both
+// overlap box j — the same four compares as cull_tile — so the tile masks are the AND of
+// per-column and per-row 38-bit masks (tx + ty sets of 38 tests instead of tx * ty).
+constexpr int kMaxBand = 64;  // columns / rows of the per-warp band masks
+__device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out, uint2* s_cm,
+                                               uint2* s_rm) {
+  const int lane = threadIdx.x & 31;
+  const TileGrid g(fo.ubox);
+  if (g.ntiles > kMaxTiles || g.tx > kMaxBand) return -1;  // the renderer culls per tile
+  const int ty = g.tx > 0 ? g.ntiles / g.tx : 0;
+  if (ty > kMaxBand) return -1;
+  for (int q = lane; q < g.tx + ty; q += 32) {
+    const bool col = q < g.tx;
+    const int lo = col ? g.x0 + q * kTileW : g.y0 + (q - g.tx) * kTileH;
+    const int hi = lo + (col ? kTileW : kTileH) - 1;
+    // box j as (lo, hi) pairs along this axis: ints 0, 2 (x) or 1, 3 (y) of fo.box[j]
+    const int* bx = reinterpret_cast<const int*>(fo.box) + (col ? 0 : 1);
+    unsigned int m0 = 0, m1 = 0;
+#pragma unroll 8
+    for (int jj = 0; jj < 32; jj++)
+      m0 |= (unsigned)(bx[4 * jj] <= hi && bx[4 * jj + 2] >= lo) << jj;
+#pragma unroll
+    for (int jj = 32; jj < kNprim; jj++)
+      m1 |= (unsigned)(bx[4 * jj] <= hi && bx[4 * jj + 2] >= lo) << (jj - 32);
+    HP_CHECK(q < g.tx + ty && q < 2 * kMaxBand);
+    if (col) s_cm[q] = make_uint2(m0, m1);
+    else s_rm[q - g.tx] = make_uint2(m0, m1);
+  }
+  __syncwarp();
+  int cnt = 0;
+  for (int base = 0; base < g.ntiles; base += 32) {  // one tile per lane
+    const int t = base + lane;
+    unsigned int lo = 0, hi = 0;
+    int X0 = 0, Y0 = 0;
+    if (t < g.ntiles) {
+      g.origin(t, X0, Y0);
+      HP_CHECK((X0 - g.x0) / kTileW < kMaxBand && (Y0 - g.y0) / kTileH < kMaxBand);
+      const uint2 c = s_cm[(X0 - g.x0) / kTileW], r = s_rm[(Y0 - g.y0) / kTileH];
+      lo = c.x & r.x;
+      hi = c.y & r.y;
+    }
+    const unsigned int m0 = lo & 0xFFFFFu, m1 = (lo >> 20) | ((hi & 0x7u) << 12), m2 = hi >> 3;
+    const bool ne = (lo | hi) != 0;
+    const unsigned int bal = __ballot_sync(0xffffffffu, ne);
+    if (ne) {
+      HP_CHECK(cnt + __popc(bal & ((1u << lane) - 1u)) < kMaxTiles);
+      out[cnt + __popc(bal & ((1u << lane) - 1u))] =
+          make_uint4((unsigned)X0 | ((unsigned)Y0 << 16), m0, m1, m2);
+    }
+    cnt += __popc(bal);
+  }
+  return cnt;
+}
+
+#ifndef HP_FK_PDL
+#define HP_FK_PDL 1  // programmatic dependent launch of k_render_persist after k_fk_batch
+#endif
+#ifndef HP_FK_WARPS
+#define HP_FK_WARPS 4  // particles (warps) per k_fk_batch CTA
+#endif
+constexpr int kFkWarps = HP_FK_WARPS;
+template <typename PoseT>
+__global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
+    k_fk_batch(const EvalArgs a) {
+  __shared__ FkScratch s_fk[kFkWarps];
+  __shared__ __align__(16) FkOut s_out[kFkWarps];
+  static_assert(sizeof(FkScratch) >= 2 * kMaxBand * sizeof(uint2), "band masks alias s_fk");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if HP_FK_PDL
+  // the renderer (launched with programmatic stream serialisation) may start its prologue
+  // on SMs this grid frees; it waits for this grid's completion before reading its output
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+  const int p = blockIdx.x * kFkWarps + warp;  // one warp per particle
+  if (p >= a.n) return;  // warp-uniform; only warp-local synchronisation below
+  const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
+  fk_team<PoseT, 1>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk[warp], s_out[warp]);
+  // the record leaves by one bulk copy while the warp builds the tile list: every lane
+  // orders its record writes before the async proxy, then lane 0 issues the copy
+  fence_proxy_async();
+  __syncwarp();
+  if (lane == 0)
+    bulk_s2g(static_cast<FkOut*>(a.fk_g) + p, &s_out[warp], (uint32_t)sizeof(FkOut));
+  FKPROF(4)
+  uint2* band = reinterpret_cast<uint2*>(&s_fk[warp]);  // FK scratch is dead by now
+  const int cnt = build_tile_list(s_out[warp], a.tiles_g + (size_t)p * kMaxTiles, band,
+                                  band + kMaxBand);
+  FKPROF(5)
+  if (lane == 0) {
+    int ntl = cnt;
+    if (!s_out[warp].near_ok) {  // some primitive may cross z_near: the exact pass renders it
+      const unsigned slot_ = atomicAdd(a.near_count, 1u);
+      HP_CHECK(slot_ < (unsigned)a.n);
+      a.near_list[slot_] = p;
+      ntl = -2;
+    }
+    a.ntl_g[p] = ntl;
+    bulk_wait_all();  // the record copy completes before the CTA's shared memory retires
+  }
+  FKPROF(6)
+}
+
+// NEAR = false: the batch renderer.  Particles whose FK found a primitive that may cross
+// z_near were queued by k_fk_batch (ntl = -2) and are skipped here; NEAR = true renders
+// exactly those (exact-solid path) in a second, normally empty launch, so the
+// near-plane code never shares a register allocation with the hot loop.
+template <int NW, bool NEAR, bool SUMS>
+__global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
+    k_render_persist(const __grid_constant__ EvalArgs a,
+                     const __grid_constant__ CUtensorMap tmap) {
+  __shared__ __align__(16) FkOut s_out[2];
+  __shared__ __align__(16) uint4 s_tiles[2][NEAR ? 1 : kMaxTiles];
+  __shared__ __align__(128) uint32_t s_obs[NW][kTileW * kTileH];
+  __shared__ __align__(8) uint64_t s_bar[NW];
+  __shared__ __align__(8) uint64_t s_full[2];
+  __shared__ unsigned long long s_acc[2][4];
+  __shared__ int s_next[2], s_done[2], s_pid[2], s_ntl[2];
+  extern __shared__ float s_ray[];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* s_dx = s_ray;
+  const float* s_dy = s_ray + ray_dx_len(a.cam.W);
+  unsigned int* const counter = a.pcount + (NEAR ? 2 : 0);  // [taken, CTAs exited]
+  // one thread: take the next particle and pull its FK record + tile list into slot b
+  auto issue = [&](int b) {
+    int p = a.n;
+    if (NEAR) {
+      const unsigned k = atomicAdd(counter, 1u);
+      if (k < __ldcg(a.near_count)) p = __ldcg(a.near_list + k);
+    } else {
+      p = (int)atomicAdd(counter, 1u);
+    }
+    s_pid[b] = p;
+    if (p < a.n) {
+      const int ntl = NEAR ? -1 : __ldcg(a.ntl_g + p);  // NEAR: cull every tile
+      s_ntl[b] = ntl;
+      if (ntl == -2) {  // queued for the near-plane pass: nothing to fetch
+        mbar_arrive(&s_full[b]);
+        return;
+      }
+      const uint32_t lb = ntl > 0 ? (uint32_t)ntl * 16u : 0u;
+      mbar_expect_tx(&s_full[b], (uint32_t)sizeof(FkOut) + lb);
+      bulk_g2s(&s_out[b], static_cast<const FkOut*>(a.fk_g) + p, (uint32_t)sizeof(FkOut),
+               &s_full[b]);
+      if (lb) bulk_g2s(s_tiles[b], a.tiles_g + (size_t)p * kMaxTiles, lb, &s_full[b]);
+    } else {
+      mbar_arrive(&s_full[b]);  // terminator: complete the phase without data
+    }
+  };
+#if HP_FK_PDL
+  // the near-plane pass may start its prologue as this grid's CTAs retire
+  if (!NEAR) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+  if (NEAR) {  // usually nothing was queued: leave before any set-up work
+    __shared__ int s_any;
+    if (threadIdx.x == 0) {
+#if HP_FK_PDL
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+      s_any = __ldcg(a.near_count) > 0u;
+    }
+    __syncthreads();
+    if (!s_any) return;  // the same for every CTA: no counter to reset
+  }
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&s_full[b], 1);
+      s_next[b] = 0;
+      s_done[b] = 0;
+      for (int k = 0; k < 4; k++) s_acc[b][k] = 0;
+    }
+    fence_mbar_init();
+    if (a.use_tma == 1) prefetch_tmap(&tmap);
+#if HP_FK_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous grid is complete
+#endif
+    issue(0);
+    issue(1);
+  }
+  {
+    const int n4 = ray_floats(a.cam.W, a.cam.H) / 4;
+    for (int i = threadIdx.x; i < n4; i += NW * 32)
+      reinterpret_cast<float4*>(s_ray)[i] = __ldg(reinterpret_cast<const float4*>(a.ray) + i);
+  }
+  __syncthreads();
+
+  uint32_t phase = 0;
+  for (int i = 0;; i++) {
+    const int b = i & 1;
+    mbar_wait(&s_full[b], (i >> 1) & 1);
+    const int p = s_pid[b];
+    if (p >= a.n) break;
+    const FkOut& fo = s_out[b];
+    const int nlist = s_ntl[b];
+    const int yoff = frame_of(a, p) * a.cam.H;
+    TileSums acc;
+    if (nlist != -2) {
+      const TileGrid g(fo.ubox);
+      const int nt = nlist >= 0 ? nlist : g.ntiles;
+      int t = 0;
+      if (lane == 0) t = atomicAdd(&s_next[b], 1);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      while (t < nt) {
+        int tn = 0;
+        if (lane == 0) tn = atomicAdd(&s_next[b], 1);
+        int X0, Y0;
+        uint3 km;
+        if (nlist >= 0) {
+          HP_CHECK(t >= 0 && t < kMaxTiles);
+          const uint4 it = s_tiles[b][t];
+          X0 = (int)(it.x & 0xFFFFu);
+          Y0 = (int)(it.x >> 16);
+          km = make_uint3(it.y, it.z, it.w);
+        } else {
+          g.origin(t, X0, Y0);
+          km = cull_tile(fo, X0, Y0);
+        }
+        if (km.x | km.y | km.z)
+          do_tile<kModeCost, NEAR, SUMS>(a, &tmap, fo, X0, Y0, km, s_obs[warp], &s_bar[warp],
+                                         phase, s_dx, s_dy, acc, yoff);
+        t = __shfl_sync(0xffffffffu, tn, 0);
+      }
+    }
+    warp_reduce(acc);
+    if (lane == 0) {
+      if (acc.rm) atomicAdd(&s_acc[b][0], (unsigned long long)acc.rm);
+      if (acc.and_) atomicAdd(&s_acc[b][1], (unsigned long long)acc.and_);
+      if (acc.num) atomicAdd(&s_acc[b][2], acc.num);
+      if (acc.both) atomicAdd(&s_acc[b][3], (unsigned long long)acc.both);
+      __threadfence_block();
+      if (atomicAdd(&s_done[b], 1) == NW - 1) {  // last warp for this particle
+        __threadfence_block();
+        unsigned long long v[4];
+        for (int k = 0; k < 4; k++) {
+          v[k] = s_acc[b][k];
+          s_acc[b][k] = 0;
+        }
+        if (nlist != -2) finalize_cost(a, p, v, fo.kc);  // queued ones: the near pass
+        s_next[b] = 0;
+        s_done[b] = 0;
+        fence_proxy_async();  // every warp's generic reads of slot b precede the refill
+        issue(b);             // particle i + 2 into the freed slot
+      }
+    }
+    __syncwarp();
+  }
+  // the last CTA to leave resets the counters for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(counter + 1, 1u) == gridDim.x - 1) {
+      counter[0] = 0;
+      counter[1] = 0;
+      if (NEAR) *a.near_count = 0;
+      __threadfence();
+    }
+  }
+}
+
+
+}  // namespace hp

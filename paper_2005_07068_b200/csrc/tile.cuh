@@ -1,0 +1,504 @@
+// tile.cuh — the per-pixel analytic ray casting (packed fp32x2), the warp tile (TMA observation load, cull masks, min depth, scoring) and the cost finalisation shared by the renderers
+// Part of the single translation unit kernels.cu (included after the observation kernels;
+// shares its macros and helpers).
+#pragma once
+
+namespace hp {
+
+// ---------------------------------------------------------------------------------------
+// Per-primitive analytic first hit for the 4 pixels of a lane (DESIGN §5 formulas).
+// Pixel ray d = (dx, dy_j, 1); t_c = (d.c)/|d|^2 re-centres the quadratic at the closest
+// approach to the primitive's local origin, so its coefficients are O(primitive size)
+// and fp32 does not cancel (a camera-origin quadratic has |c|^2 ~ 1e6 mm^2 against
+// r^2 ~ 1e2).  Depth = t (d_z = 1).
+// ---------------------------------------------------------------------------------------
+// Pixel pairs use Blackwell's packed fp32 instructions (FFMA2 / FMUL2 / FADD2: two lanes
+// of fp32 per instruction, PTX .f32x2): the lane's pixels q = (0,1) and (2,3) are processed
+// as pairs, halving the issued FP instructions of the hot loop.  Scalars broadcast into a
+// pair fold into the instruction's .F32 operand modifier (no extra moves).
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ f2 bc(float v) { return pk(v, v); }
+__device__ __forceinline__ void unpk(f2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+struct Lane4 {
+  float dx;                           // shared by the lane's pixels (one column)
+  f2 dy[kPxPerLane / 2];              // pairs of rows
+  f2 idd[kPxPerLane / 2];             // 1 / |d|^2 per pixel, paired
+  float zb[kPxPerLane];               // min depth so far
+};
+
+// Single-MUFU approximations (flush-to-zero: denormals never occur in these quantities).
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// sqrt of both halves (NaN where negative) and 1/x of both halves
+__device__ __forceinline__ f2 sqrt2(f2 x) {
+  float a, b;
+  unpk(x, a, b);
+  return mul2(x, pk(rsqrt_approx(a), rsqrt_approx(b)));
+}
+// -1/x of both halves (the negation folds into the MUFU operand)
+__device__ __forceinline__ f2 nrcp2(f2 x) {
+  float a, b;
+  unpk(x, a, b);
+  return pk(rcp_approx(-a), rcp_approx(-b));
+}
+
+// Branch-free min-depth update.  zb starts just above z_far, so z < zb also enforces
+// z <= z_far; a NaN z (no real root / axial range miss) never wins.
+// CHK = false when FK proved every primitive lies beyond z_near (the common case): then
+// a plain fminf suffices (fminf ignores a NaN operand, and zb starts above z_far).
+template <bool CHK>
+__device__ __forceinline__ void keep(float z, float& zb, float znear) {
+  if (CHK) zb = (z >= znear) & (z < zb) ? z : zb;
+  else zb = fminf(zb, z);
+}
+template <bool CHK>
+__device__ __forceinline__ void keep2(f2 z, float& zb0, float& zb1, float znear) {
+  float a, b;
+  unpk(z, a, b);
+  keep<CHK>(a, zb0, znear);
+  keep<CHK>(b, zb1, znear);
+}
+
+template <bool CHK>
+__device__ __forceinline__ void isect_sphere(const float* __restrict__ r, Lane4& L, float znear) {
+  const float4 q = *reinterpret_cast<const float4*>(r);  // c, r^2
+  const float bx = fmaf(L.dx, q.x, q.z);
+#pragma unroll
+  for (int j = 0; j < kPxPerLane / 2; j++) {
+    const f2 dy = L.dy[j], idd = L.idd[j];
+    const f2 tc = mul2(fma2(dy, bc(q.y), bc(bx)), idd);
+    const f2 ox = fma2(tc, bc(L.dx), bc(-q.x)), oy = fma2(tc, dy, bc(-q.y));
+    const f2 oz = add2(tc, bc(-q.z));
+    // m = -disc / |d|^2 with disc = r^2 - |o|^2;  z = t_c - sqrt(-m) = t_c + m rsqrt(-m)
+    // (NaN when disc < 0: no hit)
+    const f2 m = mul2(fma2(ox, ox, fma2(oy, oy, fma2(oz, oz, bc(-q.w)))), idd);
+    float m0, m1;
+    unpk(m, m0, m1);
+    if (CHK) {
+      // exact solid semantics near the camera (DESIGN §2 render definition): the smallest
+      // t > 0 on the surface — the exit root when the camera is inside the sphere
+      const f2 h = mul2(m, pk(rsqrt_approx(-m0), rsqrt_approx(-m1)));  // -sqrt(-m)
+      float t10, t11, t20, t21;
+      unpk(add2(tc, h), t10, t11);
+      unpk(sub2(tc, h), t20, t21);
+      keep<true>(t10 > 0.f ? t10 : t20, L.zb[2 * j], znear);
+      keep<true>(t11 > 0.f ? t11 : t21, L.zb[2 * j + 1], znear);
+    } else {
+      keep2<false>(fma2(m, pk(rsqrt_approx(-m0), rsqrt_approx(-m1)), tc), L.zb[2 * j],
+                   L.zb[2 * j + 1], znear);
+    }
+  }
+}
+
+template <bool CHK>
+__device__ __forceinline__ void isect_ellipsoid(const float* __restrict__ r, Lane4& L,
+                                                float znear) {
+  const float4 r0 = *reinterpret_cast<const float4*>(r + 0);   // c, -
+  const float4 r1 = *reinterpret_cast<const float4*>(r + 4);   // M00 M01 M02 M10
+  const float4 r2 = *reinterpret_cast<const float4*>(r + 8);   // M11 M12 M20 M21
+  const float4 r3 = *reinterpret_cast<const float4*>(r + 12);  // M22 cl0 cl1 cl2
+  // d_l = M (dx, dy, 1): the dx part is shared by the lane's pixels
+  const float px = fmaf(r1.x, L.dx, r1.z), py = fmaf(r1.w, L.dx, r2.y),
+              pz = fmaf(r2.z, L.dx, r3.x);
+  const float bx = fmaf(L.dx, r0.x, r0.z);
+#pragma unroll
+  for (int j = 0; j < kPxPerLane / 2; j++) {
+    const f2 dy = L.dy[j];
+    const f2 tc = mul2(fma2(dy, bc(r0.y), bc(bx)), L.idd[j]);
+    const f2 lx = fma2(bc(r1.y), dy, bc(px)), ly = fma2(bc(r2.x), dy, bc(py)),
+             lz = fma2(bc(r2.w), dy, bc(pz));
+    const f2 ox = fma2(tc, lx, bc(-r3.y)), oy = fma2(tc, ly, bc(-r3.z)),
+             oz = fma2(tc, lz, bc(-r3.w));
+    const f2 A = fma2(lx, lx, fma2(ly, ly, mul2(lz, lz)));
+    const f2 B = fma2(ox, lx, fma2(oy, ly, mul2(oz, lz)));
+    const f2 C = fma2(ox, ox, fma2(oy, oy, fma2(oz, oz, bc(-1.f))));
+    const f2 disc = sub2(mul2(B, B), mul2(A, C));
+    // A > 0: the smaller root; only the absolute error of s matters (z = t_c + s), so the
+    // plain form is accurate to ~1e-6 mm here
+    if (CHK) {  // smallest t > 0: the far root when the camera is inside
+      const f2 sq = sqrt2(disc), ia = nrcp2(A);
+      float t10, t11, t20, t21;
+      unpk(add2(tc, mul2(add2(B, sq), ia)), t10, t11);
+      unpk(add2(tc, mul2(sub2(B, sq), ia)), t20, t21);
+      keep<true>(t10 > 0.f ? t10 : t20, L.zb[2 * j], znear);
+      keep<true>(t11 > 0.f ? t11 : t21, L.zb[2 * j + 1], znear);
+    } else {
+      const f2 s = mul2(add2(B, sqrt2(disc)), nrcp2(A));
+      keep2<false>(add2(tc, s), L.zb[2 * j], L.zb[2 * j + 1], znear);
+    }
+  }
+}
+
+// Cone (and the elliptic cylinder with k = 0 in scaled coordinates):
+// x^2 + y^2 - (r_m + k z)^2 = 0 with |z| <= half length.  Only the ENTERING root
+// s = (-B - sqrt(disc)) / A is needed, for A > 0 (interior [s_lo, s_hi]) and for A < 0 (ray
+// inside the double cone's opening, interior (-inf, s_lo] U [s_hi, inf)) alike: if it is
+// outside the axial range the ray can only enter the finite solid through a cap disc, and
+// every cap disc is the equator of a joint sphere / cap ellipsoid that is hit first
+// (DESIGN §2), so the min over primitives is unchanged.
+template <bool CHK>
+__device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L, float znear) {
+  const float4 r0 = *reinterpret_cast<const float4*>(r + 0);
+  const float4 r1 = *reinterpret_cast<const float4*>(r + 4);
+  const float4 r2 = *reinterpret_cast<const float4*>(r + 8);
+  const float4 r3 = *reinterpret_cast<const float4*>(r + 12);
+  const float4 r4 = *reinterpret_cast<const float4*>(r + 16);  // rm, k, hl, -
+  const float px = fmaf(r1.x, L.dx, r1.z), py = fmaf(r1.w, L.dx, r2.y),
+              pz = fmaf(r2.z, L.dx, r3.x);
+  const float bx = fmaf(L.dx, r0.x, r0.z);
+  const float rm = r4.x, k = r4.y, hl = r4.z;
+#pragma unroll
+  for (int j = 0; j < kPxPerLane / 2; j++) {
+    const f2 dy = L.dy[j];
+    const f2 tc = mul2(fma2(dy, bc(r0.y), bc(bx)), L.idd[j]);
+    const f2 lx = fma2(bc(r1.y), dy, bc(px)), ly = fma2(bc(r2.x), dy, bc(py)),
+             lz = fma2(bc(r2.w), dy, bc(pz));
+    const f2 ox = fma2(tc, lx, bc(-r3.y)), oy = fma2(tc, ly, bc(-r3.z)),
+             oz = fma2(tc, lz, bc(-r3.w));
+    const f2 g = fma2(bc(k), oz, bc(rm)), kd = mul2(bc(k), lz);
+    const f2 A = fma2(lx, lx, fma2(ly, ly, sub2(bc(0.f), mul2(kd, kd))));
+    const f2 B = fma2(ox, lx, fma2(oy, ly, sub2(bc(0.f), mul2(kd, g))));
+    const f2 C = fma2(ox, ox, fma2(oy, oy, sub2(bc(0.f), mul2(g, g))));
+    const f2 disc = sub2(mul2(B, B), mul2(A, C));
+    if (CHK) {
+      // Exact solid near the camera: with the near plane cutting a joint sphere, the caps
+      // are no longer covered, so take the smallest t > 0 over both lateral roots in the
+      // axial range and both cap discs (as the oracle's or_first_hit does).
+      float a_[2], b_[2], dsc[2], tcv[2], lxv[2], lyv[2], lzv[2], oxv[2], oyv[2], ozv[2];
+      unpk(A, a_[0], a_[1]);
+      unpk(B, b_[0], b_[1]);
+      unpk(disc, dsc[0], dsc[1]);
+      unpk(tc, tcv[0], tcv[1]);
+      unpk(lx, lxv[0], lxv[1]);
+      unpk(ly, lyv[0], lyv[1]);
+      unpk(lz, lzv[0], lzv[1]);
+      unpk(ox, oxv[0], oxv[1]);
+      unpk(oy, oyv[0], oyv[1]);
+      unpk(oz, ozv[0], ozv[1]);
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        float best = __int_as_float(0x7f800000);
+        const float sq = sqrtf(dsc[e]), ia = 1.f / a_[e];  // NaN roots when disc < 0
+        const float sr[2] = {-(b_[e] + sq) * ia, (sq - b_[e]) * ia};
+#pragma unroll
+        for (int i = 0; i < 2; i++) {
+          const float t = tcv[e] + sr[i];
+          if (fabsf(fmaf(sr[i], lzv[e], ozv[e])) <= hl && t > 0.f) best = fminf(best, t);
+        }
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+          const float zc = c == 0 ? -hl : hl, rc = fmaf(k, zc, rm);
+          const float sc = (zc - ozv[e]) / lzv[e];
+          const float x = fmaf(sc, lxv[e], oxv[e]), y = fmaf(sc, lyv[e], oyv[e]);
+          const float t = tcv[e] + sc;
+          if (fmaf(x, x, y * y) <= rc * rc && t > 0.f) best = fminf(best, t);
+        }
+        keep<true>(best, L.zb[2 * j + e], znear);
+      }
+    } else {
+      const f2 s = mul2(add2(B, sqrt2(disc)), nrcp2(A));  // NaN when disc < 0
+      float za0, za1, z0, z1;
+      unpk(fma2(s, lz, oz), za0, za1);
+      unpk(add2(tc, s), z0, z1);
+      const float nan = __int_as_float(0x7fc00000);
+      keep<false>(fabsf(za0) <= hl ? z0 : nan, L.zb[2 * j], znear);
+      keep<false>(fabsf(za1) <= hl ? z1 : nan, L.zb[2 * j + 1], znear);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// One warp tile: TMA the observation tile, cull, ray-cast, min-depth, score.
+// ---------------------------------------------------------------------------------------
+struct TileSums {
+  unsigned int rm = 0, both = 0, and_ = 0;
+  unsigned long long num = 0;
+};
+
+// Tile geometry of a particle: the union box's x0 rounded down to 4 px, because a TMA box
+// must start 16-byte aligned in global memory (an unaligned start faults on sm_100a).
+struct TileGrid {
+  int x0, y0, tx, ntiles;
+  unsigned int magic;  // floor(2^32 / tx): t / tx = umulhi(t, magic) + {0, 1}
+  __device__ __forceinline__ explicit TileGrid(int4 ub) {
+    x0 = ub.x & ~3;
+    y0 = ub.y;
+    const int bw = ub.z - x0 + 1, bh = ub.w - ub.y + 1;
+    tx = bw > 0 ? (bw + kTileW - 1) / kTileW : 0;
+    const int ty = bh > 0 ? (bh + kTileH - 1) / kTileH : 0;
+    ntiles = tx * ty;
+    magic = tx > 1 ? 0xFFFFFFFFu / (unsigned)tx : 0u;
+  }
+  __device__ __forceinline__ void origin(int t, int& X0, int& Y0) const {
+    int qy = tx > 1 ? (int)__umulhi((unsigned)t, magic) : t;
+    int qx = t - qy * tx;
+    if (qx >= tx) {  // the estimate is low by at most one
+      qy++;
+      qx -= tx;
+    }
+    X0 = x0 + qx * kTileW;
+    Y0 = y0 + qy * kTileH;
+  }
+};
+
+// Cull the 38 conservative boxes against the tile [X0, X0+16) x [Y0, Y0+8): two ballots,
+// split into 32-bit masks per kind (spheres = prims 0..19, cones + cylinder = 20..34,
+// ellipsoids = 35..37).  Warp-collective.
+__device__ __forceinline__ uint3 cull_tile(const FkOut& fo, int X0, int Y0) {
+  const int lane = threadIdx.x & 31;
+  const int4 b = fo.box[lane];
+  const bool ov = b.x <= X0 + kTileW - 1 && b.z >= X0 && b.y <= Y0 + kTileH - 1 && b.w >= Y0;
+  bool ov2 = false;
+  if (lane < kNprim - 32) {
+    const int4 c = fo.box[32 + lane];
+    ov2 = c.x <= X0 + kTileW - 1 && c.z >= X0 && c.y <= Y0 + kTileH - 1 && c.w >= Y0;
+  }
+  const unsigned int lo = __ballot_sync(0xffffffffu, ov), hi = __ballot_sync(0xffffffffu, ov2);
+  return make_uint3(lo & 0xFFFFFu, (lo >> 20) | ((hi & 0x7u) << 12), hi >> 3);
+}
+
+// BOTH: count the both-defined pixels (only the hp_eval_sums test hook reports them; the
+// cost needs just the r_m and o_s AND r_m counts and the numerator)
+template <int MODE, bool CHK, bool BOTH = true>
+__device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tmap,
+                                        const FkOut& fo, int X0, int Y0, uint3 km,
+                                        uint32_t* obs_buf, uint64_t* bar, uint32_t& phase,
+                                        const float* s_dx, const float* s_dy, TileSums& acc,
+                                        int yoff = 0) {
+  const int lane = threadIdx.x & 31;
+  const int col = lane & 15, rowb = lane >> 4;
+  const float znear = a.cam.znear, zfar = a.cam.zfar;
+  const float zinit = __uint_as_float(__float_as_uint(zfar) + 1u);  // next float above z_far
+  if (MODE == kModeCost && a.use_tma) {
+    // no proxy fence needed: the warp's reads of the previous tile in this buffer were
+    // consumed before the __syncwarp that ended it (WAR across proxies is ordered)
+    // rows past this frame's bottom come from the next frame (or TMA zero fill): they are
+    // off-image, their rays are NaN and they are never scored
+    HP_CHECK(yoff >= 0 && Y0 < a.cam.H);
+    tma_load_2d_elect(obs_buf, a.use_tma == 2 ? a.tmap_g : tmap, X0, Y0 + yoff, bar,
+                      kTileW * kTileH * 4);
+  }
+  const unsigned int msph = km.x, mcone = km.y, mell = km.z;
+  Lane4 L;
+  const int x = X0 + col;
+  HP_CHECK(X0 >= 0 && x < ray_dx_len(a.cam.W) && Y0 >= 0 && Y0 + rowb < a.cam.H + kRayPad);
+  HP_CHECK((X0 & 3) == 0);  // TMA boxes start 16-byte aligned
+  L.dx = s_dx[x];
+  const float ddx = fmaf(L.dx, L.dx, 1.f);
+  const float4 dy4 = reinterpret_cast<const float4*>(s_dy)[Y0 + rowb];  // rows y, y+2, y+4, y+6
+  const float dyv[4] = {dy4.x, dy4.y, dy4.z, dy4.w};
+#pragma unroll
+  for (int q = 0; q < kPxPerLane; q += 2) {
+    const float dy0 = dyv[q], dy1 = dyv[q + 1];
+    L.dy[q / 2] = pk(dy0, dy1);
+    L.idd[q / 2] = pk(rcp_approx(fmaf(dy0, dy0, ddx)), rcp_approx(fmaf(dy1, dy1, ddx)));
+    L.zb[q] = zinit;
+    L.zb[q + 1] = zinit;
+  }
+  // CHK = false (the hot path): FK proved every primitive lies beyond z_near; CHK = true:
+  // exact solid semantics near the camera (instantiated only out of line, see tiles_near)
+  for (unsigned int m = msph; m; m &= m - 1) isect_sphere<CHK>(fo.rec[__ffs(m) - 1], L, znear);
+  for (unsigned int m = mcone; m; m &= m - 1)
+    isect_cone<CHK>(fo.rec[kCone0 + __ffs(m) - 1], L, znear);
+  for (unsigned int m = mell; m; m &= m - 1)
+    isect_ellipsoid<CHK>(fo.rec[kEll0 + __ffs(m) - 1], L, znear);
+
+  if (MODE == kModeDepth) {
+#pragma unroll
+    for (int q = 0; q < kPxPerLane; q++) {
+      const int y = Y0 + rowb + 2 * q;
+      if (x < a.cam.W && y < a.cam.H)
+        a.depth_out[(size_t)y * a.cam.W + x] = L.zb[q] <= zfar ? L.zb[q] : 0.f;
+    }
+  } else {
+    if (a.use_tma) {
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+    } else {
+#pragma unroll
+      for (int q = 0; q < kPxPerLane; q++) {
+        const int y = Y0 + rowb + 2 * q;
+        obs_buf[(rowb + 2 * q) * kTileW + col] =
+            (x < a.cam.W && y < a.cam.H) ? a.obs[(size_t)(y + yoff) * a.obs_pitch + x] : 0u;
+      }
+      __syncwarp();
+    }
+    const float d_m = a.cost.d_m, clampv = a.cost.clampv;
+    const float qscale = a.cost.qscale, qmagic = a.cost.qmagic;
+    bool any = false;
+#pragma unroll
+    for (int q = 0; q < kPxPerLane; q++) any |= L.zb[q] <= zfar;
+    if (__any_sync(0xffffffffu, any)) {  // nothing rendered in this tile: nothing to score
+      // numerator: round(min(|dd|, clamp) 2^qbits) from the bits of an fp32 magic-number
+      // FFMA (exact: the sum lies in [2^23, 2^24], ulp 1), summed mod 2^32 and un-biased
+      // once (the true per-lane sum is < 4 * 2^22); no float-to-int conversion on the XU
+      unsigned int num = 0u - (unsigned)kPxPerLane * __float_as_uint(qmagic);
+#pragma unroll
+      for (int q = 0; q < kPxPerLane; q++) {
+        const uint32_t w = obs_buf[(rowb + 2 * q) * kTileW + col];
+        // o_d undefined is stored as NaN (kObsUndef), so diff is NaN exactly there
+        const float diff = fabsf(__uint_as_float(w & 0x7fffffffu) - L.zb[q]);
+        // off-image pixels have NaN rays and never hit (k_ray_table)
+        const bool hit = L.zb[q] <= zfar;
+        // r_m = 1 where |r_d - o_d| < d_m or o_d undefined (AMB-4, AMB-5):
+        // !(diff >= d_m) is true for NaN
+        const unsigned int rm = hit & !(diff >= d_m);
+        const bool both = hit & (diff == diff);
+        acc.rm += rm;
+        acc.and_ += rm & (w >> 31);
+        if (BOTH) acc.both += both;
+        num += __float_as_uint(fmaf(both ? fminf(diff, clampv) : 0.f, qscale, qmagic));
+      }
+      acc.num += num;
+    }
+  }
+  __syncwarp();
+}
+
+// A warp's share of one particle's tiles.  Tiles come from the FK kernel's list
+// (nlist >= 0) or, when there is none, from the union grid with per-tile culling; the
+// warps of a CTA take them through the shared counter *next.
+struct TileRun {
+  TileSums acc;
+  uint32_t phase;
+};
+template <int MODE, bool CHK>
+__device__ __forceinline__ TileRun tile_loop(const EvalArgs& a, const CUtensorMap* tmap,
+                                             const FkOut& fo, const uint4* list, int nlist,
+                                             int first, int stride, int count, int* next,
+                                             uint32_t* obs_buf, uint64_t* bar, uint32_t phase,
+                                             const float* s_dx, const float* s_dy, int yoff) {
+  const int lane = threadIdx.x & 31;
+  const TileGrid g(fo.ubox);
+  TileRun r;
+  r.phase = phase;
+  int j = 0;
+  if (lane == 0) j = atomicAdd(next, 1);
+  j = __shfl_sync(0xffffffffu, j, 0);
+  while (j < count) {
+    int jn = 0;
+    if (lane == 0) jn = atomicAdd(next, 1);  // the next tile, fetched early
+    int X0, Y0;
+    uint3 km;
+    if (nlist >= 0) {
+      const uint4 it = list[j];
+      X0 = (int)(it.x & 0xFFFFu);
+      Y0 = (int)(it.x >> 16);
+      km = make_uint3(it.y, it.z, it.w);
+    } else {
+      g.origin(first + j * stride, X0, Y0);
+      km = cull_tile(fo, X0, Y0);
+    }
+    if (km.x | km.y | km.z)  // no primitive box touches the tile: nothing to render or score
+      do_tile<MODE, CHK>(a, tmap, fo, X0, Y0, km, obs_buf, bar, r.phase, s_dx, s_dy, r.acc,
+                         yoff);
+    j = __shfl_sync(0xffffffffu, jn, 0);
+  }
+  return r;
+}
+
+// Particles with a primitive that may cross z_near (rare: a hand within ~25 cm of the near
+// plane) take the exact-solid path out of line, so its registers never weigh on the hot
+// loop's allocation.  The kernels' EvalArgs are __grid_constant__: no copy for the reference.
+template <int MODE>
+__device__ __noinline__ TileRun tiles_near(const EvalArgs& a, const CUtensorMap* tmap,
+                                           const FkOut& fo, const uint4* list, int nlist,
+                                           int first, int stride, int count, int* next,
+                                           uint32_t* obs_buf, uint64_t* bar, uint32_t phase,
+                                           const float* s_dx, const float* s_dy, int yoff) {
+  return tile_loop<MODE, true>(a, tmap, fo, list, nlist, first, stride, count, next, obs_buf,
+                               bar, phase, s_dx, s_dy, yoff);
+}
+
+// NEARCODE = false (the speculative fit kernels): no near-plane code at all; a particle
+// that would need it raises a_.near_seen and the host re-runs the fit with NEARCODE = true.
+template <int MODE, bool NEARCODE = true>
+__device__ __forceinline__ TileRun run_tiles(const EvalArgs& a, const CUtensorMap* tmap,
+                                             const FkOut& fo, const uint4* list, int nlist,
+                                             int first, int stride, int count, int* next,
+                                             uint32_t* obs_buf, uint64_t* bar, uint32_t phase,
+                                             const float* s_dx, const float* s_dy, int yoff) {
+#if HP_NEAR_TEST
+  return tile_loop<MODE, false>(a, tmap, fo, list, nlist, first, stride, count, next,
+                                obs_buf, bar, phase, s_dx, s_dy, yoff);
+#else
+  if (!NEARCODE) {
+    if (!fo.near_ok && threadIdx.x == 0 && a.near_seen) atomicOr(a.near_seen, 1);
+    return tile_loop<MODE, false>(a, tmap, fo, list, nlist, first, stride, count, next,
+                                  obs_buf, bar, phase, s_dx, s_dy, yoff);
+  }
+  if (fo.near_ok)
+    return tile_loop<MODE, false>(a, tmap, fo, list, nlist, first, stride, count, next,
+                                  obs_buf, bar, phase, s_dx, s_dy, yoff);
+  return tiles_near<MODE>(a, tmap, fo, list, nlist, first, stride, count, next, obs_buf, bar,
+                          phase, s_dx, s_dy, yoff);
+#endif
+}
+
+__device__ __forceinline__ void warp_reduce(TileSums& s) {
+  s.rm = __reduce_add_sync(0xffffffffu, s.rm);
+  s.and_ = __reduce_add_sync(0xffffffffu, s.and_);
+  s.both = __reduce_add_sync(0xffffffffu, s.both);
+#pragma unroll
+  for (int off = 16; off; off >>= 1) s.num += __shfl_xor_sync(0xffffffffu, s.num, off);
+}
+
+// Eq. (4)-(5) in fp64 from the integer sums v = (sum r_m, sum o_s AND r_m, numerator in
+// 2^-qbits mm, both-defined count)  (AMB-1, -2, -3, -6).
+__device__ __forceinline__ double finalize_cost(const EvalArgs& a, int p,
+                                                const unsigned long long v[4], double kc) {
+  const long long s_rm = (long long)v[0], s_and = (long long)v[1];
+  const long long s_or = (long long)a.S_o[frame_of(a, p)] + s_rm - s_and;
+  double D = 0.0;
+  if (s_or > 0) {
+    const double num = ldexp((double)v[2], -a.cost.qbits);
+    const double sor = (double)s_or, sand = (double)s_and;
+    D = a.cost.depth_scale * num / sor + a.cost.lambda * (1.0 - 2.0 * sand / (sand + sor));
+  }
+  const double E = D + a.cost.lambda_k * kc;
+  if (a.costs32) a.costs32[p] = (float)E;
+  if (a.costs64) a.costs64[p] = E;
+  if (a.sums_out)  // the ABI reports the numerator in 2^-20 mm (qbits <= 20)
+    for (int k = 0; k < 4; k++)
+      a.sums_out[(size_t)p * 4 + k] = k == 2 ? v[k] << (20 - a.cost.qbits) : v[k];
+  return E;
+}
+
+
+}  // namespace hp
