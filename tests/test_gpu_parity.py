@@ -75,6 +75,32 @@ def test_fk_random_and_boxes_conservative():
         assert inside.all()
 
 
+def test_fk_boxes_tight():
+    """The device boxes are the exact silhouette bounds plus only a rounding margin: every
+    oracle box without margin lies inside a device box, every device box inside an oracle
+    box with a 1 px margin, and each primitive alone renders (oracle) inside some device
+    box (the box is what the renderer culls with, so a miss here is a wrong pixel)."""
+    ctx = ctx_for(640, 480)
+    cam = O.camera(640, 480)
+    poses = list(W.random_poses(202, 12)) + [W.NAMED[k] for k in sorted(W.NAMED)]
+    for h in poses:
+        _, boxes, _, _ = ctx.debug_fk(h)
+        dev = [tuple(int(v) for v in b) for b in boxes if b[0] <= b[2]]
+        prims, _ = O.fk(h)
+        for p in prims:
+            b0, b1 = O.prim_box(p, cam, 0), O.prim_box(p, cam, 1)
+            if b0 is None:
+                continue
+            assert any(d[0] <= b0[0] and d[1] <= b0[1] and d[2] >= b0[2] and d[3] >= b0[3]
+                       for d in dev)
+            ys, xs = np.nonzero(O.render_prims([p], cam))
+            assert any(((xs >= d[0]) & (xs <= d[2]) & (ys >= d[1]) & (ys <= d[3])).all()
+                       for d in dev)
+        for d in dev:
+            assert any(b and b[0] <= d[0] and b[1] <= d[1] and b[2] >= d[2] and b[3] >= d[3]
+                       for b in (O.prim_box(p, cam, 1) for p in prims))
+
+
 # ------------------------------------------------------------------------------ depth
 def _depth_parity(w, h, poses):
     ctx = ctx_for(w, h)
