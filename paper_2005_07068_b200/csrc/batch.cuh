@@ -18,8 +18,57 @@ namespace hp {
 // overlap box j — the same four compares as cull_tile — so the tile masks are the AND of
 // per-column and per-row 38-bit masks (tx + ty sets of 38 tests instead of tx * ty).
 constexpr int kMaxBand = 64;  // columns / rows of the per-warp band masks
+
+// Tighter per-tile shapes than the boxes for the cones (the spheres' discs would remove only
+// a fifth as much work: scripts/cull_stats.py).  A point p with |p - c| <= r projects within
+// R = f r |c| / (c_z (c_z - r)) px of the projection P(c) (f = max(f_x, f_y); the image-plane
+// offset is M (p - c) / (c_z (c_z + (p - c)_z)) with M = [[c_z, 0, -c_x], [0, c_z, -c_y]],
+// whose largest singular value is |c|).  A cone — the convex hull of its two end discs —
+// therefore lies in the 2-D capsule of radius max(R_0, R_1) around the segment
+// P(J_0) P(J_1), and a tile whose rectangle projects on the segment's normal farther than R
+// from it (separating axis) is skipped.  Stored per cone: (n_x, n_y, n . P(J_0), R); R = inf
+// (no refinement) within 1 mm of the camera plane.  Margins: 1e-4 relative + 0.02 px for
+// the fp32 / approximate-MUFU rounding of the record and of P (~1e-6 relative).
+constexpr int kNcone = kCyl - kCone0;
+__device__ __forceinline__ float proj_radius(const float c[3], float r, float f) {
+  if (!(c[2] - r > 1.f)) return __int_as_float(0x7f800000);
+  const float R = f * r * sqrt_approx(fmaf(c[0], c[0], fmaf(c[1], c[1], c[2] * c[2]))) *
+                  rcp_approx_fk(c[2] * (c[2] - r));
+  return fmaf(R, 1.0001f, 0.02f);
+}
+__device__ __forceinline__ void build_cull_shapes(const FkOut& fo, const CamParams& cam,
+                                                  float4* shp) {
+  const int lane = threadIdx.x & 31;
+  if (lane >= kNcone) return;
+  const float* r = fo.rec[kCone0 + lane];
+  // axis row M[2] from the midpoint; the radius is r_m + k z, z in [-hl, hl]
+  const float hl = r[kHl], rm = r[kRm], k = r[kK];
+  float J0[3], J1[3];
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    J0[i] = fmaf(-hl, r[kM + 6 + i], r[kC + i]);
+    J1[i] = fmaf(hl, r[kM + 6 + i], r[kC + i]);
+  }
+  const float f = fmaxf(cam.fx, cam.fy);
+  const float R = fmaxf(proj_radius(J0, fmaxf(fmaf(-k, hl, rm), 0.f), f),
+                        proj_radius(J1, fmaxf(fmaf(k, hl, rm), 0.f), f));
+  const float i0 = rcp_approx_fk(J0[2]), i1 = rcp_approx_fk(J1[2]);
+  const float p0x = fmaf(cam.fx, J0[0] * i0, cam.cx), p0y = fmaf(cam.fy, J0[1] * i0, cam.cy);
+  const float ex = fmaf(cam.fx, J1[0] * i1, cam.cx) - p0x;
+  const float ey = fmaf(cam.fy, J1[1] * i1, cam.cy) - p0y;
+  const float L = sqrt_approx(fmaf(ex, ex, ey * ey));
+  float4 o;
+  if (L > 1e-3f) {
+    const float iL = rcp_approx_fk(L);
+    o = make_float4(-ey * iL, ex * iL, (ex * p0y - ey * p0x) * iL, R);
+  } else {  // degenerate axis: a disc of radius R + L around P(J_0), tested on the x axis
+    o = make_float4(1.f, 0.f, p0x, R + L);
+  }
+  shp[lane] = o;
+}
+
 __device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out, uint2* s_cm,
-                                               uint2* s_rm) {
+                                               uint2* s_rm, const float4* shp) {
   const int lane = threadIdx.x & 31;
   const TileGrid g(fo.ubox);
   if (g.ntiles > kMaxTiles || g.tx > kMaxBand) return -1;  // the renderer culls per tile
@@ -54,6 +103,20 @@ __device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out, uint
       const uint2 c = s_cm[(X0 - g.x0) / kTileW], r = s_rm[(Y0 - g.y0) / kTileH];
       lo = c.x & r.x;
       hi = c.y & r.y;
+      // pixel x's centre is x + 1/2 in the projected coordinates f u + c
+      const float tcx = (float)X0 + 0.5f * kTileW, tcy = (float)Y0 + 0.5f * kTileH;
+      constexpr float hx = 0.5f * (kTileW - 1), hy = 0.5f * (kTileH - 1);
+      unsigned int cm = ((lo >> kCone0) | (hi << (32 - kCone0))) & ((1u << kNcone) - 1u);
+      for (unsigned int q = cm; q; q &= q - 1) {
+        const int j = __ffs(q) - 1;
+        const float4 sh = shp[j];
+        if (fabsf(fmaf(sh.x, tcx, fmaf(sh.y, tcy, -sh.z))) >
+            fmaf(hx, fabsf(sh.x), fmaf(hy, fabsf(sh.y), sh.w)))
+          cm &= ~(1u << j);
+      }
+      // cones are bits 20..31 of lo and 0..1 of hi
+      lo = (lo & ((1u << kCone0) - 1u)) | (cm << kCone0);
+      hi = (hi & ~((1u << (kNcone - (32 - kCone0))) - 1u)) | (cm >> (32 - kCone0));
     }
     const unsigned int m0 = lo & 0xFFFFFu, m1 = (lo >> 20) | ((hi & 0x7u) << 12), m2 = hi >> 3;
     const bool ne = (lo | hi) != 0;
@@ -78,9 +141,11 @@ constexpr int kFkWarps = HP_FK_WARPS;
 template <typename PoseT>
 __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
     k_fk_batch(const EvalArgs a) {
-  __shared__ FkScratch s_fk[kFkWarps];
+  __shared__ __align__(16) FkScratch s_fk[kFkWarps];
   __shared__ __align__(16) FkOut s_out[kFkWarps];
-  static_assert(sizeof(FkScratch) >= 2 * kMaxBand * sizeof(uint2), "band masks alias s_fk");
+  static_assert(sizeof(FkScratch) % 16 == 0, "the float4 cull shapes alias s_fk[warp]");
+  static_assert(sizeof(FkScratch) >= 2 * kMaxBand * sizeof(uint2) + kNcone * sizeof(float4),
+                "band masks and cull shapes alias s_fk");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #if HP_FK_PDL
   // the renderer (launched with programmatic stream serialisation) may start its prologue
@@ -99,8 +164,11 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
     bulk_s2g(static_cast<FkOut*>(a.fk_g) + p, &s_out[warp], (uint32_t)sizeof(FkOut));
   FKPROF(4)
   uint2* band = reinterpret_cast<uint2*>(&s_fk[warp]);  // FK scratch is dead by now
+  float4* shp = reinterpret_cast<float4*>(band + 2 * kMaxBand);
+  build_cull_shapes(s_out[warp], a.cam, shp);
+  __syncwarp();
   const int cnt = build_tile_list(s_out[warp], a.tiles_g + (size_t)p * kMaxTiles, band,
-                                  band + kMaxBand);
+                                  band + kMaxBand, shp);
   FKPROF(5)
   if (lane == 0) {
     int ntl = cnt;

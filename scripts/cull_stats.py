@@ -66,7 +66,10 @@ def main():
     poses = np.asarray(np.asarray(W.swarm_c4(4096), np.float32), np.float64)[:: 4096 // n][:n]
     tot = {"box": 0.0, "cap": 0.0, "exact": 0.0}
     cnt = {"box": 0, "cap": 0, "exact": 0}
+    ntiles = {"box": 0, "cap": 0, "exact": 0}
+    culled = {}
     for h in poses:
+        tiles = {"box": set(), "cap": set(), "exact": set()}
         prims, _ = O.fk(h)
         boxes = [O.prim_box(p, cam, int(os.environ.get("MARGIN", "1"))) for p in prims]
         ub = [b for b in boxes if b]
@@ -83,15 +86,15 @@ def main():
             hit = img > 0
             c = np.array(p.c)
             if p.kind == 0:
-                circ = (proj(c, cam), None, rad(c, p.s[0], cam) + 1.0)
+                circ = (proj(c, cam), None, rad(c, p.s[0], cam) + 0.02)
             elif p.kind == 2:
                 a = np.array([p.R[i][1] for i in range(3)])
                 c1 = c + p.s[2] * a
                 circ = (proj(c, cam), proj(c1, cam),
-                        max(rad(c, p.s[0], cam), rad(c1, p.s[1], cam)) + 1.0)
+                        max(rad(c, p.s[0], cam), rad(c1, p.s[1], cam)) + 0.02)
             else:
                 circ = None
-            for qy in range(ty):
+            for qy in range(ty):  # noqa: B007
                 for qx in range(tx):
                     X0, Y0 = x0 + qx * TW, y0 + qy * TH
                     if b[0] > X0 + TW - 1 or b[2] < X0 or b[1] > Y0 + TH - 1 or b[3] < Y0:
@@ -114,11 +117,21 @@ def main():
                             e = p1 - p0
                             L = np.linalg.norm(e)
                             keep = seg_rect_dist(p0, p1, ctr, hx, hy) <= R
+                    if not keep:
+                        culled[p.kind] = culled.get(p.kind, 0) + w
                     if keep:
                         tot["cap"] += w
                         cnt["cap"] += 1
+                        tiles["cap"].add((X0, Y0))
+                    tiles["box"].add((X0, Y0))
+                    if hit[Y0:Y0 + TH, X0:X0 + TW].any():
+                        tiles["exact"].add((X0, Y0))
+        for k in tiles:
+            ntiles[k] += len(tiles[k])
+    print("culled weight by kind:", {k: round(v / tot["box"], 4) for k, v in culled.items()})
     for k in tot:
-        print(f"{k:6s} pairs/hyp {cnt[k] / n:8.1f}  weighted {tot[k] / tot['box']:.3f}")
+        print(f"{k:6s} pairs/hyp {cnt[k] / n:8.1f}  weighted {tot[k] / tot['box']:.3f}"
+              f"  non-empty tiles/hyp {ntiles[k] / n:6.1f}")
 
 
 if __name__ == "__main__":

@@ -198,6 +198,12 @@ def test_full_batch_4096_sampled_parity_and_split_invariance():
     for i in (0, 1, 777, 4095):
         s1, c1, _ = gpu_costs(ctx, obs, swarm[i:i + 1])
         assert np.array_equal(s1[0], sums[i]) and c1[0] == c64[i]
+    # every pose through the split path (k_eval: per-tile box culling in the renderer) equals
+    # the batch path (FK-built tile lists with the disc / capsule refinement) bit for bit
+    assert ctx.splits_for(16) > 1
+    for i in range(0, 4096, 16):
+        s16, _, _ = gpu_costs(ctx, obs, swarm[i:i + 16])
+        assert np.array_equal(s16, sums[i:i + 16]), i
     sample = [3, 100, 2048, 4000]
     co, so, _, _ = oracle_eval(obs, swarm[sample])
     for k, i in enumerate(sample):
