@@ -197,7 +197,9 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   __shared__ __align__(128) uint32_t s_obs[NW][kTileW * kTileH];
   __shared__ __align__(8) uint64_t s_bar[NW];
   __shared__ __align__(8) uint64_t s_full[2];
-  __shared__ unsigned long long s_acc[2][4];
+  // per-warp partial sums of the particle in slot b: r_m, o_s AND r_m, numerator lo, hi
+  __shared__ __align__(16) uint4 s_part[2][NW];
+  __shared__ unsigned int s_pboth[2][NW];  // both-defined count (SUMS only)
   __shared__ int s_next[2], s_done[2], s_pid[2], s_ntl[2];
   extern __shared__ float s_ray[];
 
@@ -252,7 +254,6 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
       mbar_init(&s_full[b], 1);
       s_next[b] = 0;
       s_done[b] = 0;
-      for (int k = 0; k < 4; k++) s_acc[b][k] = 0;
     }
     fence_mbar_init();
     if (a.use_tma == 1) prefetch_tmap(&tmap);
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     const int yoff = frame_of(a, p) * a.cam.H;
     TileSums acc;
     if (nlist != -2) {
-      const TileGrid g(fo.ubox);
+      const TileGrid g(fo.ubox, nlist < 0);  // the tile origins only without a list
       const int nt = nlist >= 0 ? nlist : g.ntiles;
       int t = 0;
       if (lane == 0) t = atomicAdd(&s_next[b], 1);
@@ -306,20 +307,29 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
         t = __shfl_sync(0xffffffffu, tn, 0);
       }
     }
-    warp_reduce(acc);
+    warp_reduce<SUMS>(acc);
+    // publish this warp's partial sums; the last warp to arrive (acq_rel counter: its
+    // acquire sees every other warp's partials) reduces them and refills the slot
+    int last = 0;
     if (lane == 0) {
-      if (acc.rm) atomicAdd(&s_acc[b][0], (unsigned long long)acc.rm);
-      if (acc.and_) atomicAdd(&s_acc[b][1], (unsigned long long)acc.and_);
-      if (acc.num) atomicAdd(&s_acc[b][2], acc.num);
-      if (acc.both) atomicAdd(&s_acc[b][3], (unsigned long long)acc.both);
-      __threadfence_block();
-      if (atomicAdd(&s_done[b], 1) == NW - 1) {  // last warp for this particle
-        __threadfence_block();
-        unsigned long long v[4];
-        for (int k = 0; k < 4; k++) {
-          v[k] = s_acc[b][k];
-          s_acc[b][k] = 0;
-        }
+      s_part[b][warp] = make_uint4(acc.rm, acc.and_, (unsigned int)acc.num,
+                                   (unsigned int)(acc.num >> 32));
+      if (SUMS) s_pboth[b][warp] = acc.both;
+      last = atom_add_acq_rel_cta(&s_done[b], 1) == NW - 1;
+    }
+    if (__shfl_sync(0xffffffffu, last, 0)) {
+      __syncwarp();  // lane 0's acquire orders the other lanes' reads below
+      TileSums t;
+      if (lane < NW) {
+        const uint4 v = s_part[b][lane];
+        t.rm = v.x;
+        t.and_ = v.y;
+        t.num = ((unsigned long long)v.w << 32) | v.z;
+        if (SUMS) t.both = s_pboth[b][lane];
+      }
+      warp_reduce<SUMS>(t);
+      if (lane == 0) {
+        const unsigned long long v[4] = {t.rm, t.and_, t.num, t.both};
         if (nlist != -2) finalize_cost(a, p, v, fo.kc);  // queued ones: the near pass
         s_next[b] = 0;
         s_done[b] = 0;

@@ -256,14 +256,15 @@ struct TileSums {
 struct TileGrid {
   int x0, y0, tx, ntiles;
   unsigned int magic;  // floor(2^32 / tx): t / tx = umulhi(t, magic) + {0, 1}
-  __device__ __forceinline__ explicit TileGrid(int4 ub) {
+  // need_origin = false: only the tile counts (origin() is not called; skips the division)
+  __device__ __forceinline__ explicit TileGrid(int4 ub, bool need_origin = true) {
     x0 = ub.x & ~3;
     y0 = ub.y;
     const int bw = ub.z - x0 + 1, bh = ub.w - ub.y + 1;
     tx = bw > 0 ? (bw + kTileW - 1) / kTileW : 0;
     const int ty = bh > 0 ? (bh + kTileH - 1) / kTileH : 0;
     ntiles = tx * ty;
-    magic = tx > 1 ? 0xFFFFFFFFu / (unsigned)tx : 0u;
+    magic = need_origin && tx > 1 ? 0xFFFFFFFFu / (unsigned)tx : 0u;
   }
   __device__ __forceinline__ void origin(int t, int& X0, int& Y0) const {
     int qy = tx > 1 ? (int)__umulhi((unsigned)t, magic) : t;
@@ -471,12 +472,21 @@ __device__ __forceinline__ TileRun run_tiles(const EvalArgs& a, const CUtensorMa
 #endif
 }
 
+// Sum of a 64-bit value over the warp by two 32-bit REDUX: the low 24 bits and the rest.
+// Exact while every lane's value is < 2^51 (each part's 32-lane sum stays < 2^32): a lane's
+// numerator is < 2^24 per tile (4 pixels of <= 2^22) and a particle has < 2^17 tiles
+// (the ray table limits the image to < 2^24 pixels).
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+  const unsigned int lo = __reduce_add_sync(0xffffffffu, (unsigned int)v & 0xFFFFFFu);
+  const unsigned int hi = __reduce_add_sync(0xffffffffu, (unsigned int)(v >> 24));
+  return ((unsigned long long)hi << 24) + lo;
+}
+template <bool BOTH = true>
 __device__ __forceinline__ void warp_reduce(TileSums& s) {
   s.rm = __reduce_add_sync(0xffffffffu, s.rm);
   s.and_ = __reduce_add_sync(0xffffffffu, s.and_);
-  s.both = __reduce_add_sync(0xffffffffu, s.both);
-#pragma unroll
-  for (int off = 16; off; off >>= 1) s.num += __shfl_xor_sync(0xffffffffu, s.num, off);
+  if (BOTH) s.both = __reduce_add_sync(0xffffffffu, s.both);
+  s.num = warp_sum_u64(s.num);
 }
 
 // Eq. (4)-(5) in fp64 from the integer sums v = (sum r_m, sum o_s AND r_m, numerator in
