@@ -466,6 +466,9 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
     if (atoi(e)) ctx->zero_copy = 0;
   if (const char* e = getenv("HP_NO_PERSIST"))
     if (atoi(e)) ctx->persist_grid = 0;
+  // the persistent renderer always loads observation tiles by TMA from its kernel-parameter
+  // descriptor (compile time); the HP_NO_TMA / HP_TMA_MODE A/B switches use k_eval
+  if (ctx->use_tma != 1) ctx->persist_grid = 0;
   CKC(cudaMalloc(&ctx->tmap_g, sizeof(CUtensorMap)));
   CKC(cudaMemcpy(ctx->tmap_g, &ctx->tmap, sizeof(CUtensorMap), cudaMemcpyHostToDevice));
   // evaluation workspace

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
       s_done[b] = 0;
     }
     fence_mbar_init();
-    if (a.use_tma == 1) prefetch_tmap(&tmap);
+    prefetch_tmap(&tmap);
 #if HP_FK_PDL
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous grid is complete
 #endif
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
           km = cull_tile(fo, X0, Y0);
         }
         if (km.x | km.y | km.z)
-          do_tile<kModeCost, NEAR, SUMS>(a, &tmap, fo, X0, Y0, km, s_obs[warp], &s_bar[warp],
+          do_tile<kModeCost, NEAR, SUMS, 1>(a, &tmap, fo, X0, Y0, km, s_obs[warp], &s_bar[warp],
                                          phase, s_dx, s_dy, acc, yoff);
         t = __shfl_sync(0xffffffffu, tn, 0);
       }

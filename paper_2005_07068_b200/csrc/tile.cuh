@@ -295,8 +295,10 @@ __device__ __forceinline__ uint3 cull_tile(const FkOut& fo, int X0, int Y0) {
 }
 
 // BOTH: count the both-defined pixels (only the hp_eval_sums test hook reports them; the
-// cost needs just the r_m and o_s AND r_m counts and the numerator)
-template <int MODE, bool CHK, bool BOTH = true>
+// cost needs just the r_m and o_s AND r_m counts and the numerator).
+// TMA: the observation-tile load, a.use_tma at run time (-1) or fixed at compile time (1:
+// TMA from the kernel-parameter descriptor — the persistent renderer).
+template <int MODE, bool CHK, bool BOTH = true, int TMA = -1>
 __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tmap,
                                         const FkOut& fo, int X0, int Y0, uint3 km,
                                         uint32_t* obs_buf, uint64_t* bar, uint32_t& phase,
@@ -306,13 +308,14 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
   const int col = lane & 15, rowb = lane >> 4;
   const float znear = a.cam.znear, zfar = a.cam.zfar;
   const float zinit = __uint_as_float(__float_as_uint(zfar) + 1u);  // next float above z_far
-  if (MODE == kModeCost && a.use_tma) {
+  const int use_tma = TMA >= 0 ? TMA : a.use_tma;
+  if (MODE == kModeCost && use_tma) {
     // no proxy fence needed: the warp's reads of the previous tile in this buffer were
     // consumed before the __syncwarp that ended it (WAR across proxies is ordered)
     // rows past this frame's bottom come from the next frame (or TMA zero fill): they are
     // off-image, their rays are NaN and they are never scored
     HP_CHECK(yoff >= 0 && Y0 < a.cam.H);
-    tma_load_2d_elect(obs_buf, a.use_tma == 2 ? a.tmap_g : tmap, X0, Y0 + yoff, bar,
+    tma_load_2d_elect(obs_buf, use_tma == 2 ? a.tmap_g : tmap, X0, Y0 + yoff, bar,
                       kTileW * kTileH * 4);
   }
   const unsigned int msph = km.x, mcone = km.y, mell = km.z;
@@ -348,7 +351,7 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
         a.depth_out[(size_t)y * a.cam.W + x] = L.zb[q] <= zfar ? L.zb[q] : 0.f;
     }
   } else {
-    if (a.use_tma) {
+    if (use_tma) {
       mbar_wait(bar, phase);
       phase ^= 1u;
     } else {
