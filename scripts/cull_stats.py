@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 import oracle as O  # noqa: E402
 import workloads as W  # noqa: E402
 
-TW, TH = 16, 8
+TW, TH = int(os.environ.get("TW", "16")), int(os.environ.get("TH", "8"))
 FLOPS = {0: 20, 1: 48, 2: 56, 3: 56}
 
 
