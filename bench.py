@@ -164,8 +164,16 @@ def cpu_baseline(seconds: float, swarm: np.ndarray):
                      threads=1)
         one += 4
     one_rate = one / (time.perf_counter() - t1)
+    # the brute-force mode (every pixel x all 38 primitives, SURVEY §8(d) variant (i)) on a
+    # few poses with all cores: the dense work the culled oracle and the GPU path avoid
+    brute, t2 = 0, time.perf_counter()
+    while time.perf_counter() - t2 < min(3.0, seconds / 4):
+        O.eval_batch(np.asarray(swarm[brute % len(swarm):][:cores], np.float64), obs,
+                     culled=False, threads=cores)
+        brute += len(swarm[brute % len(swarm):][:cores])
+    brute_rate = brute / (time.perf_counter() - t2)
     return {"value": done / dt, "unit": "hyp/s", "cores": cores, "kind": "oracle",
-            "value_1core": one_rate,
+            "value_1core": one_rate, "value_brute": brute_rate,
             "sample": f"{done} poses of the C4 swarm in order (cycling after {len(swarm)}) at "
                       f"640x480, oracle culled mode (fp64, bitwise equal to brute force), "
                       f"{dt:.1f} s"}
