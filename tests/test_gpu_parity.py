@@ -419,6 +419,11 @@ def test_cold_box_batch_sampled_parity():
     for i in sample[:4]:
         s1, c1, _ = gpu_costs(ctx, obs, swarm[i:i + 1])
         assert np.array_equal(s1[0], sums[i]) and c1[0] == c64[i]
+    # every pose through the split path (renderer-side box culling, no FK tile lists)
+    assert ctx.splits_for(16) > 1
+    for i in range(0, len(swarm), 16):
+        s16, _, _ = gpu_costs(ctx, obs, swarm[i:i + 16])
+        assert np.array_equal(s16, sums[i:i + 16]), i
     co, so, _, _ = oracle_eval(obs, swarm[sample])
     for k, i in enumerate(sample):
         if int(sums[i, 0]) == so[k].s_rm and int(sums[i, 1]) == so[k].s_and:
@@ -472,3 +477,31 @@ def test_identical_poses_identical_costs_and_gpu_render_self_match():
         c = ctx.eval_costs(P).cpu().numpy()
         assert np.all(c == c[0])
         assert 0.0 <= c[0] <= E_ABS
+
+
+def test_anisotropic_off_centre_camera_batch_split_and_oracle():
+    """f_x != f_y and an off-centre principal point (the box bounds and the cone capsule
+    radius use both focal lengths): batch path == split path bit for bit on a swarm, and
+    sampled oracle parity under the same camera."""
+    w, h = 320, 240
+    intr = hp.default_intrinsics(w, h)
+    intr.fx, intr.fy, intr.cx, intr.cy = 300.0, 230.0, 150.5, 131.25
+    cam = O.camera(w, h)
+    cam.fx, cam.fy, cam.cx, cam.cy = 300.0, 230.0, 150.5, 131.25
+    ctx = hp.Context(w, h, max_particles=2048, intrinsics=intr)
+    obs = O.synthesize(W.H_A, cam)
+    swarm = np.concatenate([W.swarm_c4(768), W.cold_box(256, seed=11)]).astype(np.float32)
+    sums, c64, _ = gpu_costs(ctx, obs, swarm)
+    assert ctx.splits_for(len(swarm)) == 1 and ctx.splits_for(16) > 1
+    for i in range(0, len(swarm), 16):
+        s16, _, _ = gpu_costs(ctx, obs, swarm[i:i + 16])
+        assert np.array_equal(s16, sums[i:i + 16]), i
+    sample = [0, 5, 300, 767, 800, 1000]
+    co, so, _, _ = oracle_eval(obs, swarm[sample])
+    for k, i in enumerate(sample):
+        if int(sums[i, 0]) == so[k].s_rm and int(sums[i, 1]) == so[k].s_and:
+            assert abs(c64[i] - co[k]) <= E_REL * abs(co[k]) + E_ABS, (i, c64[i], co[k])
+        else:
+            ne = int(O.edge_mask(swarm[i].astype(np.float64), cam, obs_depth=obs.depth).sum())
+            assert abs(int(sums[i, 0]) - so[k].s_rm) <= ne
+    ctx.close()
