@@ -131,6 +131,9 @@ __device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out, uint
   return cnt;
 }
 
+#ifndef HP_PIN
+#define HP_PIN(x) pin_u32(x)
+#endif
 #ifndef HP_FK_PDL
 #define HP_FK_PDL 1  // programmatic dependent launch of k_render_persist after k_fk_batch
 #endif
@@ -271,6 +274,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   __syncthreads();
 
   uint32_t phase = 0;
+  const uint32_t obs_s = HP_PIN(smem_u32(s_obs[warp])), bar_s = HP_PIN(smem_u32(&s_bar[warp]));
   for (int i = 0;; i++) {
     const int b = i & 1;
     mbar_wait(&s_full[b], (i >> 1) & 1);
@@ -302,8 +306,8 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
           km = cull_tile(fo, X0, Y0);
         }
         if (km.x | km.y | km.z)
-          do_tile<kModeCost, NEAR, SUMS, 1>(a, &tmap, fo, X0, Y0, km, s_obs[warp], &s_bar[warp],
-                                         phase, s_dx, s_dy, acc, yoff);
+          do_tile<kModeCost, NEAR, SUMS, 1>(a, &tmap, fo, X0, Y0, km, obs_s, bar_s, phase, s_dx,
+                                            s_dy, acc, yoff);
         t = __shfl_sync(0xffffffffu, tn, 0);
       }
     }

@@ -196,16 +196,32 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar_s, uint32_t phase) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
+      "}\n" ::"r"(bar_s),
       "r"(phase)
       : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  mbar_wait_s(smem_u32(bar), phase);
+}
+// A shared-memory address the compiler must keep in a register (no rematerialisation).
+__device__ __forceinline__ uint32_t pin_u32(uint32_t v) {
+  asm volatile("" : "+r"(v));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 // Waiting with a suspend-time hint: the warp sleeps in hardware instead of spinning on
 // issue slots (used by the FK producer, which waits most of the time).
@@ -231,8 +247,9 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 // Whole-warp call (uniform control flow, warp-uniform operands): one elected lane arms
 // the mbarrier with `bytes` and issues the 2-D TMA tile load.  Keeping the issue in
 // uniform control flow spares the compiler its lane-election loop around UTMALDG.
-__device__ __forceinline__ void tma_load_2d_elect(void* dst, const CUtensorMap* map, int x,
-                                                  int y, uint64_t* bar, uint32_t bytes) {
+__device__ __forceinline__ void tma_load_2d_elect_s(uint32_t dst_s, const CUtensorMap* map,
+                                                    int x, int y, uint32_t bar_s,
+                                                    uint32_t bytes) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -240,9 +257,13 @@ __device__ __forceinline__ void tma_load_2d_elect(void* dst, const CUtensorMap* 
       "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%4], %5;\n"
       "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
       "[%0], [%1, {%2, %3}], [%4];\n"
-      "}\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "r"(bytes)
+      "}\n" ::"r"(dst_s),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_s), "r"(bytes)
       : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_elect(void* dst, const CUtensorMap* map, int x,
+                                                  int y, uint64_t* bar, uint32_t bytes) {
+  tma_load_2d_elect_s(smem_u32(dst), map, x, y, smem_u32(bar), bytes);
 }
 
 // 1-D bulk copy global -> shared (TMA unit), completing `bytes` on the mbarrier.

@@ -72,7 +72,8 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
   // this CTA owns tiles sidx, sidx + S, ...; warps take them dynamically (load balance)
   const int nmine = g.ntiles > sidx ? (g.ntiles - sidx + a.S - 1) / a.S : 0;
   TileSums acc = run_tiles<MODE, NEARCODE>(a, &tmap, s_out, nullptr, -1, sidx, a.S, nmine,
-                                           &s_next, s_obs[warp], &s_bar[warp], 0u, s_dx, s_dy,
+                                           &s_next, smem_u32(s_obs[warp]),
+                                           smem_u32(&s_bar[warp]), 0u, s_dx, s_dy,
                                            frame_of(a, p) * a.cam.H)
                      .acc;
 

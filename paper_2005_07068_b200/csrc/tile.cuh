@@ -301,7 +301,7 @@ __device__ __forceinline__ uint3 cull_tile(const FkOut& fo, int X0, int Y0) {
 template <int MODE, bool CHK, bool BOTH = true, int TMA = -1>
 __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tmap,
                                         const FkOut& fo, int X0, int Y0, uint3 km,
-                                        uint32_t* obs_buf, uint64_t* bar, uint32_t& phase,
+                                        uint32_t obs_s, uint32_t bar_s, uint32_t& phase,
                                         const float* s_dx, const float* s_dy, TileSums& acc,
                                         int yoff = 0) {
   const int lane = threadIdx.x & 31;
@@ -315,8 +315,8 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
     // rows past this frame's bottom come from the next frame (or TMA zero fill): they are
     // off-image, their rays are NaN and they are never scored
     HP_CHECK(yoff >= 0 && Y0 < a.cam.H);
-    tma_load_2d_elect(obs_buf, use_tma == 2 ? a.tmap_g : tmap, X0, Y0 + yoff, bar,
-                      kTileW * kTileH * 4);
+    tma_load_2d_elect_s(obs_s, use_tma == 2 ? a.tmap_g : tmap, X0, Y0 + yoff, bar_s,
+                        kTileW * kTileH * 4);
   }
   const unsigned int msph = km.x, mcone = km.y, mell = km.z;
   Lane4 L;
@@ -352,14 +352,14 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
     }
   } else {
     if (use_tma) {
-      mbar_wait(bar, phase);
+      mbar_wait_s(bar_s, phase);
       phase ^= 1u;
     } else {
 #pragma unroll
       for (int q = 0; q < kPxPerLane; q++) {
         const int y = Y0 + rowb + 2 * q;
-        obs_buf[(rowb + 2 * q) * kTileW + col] =
-            (x < a.cam.W && y < a.cam.H) ? a.obs[(size_t)(y + yoff) * a.obs_pitch + x] : 0u;
+        sts_u32(obs_s + 4u * ((rowb + 2 * q) * kTileW + col),
+                (x < a.cam.W && y < a.cam.H) ? a.obs[(size_t)(y + yoff) * a.obs_pitch + x] : 0u);
       }
       __syncwarp();
     }
@@ -375,7 +375,7 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
       unsigned int num = 0u - (unsigned)kPxPerLane * __float_as_uint(qmagic);
 #pragma unroll
       for (int q = 0; q < kPxPerLane; q++) {
-        const uint32_t w = obs_buf[(rowb + 2 * q) * kTileW + col];
+        const uint32_t w = lds_u32(obs_s + 4u * ((rowb + 2 * q) * kTileW + col));
         // o_d undefined is stored as NaN (kObsUndef), so diff is NaN exactly there
         const float diff = fabsf(__uint_as_float(w & 0x7fffffffu) - L.zb[q]);
         // off-image pixels have NaN rays and never hit (k_ray_table)
@@ -406,7 +406,7 @@ template <int MODE, bool CHK>
 __device__ __forceinline__ TileRun tile_loop(const EvalArgs& a, const CUtensorMap* tmap,
                                              const FkOut& fo, const uint4* list, int nlist,
                                              int first, int stride, int count, int* next,
-                                             uint32_t* obs_buf, uint64_t* bar, uint32_t phase,
+                                             uint32_t obs_s, uint32_t bar_s, uint32_t phase,
                                              const float* s_dx, const float* s_dy, int yoff) {
   const int lane = threadIdx.x & 31;
   const TileGrid g(fo.ubox);
@@ -430,7 +430,7 @@ __device__ __forceinline__ TileRun tile_loop(const EvalArgs& a, const CUtensorMa
       km = cull_tile(fo, X0, Y0);
     }
     if (km.x | km.y | km.z)  // no primitive box touches the tile: nothing to render or score
-      do_tile<MODE, CHK>(a, tmap, fo, X0, Y0, km, obs_buf, bar, r.phase, s_dx, s_dy, r.acc,
+      do_tile<MODE, CHK>(a, tmap, fo, X0, Y0, km, obs_s, bar_s, r.phase, s_dx, s_dy, r.acc,
                          yoff);
     j = __shfl_sync(0xffffffffu, jn, 0);
   }
@@ -444,10 +444,10 @@ template <int MODE>
 __device__ __noinline__ TileRun tiles_near(const EvalArgs& a, const CUtensorMap* tmap,
                                            const FkOut& fo, const uint4* list, int nlist,
                                            int first, int stride, int count, int* next,
-                                           uint32_t* obs_buf, uint64_t* bar, uint32_t phase,
+                                           uint32_t obs_s, uint32_t bar_s, uint32_t phase,
                                            const float* s_dx, const float* s_dy, int yoff) {
-  return tile_loop<MODE, true>(a, tmap, fo, list, nlist, first, stride, count, next, obs_buf,
-                               bar, phase, s_dx, s_dy, yoff);
+  return tile_loop<MODE, true>(a, tmap, fo, list, nlist, first, stride, count, next, obs_s,
+                               bar_s, phase, s_dx, s_dy, yoff);
 }
 
 // NEARCODE = false (the speculative fit kernels): no near-plane code at all; a particle
@@ -456,21 +456,21 @@ template <int MODE, bool NEARCODE = true>
 __device__ __forceinline__ TileRun run_tiles(const EvalArgs& a, const CUtensorMap* tmap,
                                              const FkOut& fo, const uint4* list, int nlist,
                                              int first, int stride, int count, int* next,
-                                             uint32_t* obs_buf, uint64_t* bar, uint32_t phase,
+                                             uint32_t obs_s, uint32_t bar_s, uint32_t phase,
                                              const float* s_dx, const float* s_dy, int yoff) {
 #if HP_NEAR_TEST
   return tile_loop<MODE, false>(a, tmap, fo, list, nlist, first, stride, count, next,
-                                obs_buf, bar, phase, s_dx, s_dy, yoff);
+                                obs_s, bar_s, phase, s_dx, s_dy, yoff);
 #else
   if (!NEARCODE) {
     if (!fo.near_ok && threadIdx.x == 0 && a.near_seen) atomicOr(a.near_seen, 1);
     return tile_loop<MODE, false>(a, tmap, fo, list, nlist, first, stride, count, next,
-                                  obs_buf, bar, phase, s_dx, s_dy, yoff);
+                                  obs_s, bar_s, phase, s_dx, s_dy, yoff);
   }
   if (fo.near_ok)
     return tile_loop<MODE, false>(a, tmap, fo, list, nlist, first, stride, count, next,
-                                  obs_buf, bar, phase, s_dx, s_dy, yoff);
-  return tiles_near<MODE>(a, tmap, fo, list, nlist, first, stride, count, next, obs_buf, bar,
+                                  obs_s, bar_s, phase, s_dx, s_dy, yoff);
+  return tiles_near<MODE>(a, tmap, fo, list, nlist, first, stride, count, next, obs_s, bar_s,
                           phase, s_dx, s_dy, yoff);
 #endif
 }
