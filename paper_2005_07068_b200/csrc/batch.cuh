@@ -275,6 +275,8 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
 
   uint32_t phase = 0;
   const uint32_t obs_s = HP_PIN(smem_u32(s_obs[warp])), bar_s = HP_PIN(smem_u32(&s_bar[warp]));
+  const uint32_t dx_s = HP_PIN(smem_u32(s_dx + (lane & 15)));
+  const uint32_t dy_s = HP_PIN(smem_u32(s_dy + 4 * (lane >> 4)));
   for (int i = 0;; i++) {
     const int b = i & 1;
     mbar_wait(&s_full[b], (i >> 1) & 1);
@@ -306,8 +308,8 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
           km = cull_tile(fo, X0, Y0);
         }
         if (km.x | km.y | km.z)
-          do_tile<kModeCost, NEAR, SUMS, 1>(a, &tmap, fo, X0, Y0, km, obs_s, bar_s, phase, s_dx,
-                                            s_dy, acc, yoff);
+          do_tile<kModeCost, NEAR, SUMS, 1>(a, &tmap, fo, X0, Y0, km, obs_s, bar_s, phase, dx_s,
+                                            dy_s, acc, yoff);
         t = __shfl_sync(0xffffffffu, tn, 0);
       }
     }

@@ -302,7 +302,7 @@ template <int MODE, bool CHK, bool BOTH = true, int TMA = -1>
 __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tmap,
                                         const FkOut& fo, int X0, int Y0, uint3 km,
                                         uint32_t obs_s, uint32_t bar_s, uint32_t& phase,
-                                        const float* s_dx, const float* s_dy, TileSums& acc,
+                                        uint32_t dx_s, uint32_t dy_s, TileSums& acc,
                                         int yoff = 0) {
   const int lane = threadIdx.x & 31;
   const int col = lane & 15, rowb = lane >> 4;
@@ -323,9 +323,10 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
   const int x = X0 + col;
   HP_CHECK(X0 >= 0 && x < ray_dx_len(a.cam.W) && Y0 >= 0 && Y0 + rowb < a.cam.H + kRayPad);
   HP_CHECK((X0 & 3) == 0);  // TMA boxes start 16-byte aligned
-  L.dx = s_dx[x];
+  // the ray table by shared address: dx_s = &dx[lane's column], dy_s = &dy4[lane's row]
+  L.dx = __uint_as_float(lds_u32(dx_s + 4u * X0));
   const float ddx = fmaf(L.dx, L.dx, 1.f);
-  const float4 dy4 = reinterpret_cast<const float4*>(s_dy)[Y0 + rowb];  // rows y, y+2, y+4, y+6
+  const float4 dy4 = lds_f4(dy_s + 16u * Y0);  // rows y, y+2, y+4, y+6
   const float dyv[4] = {dy4.x, dy4.y, dy4.z, dy4.w};
 #pragma unroll
   for (int q = 0; q < kPxPerLane; q += 2) {
@@ -430,7 +431,8 @@ __device__ __forceinline__ TileRun tile_loop(const EvalArgs& a, const CUtensorMa
       km = cull_tile(fo, X0, Y0);
     }
     if (km.x | km.y | km.z)  // no primitive box touches the tile: nothing to render or score
-      do_tile<MODE, CHK>(a, tmap, fo, X0, Y0, km, obs_s, bar_s, r.phase, s_dx, s_dy, r.acc,
+      do_tile<MODE, CHK>(a, tmap, fo, X0, Y0, km, obs_s, bar_s, r.phase,
+                         smem_u32(s_dx + (lane & 15)), smem_u32(s_dy + 4 * (lane >> 4)), r.acc,
                          yoff);
     j = __shfl_sync(0xffffffffu, jn, 0);
   }
