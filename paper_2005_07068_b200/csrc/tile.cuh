@@ -413,6 +413,11 @@ __device__ __forceinline__ TileRun tile_loop(const EvalArgs& a, const CUtensorMa
   const TileGrid g(fo.ubox);
   TileRun r;
   r.phase = phase;
+  // loop-invariant shared addresses in registers (see k_render_persist)
+  obs_s = pin_u32(obs_s);
+  bar_s = pin_u32(bar_s);
+  const uint32_t dx_s = pin_u32(smem_u32(s_dx + (lane & 15)));
+  const uint32_t dy_s = pin_u32(smem_u32(s_dy + 4 * (lane >> 4)));
   int j = 0;
   if (lane == 0) j = atomicAdd(next, 1);
   j = __shfl_sync(0xffffffffu, j, 0);
@@ -431,8 +436,7 @@ __device__ __forceinline__ TileRun tile_loop(const EvalArgs& a, const CUtensorMa
       km = cull_tile(fo, X0, Y0);
     }
     if (km.x | km.y | km.z)  // no primitive box touches the tile: nothing to render or score
-      do_tile<MODE, CHK>(a, tmap, fo, X0, Y0, km, obs_s, bar_s, r.phase,
-                         smem_u32(s_dx + (lane & 15)), smem_u32(s_dy + 4 * (lane >> 4)), r.acc,
+      do_tile<MODE, CHK>(a, tmap, fo, X0, Y0, km, obs_s, bar_s, r.phase, dx_s, dy_s, r.acc,
                          yoff);
     j = __shfl_sync(0xffffffffu, jn, 0);
   }
