@@ -179,6 +179,15 @@ def cpu_baseline(seconds: float, swarm: np.ndarray):
                       f"{dt:.1f} s"}
 
 
+def arm_config(world: int) -> dict:
+    """The workload both arms report (the reference arm times a bounded slice of it)."""
+    return {"workload": f"C4: 640x480 synthetic frame rendered from h_A, "
+                        f"{PER_RANK}-pose mid-fit swarm per GPU (seed 7068)",
+            "poses_per_gpu": PER_RANK, "resolution": "640x480",
+            "parallelism": f"particle-sharded x{world}, cost allgather",
+            "l2": "flushed between steps (256 MiB write, outside the events)"}
+
+
 def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
@@ -202,11 +211,10 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C4: 640x480 synthetic frame (h_A), mid-fit swarm; "
-                                   f"{sample} poses per step (bounded sample)",
-                       "l2": "n/a (CPU)"},
+            "config": dict(arm_config(args.gpus), l2="n/a (CPU oracle)"),
             "cpu_baseline": {"value": value, "unit": "hyp/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{sample} poses per step, oracle culled mode"},
+                             "sample": f"{sample} poses of the C4 swarm per step (a bounded "
+                                       "slice of the workload), oracle culled mode"},
             "e2e": {"value": value, "unit": "hyp/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -519,11 +527,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": f"C4: 640x480 synthetic frame rendered from h_A, "
-                                   f"{PER_RANK}-pose mid-fit swarm per GPU (seed 7068)",
-                       "poses_per_gpu": PER_RANK, "resolution": "640x480",
-                       "parallelism": f"particle-sharded x{world}, cost allgather",
-                       "l2": "flushed between steps (256 MiB write, outside the events)"},
+            "config": arm_config(world),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": ncu_traffic(),
                          "kernel": "k_render_persist (render+score+cost; FK records and tile "
