@@ -74,22 +74,34 @@ __device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out, uint
   if (g.ntiles > kMaxTiles || g.tx > kMaxBand) return -1;  // the renderer culls per tile
   const int ty = g.tx > 0 ? g.ntiles / g.tx : 0;
   if (ty > kMaxBand) return -1;
-  for (int q = lane; q < g.tx + ty; q += 32) {
-    const bool col = q < g.tx;
-    const int lo = col ? g.x0 + q * kTileW : g.y0 + (q - g.tx) * kTileH;
-    const int hi = lo + (col ? kTileW : kTileH) - 1;
-    // box j as (lo, hi) pairs along this axis: ints 0, 2 (x) or 1, 3 (y) of fo.box[j]
-    const int* bx = reinterpret_cast<const int*>(fo.box) + (col ? 0 : 1);
-    unsigned int m0 = 0, m1 = 0;
-#pragma unroll 8
-    for (int jj = 0; jj < 32; jj++)
-      m0 |= (unsigned)(bx[4 * jj] <= hi && bx[4 * jj + 2] >= lo) << jj;
+  // band masks by ballot: lane j holds primitive j's (and j + 32's) band ranges; one pair
+  // of ballots per column / row band
+  int c0[2], c1[2], r0[2], r1[2];
 #pragma unroll
-    for (int jj = 32; jj < kNprim; jj++)
-      m1 |= (unsigned)(bx[4 * jj] <= hi && bx[4 * jj + 2] >= lo) << (jj - 32);
-    HP_CHECK(q < g.tx + ty && q < 2 * kMaxBand);
-    if (col) s_cm[q] = make_uint2(m0, m1);
-    else s_rm[q - g.tx] = make_uint2(m0, m1);
+  for (int h = 0; h < 2; h++) {
+    const int j = lane + 32 * h;
+    c0[h] = r0[h] = 1;
+    c1[h] = r1[h] = 0;  // empty
+    if (j < kNprim) {
+      const int4 b = fo.box[j];
+      if (b.x <= b.z) {  // band k covers [g.x0 + 16 k, g.x0 + 16 k + 15] (rows: 8)
+        c0[h] = (b.x - g.x0) >> 4;
+        c1[h] = (b.z - g.x0) >> 4;
+        r0[h] = (b.y - g.y0) >> 3;
+        r1[h] = (b.w - g.y0) >> 3;
+      }
+    }
+  }
+  static_assert(kTileW == 16 && kTileH == 8, "band shifts assume 16x8 tiles");
+  for (int q = 0; q < g.tx; q++) {
+    const unsigned int m0 = __ballot_sync(0xffffffffu, c0[0] <= q && q <= c1[0]);
+    const unsigned int m1 = __ballot_sync(0xffffffffu, c0[1] <= q && q <= c1[1]);
+    if (lane == 0) s_cm[q] = make_uint2(m0, m1);
+  }
+  for (int q = 0; q < ty; q++) {
+    const unsigned int m0 = __ballot_sync(0xffffffffu, r0[0] <= q && q <= r1[0]);
+    const unsigned int m1 = __ballot_sync(0xffffffffu, r0[1] <= q && q <= r1[1]);
+    if (lane == 0) s_rm[q] = make_uint2(m0, m1);
   }
   __syncwarp();
   int cnt = 0;
