@@ -243,6 +243,41 @@ __device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L
   }
 }
 
+// The palm's elliptic cylinder on the fast path: the cone formulas with k = 0 in its scaled
+// coordinates (g = r_m, no k terms), entering root only (its end discs are the equators of
+// the cap ellipsoids).  It covers ~30 % of the cone loop's tile tests at C4.
+__device__ __forceinline__ void isect_cyl_fast(const float* __restrict__ r, Lane4& L) {
+  const float4 r0 = *reinterpret_cast<const float4*>(r + 0);
+  const float4 r1 = *reinterpret_cast<const float4*>(r + 4);
+  const float4 r2 = *reinterpret_cast<const float4*>(r + 8);
+  const float4 r3 = *reinterpret_cast<const float4*>(r + 12);
+  const float4 r4 = *reinterpret_cast<const float4*>(r + 16);  // rm, k (= 0), hl, -
+  const float px = fmaf(r1.x, L.dx, r1.z), py = fmaf(r1.w, L.dx, r2.y),
+              pz = fmaf(r2.z, L.dx, r3.x);
+  const float bx = fmaf(L.dx, r0.x, r0.z);
+  const float nrm2 = -r4.x * r4.x, hl = r4.z;
+#pragma unroll
+  for (int j = 0; j < kPxPerLane / 2; j++) {
+    const f2 dy = L.dy[j];
+    const f2 tc = mul2(fma2(dy, bc(r0.y), bc(bx)), L.idd[j]);
+    const f2 lx = fma2(bc(r1.y), dy, bc(px)), ly = fma2(bc(r2.x), dy, bc(py)),
+             lz = fma2(bc(r2.w), dy, bc(pz));
+    const f2 ox = fma2(tc, lx, bc(-r3.y)), oy = fma2(tc, ly, bc(-r3.z)),
+             oz = fma2(tc, lz, bc(-r3.w));
+    const f2 A = fma2(lx, lx, mul2(ly, ly));
+    const f2 B = fma2(ox, lx, mul2(oy, ly));
+    const f2 C = fma2(ox, ox, fma2(oy, oy, bc(nrm2)));
+    const f2 disc = sub2(mul2(B, B), mul2(A, C));
+    const f2 s = mul2(add2(B, sqrt2(disc)), nrcp2(A));  // NaN when disc < 0
+    float za0, za1, z0, z1;
+    unpk(fma2(s, lz, oz), za0, za1);
+    unpk(add2(tc, s), z0, z1);
+    const float nan = __int_as_float(0x7fc00000);
+    keep<false>(fabsf(za0) <= hl ? z0 : nan, L.zb[2 * j], 0.f);
+    keep<false>(fabsf(za1) <= hl ? z1 : nan, L.zb[2 * j + 1], 0.f);
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // One warp tile: TMA the observation tile, cull, ray-cast, min-depth, score.
 // ---------------------------------------------------------------------------------------
@@ -339,8 +374,12 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
   // CHK = false (the hot path): FK proved every primitive lies beyond z_near; CHK = true:
   // exact solid semantics near the camera (instantiated only out of line, see tiles_near)
   for (unsigned int m = msph; m; m &= m - 1) isect_sphere<CHK>(fo.rec[__ffs(m) - 1], L, znear);
-  for (unsigned int m = mcone; m; m &= m - 1)
+  // cones, then (fast path) the palm cylinder with its k = 0 specialisation (bitwise the
+  // cone formulas at k = 0; the exact near-plane path keeps the general code)
+  constexpr unsigned int kCylBit = 1u << (kCyl - kCone0);
+  for (unsigned int m = CHK ? mcone : (mcone & ~kCylBit); m; m &= m - 1)
     isect_cone<CHK>(fo.rec[kCone0 + __ffs(m) - 1], L, znear);
+  if (!CHK && (mcone & kCylBit)) isect_cyl_fast(fo.rec[kCyl], L);
   for (unsigned int m = mell; m; m &= m - 1)
     isect_ellipsoid<CHK>(fo.rec[kEll0 + __ffs(m) - 1], L, znear);
 
