@@ -65,11 +65,16 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-// sqrt of both halves (NaN where negative) and 1/x of both halves
+__device__ __forceinline__ float sqrt_approx_t(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// sqrt of both halves (NaN where negative): one MUFU.SQRT each (no x * rsqrt(x) multiply)
 __device__ __forceinline__ f2 sqrt2(f2 x) {
   float a, b;
   unpk(x, a, b);
-  return mul2(x, pk(rsqrt_approx(a), rsqrt_approx(b)));
+  return pk(sqrt_approx_t(a), sqrt_approx_t(b));
 }
 // -1/x of both halves (the negation folds into the MUFU operand)
 __device__ __forceinline__ f2 nrcp2(f2 x) {
