@@ -89,6 +89,12 @@ typedef struct {
   double stop_threshold;   /* stop when G's cost < this; -INFINITY = off      */
   const double* init_center; /* host [26] or NULL: init box = centre +- radius  */
   const double* init_radius; /* host [26] or NULL   intersected with Tables 1-2 */
+  /* Mutation order (P:L152 is silent; DESIGN.md AMB-17): 0 (default) = the worst particles
+   * are re-drawn right after the Eq. (6)-(7) update of generations k = period, 2 period, ...
+   * and evaluated as drawn; 1 = SPEC's order: re-drawn after generation k's
+   * evaluation and bookkeeping, so generation k + 1's update moves them before they are
+   * evaluated.  Errors: any other value. */
+  int32_t mutation_after_eval;
 } hp_pso_params;
 
 /* Fill with the defaults of DESIGN §2 / P:L130 / P:L148-152.  Errors: NULL. */
@@ -103,6 +109,11 @@ hp_status hp_bounds(double lo[26], double hi[26]);
 /* Create a context on `device` (the current CUDA device if < 0) with a workspace for up
  * to max_particles poses per call.  dims/cost may be NULL (defaults).  The observation
  * starts empty (all undefined); set it with hp_set_observation.
+ * Reading of the north star's hp_create(observation, intrinsics, model dims): creation and
+ * the observation are two calls here, so one context (its device workspace, ray table and
+ * captured fit graph) serves a whole frame sequence — hp_set_observation replaces the
+ * frame in place (row f1 tracking, row f3 ingestion) without re-creating anything;
+ * hp_create followed by hp_set_observation is the north star's call.
  * Errors: INVALID_ARG (NULL out/cam, bad intrinsics, max_particles < 1, an image whose
  * ray table (width + 4 height + 80 floats) exceeds 64 KB of shared memory), NO_DEVICE, OOM. */
 hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims,
@@ -171,15 +182,18 @@ hp_status hp_eval_costs(hp_ctx* ctx, const float* poses_dev, int64_t n, float* c
 
 /* Frame-batched objective: poses_dev [frames][n_per_frame][26] fp32, pose i of block f
  * scored against observation frame f (hp_set_observations); costs_dev [frames][n_per_frame]
- * fp32.  Bitwise equal to scoring each block with hp_eval_costs against that frame alone.
- * Local to this context even when sharded (frames shard across ranks with no collective).
- * n_per_frame = 0 is a no-op.  Async on `stream`.
- * Errors: INVALID_ARG (n_per_frame < 0, frames * n_per_frame > max_particles, NULL). */
-hp_status hp_eval_costs_frames(hp_ctx* ctx, const float* poses_dev, int64_t n_per_frame,
-                               float* costs_dev, void* stream);
+ * fp32.  `frames` states the caller's buffer layout and must equal the frame count of the
+ * current observation.  Bitwise equal to scoring each block with hp_eval_costs against that
+ * frame alone.  Local to this context even when sharded (frames shard across ranks with no
+ * collective).  n_per_frame = 0 is a no-op.  Async on `stream`.
+ * Errors: INVALID_ARG (frames != the observation's frame count, n_per_frame < 0,
+ * frames * n_per_frame > max_particles, NULL). */
+hp_status hp_eval_costs_frames(hp_ctx* ctx, const float* poses_dev, int32_t frames,
+                               int64_t n_per_frame, float* costs_dev, void* stream);
 /* Its test hook: the sums and fp64 costs of hp_eval_sums, frame-batched. */
-hp_status hp_eval_sums_frames(hp_ctx* ctx, const float* poses_dev, int64_t n_per_frame,
-                              uint64_t* sums_dev, double* costs64_dev, void* stream);
+hp_status hp_eval_sums_frames(hp_ctx* ctx, const float* poses_dev, int32_t frames,
+                              int64_t n_per_frame, uint64_t* sums_dev, double* costs64_dev,
+                              void* stream);
 
 /* Same with HOST buffers: moves poses in, scores, moves costs out, then synchronises
  * `stream` (the end-to-end path a host application calls).  Mapped page-locked buffers
@@ -198,6 +212,12 @@ hp_status hp_eval_costs_host(hp_ctx* ctx, const float* poses_host, int64_t n,
  * clamp * 2^q <= 2^22 (16 for the default 40 mm clamp); costs64_dev [n] fp64 may be NULL. */
 hp_status hp_eval_sums(hp_ctx* ctx, const float* poses_dev, int64_t n, uint64_t* sums_dev,
                        double* costs64_dev, void* stream);
+/* The same for fp64 poses (device [n][26], the precision of the PSO state):
+ * exactly the scoring a fit's generation applies to its particles, so a host PSO fed these
+ * costs retraces hp_pso_fit (the "PSO-step parity" check of DESIGN §6).  sums_dev or
+ * costs64_dev may be NULL (not both).  Async.  Errors: as hp_eval_sums. */
+hp_status hp_eval_sums_f64(hp_ctx* ctx, const double* poses_dev, int64_t n,
+                           uint64_t* sums_dev, double* costs64_dev, void* stream);
 
 /* Full PSO fit on the GPU: init, K generations of update +
  * mutation + evaluation + bookkeeping captured in one CUDA graph, one device->host copy at
@@ -222,8 +242,11 @@ hp_status hp_track(hp_ctx* ctx, const float* depth_seq, const uint8_t* mask_seq,
                    double* traces_out, void* stream);
 
 /* Final swarm state of the last hp_pso_fit / hp_debug_pso_sphere (host, synchronous):
- * X, V, P [particles][D] and Pcost [particles]; any pointer may be NULL. */
-hp_status hp_pso_state(hp_ctx* ctx, double* X, double* V, double* P, double* Pcost);
+ * X, V, P [particles][D] and Pcost [particles]; any pointer may be NULL.  particles and D
+ * state the buffers' capacity and must equal the last fit's.
+ * Errors: STATE (no fit has run), INVALID_ARG (particles / D differ). */
+hp_status hp_pso_state(hp_ctx* ctx, int32_t particles, int32_t D, double* X, double* V,
+                       double* P, double* Pcost);
 
 /* ---- test hooks ------------------------------------------------------------------- */
 /* FK of one host fp64 pose on the device (the same device function hp_eval_costs runs):
@@ -261,9 +284,20 @@ hp_status hp_nccl_available(int32_t* available);
 hp_status hp_get_nccl_id(uint8_t* id);
 /* Collective: every rank calls it with the same id.  Afterwards hp_eval_costs takes the
  * FULL batch (n <= max_particles * world), scores this rank's slice and returns all n
- * costs on every rank; hp_pso_fit runs sharded (particles >= world).  Errors:
- * INVALID_ARG, STATE (already sharded), NCCL, OOM. */
+ * costs on every rank; hp_pso_fit runs sharded (particles >= world).  If a rank's own
+ * scoring fails it still takes part in the allgather (its peers do not hang) and then
+ * returns the error.  Errors: INVALID_ARG, STATE (already sharded), NCCL, OOM.
+ * Reading of the north star's hp_create_sharded: sharding is a call on an existing
+ * context (hp_create + hp_shard), so the same context type serves both modes and the
+ * unique-id exchange (torch.distributed in the binding) stays outside the library. */
 hp_status hp_shard(hp_ctx* ctx, const uint8_t* id, int32_t rank, int32_t world);
+/* DEBUG BUILDS ONLY (compiled with -DHP_LOOPBACK_TEST=1; the product library does not
+ * export it): join an in-process loopback group of `world` contexts on ONE device, each
+ * driven by its own host thread, instead of an NCCL communicator.  The allgather is done
+ * with device copies at NCCL's offsets, ordered by events and a host barrier, so the
+ * sharded code paths (rank > 0 slices, the padded last chunk, the sharded fit) can be
+ * executed on a single-GPU box.  Errors: INVALID_ARG, STATE. */
+hp_status hp_shard_loopback(hp_ctx* ctx, const char* group, int32_t rank, int32_t world);
 
 /* Number of kernel launches the last hp_eval_costs / hp_pso_fit enqueued (bench).  A hand
  * fit first runs generation kernels without the near-plane code; if a particle needed it

@@ -68,6 +68,7 @@ void or_default_pso(or_pso_params* p) {
   p->c2 = 1.3;
   p->mutation_fraction = 0.5;
   p->stop_threshold = -INFINITY;
+  p->mutation_after_eval = 0;
 }
 
 /* AMB-12: fx = fy = 525, (cx, cy) = (320, 240) at 640x480, scaled with the width. */
@@ -563,19 +564,21 @@ void or_render(const double h[26], const or_dims* d, const or_camera* cam, int32
   or_render_prims(prims, OR_NPRIM, cam, culled, depth);
 }
 
-void or_edge_mask(const double h[26], const or_dims* d, const or_camera* cam, double delta,
-                  double depth_tol, const float* obs_depth, double d_m, double rm_tol,
-                  uint8_t* edge) {
-  or_prim prims[OR_NPRIM];
-  or_fk(h, d, prims, NULL);
+/* Edge pixels (DESIGN §6 tolerances): the hit status or the depth changes when the pixel's
+ * ray moves by +-delta px along x or y, or the r_m decision |o_d - r_d| < d_m is
+ * within rm_tol of its threshold.  Only these pixels may be decided differently by an fp32
+ * renderer. */
+void or_edge_mask_prims(const or_prim* prims, int32_t nprim, const or_camera* cam, double delta,
+                        double depth_tol, const float* obs_depth, double d_m, double rm_tol,
+                        uint8_t* edge) {
   int32_t W = cam->width, H = cam->height;
   static const double off[4][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}};
   for (int32_t v = 0; v < H; v++)
     for (int32_t u = 0; u < W; u++) {
-      float z = pixel_depth(prims, OR_NPRIM, NULL, cam, u + 0.5, v + 0.5);
+      float z = pixel_depth(prims, nprim, NULL, cam, u + 0.5, v + 0.5);
       uint8_t e = 0;
       for (int k = 0; k < 4 && !e; k++) {
-        float zk = pixel_depth(prims, OR_NPRIM, NULL, cam, u + 0.5 + delta * off[k][0],
+        float zk = pixel_depth(prims, nprim, NULL, cam, u + 0.5 + delta * off[k][0],
                                v + 0.5 + delta * off[k][1]);
         if ((zk > 0) != (z > 0)) e = 1;
         else if (z > 0 && fabs((double)zk - (double)z) > depth_tol) e = 1;
@@ -586,6 +589,14 @@ void or_edge_mask(const double h[26], const or_dims* d, const or_camera* cam, do
       }
       edge[(int64_t)v * W + u] = e;
     }
+}
+
+void or_edge_mask(const double h[26], const or_dims* d, const or_camera* cam, double delta,
+                  double depth_tol, const float* obs_depth, double d_m, double rm_tol,
+                  uint8_t* edge) {
+  or_prim prims[OR_NPRIM];
+  or_fk(h, d, prims, NULL);
+  or_edge_mask_prims(prims, OR_NPRIM, cam, delta, depth_tol, obs_depth, d_m, rm_tol, edge);
 }
 
 /* ------------------------------------------------------------------------------------ */
@@ -785,11 +796,12 @@ int32_t or_pso_run(int32_t D, const double* lo, const double* hi, const double* 
   int stop = pp->stop_threshold > -INFINITY && Pc[g] < pp->stop_threshold;
 
   for (int32_t k = 1; k < K && !stop; k++) {
-    /* mutation marks: the worst floor(N*frac) by Pcost, ties -> higher index worse (AMB-17) */
+    /* mutation marks: the worst floor(N*frac) by Pcost, ties -> higher index worse (AMB-17);
+     * in SPEC's order they are drawn after this generation's bookkeeping instead (below) */
     int do_mut = pp->mutation_period > 0 && k % pp->mutation_period == 0 && nmut > 0;
     for (int32_t i = 0; i < N; i++) {
       mark[i] = 0;
-      if (!do_mut) continue;
+      if (!do_mut || pp->mutation_after_eval) continue;
       int32_t rank = 0;
       for (int32_t j = 0; j < N; j++)
         if (Pc[j] < Pc[i] || (Pc[j] == Pc[i] && j < i)) rank++;
@@ -843,6 +855,24 @@ int32_t or_pso_run(int32_t D, const double* lo, const double* hi, const double* 
     trace[k] = Pc[g];
     ran = k + 1;
     stop = pp->stop_threshold > -INFINITY && Pc[g] < pp->stop_threshold;
+    /* SPEC's order: mutate after the evaluation, ranked by the updated Pcost; the
+     * next generation's update moves the re-drawn particles before they are evaluated.  Only
+     * when another generation follows (a mutation after the last evaluation is never seen). */
+    if (do_mut && pp->mutation_after_eval && k + 1 < K && !stop)
+      for (int32_t i = 0; i < N; i++) {
+        int32_t rank = 0;
+        for (int32_t j = 0; j < N; j++)
+          if (Pc[j] < Pc[i] || (Pc[j] == Pc[i] && j < i)) rank++;
+        if (rank < N - nmut) continue;
+        for (int32_t d = mut_lo; d < mut_hi; d++) {
+          uint32_t r[4];
+          draw4(pp->seed, (uint32_t)i, (uint32_t)d, (uint32_t)k, 2, r);
+          double u = or_u01(r[0], r[1]);
+          int64_t id = (int64_t)i * D + d;
+          X[id] = lo[d] + u * (hi[d] - lo[d]);
+          V[id] = 0.0;
+        }
+      }
   }
   for (int32_t k = ran; k < K; k++) trace[k] = trace[ran - 1];
   memcpy(best_x, G, sizeof(double) * D);

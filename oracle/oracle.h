@@ -19,7 +19,11 @@
  *   or_first_hit / or_render . pinned (analytic sphere depths, disk area, brute force)
  *   or_score / or_cost ....... pinned (worked 2x2 example, invariants, self-match 0)
  *   or_kc .................... pinned (closed-form pair examples)
- *   or_pso_run ............... pinned (w closed form, fixed point, sphere convergence)
+ *   or_pso_run ............... pinned (w closed form, fixed point, sphere convergence; Eq. 6
+ *                              coefficient / r1-r2 assignment by a hand-derived 2-particle
+ *                              trajectory and the c2 = 0 / c1 = 0 limits; both mutation orders)
+ *   or_edge_mask ............. pinned (the analytic silhouette / depth / r_m rings of an
+ *                              on-axis sphere)
  *   or_pso_fit_hand .......... parity unpinned: the paper prints no trajectory (Figs. 6-9 absent)
  *   or_segment ............... pinned (recovers a rendered hand in front of a background
  *                              plane exactly; dropout / skin / empty-frame special cases)
@@ -99,6 +103,11 @@ typedef struct {
   int32_t particles, generations, mutation_period, per_dim_r;
   double c1, c2, mutation_fraction;
   double stop_threshold; /* -INFINITY = off */
+  /* AMB-17 (P:L152 is silent on the order): 0 = mutate after the Eq. 6-7 update and before
+   * the evaluation of generations k = period, 2 period, ... (mutated poses are evaluated as
+   * drawn); 1 = SPEC's order: mutate after generation k's evaluation and
+   * bookkeeping, so the next update moves the mutated particles before they are evaluated. */
+  int32_t mutation_after_eval;
 } or_pso_params;
 
 /* Batch objective: costs[i] = f(X[i*D .. i*D+D-1]); NaN is treated as +inf by the PSO. */
@@ -127,6 +136,9 @@ void or_render_prims(const or_prim* prims, int32_t nprim, const or_camera* cam, 
 void or_render(const double h[26], const or_dims* d, const or_camera* cam, int32_t culled, float* depth);
 /* edge mask: 1 where hit status or depth (> depth_tol mm) changes when the ray moves by
  * +-delta px in u or v, or where ||o_d - r_d| - d_m| < rm_tol (obs_depth may be NULL). */
+void or_edge_mask_prims(const or_prim* prims, int32_t nprim, const or_camera* cam, double delta,
+                        double depth_tol, const float* obs_depth, double d_m, double rm_tol,
+                        uint8_t* edge);
 void or_edge_mask(const double h[26], const or_dims* d, const or_camera* cam, double delta,
                   double depth_tol, const float* obs_depth, double d_m, double rm_tol, uint8_t* edge);
 /* conservative pixel box [x0,x1]x[y0,y1] of one primitive (inclusive), margin in px;

@@ -69,7 +69,7 @@ class PsoParams(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("particles", C.c_int32), ("generations", C.c_int32),
                 ("mutation_period", C.c_int32), ("per_dim_r", C.c_int32), ("c1", C.c_double),
                 ("c2", C.c_double), ("mutation_fraction", C.c_double),
-                ("stop_threshold", C.c_double)]
+                ("stop_threshold", C.c_double), ("mutation_after_eval", C.c_int32)]
 
 
 _lib = None
@@ -182,6 +182,17 @@ def edge_mask(h, cam: Camera, dims: Dims | None = None, delta: float = 1e-3,
     lib().or_edge_mask(_p(h, C.c_double), C.byref(dims or default_dims()), C.byref(cam),
                        C.c_double(delta), C.c_double(depth_tol), _p(od, C.c_float),
                        C.c_double(d_m), C.c_double(rm_tol), _p(out, C.c_uint8))
+    return out
+
+
+def edge_mask_prims(prims, cam: Camera, delta: float = 1e-3, depth_tol: float = 1e-2,
+                    obs_depth=None, d_m: float = 10.0, rm_tol: float = 2e-3) -> np.ndarray:
+    arr = (Prim * max(len(prims), 1))(*prims)
+    out = np.zeros((cam.height, cam.width), dtype=np.uint8)
+    od = None if obs_depth is None else np.ascontiguousarray(obs_depth, dtype=np.float32)
+    lib().or_edge_mask_prims(arr, len(prims), C.byref(cam), C.c_double(delta),
+                             C.c_double(depth_tol), _p(od, C.c_float), C.c_double(d_m),
+                             C.c_double(rm_tol), _p(out, C.c_uint8))
     return out
 
 
@@ -305,6 +316,31 @@ def pso_sphere(D, lo, hi, init_lo, init_hi, mut_lo, mut_hi, centre, pp: PsoParam
                              _p(arrs[4], C.c_double), C.byref(pp), _p(bx, C.c_double),
                              C.byref(bc), _p(tr, C.c_double), C.byref(gr), _p(X, C.c_double),
                              _p(V, C.c_double), _p(P, C.c_double), _p(Pc, C.c_double))
+    if rc != 0:
+        raise ValueError("invalid PSO parameters")
+    return PsoResult(bx, bc.value, tr, gr.value, X, V, P, Pc)
+
+
+BATCH_FN = C.CFUNCTYPE(None, C.POINTER(C.c_double), C.c_int32, C.c_int32,
+                       C.POINTER(C.c_double), C.c_void_p)
+
+
+def pso_run(D, lo, hi, init_lo, init_hi, mut_lo, mut_hi, pp: PsoParams, objective) -> PsoResult:
+    """or_pso_run with a Python batch objective: objective(X (n, D) array) -> n costs."""
+    arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (lo, hi, init_lo, init_hi)]
+
+    def cb(xp, n, d, costs, user):
+        X = np.ctypeslib.as_array(xp, shape=(n, d)).copy()
+        out = np.asarray(objective(X), dtype=np.float64)
+        for i in range(n):
+            costs[i] = float(out[i])
+
+    fn = BATCH_FN(cb)
+    bx, bc, tr, gr, X, V, P, Pc = _pso_outputs(pp.particles, D, pp.generations)
+    rc = lib().or_pso_run(D, *[_p(a, C.c_double) for a in arrs], mut_lo, mut_hi, C.byref(pp),
+                          fn, None, _p(bx, C.c_double), C.byref(bc), _p(tr, C.c_double),
+                          C.byref(gr), _p(X, C.c_double), _p(V, C.c_double), _p(P, C.c_double),
+                          _p(Pc, C.c_double))
     if rc != 0:
         raise ValueError("invalid PSO parameters")
     return PsoResult(bx, bc.value, tr, gr.value, X, V, P, Pc)

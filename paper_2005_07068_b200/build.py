@@ -16,6 +16,9 @@ DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "fk.cuh", "p
                                                       "tile.cuh", "eval.cuh", "batch.cuh")] + [
     os.path.join(os.path.dirname(HERE), "include", "hp.h")]
 LIB = os.path.join(HERE, "libhp.so")
+# debug build for the single-GPU loopback test of the sharded paths (include/hp.h
+# hp_shard_loopback); never loaded by the product binding unless a test asks for it
+LOOPBACK_LIB = os.path.join(HERE, "libhp_loopback.so")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177"]
@@ -40,6 +43,10 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     subprocess.check_call(cmd)
     os.replace(tmp, out)
     return out
+
+
+def build_loopback(force: bool = False) -> str:
+    return build(force=force, out=LOOPBACK_LIB, defines=["HP_LOOPBACK_TEST=1"])
 
 
 if __name__ == "__main__":

@@ -7,7 +7,11 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
+#include <condition_variable>
+#include <map>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -59,10 +63,45 @@ NcclApi* nccl_api() {
 
 thread_local std::string g_err = "";
 
+#if HP_LOOPBACK_TEST
+// DEBUG BUILDS ONLY (-DHP_LOOPBACK_TEST=1, never the product library): W contexts on ONE
+// GPU, each driven by its own host thread, stand in for W ranks.  The in-place allgather is
+// performed with device copies at exactly ncclAllGather's offsets (rank r's chunk at
+// r * chunk); ordering is by CUDA events recorded before a host barrier and waited on
+// after it, so no kernel ever waits on another rank's kernel.  This executes the rank > 0
+// slice offsets, the padded last chunk and the sharded fit's update -> eval -> allgather ->
+// bookkeeping sequence without a multi-GPU box; NCCL stays the only product transport.
+struct LoopGroup {
+  int world = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t phase = 0;
+  std::vector<void*> buf;
+  std::vector<cudaEvent_t> ready, read;
+};
+std::mutex g_loop_m;
+std::map<std::string, LoopGroup*> g_loop;
+
+// generation-counting barrier; false on timeout (a rank that failed never arrives)
+bool loop_barrier(LoopGroup* g) {
+  std::unique_lock<std::mutex> lk(g->m);
+  const uint64_t ph = g->phase;
+  if (++g->arrived == g->world) {
+    g->arrived = 0;
+    g->phase++;
+    g->cv.notify_all();
+    return true;
+  }
+  return g->cv.wait_for(lk, std::chrono::seconds(120), [&] { return g->phase != ph; });
+}
+#endif
+
 struct Graph {
   cudaGraphExec_t exec = nullptr;
   int N = -1, D = -1, K = -1, period = -1, per_dim_r = -1, nmut = -1, mut_lo = -1, mut_hi = -1;
   int sphere = -1;
+  int mut_after = -1;
   int world = -1;
   int exact = -1;  // 1: generation kernels with the near-plane code (after a speculative miss)
 };
@@ -127,6 +166,9 @@ struct hp_ctx {
   int blocks_per_sm = 0;           // resident k_eval CTAs per SM
   // particle-sharded mode (hp_shard): rank r owns poses [r chunk, (r + 1) chunk)
   ncclComm_t comm = nullptr;
+#if HP_LOOPBACK_TEST
+  LoopGroup* loop = nullptr;
+#endif
   int rank = 0, world = 1;
   float* gat32 = nullptr;    // [chunk * world] allgather buffer (hp_eval_costs)
   double* gat64 = nullptr;   // [chunk * world] allgather buffer (hp_pso_fit costs)
@@ -160,6 +202,14 @@ struct hp_ctx {
   } while (0)
 
 static double deg2rad(double d) { return d * (M_PI / 180.0); }
+
+// particle-sharded mode (NCCL, or the debug loopback group)
+static inline bool sharded(const hp_ctx* ctx) {
+#if HP_LOOPBACK_TEST
+  if (ctx->loop) return true;
+#endif
+  return ctx->comm != nullptr;
+}
 
 extern "C" {
 
@@ -208,6 +258,7 @@ hp_status hp_default_pso(hp_pso_params* p) {
   p->stop_threshold = -INFINITY;
   p->init_center = nullptr;
   p->init_radius = nullptr;
+  p->mutation_after_eval = 0;
   return HP_OK;
 }
 
@@ -713,9 +764,9 @@ hp_status hp_debug_render(hp_ctx* ctx, const float* pose_dev, float* depth_dev, 
   return render_depth(ctx, pose_dev, false, depth_dev, (cudaStream_t)stream);
 }
 
-static hp_status eval_common(hp_ctx* ctx, const float* poses, int64_t n, float* costs32,
+static hp_status eval_common(hp_ctx* ctx, const void* poses, int64_t n, float* costs32,
                              double* costs64, uint64_t* sums, cudaStream_t s,
-                             int64_t frame_n = 0) {
+                             int64_t frame_n = 0, bool pose_double = false) {
   EvalArgs a = base_args(ctx);
   a.poses = poses;
   a.n = (int)n;
@@ -724,7 +775,7 @@ static hp_status eval_common(hp_ctx* ctx, const float* poses, int64_t n, float* 
   a.costs32 = costs32;
   a.costs64 = costs64;
   a.sums_out = reinterpret_cast<unsigned long long*>(sums);
-  CK(launch_eval(a, false, kModeCost, &ctx->tmap, s, ctx->timing ? ctx->tev : nullptr));
+  CK(launch_eval(a, pose_double, kModeCost, &ctx->tmap, s, ctx->timing ? ctx->tev : nullptr));
   ctx->timed = ctx->timing;
   if (ctx->sync_debug) CK(cudaStreamSynchronize(s));
   // the batch path is three kernels (FK, the persistent renderer, its near-plane pass)
@@ -740,6 +791,51 @@ static inline void shard_range(int64_t n, int rank, int world, int64_t* b, int64
 
 // Sharded objective: this rank scores its slice of the N poses into its chunk of the
 // allgather buffer; ncclAllGather (in place) gives every rank all N costs.
+// In-place allgather of `chunk` elements per rank (rank r's at buf + r chunk): NCCL over
+// NVLink / NVSwitch in the product; device copies between same-GPU contexts in the debug
+// loopback build.
+static hp_status allgather(hp_ctx* ctx, void* buf, int64_t chunk, int dtype, cudaStream_t s) {
+  const size_t es = dtype == kNcclFloat64 ? 8 : 4;
+#if HP_LOOPBACK_TEST
+  if (LoopGroup* g = ctx->loop) {
+    const int r = ctx->rank;
+    g->buf[r] = buf;
+    CK(cudaEventRecord(g->ready[r], s));
+    if (!loop_barrier(g)) {
+      ctx->err = "loopback allgather: barrier timeout";
+      return HP_ERR_NCCL;
+    }
+    for (int j = 0; j < g->world; j++) {
+      if (j == r) continue;
+      CK(cudaStreamWaitEvent(s, g->ready[j], 0));
+      CK(cudaMemcpyAsync(static_cast<char*>(buf) + (size_t)j * chunk * es,
+                         static_cast<const char*>(g->buf[j]) + (size_t)j * chunk * es,
+                         (size_t)chunk * es, cudaMemcpyDeviceToDevice, s));
+    }
+    CK(cudaEventRecord(g->read[r], s));
+    if (!loop_barrier(g)) {
+      ctx->err = "loopback allgather: barrier timeout";
+      return HP_ERR_NCCL;
+    }
+    // a rank's next write to its own chunk is ordered after every peer's read of it
+    for (int j = 0; j < g->world; j++)
+      if (j != r) CK(cudaStreamWaitEvent(s, g->read[j], 0));
+    return HP_OK;
+  }
+#endif
+  char* mine = static_cast<char*>(buf) + (size_t)ctx->rank * chunk * es;
+  const ncclResult_t nr = nccl_api()->allGather(mine, buf, (size_t)chunk, dtype, ctx->comm, s);
+  if (nr != 0) {
+    ctx->err = std::string("ncclAllGather: ") + nccl_api()->errorString(nr);
+    return HP_ERR_NCCL;
+  }
+  return HP_OK;
+}
+
+// Sharded objective: this rank scores its slice of the N poses into its chunk of the
+// allgather buffer; the in-place allgather gives every rank all N costs.  A rank whose own
+// scoring fails still takes part in the collective (so its peers do not hang in it) and
+// then reports the error.
 static hp_status eval_sharded(hp_ctx* ctx, const float* poses, int64_t n, float* costs,
                               cudaStream_t s) {
   const int64_t chunk = (n + ctx->world - 1) / ctx->world;
@@ -750,18 +846,19 @@ static hp_status eval_sharded(hp_ctx* ctx, const float* poses, int64_t n, float*
   int64_t b, e;
   shard_range(n, ctx->rank, ctx->world, &b, &e);
   int64_t launches = 0;
+  hp_status r = HP_OK;
   if (e > b) {
-    hp_status r = eval_common(ctx, poses + b * kNdof, e - b, ctx->gat32 + ctx->rank * chunk,
-                              nullptr, nullptr, s);
-    if (r != HP_OK) return r;
-    launches = 1;
+    r = eval_common(ctx, poses + b * kNdof, e - b, ctx->gat32 + ctx->rank * chunk, nullptr,
+                    nullptr, s);
+    launches = ctx->last_launches;
   }
-  ncclResult_t nr = nccl_api()->allGather(ctx->gat32 + ctx->rank * chunk, ctx->gat32,
-                                          (size_t)chunk, kNcclFloat32, ctx->comm, s);
-  if (nr != 0) {
-    ctx->err = std::string("ncclAllGather: ") + nccl_api()->errorString(nr);
-    return HP_ERR_NCCL;
+  const std::string local_err = ctx->err;
+  hp_status g = allgather(ctx, ctx->gat32, chunk, kNcclFloat32, s);
+  if (r != HP_OK) {
+    ctx->err = local_err;
+    return r;
   }
+  if (g != HP_OK) return g;
   CK(cudaMemcpyAsync(costs, ctx->gat32, (size_t)n * sizeof(float), cudaMemcpyDeviceToDevice, s));
   ctx->last_launches = launches;
   return HP_OK;
@@ -774,13 +871,15 @@ hp_status hp_eval_costs(hp_ctx* ctx, const float* poses, int64_t n, float* costs
   if (n == 0) return HP_OK;
   ARG(poses && costs, "hp_eval_costs: NULL buffer");
   cudaSetDevice(ctx->device);
-  if (ctx->comm) return eval_sharded(ctx, poses, n, costs, (cudaStream_t)stream);
+  if (sharded(ctx)) return eval_sharded(ctx, poses, n, costs, (cudaStream_t)stream);
   return eval_common(ctx, poses, n, costs, nullptr, nullptr, (cudaStream_t)stream);
 }
 
-hp_status hp_eval_costs_frames(hp_ctx* ctx, const float* poses, int64_t n_per_frame,
-                               float* costs, void* stream) {
+hp_status hp_eval_costs_frames(hp_ctx* ctx, const float* poses, int32_t frames,
+                               int64_t n_per_frame, float* costs, void* stream) {
   ARG(ctx, "hp_eval_costs_frames: NULL context");
+  ARG(frames == ctx->frames, "hp_eval_costs_frames: frames differs from the frame count of "
+                             "the current observation (hp_set_observations)");
   const int64_t total = n_per_frame * ctx->frames;
   ARG(n_per_frame >= 0 && total <= ctx->max_n,
       "hp_eval_costs_frames: n_per_frame * frames must be in [0, max_particles]");
@@ -792,9 +891,12 @@ hp_status hp_eval_costs_frames(hp_ctx* ctx, const float* poses, int64_t n_per_fr
                      n_per_frame);
 }
 
-hp_status hp_eval_sums_frames(hp_ctx* ctx, const float* poses, int64_t n_per_frame,
-                              uint64_t* sums, double* costs64, void* stream) {
+hp_status hp_eval_sums_frames(hp_ctx* ctx, const float* poses, int32_t frames,
+                              int64_t n_per_frame, uint64_t* sums, double* costs64,
+                              void* stream) {
   ARG(ctx, "hp_eval_sums_frames: NULL context");
+  ARG(frames == ctx->frames, "hp_eval_sums_frames: frames differs from the frame count of "
+                             "the current observation (hp_set_observations)");
   const int64_t total = n_per_frame * ctx->frames;
   ARG(n_per_frame >= 0 && total <= ctx->max_n,
       "hp_eval_sums_frames: n_per_frame * frames must be in [0, max_particles]");
@@ -826,27 +928,37 @@ hp_status hp_eval_costs_host(hp_ctx* ctx, const float* poses, int64_t n, float* 
   ARG(poses && costs, "hp_eval_costs_host: NULL buffer");
   cudaSetDevice(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
-  if (ctx->comm) {
+  if (sharded(ctx)) {
     // sharded: upload only this rank's slice, score it, allgather, download all costs
     const int64_t chunk = (n + ctx->world - 1) / ctx->world;
+    if (chunk > ctx->gat_cap) {
+      ctx->err = "sharded eval: n exceeds max_particles * world";
+      return HP_ERR_INVALID_ARG;
+    }
     int64_t b, e;
     shard_range(n, ctx->rank, ctx->world, &b, &e);
     const size_t in_bytes = (size_t)(e - b) * kNdof * sizeof(float);
     const bool in_pinned = is_pinned(poses), out_pinned = is_pinned(costs);
     if (!in_pinned) memcpy(ctx->h_poses, poses + b * kNdof, in_bytes);
+    hp_status r = HP_OK;
     if (e > b) {
-      CK(cudaMemcpyAsync(ctx->poses32, in_pinned ? poses + b * kNdof : ctx->h_poses, in_bytes,
-                         cudaMemcpyHostToDevice, s));
-      hp_status r = eval_common(ctx, ctx->poses32, e - b, ctx->gat32 + ctx->rank * chunk,
-                                nullptr, nullptr, s);
-      if (r != HP_OK) return r;
+      cudaError_t ce = cudaMemcpyAsync(ctx->poses32, in_pinned ? poses + b * kNdof : ctx->h_poses,
+                                       in_bytes, cudaMemcpyHostToDevice, s);
+      if (ce != cudaSuccess) {
+        ctx->err = std::string("cudaMemcpyAsync: ") + cudaGetErrorString(ce);
+        r = HP_ERR_CUDA;
+      } else {
+        r = eval_common(ctx, ctx->poses32, e - b, ctx->gat32 + ctx->rank * chunk, nullptr,
+                        nullptr, s);
+      }
     }
-    ncclResult_t nr = nccl_api()->allGather(ctx->gat32 + ctx->rank * chunk, ctx->gat32,
-                                            (size_t)chunk, kNcclFloat32, ctx->comm, s);
-    if (nr != 0) {
-      ctx->err = std::string("ncclAllGather: ") + nccl_api()->errorString(nr);
-      return HP_ERR_NCCL;
+    const std::string local_err = ctx->err;
+    hp_status g = allgather(ctx, ctx->gat32, chunk, kNcclFloat32, s);  // always take part
+    if (r != HP_OK) {
+      ctx->err = local_err;
+      return r;
     }
+    if (g != HP_OK) return g;
     CK(cudaMemcpyAsync(out_pinned ? costs : ctx->h_costs, ctx->gat32, (size_t)n * sizeof(float),
                        cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -893,6 +1005,16 @@ hp_status hp_eval_sums(hp_ctx* ctx, const float* poses, int64_t n, uint64_t* sum
   return eval_common(ctx, poses, n, nullptr, costs64, sums, (cudaStream_t)stream);
 }
 
+hp_status hp_eval_sums_f64(hp_ctx* ctx, const double* poses, int64_t n, uint64_t* sums,
+                           double* costs64, void* stream) {
+  ARG(ctx, "hp_eval_sums_f64: NULL ctx");
+  ARG(n >= 0 && n <= ctx->max_n, "hp_eval_sums_f64: n < 0 or n > max_particles");
+  if (n == 0) return HP_OK;
+  ARG(poses && (sums || costs64), "hp_eval_sums_f64: NULL buffer");
+  cudaSetDevice(ctx->device);
+  return eval_common(ctx, poses, n, nullptr, costs64, sums, (cudaStream_t)stream, 0, true);
+}
+
 hp_status hp_debug_fk(hp_ctx* ctx, const double* pose, float* records, int32_t* boxes,
                       double* joints, double* kc) {
   ARG(ctx && pose, "hp_debug_fk: NULL argument");
@@ -919,11 +1041,13 @@ hp_status hp_debug_fk(hp_ctx* ctx, const double* pose, float* records, int32_t* 
 static hp_status validate_pso(hp_ctx* ctx, const hp_pso_params* p) {
   ARG(p, "pso: NULL params");
   ARG(p->particles >= 1 && p->particles <= ctx->max_n, "pso: particles < 1 or > max_particles");
-  ARG(!ctx->comm || p->particles >= ctx->world, "pso: sharded fit needs particles >= world");
+  ARG(!sharded(ctx) || p->particles >= ctx->world, "pso: sharded fit needs particles >= world");
   ARG(p->generations >= 1, "pso: generations < 1");
   ARG(p->c1 + p->c2 > 4.0, "pso: c1 + c2 must exceed 4 (P:L150 constriction)");
   ARG(p->mutation_fraction >= 0.0 && p->mutation_fraction <= 1.0, "pso: mutation_fraction");
   ARG(p->mutation_period >= 0, "pso: mutation_period < 0");
+  ARG(p->mutation_after_eval == 0 || p->mutation_after_eval == 1,
+      "pso: mutation_after_eval must be 0 or 1");
   return HP_OK;
 }
 
@@ -937,6 +1061,7 @@ static PsoDev pso_dev(hp_ctx* ctx, int N, int D, const hp_pso_params* p, int mut
   d.nmut = (int)floor((double)N * p->mutation_fraction);
   d.mut_lo = mut_lo;
   d.mut_hi = mut_hi;
+  d.mut_after = p->mutation_after_eval;
   d.dyn = ctx->dyn;
   d.lo = ctx->bnd;
   d.hi = ctx->bnd + 64;
@@ -974,7 +1099,7 @@ static hp_status enqueue_fit(hp_ctx* ctx, const PsoDev& d, bool sphere, cudaStre
       CK(launch_pso_book(d, k, s));
       n += 3;
     }
-  } else if (ctx->comm) {
+  } else if (sharded(ctx)) {
     // sharded hand fit: every rank updates ALL particles (identical bits everywhere),
     // scores its slice, allgathers the costs, and runs the identical bookkeeping
     const int64_t chunk = (d.N + ctx->world - 1) / ctx->world;
@@ -996,12 +1121,8 @@ static hp_status enqueue_fit(hp_ctx* ctx, const PsoDev& d, bool sphere, cudaStre
         CK(launch_eval(a, true, kModeCost, &ctx->tmap, s));
         n++;
       }
-      ncclResult_t nr = nccl_api()->allGather(ctx->gat64 + ctx->rank * chunk, ctx->gat64,
-                                              (size_t)chunk, kNcclFloat64, ctx->comm, s);
-      if (nr != 0) {
-        ctx->err = std::string("ncclAllGather: ") + nccl_api()->errorString(nr);
-        return HP_ERR_NCCL;
-      }
+      hp_status gr = allgather(ctx, ctx->gat64, chunk, kNcclFloat64, s);
+      if (gr != HP_OK) return gr;
       CK(launch_pso_book(d, k, s));
       n++;
     }
@@ -1077,7 +1198,7 @@ static hp_status run_fit(hp_ctx* ctx, const hp_pso_params* p, int D, const doubl
   CK(cudaMemcpyAsync(ctx->bnd, hbv.data(), 256 * sizeof(double), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(ctx->dyn, &dyn, sizeof dyn, cudaMemcpyHostToDevice, s));
   PsoDev d = pso_dev(ctx, N, D, p, mut_lo, mut_hi);
-  if (ctx->comm && !sphere) {
+  if (sharded(ctx) && !sphere) {
     if ((N + ctx->world - 1) / ctx->world > ctx->gat_cap) {
       ctx->err = "sharded fit: particles exceed max_particles * world";
       return HP_ERR_INVALID_ARG;
@@ -1088,14 +1209,21 @@ static hp_status run_fit(hp_ctx* ctx, const hp_pso_params* p, int D, const doubl
   // the fused hand fit runs speculatively without the near-plane code first (exact = 0);
   // only if some particle needed it is the whole fit repeated with the exact kernels
   // (same seed: the same trajectory, now exact).  Sphere / sharded fits never use it.
-  const bool fused = !sphere && !ctx->comm;
+  const bool fused = !sphere && !sharded(ctx);
   double* ho = ctx->h_out;
   int64_t launches = 0, total_launches = 0;
   for (int exact = fused ? 0 : 1;; exact++) {
     const bool same = g.exec && g.N == N && g.D == D && g.K == K && g.period == d.period &&
                       g.per_dim_r == d.per_dim_r && g.nmut == d.nmut &&
                       g.mut_lo == mut_lo && g.mut_hi == mut_hi && g.sphere == (int)sphere &&
+                      g.mut_after == d.mut_after &&
                       g.world == ctx->world && g.exact == exact;
+#if HP_LOOPBACK_TEST
+    if (ctx->loop) {  // debug loopback ranks: eager launches (host barriers between them)
+      hp_status r = enqueue_fit(ctx, d, sphere, s, &launches, exact != 0);
+      if (r != HP_OK) return r;
+    } else
+#endif
     if (!same) {
       if (g.exec) cudaGraphExecDestroy(g.exec);
       g.exec = nullptr;
@@ -1117,13 +1245,17 @@ static hp_status run_fit(hp_ctx* ctx, const hp_pso_params* p, int D, const doubl
       g.mut_lo = mut_lo;
       g.mut_hi = mut_hi;
       g.sphere = sphere;
+      g.mut_after = d.mut_after;
       g.world = ctx->world;
       g.exact = exact;
     } else {
       launches = ctx->last_fit_launches;
     }
     if (!exact) CK(cudaMemsetAsync(ctx->flags + 2, 0, sizeof(int), s));
-    CK(cudaGraphLaunch(g.exec, s));
+#if HP_LOOPBACK_TEST
+    if (!ctx->loop)
+#endif
+      CK(cudaGraphLaunch(g.exec, s));
     CK(cudaMemcpyAsync(ho, ctx->G, D * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(ho + 64, ctx->Gc, sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(ho + 65, ctx->flags + 1, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1144,7 +1276,7 @@ static hp_status run_fit(hp_ctx* ctx, const hp_pso_params* p, int D, const doubl
   memcpy(&gr, ho + 65, sizeof(int));
   if (gens_run) *gens_run = gr;
   ctx->last_gens = gr;
-  ctx->last_fused = !sphere && !ctx->comm;
+  ctx->last_fused = !sphere && !sharded(ctx);
   if (trace) {
     for (int k = 0; k < K; k++) trace[k] = k < gr ? ho[72 + k] : ho[72 + gr - 1];
   }
@@ -1220,12 +1352,15 @@ hp_status hp_debug_pso_sphere(hp_ctx* ctx, int32_t D, const double* lo, const do
                  trace, gens_run, (cudaStream_t)stream);
 }
 
-hp_status hp_pso_state(hp_ctx* ctx, double* X, double* V, double* P, double* Pcost) {
+hp_status hp_pso_state(hp_ctx* ctx, int32_t particles, int32_t D, double* X, double* V,
+                       double* P, double* Pcost) {
   ARG(ctx, "hp_pso_state: NULL ctx");
   if (ctx->last_N == 0) {
     ctx->err = "hp_pso_state: no fit has run";
     return HP_ERR_STATE;
   }
+  ARG(particles == ctx->last_N && D == ctx->last_D,
+      "hp_pso_state: particles / D differ from the last fit's (the buffers' capacity)");
   cudaSetDevice(ctx->device);
   const size_t nd = (size_t)ctx->last_N * ctx->last_D * sizeof(double);
   // the fused hand fit double-buffers X, V: generation g lives in buffer g & 1
@@ -1269,10 +1404,12 @@ hp_status hp_get_nccl_id(uint8_t* id) {
   return HP_OK;
 }
 
+static hp_status shard_buffers(hp_ctx* ctx, int rank, int world);
+
 hp_status hp_shard(hp_ctx* ctx, const uint8_t* id, int32_t rank, int32_t world) {
   ARG(ctx && id, "hp_shard: NULL argument");
   ARG(world >= 1 && rank >= 0 && rank < world, "hp_shard: bad rank/world");
-  if (ctx->comm) {
+  if (sharded(ctx)) {
     ctx->err = "hp_shard: context is already sharded";
     return HP_ERR_STATE;
   }
@@ -1290,6 +1427,42 @@ hp_status hp_shard(hp_ctx* ctx, const uint8_t* id, int32_t rank, int32_t world) 
     ctx->err = std::string("ncclCommInitRank: ") + api->errorString(r);
     return HP_ERR_NCCL;
   }
+  return shard_buffers(ctx, rank, world);
+}
+
+#if HP_LOOPBACK_TEST
+// Debug builds only (see LoopGroup): join loopback group `group` as rank/world.  Every
+// member is a context on the same device, driven by its own host thread.
+hp_status hp_shard_loopback(hp_ctx* ctx, const char* group, int32_t rank, int32_t world) {
+  ARG(ctx && group, "hp_shard_loopback: NULL argument");
+  ARG(world >= 1 && rank >= 0 && rank < world, "hp_shard_loopback: bad rank/world");
+  if (sharded(ctx)) {
+    ctx->err = "hp_shard_loopback: context is already sharded";
+    return HP_ERR_STATE;
+  }
+  cudaSetDevice(ctx->device);
+  LoopGroup* g;
+  {
+    std::lock_guard<std::mutex> lk(g_loop_m);
+    LoopGroup*& slot = g_loop[group];
+    if (!slot) {
+      slot = new LoopGroup();
+      slot->world = world;
+      slot->buf.assign(world, nullptr);
+      slot->ready.assign(world, nullptr);
+      slot->read.assign(world, nullptr);
+    }
+    g = slot;
+  }
+  ARG(g->world == world, "hp_shard_loopback: world differs from the group's");
+  CK(cudaEventCreateWithFlags(&g->ready[rank], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&g->read[rank], cudaEventDisableTiming));
+  ctx->loop = g;
+  return shard_buffers(ctx, rank, world);
+}
+#endif
+
+static hp_status shard_buffers(hp_ctx* ctx, int rank, int world) {
   ctx->rank = rank;
   ctx->world = world;
   ctx->gat_cap = ctx->max_n;  // chunk <= max_particles

@@ -84,6 +84,8 @@ struct PsoDyn {  // per-fit values, read from device memory so a captured graph 
 };
 struct PsoDev {
   int N, D, K, period, per_dim_r, nmut, mut_lo, mut_hi;
+  int mut_after;  // AMB-17 order: 0 mutate after the update of generation k = period, ...;
+                  // 1 SPEC's: after generation k's bookkeeping, before k + 1's update
   const PsoDyn* dyn;
   const double *lo, *hi, *ilo, *ihi;  // [D]
   double *X, *V, *P, *Pc, *E, *G, *Gc, *trace;

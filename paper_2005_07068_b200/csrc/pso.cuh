@@ -75,7 +75,7 @@ __device__ __forceinline__ void pso_update_warp(const PsoDev& p, int i, int k, c
       r2 = u01(r.z, r.w);
     }
     const long long id = (long long)i * p.D + d;
-    const double x0 = Xin[id];
+    double x0 = Xin[id];  // the position generation k - 1 evaluated
     double pb, gb;
     if (deferred) {
       pb = imp_i ? x0 : p.P[id];
@@ -86,9 +86,18 @@ __device__ __forceinline__ void pso_update_warp(const PsoDev& p, int i, int k, c
       pb = p.P[id];
       gb = p.G[d];
     }
+    double v0 = Vin[id];
+    const bool mdim = marked && d >= p.mut_lo && d < p.mut_hi;
+    if (p.mut_after && mdim) {
+      // SPEC's order: the particle was re-drawn after generation k - 1's
+      // bookkeeping (counter generation k - 1), so this update moves the re-drawn position
+      const uint4 r = draw(dyn.seed, (uint32_t)i, (uint32_t)d, (uint32_t)(k - 1), 2u);
+      x0 = lerp_rn(p.lo[d], p.hi[d], u01(r.x, r.y));
+      v0 = 0.0;
+    }
     // Eq. (6): v = w (v + c1 r1 (P - x) + c2 r2 (G - x));  Eq. (7): x = x + v
     const double t1 = __dmul_rn(__dmul_rn(dyn.c1, r1), __dsub_rn(pb, x0));
-    const double t2 = __dadd_rn(Vin[id], t1);
+    const double t2 = __dadd_rn(v0, t1);
     const double t3 = __dmul_rn(__dmul_rn(dyn.c2, r2), __dsub_rn(gb, x0));
     double v = __dmul_rn(dyn.w, __dadd_rn(t2, t3));
     double x = __dadd_rn(x0, v);
@@ -99,7 +108,7 @@ __device__ __forceinline__ void pso_update_warp(const PsoDev& p, int i, int k, c
       x = p.hi[d];
       v = 0.0;
     }
-    if (marked && d >= p.mut_lo && d < p.mut_hi) {  // P:L152 mutation (AMB-17)
+    if (!p.mut_after && mdim) {  // P:L152 mutation (AMB-17: after the update)
       const uint4 r = draw(dyn.seed, (uint32_t)i, (uint32_t)d, (uint32_t)k, 2u);
       x = lerp_rn(p.lo[d], p.hi[d], u01(r.x, r.y));
       v = 0.0;
@@ -110,6 +119,16 @@ __device__ __forceinline__ void pso_update_warp(const PsoDev& p, int i, int k, c
     }
     if (pose) pose[d] = x;
   }
+}
+
+// Are mutation marks for generation k + 1's update drawn at the end of generation k?
+// Order 0 (AMB-17): generation k + 1 is a mutation generation (k + 1 = period, 2 period, ...).
+// Order 1: generation k >= 1 is one, and the update of k + 1 moves the re-drawn
+// particles.  Never after the last generation (nothing would see them).
+__device__ __forceinline__ bool mutation_marks_due(const PsoDev& p, int k) {
+  const int kn = k + 1;
+  if (!(p.period > 0 && kn < p.K && p.nmut > 0)) return false;
+  return p.mut_after ? (k >= 1 && k % p.period == 0) : (kn % p.period == 0);
 }
 
 // One block (any size, multiple of 32): bookkeeping after generation k's evaluation of the
@@ -204,8 +223,7 @@ __device__ __forceinline__ void pso_book_block(const PsoDev& p, int k, const dou
   __syncthreads();
   const int g = s_g;
   for (int d = tid; d < p.D; d += nt) p.G[d] = p.P[(long long)g * p.D + d];
-  const int kn = k + 1;
-  const bool mut = p.period > 0 && kn < p.K && kn % p.period == 0 && p.nmut > 0;
+  const bool mut = mutation_marks_due(p, k);
   for (int i = tid; i < p.N; i += nt) {
     int m = 0;
     if (mut) {
@@ -279,8 +297,7 @@ __device__ __forceinline__ void pso_book_tail(const PsoDev& p, int k, const doub
     p.gsel[0] = g;
     p.gsel[1] = p.pimp[g];
   }
-  const int kn = k + 1;
-  const bool mut = p.period > 0 && kn < p.K && kn % p.period == 0 && p.nmut > 0;
+  const bool mut = mutation_marks_due(p, k);
   for (int i = tid; i < p.N; i += nt) {
     int m = 0;
     if (mut) {

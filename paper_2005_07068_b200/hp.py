@@ -55,10 +55,10 @@ class PsoParams(C.Structure):
                 ("mutation_period", C.c_int32), ("per_dim_r", C.c_int32), ("c1", C.c_double),
                 ("c2", C.c_double), ("mutation_fraction", C.c_double),
                 ("stop_threshold", C.c_double), ("init_center", C.POINTER(C.c_double)),
-                ("init_radius", C.POINTER(C.c_double))]
+                ("init_radius", C.POINTER(C.c_double)), ("mutation_after_eval", C.c_int32)]
 
 
-_lib = None
+_libs = {}
 _VP = C.c_void_p
 
 
@@ -68,14 +68,15 @@ class SegmentParams(C.Structure):
                 ("width_mm", C.c_int32), ("keep_background", C.c_int32)]
 
 
-def lib() -> C.CDLL:
-    """Load libhp.so (raises if it was not built: run ``python -m paper_2005_07068_b200.build``)."""
-    global _lib
-    if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise ImportError(f"{LIB_PATH} not found: build it with "
+def lib(path: str | None = None) -> C.CDLL:
+    """Load libhp.so (raises if it was not built: run ``python -m paper_2005_07068_b200.build``).
+    `path` selects another build of the same ABI (e.g. the debug loopback build)."""
+    path = path or LIB_PATH
+    if path not in _libs:
+        if not os.path.exists(path):
+            raise ImportError(f"{path} not found: build it with "
                               "`python -m paper_2005_07068_b200.build` (no CPU fallback)")
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(path)
         sig = {
             "hp_default_dims": [C.POINTER(HandDims)],
             "hp_default_cost": [C.POINTER(CostParams)],
@@ -89,8 +90,9 @@ def lib() -> C.CDLL:
             "hp_eval_costs": [_VP, _VP, C.c_int64, _VP, _VP],
             "hp_eval_costs_host": [_VP, _VP, C.c_int64, _VP, _VP],
             "hp_eval_sums": [_VP, _VP, C.c_int64, _VP, _VP, _VP],
+            "hp_eval_sums_f64": [_VP, _VP, C.c_int64, _VP, _VP, _VP],
             "hp_pso_fit": [_VP, C.POINTER(PsoParams), _VP, _VP, _VP, _VP, _VP],
-            "hp_pso_state": [_VP, _VP, _VP, _VP, _VP],
+            "hp_pso_state": [_VP, C.c_int32, C.c_int32, _VP, _VP, _VP, _VP],
             "hp_debug_fk": [_VP, _VP, _VP, _VP, _VP, _VP],
             "hp_debug_render": [_VP, _VP, _VP, _VP],
             "hp_debug_pso_sphere": [_VP, C.c_int32, _VP, _VP, _VP, _VP, C.c_int32, C.c_int32, _VP,
@@ -108,14 +110,17 @@ def lib() -> C.CDLL:
             "hp_set_observation_kinect": [_VP, _VP, _VP, C.c_int32, C.POINTER(SegmentParams),
                                           C.c_int32, _VP, _VP],
             "hp_get_observation": [_VP, C.c_int32, _VP, _VP, _VP],
-            "hp_eval_costs_frames": [_VP, _VP, C.c_int64, _VP, _VP],
-            "hp_eval_sums_frames": [_VP, _VP, C.c_int64, _VP, _VP, _VP],
+            "hp_eval_costs_frames": [_VP, _VP, C.c_int32, C.c_int64, _VP, _VP],
+            "hp_eval_sums_frames": [_VP, _VP, C.c_int32, C.c_int64, _VP, _VP, _VP],
             "hp_last_kernel_ms": [_VP, _VP],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = C.c_int
+        if hasattr(L, "hp_shard_loopback"):  # debug builds only (-DHP_LOOPBACK_TEST=1)
+            L.hp_shard_loopback.argtypes = [_VP, C.c_char_p, C.c_int32, C.c_int32]
+            L.hp_shard_loopback.restype = C.c_int
         L.hp_last_error.argtypes = [_VP]
         L.hp_last_error.restype = C.c_char_p
         L.hp_last_launch_count.argtypes = [_VP]
@@ -124,15 +129,16 @@ def lib() -> C.CDLL:
         L.hp_splits_for.restype = C.c_int32
         L.hp_destroy.argtypes = [_VP]
         L.hp_destroy.restype = None
-        _lib = L
-    return _lib
+        _libs[path] = L
+    return _libs[path]
 
 
 def exported_symbols():
     """Names of every function include/hp.h declares (used by the CPU load test)."""
     return ["hp_default_dims", "hp_default_cost", "hp_default_pso", "hp_default_intrinsics",
             "hp_bounds", "hp_create", "hp_set_observation", "hp_render_observation",
-            "hp_eval_costs", "hp_eval_costs_host", "hp_eval_sums", "hp_pso_fit", "hp_pso_state",
+            "hp_eval_costs", "hp_eval_costs_host", "hp_eval_sums", "hp_eval_sums_f64", "hp_pso_fit",
+            "hp_pso_state",
             "hp_debug_fk", "hp_debug_render", "hp_debug_pso_sphere", "hp_last_launch_count",
             "hp_splits_for", "hp_last_error", "hp_destroy", "hp_shard_range",
             "hp_nccl_available", "hp_get_nccl_id", "hp_shard", "hp_track",
@@ -141,9 +147,9 @@ def exported_symbols():
             "hp_set_observation_kinect", "hp_get_observation"]
 
 
-def _check(status: int, ctx=None):
+def _check(status: int, ctx=None, L=None):
     if status != HP_OK:
-        msg = lib().hp_last_error(ctx)
+        msg = (L or lib()).hp_last_error(ctx)
         raise HPError(status, msg.decode() if msg else "")
 
 
@@ -259,8 +265,8 @@ class Context:
 
     def __init__(self, width: int = 640, height: int = 480, max_particles: int = 4096,
                  intrinsics: Intrinsics | None = None, dims: HandDims | None = None,
-                 cost: CostParams | None = None, device: int = -1):
-        self._L = lib()
+                 cost: CostParams | None = None, device: int = -1, lib_path: str | None = None):
+        self._L = lib(lib_path)
         self.cam = intrinsics or default_intrinsics(width, height)
         self.width, self.height = self.cam.width, self.cam.height
         self.max_particles = max_particles
@@ -268,7 +274,7 @@ class Context:
         st = self._L.hp_create(C.byref(self.cam), C.byref(dims) if dims else None,
                                C.byref(cost) if cost else None, max_particles, device,
                                C.byref(h))
-        _check(st, None)
+        _check(st, None, self._L)
         self._h = h
 
     # -- lifetime
@@ -302,11 +308,11 @@ class Context:
             m = np.ascontiguousarray(mask, dtype=np.uint8)
             assert d.shape == (self.height, self.width) and m.shape == d.shape
             _check(self._L.hp_set_observation(self._h, d.ctypes.data, m.ctypes.data, 0,
-                                              _stream(stream)), self._h)
+                                              _stream(stream)), self._h, self._L)
         else:
             assert tuple(depth.shape) == (self.height, self.width)
             _check(self._L.hp_set_observation(self._h, _dptr(depth), _dptr(mask), 1,
-                                              _stream(stream)), self._h)
+                                              _stream(stream)), self._h, self._L)
         self.frames = 1
 
     def set_observations(self, depth, mask, stream=None):
@@ -316,12 +322,12 @@ class Context:
             m = np.ascontiguousarray(mask, dtype=np.uint8)
             assert d.ndim == 3 and d.shape[1:] == (self.height, self.width) and m.shape == d.shape
             _check(self._L.hp_set_observations(self._h, d.ctypes.data, m.ctypes.data, d.shape[0],
-                                               0, _stream(stream)), self._h)
+                                               0, _stream(stream)), self._h, self._L)
         else:
             assert depth.dim() == 3 and tuple(depth.shape[1:]) == (self.height, self.width)
             assert depth.is_contiguous() and mask.is_contiguous()
             _check(self._L.hp_set_observations(self._h, _dptr(depth), _dptr(mask),
-                                               depth.shape[0], 1, _stream(stream)), self._h)
+                                               depth.shape[0], 1, _stream(stream)), self._h, self._L)
         self.frames = int(depth.shape[0])
 
     def set_observation_kinect(self, depth_u16, skin=None, mode: int = 1, lo_mm: int = 0,
@@ -345,7 +351,7 @@ class Context:
         assert tuple(shape[-2:]) == (self.height, self.width)
         band = np.zeros((frames, 2), np.int32)
         _check(self._L.hp_set_observation_kinect(self._h, dp, sp, frames, C.byref(seg), dev,
-                                                 band.ctypes.data, _stream(stream)), self._h)
+                                                 band.ctypes.data, _stream(stream)), self._h, self._L)
         self.frames = frames
         return band
 
@@ -356,7 +362,7 @@ class Context:
         d = torch.empty((self.height, self.width), dtype=torch.float32, device="cuda")
         m = torch.empty((self.height, self.width), dtype=torch.uint8, device="cuda")
         _check(self._L.hp_get_observation(self._h, frame, _dptr(d), _dptr(m), _stream(stream)),
-               self._h)
+               self._h, self._L)
         return d, m
 
     def render_observation(self, h_ref, stream=None):
@@ -367,7 +373,7 @@ class Context:
         depth = torch.empty((self.height, self.width), dtype=torch.float32, device="cuda")
         mask = torch.empty((self.height, self.width), dtype=torch.uint8, device="cuda")
         _check(self._L.hp_render_observation(self._h, h.ctypes.data, _dptr(depth), _dptr(mask),
-                                             _stream(stream)), self._h)
+                                             _stream(stream)), self._h, self._L)
         return depth, mask
 
     # -- evaluation
@@ -380,7 +386,7 @@ class Context:
         if out is None:
             out = torch.empty(n, dtype=torch.float32, device=poses.device)
         _check(self._L.hp_eval_costs(self._h, _dptr(poses), n, _dptr(out), _stream(stream)),
-               self._h)
+               self._h, self._L)
         return out
 
     def eval_costs_frames(self, poses, out=None, stream=None):
@@ -390,21 +396,29 @@ class Context:
         assert poses.dtype == torch.float32 and poses.dim() == 3 and poses.shape[-1] == NDOF
         assert poses.is_contiguous()
         m, n = poses.shape[0], poses.shape[1]
+        if m != self.frames:
+            raise ValueError(f"poses hold {m} frames, the observation {self.frames}")
         if out is None:
             out = torch.empty((m, n), dtype=torch.float32, device=poses.device)
-        _check(self._L.hp_eval_costs_frames(self._h, _dptr(poses), n, _dptr(out),
-                                            _stream(stream)), self._h)
+        if out.dtype != torch.float32 or tuple(out.shape) != (m, n) or not out.is_contiguous():
+            raise ValueError("out must be a contiguous float32 tensor of shape (frames, n)")
+        _check(self._L.hp_eval_costs_frames(self._h, _dptr(poses), m, n, _dptr(out),
+                                            _stream(stream)), self._h, self._L)
         return out
 
     def eval_sums_frames(self, poses, stream=None):
         """(sums [M][n][4] int64, costs fp64 [M][n]) of the frame-batched evaluation."""
         import torch
 
+        assert poses.dtype == torch.float32 and poses.dim() == 3 and poses.shape[-1] == NDOF
+        assert poses.is_contiguous()
         m, n = poses.shape[0], poses.shape[1]
+        if m != self.frames:
+            raise ValueError(f"poses hold {m} frames, the observation {self.frames}")
         sums = torch.zeros((m, n, 4), dtype=torch.int64, device=poses.device)
         costs = torch.empty((m, n), dtype=torch.float64, device=poses.device)
-        _check(self._L.hp_eval_sums_frames(self._h, _dptr(poses), n, _dptr(sums), _dptr(costs),
-                                           _stream(stream)), self._h)
+        _check(self._L.hp_eval_sums_frames(self._h, _dptr(poses), m, n, _dptr(sums),
+                                           _dptr(costs), _stream(stream)), self._h, self._L)
         return sums, costs
 
     def eval_costs_host(self, poses: np.ndarray, out: np.ndarray | None = None,
@@ -416,7 +430,7 @@ class Context:
             out = np.empty(p.shape[0], dtype=np.float32)
         assert out.dtype == np.float32 and out.flags.c_contiguous and out.size >= p.shape[0]
         _check(self._L.hp_eval_costs_host(self._h, p.ctypes.data, p.shape[0], out.ctypes.data,
-                                          _stream(stream)), self._h)
+                                          _stream(stream)), self._h, self._L)
         return out
 
     def eval_sums(self, poses, stream=None):
@@ -427,8 +441,29 @@ class Context:
         sums = torch.zeros((n, 4), dtype=torch.int64, device=poses.device)
         costs = torch.empty(n, dtype=torch.float64, device=poses.device)
         _check(self._L.hp_eval_sums(self._h, _dptr(poses), n, _dptr(sums), _dptr(costs),
-                                    _stream(stream)), self._h)
+                                    _stream(stream)), self._h, self._L)
         return sums, costs
+
+    def eval_sums_f64(self, poses, stream=None):
+        """(sums [N][4], costs fp64 [N]) of fp64 poses [N][26] (CUDA tensor): the scoring a
+        fit applies to its fp64 particles (hp_eval_sums_f64)."""
+        import torch
+
+        assert poses.dtype == torch.float64 and poses.dim() == 2 and poses.shape[1] == NDOF
+        assert poses.is_contiguous()
+        n = poses.shape[0]
+        sums = torch.zeros((n, 4), dtype=torch.int64, device=poses.device)
+        costs = torch.empty(n, dtype=torch.float64, device=poses.device)
+        _check(self._L.hp_eval_sums_f64(self._h, _dptr(poses), n, _dptr(sums), _dptr(costs),
+                                        _stream(stream)), self._h, self._L)
+        return sums, costs
+
+    def shard_loopback(self, group: str, rank: int, world: int):
+        """Debug builds only: join an in-process loopback group (hp_shard_loopback)."""
+        if not hasattr(self._L, "hp_shard_loopback"):
+            raise RuntimeError("hp_shard_loopback exists only in -DHP_LOOPBACK_TEST builds")
+        _check(self._L.hp_shard_loopback(self._h, group.encode(), rank, world), self._h, self._L)
+        self.rank, self.world = rank, world
 
     def shard(self, rank: int, world: int, nccl_id: bytes | None = None, group=None):
         """Particle-sharded mode (hp_shard): collective over the `world` ranks."""
@@ -436,7 +471,7 @@ class Context:
         if nccl_id is None:
             nccl_id = exchange_nccl_id(rank, group)
         buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
-        _check(self._L.hp_shard(self._h, buf, rank, world), self._h)
+        _check(self._L.hp_shard(self._h, buf, rank, world), self._h, self._L)
         self.rank, self.world = rank, world
 
     def splits_for(self, n: int) -> int:
@@ -447,12 +482,12 @@ class Context:
 
     def set_timing(self, on: bool = True):
         """Record per-launch CUDA events around every later evaluation (hp_set_timing)."""
-        _check(self._L.hp_set_timing(self._h, 1 if on else 0), self._h)
+        _check(self._L.hp_set_timing(self._h, 1 if on else 0), self._h, self._L)
 
     def last_kernel_ms(self) -> tuple[float, float]:
         """(first launch, renderer) device ms of the last timed evaluation."""
         ms = (C.c_float * 2)()
-        _check(self._L.hp_last_kernel_ms(self._h, ms), self._h)
+        _check(self._L.hp_last_kernel_ms(self._h, ms), self._h, self._L)
         return float(ms[0]), float(ms[1])
 
     # -- PSO
@@ -460,10 +495,11 @@ class Context:
                 mutation_period: int = 3, c1: float = 2.8, c2: float = 1.3,
                 mutation_fraction: float = 0.5, per_dim_r: bool = False,
                 stop_threshold: float = -math.inf, init_center=None, init_radius=None,
-                stream=None) -> FitResult:
+                mutation_after_eval: int = 0, stream=None) -> FitResult:
         """The paper's PSO fit on the GPU; synchronous."""
         p = PsoParams()
-        _check(self._L.hp_default_pso(C.byref(p)))
+        _check(self._L.hp_default_pso(C.byref(p)), None, self._L)
+        p.mutation_after_eval = int(mutation_after_eval)
         p.seed, p.particles, p.generations = seed, particles, generations
         p.mutation_period, p.c1, p.c2 = mutation_period, c1, c2
         p.mutation_fraction, p.per_dim_r, p.stop_threshold = mutation_fraction, int(per_dim_r), \
@@ -480,19 +516,20 @@ class Context:
         trace = np.zeros(generations)
         gr = C.c_int32()
         _check(self._L.hp_pso_fit(self._h, C.byref(p), best.ctypes.data, C.byref(cost),
-                                  trace.ctypes.data, C.byref(gr), _stream(stream)), self._h)
+                                  trace.ctypes.data, C.byref(gr), _stream(stream)), self._h, self._L)
         return FitResult(best, cost.value, trace, gr.value)
 
     def track(self, depth_seq, mask_seq, track_radius, seed: int = 0, particles: int = 64,
               generations: int = 30, mutation_period: int = 3, init_center=None,
-              init_radius=None, stream=None):
+              init_radius=None, mutation_after_eval: int = 0, stream=None):
         """Temporal tracking (hp_track): per-frame fit warm-started at the previous best
         pose +- track_radius.  depth_seq / mask_seq: [F][H][W] numpy (host) or CUDA
         tensors.  Returns (poses [F][26], costs [F], traces [F][generations])."""
         p = PsoParams()
-        _check(self._L.hp_default_pso(C.byref(p)))
+        _check(self._L.hp_default_pso(C.byref(p)), None, self._L)
         p.seed, p.particles, p.generations, p.mutation_period = (seed, particles, generations,
                                                                  mutation_period)
+        p.mutation_after_eval = int(mutation_after_eval)
         keep = []
         if init_center is not None:
             ic = np.ascontiguousarray(init_center, dtype=np.float64)
@@ -512,9 +549,12 @@ class Context:
         poses = np.zeros((F, NDOF))
         costs = np.zeros(F)
         traces = np.zeros((F, generations))
-        _check(self._L.hp_track(self._h, dp, mp_, F, dev, C.byref(p), tr.ctypes.data,
-                                poses.ctypes.data, costs.ctypes.data, traces.ctypes.data,
-                                _stream(stream)), self._h)
+        try:
+            _check(self._L.hp_track(self._h, dp, mp_, F, dev, C.byref(p), tr.ctypes.data,
+                                    poses.ctypes.data, costs.ctypes.data, traces.ctypes.data,
+                                    _stream(stream)), self._h, self._L)
+        finally:
+            self.frames = 1  # hp_track sets one observation frame at a time
         return poses, costs, traces
 
     def pso_state(self, particles: int, D: int = NDOF):
@@ -522,15 +562,17 @@ class Context:
         V = np.zeros((particles, D))
         P = np.zeros((particles, D))
         Pc = np.zeros(particles)
-        _check(self._L.hp_pso_state(self._h, X.ctypes.data, V.ctypes.data, P.ctypes.data,
-                                    Pc.ctypes.data), self._h)
+        _check(self._L.hp_pso_state(self._h, particles, D, X.ctypes.data, V.ctypes.data,
+                                    P.ctypes.data, Pc.ctypes.data), self._h, self._L)
         return X, V, P, Pc
 
     def debug_pso_sphere(self, D, lo, hi, init_lo, init_hi, mut_lo, mut_hi, centre, seed=0,
                          particles=64, generations=30, mutation_period=3, c1=2.8, c2=1.3,
-                         mutation_fraction=0.5, per_dim_r=False, stop_threshold=-math.inf):
+                         mutation_fraction=0.5, per_dim_r=False, stop_threshold=-math.inf,
+                         mutation_after_eval=0):
         p = PsoParams()
-        _check(self._L.hp_default_pso(C.byref(p)))
+        _check(self._L.hp_default_pso(C.byref(p)), None, self._L)
+        p.mutation_after_eval = int(mutation_after_eval)
         p.seed, p.particles, p.generations = seed, particles, generations
         p.mutation_period, p.c1, p.c2 = mutation_period, c1, c2
         p.mutation_fraction, p.per_dim_r, p.stop_threshold = mutation_fraction, int(per_dim_r), \
@@ -544,7 +586,7 @@ class Context:
         _check(self._L.hp_debug_pso_sphere(self._h, D, *[a.ctypes.data for a in arrs[:4]],
                                            mut_lo, mut_hi, arrs[4].ctypes.data, C.byref(p),
                                            best.ctypes.data, C.byref(cost), trace.ctypes.data,
-                                           C.byref(gr), None), self._h)
+                                           C.byref(gr), None), self._h, self._L)
         return FitResult(best, cost.value, trace, gr.value)
 
     # -- test hooks
@@ -555,7 +597,7 @@ class Context:
         joints = np.zeros((5, 4, 3))
         kc = C.c_double()
         _check(self._L.hp_debug_fk(self._h, h.ctypes.data, rec.ctypes.data, boxes.ctypes.data,
-                                   joints.ctypes.data, C.byref(kc)), self._h)
+                                   joints.ctypes.data, C.byref(kc)), self._h, self._L)
         return rec, boxes, joints, kc.value
 
     def debug_render(self, pose_dev, stream=None):
@@ -563,5 +605,5 @@ class Context:
 
         depth = torch.empty((self.height, self.width), dtype=torch.float32, device="cuda")
         _check(self._L.hp_debug_render(self._h, _dptr(pose_dev), _dptr(depth), _stream(stream)),
-               self._h)
+               self._h, self._L)
         return depth

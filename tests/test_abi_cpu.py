@@ -28,13 +28,23 @@ def test_library_builds_for_sm100a():
     assert "sm_100a" in out
 
 
+DEBUG_ONLY = {"hp_shard_loopback"}  # declared in hp.h for -DHP_LOOPBACK_TEST builds only
+
+
 def test_every_header_symbol_is_exported():
     syms = _header_symbols()
     assert len(syms) >= 18
     L = hp.lib()
     for s in syms:
+        assert hasattr(L, s) == (s not in DEBUG_ONLY), s
+    assert sorted(hp.exported_symbols()) == sorted(set(syms) - DEBUG_ONLY)
+
+
+def test_loopback_debug_build_exports_the_same_abi_plus_the_loopback_hook():
+    path = hpbuild.build_loopback()
+    L = hp.lib(path)
+    for s in _header_symbols():
         assert hasattr(L, s), s
-    assert sorted(hp.exported_symbols()) == syms
 
 
 def test_sass_has_tma_loads():
@@ -100,7 +110,7 @@ def test_binding_refuses_missing_library(tmp_path, monkeypatch):
 
     mod = importlib.import_module("paper_2005_07068_b200.hp")
     monkeypatch.setattr(mod, "LIB_PATH", str(tmp_path / "missing.so"))
-    monkeypatch.setattr(mod, "_lib", None)
+    monkeypatch.setattr(mod, "_libs", {})
     with pytest.raises(ImportError):
         mod.lib()
 

@@ -11,6 +11,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_2005_07068_b200 as hp  # noqa: E402
+from parity_check import check_sample  # noqa: E402
 
 E_REL, E_ABS = 1e-5, 2.5e-5
 
@@ -44,17 +45,8 @@ def _poses(names, n, seed):
 def _check_frame(obs, poses, sums, c64, w, h):
     p64 = np.asarray(poses, np.float64)
     co, so, _, _ = O.eval_batch(p64, obs, with_sums=True)
-    n_edge = 0
-    for i in range(len(co)):
-        if int(sums[i, 0]) == so[i].s_rm and int(sums[i, 1]) == so[i].s_and and \
-                int(sums[i, 3]) == so[i].n_both:
-            assert abs(c64[i] - co[i]) <= E_REL * abs(co[i]) + E_ABS, (i, c64[i], co[i])
-        else:  # a silhouette-edge pixel decided differently: bounded by the edge
-            n_edge += 1
-            ne = int(O.edge_mask(p64[i], O.camera(w, h), obs_depth=obs.depth).sum())
-            assert abs(int(sums[i, 0]) - so[i].s_rm) <= ne
-            assert abs(int(sums[i, 1]) - so[i].s_and) <= ne
-    assert n_edge <= 0.1 * len(co) + 1
+    check_sample(sums, c64, so, co, p64, range(len(co)), O.camera(w, h), obs,
+                 max_edge=0.1 * len(co) + 1)
 
 
 @pytest.mark.parametrize("n", [13, 160])  # split path (S > 1) and batch path (S = 1)
@@ -129,6 +121,16 @@ def test_frames_edge_cases():
         ctx.eval_costs_frames(P)
     with pytest.raises(AssertionError):
         ctx.set_observations(depth[:, :10], mask[:, :10])
+    # the poses' frame count must be the observation's (binding and C ABI both check)
+    P2 = torch.zeros((2, 5, 26), dtype=torch.float32, device="cuda")
+    with pytest.raises(ValueError):
+        ctx.eval_costs_frames(P2)
+    out = torch.empty((3, 5), dtype=torch.float32, device="cuda")
+    st = ctx._L.hp_eval_costs_frames(ctx.handle, P2.data_ptr(), 2, 5, out.data_ptr(), None)
+    assert st == hp.hp.HP_ERR_INVALID_ARG
+    with pytest.raises(ValueError):
+        ctx.eval_costs_frames(torch.zeros((3, 5, 26), dtype=torch.float32, device="cuda"),
+                              out=torch.empty((3, 4), dtype=torch.float32, device="cuda"))
 
 
 def test_frames_growth_keeps_fit_graph_valid():

@@ -12,6 +12,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_2005_07068_b200 as hp  # noqa: E402
+from parity_check import check_sample  # noqa: E402
 
 E_REL, E_ABS = 1e-5, 2.5e-5
 
@@ -82,17 +83,8 @@ def test_costs_on_noisy_segmented_frame_match_oracle(keep):
     torch.cuda.synchronize()
     sums, c64 = sums.cpu().numpy(), c64.cpu().numpy()
     co, so, _, _ = O.eval_batch(p32.astype(np.float64), obs, with_sums=True)
-    n_edge = 0
-    for i in range(len(co)):
-        if int(sums[i, 0]) == so[i].s_rm and int(sums[i, 1]) == so[i].s_and and \
-                int(sums[i, 3]) == so[i].n_both:
-            assert abs(c64[i] - co[i]) <= E_REL * abs(co[i]) + E_ABS, (i, c64[i], co[i])
-        else:
-            n_edge += 1
-            ne = int(O.edge_mask(p32[i].astype(np.float64), O.camera(w, h),
-                                 obs_depth=obs.depth).sum())
-            assert abs(int(sums[i, 0]) - so[i].s_rm) <= ne
-    assert n_edge <= 0.1 * len(co) + 1
+    check_sample(sums, c64, so, co, p32, range(len(co)), O.camera(w, h), obs,
+                 max_edge=0.1 * len(co) + 1)
 
 
 def test_fit_is_robust_to_kinect_noise():

@@ -13,6 +13,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_2005_07068_b200 as hp  # noqa: E402
+from parity_check import check_sample  # noqa: E402
 
 DEPTH_TOL = 1e-3        # mm, where both sides hit (north star / SURVEY §8(c))
 SIL_FRAC = 1e-3         # <= 0.1 % of union pixels may differ, all at edges
@@ -142,23 +143,10 @@ def _cost_parity(w, h, h_ref, poses, max_edge_frac=0.1):
     obs = obs_for(h_ref, w, h)
     sums, c64, c32 = gpu_costs(ctx, obs, poses)
     co, so, kco, Do = oracle_eval(obs, poses)
-    n_edge = 0
+    n_edge = check_sample(sums, c64, so, co, poses, range(len(co)), O.camera(w, h), obs,
+                           max_edge=max_edge_frac * len(co) + 1)
     for i in range(len(co)):
-        s_rm_eq = int(sums[i, 0]) == so[i].s_rm and int(sums[i, 1]) == so[i].s_and
-        if s_rm_eq and int(sums[i, 3]) == so[i].n_both:
-            assert abs(c64[i] - co[i]) <= E_REL * abs(co[i]) + E_ABS, (i, c64[i], co[i])
-            num_g = sums[i, 2] / 2.0 ** 20
-            assert abs(num_g - so[i].num) <= 2.5e-4 * max(so[i].n_both, 1) + 1e-6
-        else:
-            n_edge += 1
-            cam = O.camera(w, h)
-            p = np.asarray(np.asarray(poses[i], np.float32), np.float64)
-            edge = O.edge_mask(p, cam, obs_depth=obs.depth)
-            ne = int(edge.sum())
-            assert abs(int(sums[i, 0]) - so[i].s_rm) <= ne
-            assert abs(int(sums[i, 1]) - so[i].s_and) <= ne
         assert abs(c32[i] - np.float32(c64[i])) <= 1e-6 * max(1.0, abs(c64[i]))
-    assert n_edge <= max_edge_frac * len(co) + 1
     return n_edge
 
 
@@ -204,11 +192,9 @@ def test_full_batch_4096_sampled_parity_and_split_invariance():
     for i in range(0, 4096, 16):
         s16, _, _ = gpu_costs(ctx, obs, swarm[i:i + 16])
         assert np.array_equal(s16, sums[i:i + 16]), i
-    sample = [3, 100, 2048, 4000]
+    sample = [3, 100, 777, 1500, 2048, 3333, 4000, 4095]
     co, so, _, _ = oracle_eval(obs, swarm[sample])
-    for k, i in enumerate(sample):
-        if int(sums[i, 0]) == so[k].s_rm and int(sums[i, 1]) == so[k].s_and:
-            assert abs(c64[i] - co[k]) <= E_REL * abs(co[k]) + E_ABS
+    check_sample(sums, c64, so, co, swarm, sample, O.camera(640, 480), obs, max_edge=2)
     assert np.all(np.isfinite(c32)) and np.all(c32 >= 0)
 
 
@@ -326,6 +312,74 @@ def test_pso_hand_fit_parity_c1():
         assert np.all(np.diff(g.trace) <= 0)
 
 
+def _replay_fit(ctx, obs, seed, N, K, centre, radius, mutation_after_eval=0):
+    """The oracle's PSO (or_pso_run, the paper's Eq. 6-7 + bookkeeping) driven by the GPU's
+    costs of the exact fp64 particles it asks for (hp_eval_sums_f64), with every one of
+    those evaluations also scored by the oracle and compared ("PSO-step
+    parity").  Returns (the oracle-PSO result, number of edge poses, evaluations)."""
+    lo, hi = O.bounds()
+    ilo, ihi = np.maximum(lo, centre - radius), np.minimum(hi, centre + radius)
+    cam = obs.cam
+    stats = {"edge": 0, "n": 0}
+
+    def objective(X):
+        P = torch.tensor(X, dtype=torch.float64, device="cuda")
+        sums, c64 = ctx.eval_sums_f64(P)
+        sums, c64 = sums.cpu().numpy(), c64.cpu().numpy()
+        co, so, _, _ = O.eval_batch(X, obs, with_sums=True)
+        stats["edge"] += check_sample(sums, c64, so, co, X, range(len(X)), cam, obs,
+                                      pose_f32=False)
+        stats["n"] += len(X)
+        return c64
+
+    pp = O.default_pso(seed=seed, particles=N, generations=K,
+                       mutation_after_eval=mutation_after_eval)
+    r = O.pso_run(26, lo, hi, ilo, ihi, 6, 26, pp, objective)
+    return r, stats["edge"], stats["n"]
+
+
+@pytest.mark.parametrize("res", ["320x240", "640x480"])
+def test_pso_hand_fit_parity_c2_c3(res):
+    """C2 (320x240) and C3 (640x480, the north star's Target): the paper-scale fit, 64
+    particles x 40 generations with mutation every 3.
+    (1) PSO-step parity: the oracle's PSO fed the GPU's costs retraces the GPU fit bit for
+        bit (positions, velocities, personal bests, trace) — the GPU PSO is the paper's;
+    (2) every one of the 2560 evaluations on that trajectory matches the oracle's cost of
+        the same fp64 pose (sums exact, or differing only at oracle-flagged edge pixels
+        with the cost bounded by them);
+    (3) the oracle's own fit (oracle costs throughout) against the GPU fit: within 1e-4 per
+        DOF unless a comparison of two costs closer than (2)'s discrepancy flipped (AMB-24:
+        then the trajectories fork; the seed is reported as ambiguous).  At least 2 of the 4
+        seeds must match."""
+    w, h = W.RESOLUTIONS[res]
+    ctx = ctx_for(w, h, max_particles=64)
+    obs = obs_for(W.H_A, w, h)
+    ctx.set_observation(obs.depth, obs.mask)
+    c, rad = W.local_init_box()
+    matched, report = 0, []
+    for seed in (1, 2, 3, 4):
+        g = ctx.pso_fit(seed=seed, particles=64, generations=40, init_center=c, init_radius=rad)
+        X, V, P, Pc = ctx.pso_state(64)
+        rp, n_edge, n_eval = _replay_fit(ctx, obs, seed, 64, 40, c, rad)
+        assert n_eval == 64 * 40
+        assert n_edge <= 0.1 * n_eval, n_edge
+        assert np.array_equal(rp.best_x, g.best_pose) and rp.best_cost == g.best_cost
+        assert np.array_equal(rp.trace, g.trace)
+        assert np.array_equal(rp.X, X) and np.array_equal(rp.V, V)
+        assert np.array_equal(rp.P, P) and np.array_equal(rp.Pcost, Pc)
+        r = O.pso_fit_hand(obs, O.default_pso(seed=seed, particles=64, generations=40), c, rad)
+        dev = float(np.max(np.abs(g.best_pose - r.best_x)))
+        ok = dev <= 1e-4
+        if ok:
+            assert abs(g.best_cost - r.best_cost) <= E_REL * abs(r.best_cost) + E_ABS
+            np.testing.assert_allclose(g.trace, r.trace, rtol=E_REL, atol=E_ABS)
+        matched += ok
+        report.append((seed, dev, n_edge))
+        assert np.all(np.diff(g.trace) <= 0)
+    print(res, report)
+    assert matched >= 2, report
+
+
 def test_batch_path_close_up_poses_beyond_tile_list_capacity():
     """Hands close to the camera have union boxes of more than kMaxTiles (512) 16x8 tiles;
     the FK kernel then hands the renderer no tile list and it culls every tile itself.
@@ -358,13 +412,7 @@ def test_batch_path_close_up_poses_beyond_tile_list_capacity():
         assert np.array_equal(s1[0], sums[off + k]) and c1[0] == c64[off + k]
     sample = [0, 4, 8, 11]
     co, so, _, _ = oracle_eval(obs, close[sample])
-    for j, k in enumerate(sample):
-        if int(sums[off + k, 0]) == so[j].s_rm and int(sums[off + k, 1]) == so[j].s_and:
-            assert abs(c64[off + k] - co[j]) <= E_REL * abs(co[j]) + E_ABS
-        else:  # edge pixels only
-            ne = int(O.edge_mask(close[k].astype(np.float64), O.camera(640, 480),
-                                 obs_depth=obs.depth).sum())
-            assert abs(int(sums[off + k, 0]) - so[j].s_rm) <= ne
+    check_sample(sums, c64, so, co, batch, [off + k for k in sample], O.camera(640, 480), obs)
 
 
 def test_max_batch_16384_sampled_parity():
@@ -380,9 +428,7 @@ def test_max_batch_16384_sampled_parity():
         assert np.array_equal(s1[0], sums[i]) and c1[0] == c64[i]
     sample = [5, 6000, 12287, 12288, 16000]
     co, so, _, _ = oracle_eval(obs, swarm[sample])
-    for k, i in enumerate(sample):
-        if int(sums[i, 0]) == so[k].s_rm and int(sums[i, 1]) == so[k].s_and:
-            assert abs(c64[i] - co[k]) <= E_REL * abs(co[k]) + E_ABS
+    check_sample(sums, c64, so, co, swarm, sample, O.camera(640, 480), obs, max_edge=2)
     with pytest.raises(hp.HPError):
         ctx.eval_costs(torch.zeros((16385, 26), device="cuda"))
     ctx.close()
@@ -396,13 +442,7 @@ def test_large_image_ray_table_beyond_48kb():
     poses = np.stack([W.H_A, W.NAMED["fist"]]).astype(np.float32)
     sums, c64, _ = gpu_costs(ctx, obs, poses)
     co, so, _, _ = oracle_eval(obs, poses)
-    for i in range(2):
-        if int(sums[i, 0]) == so[i].s_rm and int(sums[i, 1]) == so[i].s_and:
-            assert abs(c64[i] - co[i]) <= E_REL * abs(co[i]) + E_ABS
-        else:
-            ne = int(O.edge_mask(poses[i].astype(np.float64), O.camera(w, h),
-                                 obs_depth=obs.depth).sum())
-            assert abs(int(sums[i, 0]) - so[i].s_rm) <= ne
+    check_sample(sums, c64, so, co, poses, range(2), O.camera(w, h), obs)
     ctx.close()
 
 
@@ -425,13 +465,7 @@ def test_cold_box_batch_sampled_parity():
         s16, _, _ = gpu_costs(ctx, obs, swarm[i:i + 16])
         assert np.array_equal(s16, sums[i:i + 16]), i
     co, so, _, _ = oracle_eval(obs, swarm[sample])
-    for k, i in enumerate(sample):
-        if int(sums[i, 0]) == so[k].s_rm and int(sums[i, 1]) == so[k].s_and:
-            assert abs(c64[i] - co[k]) <= E_REL * abs(co[k]) + E_ABS, (i, c64[i], co[k])
-        else:
-            ne = int(O.edge_mask(swarm[i].astype(np.float64), O.camera(640, 480),
-                                 obs_depth=obs.depth).sum())
-            assert abs(int(sums[i, 0]) - so[k].s_rm) <= ne
+    check_sample(sums, c64, so, co, swarm, sample, O.camera(640, 480), obs, max_edge=2)
 
 
 def test_speculative_fit_reruns_exactly_when_a_particle_crosses_the_near_plane():
@@ -498,10 +532,5 @@ def test_anisotropic_off_centre_camera_batch_split_and_oracle():
         assert np.array_equal(s16, sums[i:i + 16]), i
     sample = [0, 5, 300, 767, 800, 1000]
     co, so, _, _ = oracle_eval(obs, swarm[sample])
-    for k, i in enumerate(sample):
-        if int(sums[i, 0]) == so[k].s_rm and int(sums[i, 1]) == so[k].s_and:
-            assert abs(c64[i] - co[k]) <= E_REL * abs(co[k]) + E_ABS, (i, c64[i], co[k])
-        else:
-            ne = int(O.edge_mask(swarm[i].astype(np.float64), cam, obs_depth=obs.depth).sum())
-            assert abs(int(sums[i, 0]) - so[k].s_rm) <= ne
+    check_sample(sums, c64, so, co, swarm, sample, cam, obs, max_edge=2)
     ctx.close()

@@ -118,6 +118,31 @@ def test_fk_flat_hand_coplanar():
     assert np.all(np.abs(J[0, :, 2] - 992.0) < 1e-9)
 
 
+def test_fk_wrist_rotations_closed_form():
+    """Non-zero wrist angles (AMB-10): at 90 degrees each rotation is a coordinate permutation
+    written out by hand in the golden file; combined angles pin the order (x, then y, then
+    z), the 30-degree cases the signs of Ry and Rx away from the permutations."""
+    for case, ax, ay, az, name, k, x, y, z in _rows("fk_wrist_pins.txt"):
+        h = np.zeros(26)
+        h[2] = 800.0
+        h[3:6] = [math.radians(float(ax)), math.radians(float(ay)), math.radians(float(az))]
+        _, J = O.fk(h)
+        np.testing.assert_allclose(J[FINGER[name], int(k)], [float(x), float(y), float(z)],
+                                   atol=1e-7, err_msg=case)
+
+
+def test_fk_thumb_and_finger_flexion_abduction_closed_form():
+    """Thumb flexion sweeps it across the palm, thumb abduction lifts it palmarly, finger
+    flexion curls towards the palm (hand derivations in the golden file)."""
+    for case, dof, deg, name, k, x, y, z in _rows("fk_thumb_finger_pins.txt"):
+        h = np.zeros(26)
+        h[2] = 800.0
+        h[int(dof)] = math.radians(float(deg))
+        _, J = O.fk(h)
+        np.testing.assert_allclose(J[FINGER[name], int(k)], [float(x), float(y), float(z)],
+                                   atol=1e-7, err_msg=case)
+
+
 def test_fk_primitive_structure():
     """38 primitives: 1 cylinder, 3 ellipsoids, 14 cones, 20 spheres."""
     h = W.random_poses(3, 1)[0]
@@ -288,6 +313,56 @@ def test_first_hit_matches_ray_marching(name):
                 hits += 1
                 assert abs(t_or - t_bf) < 1e-6, (u, v, t_or, t_bf)
     assert hits > 0
+
+
+def test_edge_mask_on_axis_sphere_analytic():
+    """or_edge_mask's three rules on a sphere on the optical axis, whose silhouette, depth
+    and r_m boundaries have closed forms: ray d = (x, y, 1) hits the sphere |p - c| = r,
+    c = (0, 0, Z), iff Z^2 - |d|^2 (Z^2 - r^2) >= 0, at depth t = (Z - sqrt(.)) / |d|^2.
+    A pixel is an edge pixel iff moving its ray by +-delta px along u or v flips the hit
+    status or moves the (fp32) depth by more than depth_tol, or | |o_d - z| - d_m | < rm_tol
+    (DESIGN §6).  Decisions within 1e-6 of a threshold are not compared."""
+    Z, r = 1000.0, 200.0
+    cam = O.camera(160, 120)
+    delta, dtol, rmtol, dm = 0.25, 0.5, 0.5, 10.0
+    od = np.full((cam.height, cam.width), 820.0, np.float32)
+    got = O.edge_mask_prims([_sphere((0.0, 0.0, Z), r)], cam, delta, dtol, od, dm, rmtol)
+
+    def hit(u, v):
+        x, y = (u - cam.cx) / cam.fx, (v - cam.cy) / cam.fy
+        dd = 1.0 + x * x + y * y
+        disc = Z * Z - dd * (Z * Z - r * r)
+        if disc < 0:
+            return None, abs(disc) / (Z * Z)
+        return float(np.float32((Z - math.sqrt(disc)) / dd)), abs(disc) / (Z * Z)
+
+    n_edge = n_amb = 0
+    for v in range(cam.height):
+        for u in range(cam.width):
+            z, m0 = hit(u + 0.5, v + 0.5)
+            amb = m0 < 1e-6
+            e = False
+            for du, dv in ((delta, 0), (-delta, 0), (0, delta), (0, -delta)):
+                zk, mk = hit(u + 0.5 + du, v + 0.5 + dv)
+                amb |= mk < 1e-6
+                if (zk is None) != (z is None):
+                    e = True
+                elif z is not None:
+                    amb |= abs(abs(zk - z) - dtol) < 1e-6
+                    e |= abs(zk - z) > dtol
+            if not e and z is not None:
+                margin = abs(abs(820.0 - z) - dm) - rmtol
+                amb |= abs(margin) < 1e-6
+                e = margin < 0
+            if amb:
+                n_amb += 1
+                continue
+            assert bool(got[v, u]) == e, (u, v, z)
+            n_edge += e
+    assert n_amb < 10 and n_edge > 100  # the three rings are all populated
+    # without an observation only the silhouette and depth-gradient rings remain
+    got2 = O.edge_mask_prims([_sphere((0.0, 0.0, Z), r)], cam, delta, dtol, None, dm, rmtol)
+    assert got2.sum() < got.sum() and np.all(got2 <= got)
 
 
 def test_render_culled_equals_brute():
@@ -514,6 +589,105 @@ def test_pso_mutation_marks_worst_half(N):
     # re-drawn uniformly in the search bounds (+-1e7 here), not in the +-10 init box
     marked = sorted(expected)
     assert np.all(np.abs(r4.X[marked][:, 2:]).max(axis=1) > 10.0)
+
+
+def _golden_kv(name):
+    out = {}
+    for r in _rows(name):
+        out[r[0]] = [float(x) for x in r[1:]]
+    return out
+
+
+def _scripted(costs_by_gen):
+    """A batch objective returning fixed costs per generation (it ignores X)."""
+    calls = []
+
+    def f(X):
+        calls.append(X.copy())
+        return costs_by_gen[len(calls) - 1]
+    return f, calls
+
+
+def test_pso_eq6_hand_derived_two_particle_trajectory():
+    """Eq. 6's coefficient and random-number assignment: c1 r1 multiplies
+    (P - x), c2 r2 multiplies (G - x).  Scenario A of tests/golden/pso_eq6_hand.txt (hand
+    derivation, scripts/gen_golden_pso.py): at k = 1 only c2 r2 acts on particle 1 (P = x),
+    at k = 2 its c1 r1 term acts too.  A c1 <-> c2 or r1 <-> r2 swap changes every value."""
+    g = _golden_kv("pso_eq6_hand.txt")
+    assert abs(g["w"][0] - 0.729843788128) < 1e-12
+    lo, hi = np.array([-100.0]), np.array([100.0])
+    ilo, ihi = np.array([-10.0]), np.array([10.0])
+    costs = [[1.0, 2.0], [1.0, 5.0], [0.5, 5.0]]
+    for K in (2, 3):
+        f, calls = _scripted(costs)
+        pp = O.default_pso(seed=int(g["seed"][0]), particles=2, generations=K,
+                           mutation_period=0)
+        r = O.pso_run(1, lo, hi, ilo, ihi, 0, 0, pp, f)
+        np.testing.assert_allclose(calls[0][:, 0], [g["A.x0_init"][0], g["A.x1_init"][0]],
+                                   rtol=0, atol=1e-13)
+        for key, arr in (("X", r.X[:, 0]), ("V", r.V[:, 0]), ("P", r.P[:, 0]),
+                         ("Pcost", r.Pcost)):
+            np.testing.assert_allclose(arr, g[f"A.K{K}.{key}"], rtol=1e-12, atol=1e-13,
+                                       err_msg=f"K={K} {key}")
+    np.testing.assert_array_equal(r.trace, g["A.K3.trace"])
+
+
+def test_pso_mutation_orders_hand_derived():
+    """Both mutation orders (AMB-17 reading 0; SPEC S:L447 order 1) on scenario B of the
+    golden file: the worse particle's dim 1 re-drawn at k = 1 and evaluated as drawn
+    (order 0), or re-drawn after k = 1's evaluation and moved by k = 2's update (order 1)."""
+    g = _golden_kv("pso_eq6_hand.txt")
+    lo, hi = np.full(2, -100.0), np.full(2, 100.0)
+    ilo, ihi = np.full(2, -10.0), np.full(2, 10.0)
+    costs = [[1.0, 2.0], [1.0, 5.0], [0.5, 5.0]]
+    for order, K in ((0, 2), (1, 3)):
+        f, calls = _scripted(costs)
+        pp = O.default_pso(seed=int(g["seed"][0]), particles=2, generations=K,
+                           mutation_period=1, mutation_fraction=0.5, mutation_after_eval=order)
+        r = O.pso_run(2, lo, hi, ilo, ihi, 1, 2, pp, f)
+        np.testing.assert_allclose(r.X.ravel(), g[f"B.order{order}.K{K}.X"], rtol=1e-12,
+                                   atol=1e-13, err_msg=f"order {order}")
+        np.testing.assert_allclose(r.V.ravel(), g[f"B.order{order}.K{K}.V"], rtol=1e-12,
+                                   atol=1e-13, err_msg=f"order {order}")
+    # order 0 evaluates the re-drawn coordinate at k = 1; order 1 first at k = 2, moved
+    f, calls = _scripted(costs)
+    O.pso_run(2, lo, hi, ilo, ihi, 1, 2,
+              O.default_pso(seed=int(g["seed"][0]), particles=2, generations=3,
+                            mutation_period=1, mutation_fraction=0.5), f)
+    assert calls[1][1, 1] == g["B.order0.K2.X"][3]
+    f, calls = _scripted(costs)
+    O.pso_run(2, lo, hi, ilo, ihi, 1, 2,
+              O.default_pso(seed=int(g["seed"][0]), particles=2, generations=3,
+                            mutation_period=1, mutation_fraction=0.5, mutation_after_eval=1), f)
+    assert calls[1][1, 1] != g["B.order0.K2.X"][3]
+    assert calls[2][1, 1] == g["B.order1.K3.X"][3]
+
+
+def test_pso_c2_zero_ignores_the_global_best_c1_zero_ignores_the_personal_best():
+    """Eq. 6's two attractors in the limits: with c2 = 0 nothing pulls a particle
+    towards G, and at generation 0 every P = x with v = 0, so no particle ever moves; with
+    c1 = 0 (same psi = 4.1, so the same w) every particle but the best moves towards G."""
+    D, N = 3, 12
+    lo, hi = _box(D, -100.0, 100.0)
+    ilo, ihi = _box(D)
+    base = O.pso_sphere(D, lo, hi, ilo, ihi, 0, 0, np.full(D, 50.0),
+                        O.default_pso(seed=7, particles=N, generations=1, mutation_period=0))
+    a = O.pso_sphere(D, lo, hi, ilo, ihi, 0, 0, np.full(D, 50.0),
+                     O.default_pso(seed=7, particles=N, generations=6, mutation_period=0,
+                                   c1=4.1, c2=0.0))
+    assert np.array_equal(a.X, base.X) and np.all(a.V == 0)
+    b = O.pso_sphere(D, lo, hi, ilo, ihi, 0, 0, np.full(D, 50.0),
+                     O.default_pso(seed=7, particles=N, generations=2, mutation_period=0,
+                                   c1=0.0, c2=4.1))
+    best = int(np.argmin(base.Pcost))
+    moved = np.any(b.X != base.X, axis=1)
+    assert not moved[best] and moved.sum() == N - 1
+    # each moved particle stepped along G - x (c2 r2 (G - x), r2 >= 0, w > 0)
+    G = base.X[best]
+    for i in np.nonzero(moved)[0]:
+        step, toward = b.X[i] - base.X[i], G - base.X[i]
+        cos = step @ toward / (np.linalg.norm(step) * np.linalg.norm(toward))
+        assert cos > 1 - 1e-12
 
 
 def test_pso_hand_fit_recovers_from_local_init():
