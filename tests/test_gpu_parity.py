@@ -320,21 +320,26 @@ def _replay_fit(ctx, obs, seed, N, K, centre, radius, mutation_after_eval=0):
     lo, hi = O.bounds()
     ilo, ihi = np.maximum(lo, centre - radius), np.minimum(hi, centre + radius)
     cam = obs.cam
-    stats = {"edge": 0, "n": 0}
+    stats = {"edge": 0, "n": 0, "err": None}
 
     def objective(X):
         P = torch.tensor(X, dtype=torch.float64, device="cuda")
         sums, c64 = ctx.eval_sums_f64(P)
         sums, c64 = sums.cpu().numpy(), c64.cpu().numpy()
-        co, so, _, _ = O.eval_batch(X, obs, with_sums=True)
-        stats["edge"] += check_sample(sums, c64, so, co, X, range(len(X)), cam, obs,
-                                      pose_f32=False)
+        try:  # an exception cannot cross the C callback: keep it and re-raise below
+            co, so, _, _ = O.eval_batch(X, obs, with_sums=True)
+            stats["edge"] += check_sample(sums, c64, so, co, X, range(len(X)), cam, obs,
+                                          pose_f32=False)
+        except Exception as e:  # noqa: BLE001
+            stats["err"] = stats["err"] or e
         stats["n"] += len(X)
         return c64
 
     pp = O.default_pso(seed=seed, particles=N, generations=K,
                        mutation_after_eval=mutation_after_eval)
     r = O.pso_run(26, lo, hi, ilo, ihi, 6, 26, pp, objective)
+    if stats["err"] is not None:
+        raise stats["err"]
     return r, stats["edge"], stats["n"]
 
 
