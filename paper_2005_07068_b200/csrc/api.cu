@@ -121,7 +121,8 @@ struct hp_ctx {
   uint32_t* obs = nullptr;
   int pitch_words = 0;
   unsigned long long* S_o = nullptr;
-  CUtensorMap tmap{};
+  CUtensorMap tmap{};    // 16 x 8 observation boxes (k_eval, the near-plane pass)
+  CUtensorMap tmap16{};  // 16 x 16 (the batch renderer's warp blocks)
   float* up_depth = nullptr;  // staging for host uploads
   uint8_t* up_mask = nullptr;
   int frames = 1;      // observation frames currently set (hp_set_observations)
@@ -158,6 +159,7 @@ struct hp_ctx {
   unsigned int* pcount = nullptr;  // persistent-kernel counters (zero between launches)
   int persist_grid = 0;            // CTAs of the persistent kernels (0 = never use them)
   void* fk_g = nullptr;            // FkOut [max_n]
+  void* fkx_g = nullptr;           // FkExact [max_n] (near-plane poses only)
   uint4* tiles_g = nullptr;        // [max_n][kMaxTiles]
   int* ntl_g = nullptr;            // [max_n]
   int* near_list = nullptr;        // [max_n] near-plane pass queue
@@ -345,7 +347,7 @@ void hp_destroy(hp_ctx* ctx) {
                  ctx->poses32, ctx->costs32, ctx->scratch, ctx->X, ctx->V, ctx->P, ctx->Pc,
                  ctx->E, ctx->G, ctx->Gc, ctx->trace, ctx->bnd, ctx->centre, ctx->mark,
                  ctx->flags, ctx->dyn, ctx->tmap_g, ctx->ray, ctx->pcount, ctx->X2,
-                 ctx->V2, ctx->gcount, ctx->fk_g, ctx->tiles_g, ctx->ntl_g, ctx->near_list,
+                 ctx->V2, ctx->gcount, ctx->fk_g, ctx->fkx_g, ctx->tiles_g, ctx->ntl_g, ctx->near_list,
                  ctx->near_count, ctx->kc_g, ctx->pimp, ctx->gsel};
   for (void* p : dev)
     if (p) cudaFree(p);
@@ -375,14 +377,17 @@ static hp_status make_tmap(hp_ctx* ctx) {
   cuuint64_t gdim[2] = {(cuuint64_t)ctx->cam.width,
                         (cuuint64_t)ctx->cam.height * (cuuint64_t)ctx->frames_cap};
   cuuint64_t gstride[1] = {(cuuint64_t)ctx->pitch_words * 4};
-  cuuint32_t box[2] = {(cuuint32_t)kTileW, (cuuint32_t)kTileH};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = encode(&ctx->tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, ctx->obs, gdim, gstride,
-                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    ctx->err = "cuTensorMapEncodeTiled failed: " + std::to_string((int)r);
-    return HP_ERR_CUDA;
+  for (int m = 0; m < 2; m++) {
+    cuuint32_t box[2] = {(cuuint32_t)kTileW, (cuuint32_t)(m == 0 ? kTileH : kBlockH)};
+    CUresult r = encode(m == 0 ? &ctx->tmap : &ctx->tmap16, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
+                        ctx->obs, gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      ctx->err = "cuTensorMapEncodeTiled failed: " + std::to_string((int)r);
+      return HP_ERR_CUDA;
+    }
   }
   return HP_OK;
 }
@@ -503,6 +508,7 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   CKC(cudaMalloc(&ctx->ray, (size_t)ray_floats(W, H) * sizeof(float)));
   CKC(launch_ray_table(ctx->camp, ctx->ray, ctx->st));
   CKC(cudaMalloc(&ctx->fk_g, (size_t)max_particles * fk_record_bytes()));
+  CKC(cudaMalloc(&ctx->fkx_g, (size_t)max_particles * fk_exact_bytes()));
   CKC(cudaMalloc(&ctx->tiles_g, (size_t)max_particles * kMaxTiles * sizeof(uint4)));
   CKC(cudaMalloc(&ctx->ntl_g, (size_t)max_particles * sizeof(int)));
   CKC(cudaMalloc(&ctx->pcount, 4 * sizeof(unsigned int)));
@@ -725,6 +731,7 @@ static EvalArgs base_args(hp_ctx* ctx) {
   a.pcount = ctx->pcount;
   a.persist_grid = ctx->persist_grid;
   a.fk_g = ctx->fk_g;
+  a.fkx_g = ctx->fkx_g;
   a.tiles_g = ctx->tiles_g;
   a.ntl_g = ctx->ntl_g;
   a.near_list = ctx->near_list;
@@ -775,7 +782,8 @@ static hp_status eval_common(hp_ctx* ctx, const void* poses, int64_t n, float* c
   a.costs32 = costs32;
   a.costs64 = costs64;
   a.sums_out = reinterpret_cast<unsigned long long*>(sums);
-  CK(launch_eval(a, pose_double, kModeCost, &ctx->tmap, s, ctx->timing ? ctx->tev : nullptr));
+  CK(launch_eval(a, pose_double, kModeCost, &ctx->tmap, s, ctx->timing ? ctx->tev : nullptr,
+                 &ctx->tmap16));
   ctx->timed = ctx->timing;
   if (ctx->sync_debug) CK(cudaStreamSynchronize(s));
   // the batch path is three kernels (FK, the persistent renderer, its near-plane pass)

@@ -7,8 +7,9 @@ namespace hp {
 
 // ---------------------------------------------------------------------------------------
 // Two-kernel batch path for large swarms.
-//   k_fk_batch      : one warp per particle — FK (fp64) and the particle's non-empty tile
-//                     list with cull masks, written to global memory (L2-resident).
+//   k_fk_batch      : one warp per particle — FK (fp64) and the particle's list of
+//                     non-empty 16 x 16 blocks with the cull masks of their two 16 x 8
+//                     halves, written to global memory (L2-resident).
 //   k_render_persist: persistent CTAs, ALL warps render.  Per particle one thread pulls the
 //                     FK record and tile list into shared memory with 1-D TMA bulk copies
 //                     (double-buffered: particle i + 2 is fetched as soon as particle i is
@@ -29,51 +30,39 @@ constexpr int kMaxBand = 64;  // columns / rows of the per-warp band masks
 // from it (separating axis) is skipped.  Stored per cone: (n_x, n_y, n . P(J_0), R); R = inf
 // (no refinement) within 1 mm of the camera plane.  Margins: 1e-4 relative + 0.02 px for
 // the fp32 / approximate-MUFU rounding of the record and of P (~1e-6 relative).
-constexpr int kNcone = kCyl - kCone0;
-__device__ __forceinline__ float proj_radius(const float c[3], float r, float f) {
-  if (!(c[2] - r > 1.f)) return __int_as_float(0x7f800000);
-  const float R = f * r * sqrt_approx(fmaf(c[0], c[0], fmaf(c[1], c[1], c[2] * c[2]))) *
-                  rcp_approx_fk(c[2] * (c[2] - r));
-  return fmaf(R, 1.0001f, 0.02f);
-}
-__device__ __forceinline__ void build_cull_shapes(const FkOut& fo, const CamParams& cam,
-                                                  float4* shp) {
-  const int lane = threadIdx.x & 31;
-  if (lane >= kNcone) return;
-  const float* r = fo.rec[kCone0 + lane];
-  // axis row M[2] from the midpoint; the radius is r_m + k z, z in [-hl, hl]
-  const float hl = r[kHl], rm = r[kRm], k = r[kK];
-  float J0[3], J1[3];
-#pragma unroll
-  for (int i = 0; i < 3; i++) {
-    J0[i] = fmaf(-hl, r[kM + 6 + i], r[kC + i]);
-    J1[i] = fmaf(hl, r[kM + 6 + i], r[kC + i]);
+// A 16 x 8 tile's 38-bit cull mask: its column band's and row band's masks ANDed, then each
+// cone's bit cleared if its projected capsule misses the tile (separating axis).
+__device__ __forceinline__ uint2 tile_mask(uint2 c, uint2 r, int X0, int Y0, const float4* shp) {
+  unsigned int lo = c.x & r.x, hi = c.y & r.y;
+  // pixel x's centre is x + 1/2 in the projected coordinates f u + c
+  const float tcx = (float)X0 + 0.5f * kTileW, tcy = (float)Y0 + 0.5f * kTileH;
+  constexpr float hx = 0.5f * (kTileW - 1), hy = 0.5f * (kTileH - 1);
+  unsigned int cm = ((lo >> kCone0) | (hi << (32 - kCone0))) & ((1u << kNcone) - 1u);
+  for (unsigned int q = cm; q; q &= q - 1) {
+    const int j = __ffs(q) - 1;
+    const float4 sh = shp[j];
+    if (fabsf(fmaf(sh.x, tcx, fmaf(sh.y, tcy, -sh.z))) >
+        fmaf(hx, fabsf(sh.x), fmaf(hy, fabsf(sh.y), sh.w)))
+      cm &= ~(1u << j);
   }
-  const float f = fmaxf(cam.fx, cam.fy);
-  const float R = fmaxf(proj_radius(J0, fmaxf(fmaf(-k, hl, rm), 0.f), f),
-                        proj_radius(J1, fmaxf(fmaf(k, hl, rm), 0.f), f));
-  const float i0 = rcp_approx_fk(J0[2]), i1 = rcp_approx_fk(J1[2]);
-  const float p0x = fmaf(cam.fx, J0[0] * i0, cam.cx), p0y = fmaf(cam.fy, J0[1] * i0, cam.cy);
-  const float ex = fmaf(cam.fx, J1[0] * i1, cam.cx) - p0x;
-  const float ey = fmaf(cam.fy, J1[1] * i1, cam.cy) - p0y;
-  const float L = sqrt_approx(fmaf(ex, ex, ey * ey));
-  float4 o;
-  if (L > 1e-3f) {
-    const float iL = rcp_approx_fk(L);
-    o = make_float4(-ey * iL, ex * iL, (ex * p0y - ey * p0x) * iL, R);
-  } else {  // degenerate axis: a disc of radius R + L around P(J_0), tested on the x axis
-    o = make_float4(1.f, 0.f, p0x, R + L);
-  }
-  shp[lane] = o;
+  // cones are bits 20..31 of lo and 0..1 of hi
+  lo = (lo & ((1u << kCone0) - 1u)) | (cm << kCone0);
+  hi = (hi & ~((1u << (kNcone - (32 - kCone0))) - 1u)) | (cm >> (32 - kCone0));
+  return make_uint2(lo, hi);
 }
 
-__device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out, uint2* s_cm,
-                                               uint2* s_rm, const float4* shp) {
+// The particle's non-empty 16 x 16 blocks of its union grid (16 x 8 tiles, rows paired),
+// each with its two halves' masks: uint4 (X0 | Y0 << 16, top prims 0..31, bottom prims
+// 0..31, top 32..37 | bottom 32..37 << 8).  Returns the count, or -1 (too large: the
+// renderer culls per tile).
+__device__ __forceinline__ int build_block_list(const FkOut& fo, uint4* out, uint2* s_cm,
+                                                uint2* s_rm, const float4* shp) {
   const int lane = threadIdx.x & 31;
   const TileGrid g(fo.ubox);
-  if (g.ntiles > kMaxTiles || g.tx > kMaxBand) return -1;  // the renderer culls per tile
+  if (g.tx > kMaxBand) return -1;
   const int ty = g.tx > 0 ? g.ntiles / g.tx : 0;
-  if (ty > kMaxBand) return -1;
+  const int by = (ty + 1) >> 1;  // block rows
+  if (ty > kMaxBand || g.tx * by > kMaxTiles) return -1;
   // band masks by ballot: lane j holds primitive j's (and j + 32's) band ranges; one pair
   // of ballots per column / row band
   int c0[2], c1[2], r0[2], r1[2];
@@ -98,45 +87,33 @@ __device__ __forceinline__ int build_tile_list(const FkOut& fo, uint4* out, uint
     const unsigned int m1 = __ballot_sync(0xffffffffu, c0[1] <= q && q <= c1[1]);
     if (lane == 0) s_cm[q] = make_uint2(m0, m1);
   }
-  for (int q = 0; q < ty; q++) {
+  for (int q = 0; q < 2 * by; q++) {  // an odd last row of tiles pairs with an empty band
     const unsigned int m0 = __ballot_sync(0xffffffffu, r0[0] <= q && q <= r1[0]);
     const unsigned int m1 = __ballot_sync(0xffffffffu, r0[1] <= q && q <= r1[1]);
     if (lane == 0) s_rm[q] = make_uint2(m0, m1);
   }
   __syncwarp();
+  const int nb = g.tx * by;
   int cnt = 0;
-  for (int base = 0; base < g.ntiles; base += 32) {  // one tile per lane
+  for (int base = 0; base < nb; base += 32) {  // one block per lane
     const int t = base + lane;
-    unsigned int lo = 0, hi = 0;
+    uint2 top = make_uint2(0u, 0u), bot = make_uint2(0u, 0u);
     int X0 = 0, Y0 = 0;
-    if (t < g.ntiles) {
-      g.origin(t, X0, Y0);
-      HP_CHECK((X0 - g.x0) / kTileW < kMaxBand && (Y0 - g.y0) / kTileH < kMaxBand);
-      const uint2 c = s_cm[(X0 - g.x0) / kTileW], r = s_rm[(Y0 - g.y0) / kTileH];
-      lo = c.x & r.x;
-      hi = c.y & r.y;
-      // pixel x's centre is x + 1/2 in the projected coordinates f u + c
-      const float tcx = (float)X0 + 0.5f * kTileW, tcy = (float)Y0 + 0.5f * kTileH;
-      constexpr float hx = 0.5f * (kTileW - 1), hy = 0.5f * (kTileH - 1);
-      unsigned int cm = ((lo >> kCone0) | (hi << (32 - kCone0))) & ((1u << kNcone) - 1u);
-      for (unsigned int q = cm; q; q &= q - 1) {
-        const int j = __ffs(q) - 1;
-        const float4 sh = shp[j];
-        if (fabsf(fmaf(sh.x, tcx, fmaf(sh.y, tcy, -sh.z))) >
-            fmaf(hx, fabsf(sh.x), fmaf(hy, fabsf(sh.y), sh.w)))
-          cm &= ~(1u << j);
-      }
-      // cones are bits 20..31 of lo and 0..1 of hi
-      lo = (lo & ((1u << kCone0) - 1u)) | (cm << kCone0);
-      hi = (hi & ~((1u << (kNcone - (32 - kCone0))) - 1u)) | (cm >> (32 - kCone0));
+    if (t < nb) {
+      const int qy = t / g.tx, qx = t - qy * g.tx;
+      X0 = g.x0 + qx * kTileW;
+      Y0 = g.y0 + qy * kBlockH;
+      HP_CHECK(qx < kMaxBand && 2 * qy + 1 < kMaxBand);
+      const uint2 c = s_cm[qx];
+      top = tile_mask(c, s_rm[2 * qy], X0, Y0, shp);
+      bot = tile_mask(c, s_rm[2 * qy + 1], X0, Y0 + kTileH, shp);
     }
-    const unsigned int m0 = lo & 0xFFFFFu, m1 = (lo >> 20) | ((hi & 0x7u) << 12), m2 = hi >> 3;
-    const bool ne = (lo | hi) != 0;
+    const bool ne = (top.x | top.y | bot.x | bot.y) != 0;
     const unsigned int bal = __ballot_sync(0xffffffffu, ne);
     if (ne) {
       HP_CHECK(cnt + __popc(bal & ((1u << lane) - 1u)) < kMaxTiles);
       out[cnt + __popc(bal & ((1u << lane) - 1u))] =
-          make_uint4((unsigned)X0 | ((unsigned)Y0 << 16), m0, m1, m2);
+          make_uint4((unsigned)X0 | ((unsigned)Y0 << 16), top.x, bot.x, top.y | (bot.y << 8));
     }
     cnt += __popc(bal);
   }
@@ -158,9 +135,8 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
     k_fk_batch(const EvalArgs a) {
   __shared__ __align__(16) FkScratch s_fk[kFkWarps];
   __shared__ __align__(16) FkOut s_out[kFkWarps];
-  static_assert(sizeof(FkScratch) % 16 == 0, "the float4 cull shapes alias s_fk[warp]");
-  static_assert(sizeof(FkScratch) >= 2 * kMaxBand * sizeof(uint2) + kNcone * sizeof(float4),
-                "band masks and cull shapes alias s_fk");
+  __shared__ __align__(16) float4 s_shp[kFkWarps][kNcone];  // cone capsules (fk_team)
+  static_assert(sizeof(FkScratch) >= 2 * kMaxBand * sizeof(uint2), "band masks alias s_fk");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #if HP_FK_PDL
   // the renderer (launched with programmatic stream serialisation) may start its prologue
@@ -170,7 +146,8 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
   const int p = blockIdx.x * kFkWarps + warp;  // one warp per particle
   if (p >= a.n) return;  // warp-uniform; only warp-local synchronisation below
   const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
-  fk_team<PoseT, 1>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk[warp], s_out[warp]);
+  fk_team<PoseT, 1>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk[warp], s_out[warp], nullptr,
+                    s_shp[warp]);
   // the record leaves by one bulk copy while the warp builds the tile list: every lane
   // orders its record writes before the async proxy, then lane 0 issues the copy
   fence_proxy_async();
@@ -178,12 +155,15 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
   if (lane == 0)
     bulk_s2g(static_cast<FkOut*>(a.fk_g) + p, &s_out[warp], (uint32_t)sizeof(FkOut));
   FKPROF(4)
-  uint2* band = reinterpret_cast<uint2*>(&s_fk[warp]);  // FK scratch is dead by now
-  float4* shp = reinterpret_cast<float4*>(band + 2 * kMaxBand);
-  build_cull_shapes(s_out[warp], a.cam, shp);
+  // a pose that may cross z_near (rare): its EXACT records for the near-plane pass, while
+  // the FK scratch still holds its frames
+  if (!s_out[warp].near_ok) fk_warp_exact(s_fk[warp], a.dims, a.cam, static_cast<FkExact*>(a.fkx_g) + p);
   __syncwarp();
-  const int cnt = build_tile_list(s_out[warp], a.tiles_g + (size_t)p * kMaxTiles, band,
-                                  band + kMaxBand, shp);
+  uint2* band = reinterpret_cast<uint2*>(&s_fk[warp]);  // FK scratch is dead by now
+  const float4* shp = s_shp[warp];
+  __syncwarp();
+  const int cnt = build_block_list(s_out[warp], a.tiles_g + (size_t)p * kMaxTiles, band,
+                                   band + kMaxBand, shp);
   FKPROF(5)
   if (lane == 0) {
     int ntl = cnt;
@@ -199,17 +179,20 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
   FKPROF(6)
 }
 
-// NEAR = false: the batch renderer.  Particles whose FK found a primitive that may cross
-// z_near were queued by k_fk_batch (ntl = -2) and are skipped here; NEAR = true renders
-// exactly those (exact-solid path) in a second, normally empty launch, so the
-// near-plane code never shares a register allocation with the hot loop.
+// NEAR = false: the batch renderer, 16 x 16 warp blocks from k_fk_batch's block list (the
+// tensor map's box is 16 x 16).  Particles whose FK found a primitive that may cross z_near
+// were queued by k_fk_batch (ntl = -2) and are skipped here; NEAR = true renders exactly
+// those (exact-solid path from their EXACT records; 16 x 8 tiles, box 16 x 8)
+// in a second, normally empty launch, so the near-plane code never shares a register
+// allocation with the hot loop.
 template <int NW, bool NEAR, bool SUMS>
 __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     k_render_persist(const __grid_constant__ EvalArgs a,
                      const __grid_constant__ CUtensorMap tmap) {
   __shared__ __align__(16) FkOut s_out[2];
+  __shared__ __align__(16) FkExact s_x[NEAR ? 2 : 1];
   __shared__ __align__(16) uint4 s_tiles[2][NEAR ? 1 : kMaxTiles];
-  __shared__ __align__(128) uint32_t s_obs[NW][kTileW * kTileH];
+  __shared__ __align__(128) uint32_t s_obs[NW][kTileW * (NEAR ? kTileH : kBlockH)];
   __shared__ __align__(8) uint64_t s_bar[NW];
   __shared__ __align__(8) uint64_t s_full[2];
   // per-warp partial sums of the particle in slot b: r_m, o_s AND r_m, numerator lo, hi
@@ -240,9 +223,12 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
         return;
       }
       const uint32_t lb = ntl > 0 ? (uint32_t)ntl * 16u : 0u;
-      mbar_expect_tx(&s_full[b], (uint32_t)sizeof(FkOut) + lb);
+      const uint32_t xb = NEAR ? (uint32_t)sizeof(FkExact) : 0u;
+      mbar_expect_tx(&s_full[b], (uint32_t)sizeof(FkOut) + lb + xb);
       bulk_g2s(&s_out[b], static_cast<const FkOut*>(a.fk_g) + p, (uint32_t)sizeof(FkOut),
                &s_full[b]);
+      if (NEAR)
+        bulk_g2s(&s_x[NEAR ? b : 0], static_cast<const FkExact*>(a.fkx_g) + p, xb, &s_full[b]);
       if (lb) bulk_g2s(s_tiles[b], a.tiles_g + (size_t)p * kMaxTiles, lb, &s_full[b]);
     } else {
       mbar_arrive(&s_full[b]);  // terminator: complete the phase without data
@@ -300,28 +286,40 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     TileSums acc;
     if (nlist != -2) {
       const TileGrid g(fo.ubox, nlist < 0);  // the tile origins only without a list
-      const int nt = nlist >= 0 ? nlist : g.ntiles;
+      // NEAR: every 16 x 8 tile of the union grid, culled here; otherwise the block list,
+      // or (a close-up pose with more blocks than the list holds) every 16 x 16 block of
+      // the union grid, both halves culled here
+      const int nby = (g.ntiles / (g.tx > 0 ? g.tx : 1) + 1) >> 1;
+      const int nt = NEAR ? g.ntiles : (nlist >= 0 ? nlist : g.tx * nby);
       int t = 0;
       if (lane == 0) t = atomicAdd(&s_next[b], 1);
       t = __shfl_sync(0xffffffffu, t, 0);
       while (t < nt) {
         int tn = 0;
         if (lane == 0) tn = atomicAdd(&s_next[b], 1);
-        int X0, Y0;
-        uint3 km;
-        if (nlist >= 0) {
-          HP_CHECK(t >= 0 && t < kMaxTiles);
-          const uint4 it = s_tiles[b][t];
-          X0 = (int)(it.x & 0xFFFFu);
-          Y0 = (int)(it.x >> 16);
-          km = make_uint3(it.y, it.z, it.w);
-        } else {
+        if (NEAR) {
+          int X0, Y0;
           g.origin(t, X0, Y0);
-          km = cull_tile(fo, X0, Y0);
+          const uint3 km = cull_tile(fo, X0, Y0);
+          if (km.x | km.y | km.z)
+            do_tile<kModeCost, true, SUMS, 1>(a, &tmap, fo, &s_x[NEAR ? b : 0], X0, Y0, km,
+                                              obs_s, bar_s, phase, dx_s, dy_s, acc, yoff);
+        } else {
+          uint4 ent;
+          if (nlist >= 0) {
+            HP_CHECK(t >= 0 && t < kMaxTiles);
+            ent = s_tiles[b][t];
+          } else {
+            const int qy = t / g.tx, qx = t - qy * g.tx;
+            const int X0 = g.x0 + qx * kTileW, Y0 = g.y0 + qy * kBlockH;
+            const uint3 kt = cull_tile(fo, X0, Y0), kb = cull_tile(fo, X0, Y0 + kTileH);
+            ent = make_uint4((unsigned)X0 | ((unsigned)Y0 << 16), kt.x | (kt.y << 20),
+                             kb.x | (kb.y << 20),
+                             ((kt.y >> 12) | (kt.z << 3)) | (((kb.y >> 12) | (kb.z << 3)) << 8));
+          }
+          if (ent.y | ent.z | ent.w)
+            do_block<SUMS>(a, &tmap, fo, ent, obs_s, bar_s, phase, dx_s, dy_s, acc, yoff);
         }
-        if (km.x | km.y | km.z)
-          do_tile<kModeCost, NEAR, SUMS, 1>(a, &tmap, fo, X0, Y0, km, obs_s, bar_s, phase, dx_s,
-                                            dy_s, acc, yoff);
         t = __shfl_sync(0xffffffffu, tn, 0);
       }
     }

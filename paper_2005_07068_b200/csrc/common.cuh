@@ -20,7 +20,9 @@ constexpr int kRec = 24;   // floats per primitive record (96 B)
 constexpr int kPxPerLane = HP_PX;       // pixels per lane (one column, every other row)
 constexpr int kTileW = 16;              // warp tile: 16 x (2 * kPxPerLane) pixels
 constexpr int kTileH = 2 * kPxPerLane;
-constexpr int kMaxTiles = 512;          // producer tile list capacity per particle
+constexpr int kMaxTiles = 512;          // producer block list capacity per particle
+constexpr int kBlockH = 2 * kTileH;     // the batch renderer's warp block: two 16 x 8 tiles
+                                        // (top / bottom half, each with its own cull masks)
 constexpr int kRayPad = 16;             // ray-table slack for tiles overhanging the image
 static_assert(kPxPerLane == 4, "the row table packs a lane's 4 rows into one float4");
 // Ray table (k_ray_table), staged in shared memory by the evaluation kernels:
@@ -47,7 +49,7 @@ constexpr uint64_t kSphereMask = (1ull << 20) - 1;
 constexpr uint64_t kConeMask = ((1ull << 35) - 1) ^ kSphereMask;
 constexpr uint64_t kEllMask = ((1ull << 38) - 1) ^ ((1ull << 35) - 1);
 
-// Record layout, all camera frame, fp32:
+// EXACT record layout (the near-plane path, FkExact), camera frame, fp32:
 //   [0..2]  c: local origin (sphere/ellipsoid centre, cone/cylinder axis midpoint)
 //   [3]     r^2 (sphere)
 //   [4..12] M row-major: camera offset -> local (ellipsoid: diag(1/s) R^T;
@@ -55,6 +57,19 @@ constexpr uint64_t kEllMask = ((1ull << 38) - 1) ^ ((1ull << 35) - 1);
 //   [13..15] c_l = M c
 //   [16] r_mid  [17] slope k  [18] half length (cone / cylinder)
 enum RecField { kC = 0, kR2 = 3, kM = 4, kCl = 13, kRm = 16, kK = 17, kHl = 18 };
+// FAST record layout (FkOut.rec, the hot loops; DESIGN §9 "polynomial form").  Spheres keep
+// [c, r^2] (fields kC, kR2 above: the re-centred sphere test).  Ellipsoids, cones and the
+// palm cylinder: with local coordinates l = M (p - c), implicit F(l) = l'Q l + 2 g.l + h and
+// the pixel ray p = t d, d = (x, y, 1), F = 0 reads a t^2 - 2 b t + c0 = 0 with
+//   a = dl'Q dl, b = dl'Q cl - g.dl, c0 = cl'Q cl - 2 g.cl + h   (dl = M d, cl = M c),
+// entering root t = (b - sqrt(D)) / a, D = b^2 - a c0.  a and D are quadratic, b affine in
+// (x, y); FK expands them in fp64 about the projected centre (xp, yp) and stores fp32
+// coefficients of x' = x - xp, y' = y - yp (all terms O(D) over the primitive's box, so the
+// fp32 Horner evaluation does not cancel):
+//   [0] xp [1] yp  [2..7] D: d00 d10 d01 d20 d11 d02  [8..10] b: b0 bx by  [11] cl_z
+//   [12..17] a: a00 a10 a01 a20 a11 a02  [18..20] axis row of M (raw x, y, 1 coefficients:
+//   the axial coordinate at t is t (lzx x + lzy y + lz1) - cl_z)  [21] half length
+enum FastField { kFxp = 0, kFyp = 1, kFd = 2, kFb = 8, kFclz = 11, kFa = 12, kFlz = 18, kFhl = 21 };
 
 struct CamParams {
   int W, H;
@@ -136,7 +151,9 @@ struct EvalArgs {
   // two-kernel batch path: k_fk_batch writes each particle's FK output and tile list here,
   // k_render_persist bulk-copies them into shared memory
   void* fk_g;                     // FkOut [n] (16-byte aligned records)
-  uint4* tiles_g;                 // [n][kMaxTiles] (X0 | Y0 << 16, sphere, cone, ell masks)
+  void* fkx_g;                    // FkExact [n]: exact records, written for near-plane poses
+  uint4* tiles_g;                 // [n][kMaxTiles] 16x16 blocks: X0 | Y0 << 16, the top
+                                  // half's prims 0..31, the bottom's, both halves' 32..37
   int* ntl_g;                     // [n] tile-list length (-1: box too large, cull on the fly;
                                   // -2: queued for the near-plane pass)
   int* near_list;                 // [n] particles whose primitives may cross z_near
@@ -321,8 +338,11 @@ cudaError_t launch_unpack_obs(const uint32_t* obs, int W, int H, int pitch_words
                               uint8_t* mask, cudaStream_t st);
 // tev (optional, 3 events): recorded before the first launch, between the two launches of
 // the batch path, and after the last (hp_set_timing); null when timing is off
+// map: 16 x 8 observation boxes (k_eval, the near-plane pass); map16: 16 x 16 (the batch
+// renderer's blocks; null = map, only for paths that never take the batch renderer)
 cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUtensorMap* map,
-                        cudaStream_t st, cudaEvent_t* tev = nullptr);
+                        cudaStream_t st, cudaEvent_t* tev = nullptr,
+                        const CUtensorMap* map16 = nullptr);
 cudaError_t launch_fk_debug(const double* pose_dev, const DimsD& dims, const CamParams& cam,
                             float* rec, int* boxes, double* joints, double* kc,
                             cudaStream_t st);
@@ -331,6 +351,7 @@ cudaError_t launch_depth_to_mask(const float* depth, uint8_t* mask, int npx, cud
 int persist_blocks_per_sm(const CamParams& cam);
 int eval_blocks_per_sm(const CamParams& cam);  // resident k_eval CTAs per SM
 size_t fk_record_bytes();
+size_t fk_exact_bytes();
 
 // PSO (pso.cu)
 cudaError_t launch_pso_init(const PsoDev& p, cudaStream_t st);

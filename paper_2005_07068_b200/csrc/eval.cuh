@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
     k_eval(const __grid_constant__ EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
   __shared__ FkScratch s_fk;
   __shared__ __align__(16) FkOut s_out;
+  __shared__ __align__(16) FkExact s_x;  // exact records: the near-plane tile loop's
   __shared__ __align__(128) uint32_t s_obs[NW][kTileW * kTileH];
   __shared__ __align__(8) uint64_t s_bar[NW];
   __shared__ unsigned long long s_red[NW][4];
@@ -48,10 +49,12 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
         pso_update_warp(a.pso, p, a.pso_k, a.x_in, a.v_in, a.x_out, a.v_out, sidx == 0, s_pose,
                         /*deferred=*/true);
       __syncwarp();
-      fk_team<double, kEvalFkTeam>(s_pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
+      fk_team<double, kEvalFkTeam>(s_pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out,
+                                   NEARCODE ? &s_x : nullptr);
     } else {
       const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
-      fk_team<PoseT, kEvalFkTeam>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out);
+      fk_team<PoseT, kEvalFkTeam>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out,
+                                  NEARCODE ? &s_x : nullptr);
     }
   } else {
     // while the FK team runs: stage the per-column / per-row ray directions (k_ray_table)
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
   const TileGrid g(s_out.ubox);
   // this CTA owns tiles sidx, sidx + S, ...; warps take them dynamically (load balance)
   const int nmine = g.ntiles > sidx ? (g.ntiles - sidx + a.S - 1) / a.S : 0;
-  TileSums acc = run_tiles<MODE, NEARCODE>(a, &tmap, s_out, nullptr, -1, sidx, a.S, nmine,
+  TileSums acc = run_tiles<MODE, NEARCODE>(a, &tmap, s_out, &s_x, sidx, a.S, nmine,
                                            &s_next, smem_u32(s_obs[warp]),
                                            smem_u32(&s_bar[warp]), 0u, s_dx, s_dy,
                                            frame_of(a, p) * a.cam.H)

@@ -19,8 +19,13 @@ struct FkScratch {
   int nearf[kNprim];        // primitive lies entirely beyond z_near
 };
 
-struct __align__(16) FkOut {
+// Exact records (common.cuh EXACT layout): only the near-plane path reads them.
+struct __align__(16) FkExact {
   float rec[kNprim][kRec];
+};
+
+struct __align__(16) FkOut {
+  float rec[kNprim][kRec];  // FAST layout (common.cuh)
   int4 box[kNprim];  // x0, y0, x1, y1 inclusive; x0 > x1 = empty
   int4 ubox;
   double kc;
@@ -136,25 +141,120 @@ __device__ __forceinline__ int4 prim_box(int ng, const float c[2][3], const floa
   return finish_box(any, full, u0, u1, v0, v1, cam);
 }
 
+// Tile-list cull shape of a cone (k_fk_batch): a point p with |p - c| <= r projects within
+// R = f r |c| / (c_z (c_z - r)) px of the projection P(c) (f = max(f_x, f_y); the image-plane
+// offset is M (p - c) / (c_z (c_z + (p - c)_z)) with M = [[c_z, 0, -c_x], [0, c_z, -c_y]],
+// whose largest singular value is |c|).  A cone — the convex hull of its two end discs —
+// therefore lies in the 2-D capsule of radius max(R_0, R_1) around the segment
+// P(J_0) P(J_1), and a tile whose rectangle projects on the segment's normal farther than R
+// from it (separating axis) is skipped.  Stored per cone: (n_x, n_y, n . P(J_0), R); R = inf
+// (no refinement) within 1 mm of the camera plane.  Margins: 1e-4 relative + 0.02 px for
+// the fp32 / approximate-MUFU rounding of P (~1e-6 relative).
+constexpr int kNcone = kCyl - kCone0;
+__device__ __forceinline__ float proj_radius(const float c[3], float r, float f) {
+  if (!(c[2] - r > 1.f)) return __int_as_float(0x7f800000);
+  const float R = f * r * sqrt_approx(fmaf(c[0], c[0], fmaf(c[1], c[1], c[2] * c[2]))) *
+                  rcp_approx_fk(c[2] * (c[2] - r));
+  return fmaf(R, 1.0001f, 0.02f);
+}
+__device__ __forceinline__ float4 cone_capsule(const float J0[3], const float J1[3], float r0,
+                                               float r1, const CamParams& cam) {
+  const float f = fmaxf(cam.fx, cam.fy);
+  const float R = fmaxf(proj_radius(J0, r0, f), proj_radius(J1, r1, f));
+  const float i0 = rcp_approx_fk(J0[2]), i1 = rcp_approx_fk(J1[2]);
+  const float p0x = fmaf(cam.fx, J0[0] * i0, cam.cx), p0y = fmaf(cam.fy, J0[1] * i0, cam.cy);
+  const float ex = fmaf(cam.fx, J1[0] * i1, cam.cx) - p0x;
+  const float ey = fmaf(cam.fy, J1[1] * i1, cam.cy) - p0y;
+  const float L = sqrt_approx(fmaf(ex, ex, ey * ey));
+  if (L > 1e-3f) {
+    const float iL = rcp_approx_fk(L);
+    return make_float4(-ey * iL, ex * iL, (ex * p0y - ey * p0x) * iL, R);
+  }
+  return make_float4(1.f, 0.f, p0x, R + L);  // degenerate axis: a disc of radius R + L
+}
+
 __device__ __forceinline__ void put3(float* r, int off, const double v[3]) {
   r[off + 0] = (float)v[0];
   r[off + 1] = (float)v[1];
   r[off + 2] = (float)v[2];
 }
 
-// Build record + box of device primitive j (see common.cuh for the order).
-__device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const CamParams& cam,
-                           float* rec, int4& box, float& zmin) {
+// FAST record of a quadric primitive (common.cuh "FAST record layout"): local origin cen,
+// rows of M, Q = diag(q), g = (0, 0, g2), h; fp64 throughout, fp32 coefficients out.  The
+// expansion point is the projection of cen, rounded to fp32 first so the coefficients
+// belong to the point the kernel subtracts.  axis (may be null): the axial row of M and
+// the half length (cones / cylinder).
+__device__ __noinline__ void write_fast_quadric(float* rec, const double cen[3], const double M[3][3],
+                                   const double q[3], double g2, double h, bool axial,
+                                   double hl) {
+  double cl[3];
+  for (int a = 0; a < 3; a++) cl[a] = M[a][0] * cen[0] + M[a][1] * cen[1] + M[a][2] * cen[2];
+  float xp = 0.f, yp = 0.f;
+  if (cen[2] > 1e-3) {
+    xp = (float)(cen[0] / cen[2]);
+    yp = (float)(cen[1] / cen[2]);
+  }
+  const double dp[3] = {(double)xp, (double)yp, 1.0};
+  double m0[3], m1[3], dl[3];
+  for (int a = 0; a < 3; a++) {
+    m0[a] = M[a][0];
+    m1[a] = M[a][1];
+    dl[a] = M[a][0] * dp[0] + M[a][1] * dp[1] + M[a][2];
+  }
+  auto QX = [&](const double u[3], const double v[3]) {
+    return q[0] * u[0] * v[0] + q[1] * u[1] * v[1] + q[2] * u[2] * v[2];
+  };
+  const double A[6] = {QX(dl, dl), 2.0 * QX(m0, dl), 2.0 * QX(m1, dl),
+                       QX(m0, m0), 2.0 * QX(m0, m1), QX(m1, m1)};
+  const double b0 = QX(dl, cl) - g2 * dl[2], bx = QX(m0, cl) - g2 * m0[2],
+               by = QX(m1, cl) - g2 * m1[2];
+  const double c0 = QX(cl, cl) - 2.0 * g2 * cl[2] + h;
+  const double D[6] = {b0 * b0 - c0 * A[0],       2.0 * b0 * bx - c0 * A[1],
+                       2.0 * b0 * by - c0 * A[2], bx * bx - c0 * A[3],
+                       2.0 * bx * by - c0 * A[4], by * by - c0 * A[5]};
+  rec[kFxp] = xp;
+  rec[kFyp] = yp;
+  for (int i = 0; i < 6; i++) {
+    rec[kFd + i] = (float)D[i];
+    rec[kFa + i] = (float)A[i];
+  }
+  rec[kFb + 0] = (float)b0;
+  rec[kFb + 1] = (float)bx;
+  rec[kFb + 2] = (float)by;
+  rec[kFclz] = (float)cl[2];
+  if (axial) {
+    rec[kFlz + 0] = (float)M[2][0];
+    rec[kFlz + 1] = (float)M[2][1];
+    rec[kFlz + 2] = (float)M[2][2];
+    rec[kFhl] = (float)hl;
+  }
+}
+
+// Records + box of device primitive j (see common.cuh for the order): `fast` (FAST layout,
+// may be null), `exact` (EXACT layout, may be null), `box` (may be null; then zmin is not
+// computed either).
+// shape (may be null): a cone's tile-list capsule (cone_capsule).
+__device__ __noinline__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const CamParams& cam,
+                           float* fast, float* exact, int4* box, float& zmin,
+                           float4* shape = nullptr) {
+  float* rec = exact;  // the exact record (written only when requested)
+  if (rec)
 #pragma unroll
-  for (int i = 0; i < kRec; i++) rec[i] = 0.f;
+    for (int i = 0; i < kRec; i++) rec[i] = 0.f;
   float gc[2][3], gA[2][3][3];
   int ng = 0;
   if (j < kCone0) {  // sphere at joint (f, k)
     int f = j >> 2, k = j & 3;
     double r = dm.rad[f][k];
     const double* c = s.J[f][k];
-    put3(rec, kC, c);
-    rec[kR2] = (float)(r * r);
+    if (rec) {
+      put3(rec, kC, c);
+      rec[kR2] = (float)(r * r);
+    }
+    if (fast) {  // spheres keep the re-centred test: the fast record is the exact one's head
+      put3(fast, kC, c);
+      fast[kR2] = (float)(r * r);
+    }
     for (int i = 0; i < 3; i++) gc[0][i] = (float)c[i];
     for (int a = 0; a < 3; a++)
       for (int b = 0; b < 3; b++) gA[0][a][b] = (a == b) ? (float)(r * r) : 0.f;
@@ -179,20 +279,28 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
       e2[i] = s.Rs[f][k][i][2];
       m[i] = 0.5 * (J0[i] + J1[i]);
     }
-    put3(rec, kC, m);
     double rows[3][3] = {{e1[0], e1[1], e1[2]}, {e2[0], e2[1], e2[2]}, {ax[0], ax[1], ax[2]}};
-    for (int a = 0; a < 3; a++) {
-      put3(rec, kM + 3 * a, rows[a]);
-      rec[kCl + a] = (float)(rows[a][0] * m[0] + rows[a][1] * m[1] + rows[a][2] * m[2]);
+    if (rec) {
+      put3(rec, kC, m);
+      for (int a = 0; a < 3; a++) {
+        put3(rec, kM + 3 * a, rows[a]);
+        rec[kCl + a] = (float)(rows[a][0] * m[0] + rows[a][1] * m[1] + rows[a][2] * m[2]);
+      }
+      rec[kRm] = (float)(0.5 * (r0 + r1));
+      rec[kK] = (float)dm.cone_k[f][k];
+      rec[kHl] = (float)(0.5 * L);
     }
-    rec[kRm] = (float)(0.5 * (r0 + r1));
-    rec[kK] = (float)dm.cone_k[f][k];
-    rec[kHl] = (float)(0.5 * L);
+    if (fast) {  // x^2 + y^2 - (r_m + k z)^2: Q = diag(1, 1, -k^2), g = (0, 0, -r_m k), h = -r_m^2
+      const double rm = 0.5 * (r0 + r1), kk = dm.cone_k[f][k];
+      const double q[3] = {1.0, 1.0, -kk * kk};
+      write_fast_quadric(fast, m, rows, q, -rm * kk, -rm * rm, true, 0.5 * L);
+    }
     float axf[3] = {(float)ax[0], (float)ax[1], (float)ax[2]};
     for (int i = 0; i < 3; i++) {
       gc[0][i] = (float)J0[i];
       gc[1][i] = (float)J1[i];
     }
+    if (shape) *shape = cone_capsule(gc[0], gc[1], (float)r0, (float)r1, cam);
     disc_shape(axf, (float)r0, gA[0]);
     disc_shape(axf, (float)r1, gA[1]);
     ng = 2;
@@ -204,7 +312,6 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
       cz[i] = s.RW[i][2];
       m[i] = s.h[i] - 0.5 * dm.palm_len * cy[i];
     }
-    put3(rec, kC, m);
     double rows[3][3];
     const double iw = 1.0 / dm.palm_half_w, it = 1.0 / dm.palm_half_t;
     for (int i = 0; i < 3; i++) {
@@ -212,13 +319,20 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
       rows[1][i] = cz[i] * it;
       rows[2][i] = cy[i];
     }
-    for (int a = 0; a < 3; a++) {
-      put3(rec, kM + 3 * a, rows[a]);
-      rec[kCl + a] = (float)(rows[a][0] * m[0] + rows[a][1] * m[1] + rows[a][2] * m[2]);
+    if (rec) {
+      put3(rec, kC, m);
+      for (int a = 0; a < 3; a++) {
+        put3(rec, kM + 3 * a, rows[a]);
+        rec[kCl + a] = (float)(rows[a][0] * m[0] + rows[a][1] * m[1] + rows[a][2] * m[2]);
+      }
+      rec[kRm] = 1.f;
+      rec[kK] = 0.f;
+      rec[kHl] = (float)(0.5 * dm.palm_len);
     }
-    rec[kRm] = 1.f;
-    rec[kK] = 0.f;
-    rec[kHl] = (float)(0.5 * dm.palm_len);
+    if (fast) {  // (x/a)^2 + (z/b)^2 - 1 in the scaled rows: Q = diag(1, 1, 0), h = -1
+      const double q[3] = {1.0, 1.0, 0.0};
+      write_fast_quadric(fast, m, rows, q, 0.0, -1.0, true, 0.5 * dm.palm_len);
+    }
     float cols[3][3], sd[3] = {(float)dm.palm_half_w, 0.f, (float)dm.palm_half_t};
     for (int i = 0; i < 3; i++) {
       cols[0][i] = (float)cx[i];
@@ -249,12 +363,21 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
       sd[1] = dm.cap_half;
       sd[2] = dm.palm_half_t;
     }
-    put3(rec, kC, c);
+    double rows[3][3];
     for (int a = 0; a < 3; a++) {
       const double is = 1.0 / sd[a];
-      double row[3] = {cols[a][0] * is, cols[a][1] * is, cols[a][2] * is};
-      put3(rec, kM + 3 * a, row);
-      rec[kCl + a] = (float)(row[0] * c[0] + row[1] * c[1] + row[2] * c[2]);
+      for (int i = 0; i < 3; i++) rows[a][i] = cols[a][i] * is;
+    }
+    if (rec) {
+      put3(rec, kC, c);
+      for (int a = 0; a < 3; a++) {
+        put3(rec, kM + 3 * a, rows[a]);
+        rec[kCl + a] = (float)(rows[a][0] * c[0] + rows[a][1] * c[1] + rows[a][2] * c[2]);
+      }
+    }
+    if (fast) {  // |l|^2 - 1
+      const double q[3] = {1.0, 1.0, 1.0};
+      write_fast_quadric(fast, c, rows, q, 0.0, -1.0, false, 0.0);
     }
     float colf[3][3], sdf[3] = {(float)sd[0], (float)sd[1], (float)sd[2]};
     for (int a = 0; a < 3; a++)
@@ -263,7 +386,7 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const Cam
     shape_from_axes(colf, sdf, gA[0]);
     ng = 1;
   }
-  box = prim_box(ng, gc, gA, cam, zmin);
+  if (box) *box = prim_box(ng, gc, gA, cam, zmin);
 }
 
 // FK on a team of 1 or 2 warps (warp 0 = the team leader).  pose: 26 values (float or
@@ -283,9 +406,12 @@ __device__ unsigned long long g_fkprof[16];
 #else
 #define FKPROF(i)
 #endif
+// xrec (may be null): also write the EXACT records (the near-plane path's).
+// shp (may be null): the cones' tile-list capsules [kNcone] (cone_capsule).
 template <typename PoseT, int TEAM>
 __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam,
-                        double kc_rest, FkScratch& s, FkOut& out) {
+                        double kc_rest, FkScratch& s, FkOut& out, FkExact* xrec = nullptr,
+                        float4* shp = nullptr) {
   FKPROF(0)
   static_assert(TEAM >= 1 && TEAM <= 3, "FK teams of 1..3 warps (warps 0..TEAM-1 of the CTA)");
   const int lane = threadIdx.x & 31, w = TEAM >= 2 ? (int)(threadIdx.x >> 5) : 0;
@@ -369,7 +495,8 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
     const int j = j0 + lane;
     if (j < j1) {
       float zmin;
-      build_prim(j, s, dm, cam, out.rec[j], out.box[j], zmin);
+      build_prim(j, s, dm, cam, out.rec[j], xrec ? xrec->rec[j] : nullptr, &out.box[j], zmin,
+                 shp && j >= kCone0 && j < kCyl ? shp + (j - kCone0) : nullptr);
       s.nearf[j] = zmin > cam.znear * 1.001f;
     }
     if (w != 0) {
@@ -386,7 +513,8 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
     for (int k = 0; k < nj; k++) {
       const int j = lane < 10 ? 2 * lane + k : lane + 10;
       float zmin;
-      build_prim(j, s, dm, cam, out.rec[j], out.box[j], zmin);
+      build_prim(j, s, dm, cam, out.rec[j], xrec ? xrec->rec[j] : nullptr, &out.box[j], zmin,
+                 shp && j >= kCone0 && j < kCyl ? shp + (j - kCone0) : nullptr);
       s.nearf[j] = zmin > cam.znear * 1.001f;
     }
     __syncwarp();
@@ -431,8 +559,22 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
 
 template <typename PoseT>
 __device__ __forceinline__ void fk_warp(const PoseT* pose, const DimsD& dm, const CamParams& cam,
-                                        double kc_rest, FkScratch& s, FkOut& out) {
-  fk_team<PoseT, 1>(pose, dm, cam, kc_rest, s, out);
+                                        double kc_rest, FkScratch& s, FkOut& out,
+                                        FkExact* xrec = nullptr) {
+  fk_team<PoseT, 1>(pose, dm, cam, kc_rest, s, out, xrec);
+}
+
+// After fk_warp on a pose that is not near_ok: its EXACT records straight to global memory
+// (the FK scratch must still hold the pose's frames).  Same lane map as fk_team<1>.
+__device__ __forceinline__ void fk_warp_exact(const FkScratch& s, const DimsD& dm,
+                                              const CamParams& cam, FkExact* xg) {
+  const int lane = threadIdx.x & 31;
+  const int nj = lane < 10 ? 2 : (lane < 28 ? 1 : 0);
+  for (int k = 0; k < nj; k++) {
+    const int j = lane < 10 ? 2 * lane + k : lane + 10;
+    float zmin;
+    build_prim(j, s, dm, cam, nullptr, xg->rec[j], nullptr, zmin);
+  }
 }
 
 }  // namespace hp

@@ -214,6 +214,7 @@ static void set_carveouts() {
 }
 
 size_t fk_record_bytes() { return sizeof(FkOut); }
+size_t fk_exact_bytes() { return sizeof(FkExact); }
 
 int eval_blocks_per_sm(const CamParams& cam) {
   set_carveouts();
@@ -280,7 +281,8 @@ cudaError_t launch_depth_to_mask(const float* depth, uint8_t* mask, int npx, cud
 }
 
 cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUtensorMap* map,
-                        cudaStream_t st, cudaEvent_t* tev) {
+                        cudaStream_t st, cudaEvent_t* tev, const CUtensorMap* map16) {
+  if (!map16) map16 = map;
   const long long blocks = (long long)a.n * a.S;
   if (blocks == 0) return cudaSuccess;
   const bool two = mode == kModeCost && a.S == 1 && a.persist_grid > 0;
@@ -311,8 +313,8 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const bool sums = a.sums_out != nullptr;
-    e = sums ? cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, false, true>, a, *map)
-             : cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, false, false>, a, *map);
+    e = sums ? cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, false, true>, a, *map16)
+             : cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, false, false>, a, *map16);
     if (e != cudaSuccess) return e;
     // the near-plane pass (exits at once when k_fk_batch queued nothing)
     cfg.gridDim = dim3((unsigned)(pgrid.x < 148u ? pgrid.x : 148u));
@@ -321,11 +323,11 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     if (e != cudaSuccess) return e;
 #else
     if (a.sums_out) {
-      k_render_persist<kRenderWarps, false, true><<<pgrid, rblock, dyn, st>>>(a, *map);
+      k_render_persist<kRenderWarps, false, true><<<pgrid, rblock, dyn, st>>>(a, *map16);
       k_render_persist<kRenderWarps, true, true><<<dim3(pgrid.x < 148u ? pgrid.x : 148u), rblock,
                                                  dyn, st>>>(a, *map);
     } else {
-      k_render_persist<kRenderWarps, false, false><<<pgrid, rblock, dyn, st>>>(a, *map);
+      k_render_persist<kRenderWarps, false, false><<<pgrid, rblock, dyn, st>>>(a, *map16);
       k_render_persist<kRenderWarps, true, false><<<dim3(pgrid.x < 148u ? pgrid.x : 148u), rblock,
                                                   dyn, st>>>(a, *map);
     }

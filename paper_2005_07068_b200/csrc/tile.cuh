@@ -1,4 +1,4 @@
-// tile.cuh — the per-pixel analytic ray casting (packed fp32x2), the warp tile (TMA observation load, cull masks, min depth, scoring) and the cost finalisation shared by the renderers
+// tile.cuh — the per-pixel analytic ray casting (packed fp32x2), the warp tile / warp block (TMA observation load, cull masks, min depth, scoring) and the cost finalisation shared by the renderers
 // Part of the single translation unit kernels.cu (included after the observation kernels;
 // shares its macros and helpers).
 #pragma once
@@ -248,39 +248,98 @@ __device__ __forceinline__ void isect_cone(const float* __restrict__ r, Lane4& L
   }
 }
 
-// The palm's elliptic cylinder on the fast path: the cone formulas with k = 0 in its scaled
-// coordinates (g = r_m, no k terms), entering root only (its end discs are the equators of
-// the cap ellipsoids).  It covers ~30 % of the cone loop's tile tests at C4.
-__device__ __forceinline__ void isect_cyl_fast(const float* __restrict__ r, Lane4& L) {
-  const float4 r0 = *reinterpret_cast<const float4*>(r + 0);
-  const float4 r1 = *reinterpret_cast<const float4*>(r + 4);
-  const float4 r2 = *reinterpret_cast<const float4*>(r + 8);
-  const float4 r3 = *reinterpret_cast<const float4*>(r + 12);
-  const float4 r4 = *reinterpret_cast<const float4*>(r + 16);  // rm, k (= 0), hl, -
-  const float px = fmaf(r1.x, L.dx, r1.z), py = fmaf(r1.w, L.dx, r2.y),
-              pz = fmaf(r2.z, L.dx, r3.x);
-  const float bx = fmaf(L.dx, r0.x, r0.z);
-  const float nrm2 = -r4.x * r4.x, hl = r4.z;
-#pragma unroll
-  for (int j = 0; j < kPxPerLane / 2; j++) {
-    const f2 dy = L.dy[j];
-    const f2 tc = mul2(fma2(dy, bc(r0.y), bc(bx)), L.idd[j]);
-    const f2 lx = fma2(bc(r1.y), dy, bc(px)), ly = fma2(bc(r2.x), dy, bc(py)),
-             lz = fma2(bc(r2.w), dy, bc(pz));
-    const f2 ox = fma2(tc, lx, bc(-r3.y)), oy = fma2(tc, ly, bc(-r3.z)),
-             oz = fma2(tc, lz, bc(-r3.w));
-    const f2 A = fma2(lx, lx, mul2(ly, ly));
-    const f2 B = fma2(ox, lx, mul2(oy, ly));
-    const f2 C = fma2(ox, ox, fma2(oy, oy, bc(nrm2)));
-    const f2 disc = sub2(mul2(B, B), mul2(A, C));
-    const f2 s = mul2(add2(B, sqrt2(disc)), nrcp2(A));  // NaN when disc < 0
-    float za0, za1, z0, z1;
-    unpk(fma2(s, lz, oz), za0, za1);
-    unpk(add2(tc, s), z0, z1);
-    const float nan = __int_as_float(0x7fc00000);
-    keep<false>(fabsf(za0) <= hl ? z0 : nan, L.zb[2 * j], 0.f);
-    keep<false>(fabsf(za1) <= hl ? z1 : nan, L.zb[2 * j + 1], 0.f);
+// 1/x of both halves (one MUFU.RCP each)
+__device__ __forceinline__ f2 rcp2(f2 x) {
+  float a, b;
+  unpk(x, a, b);
+  return pk(rcp_approx(a), rcp_approx(b));
+}
+
+// ---------------------------------------------------------------------------------------
+// Fast path, ellipsoids / cones / the palm cylinder: the polynomial form (common.cuh FAST
+// record layout).  Per lane (one column x): x' = x - xp and the y-Horner coefficients of D
+// and a, b's affine part; per pixel pair: y' = y - yp, D, a by Horner in y', b, the entering
+// root t = (b - sqrt(D)) / a — 10 packed fp32x2 instructions and 4 MUFU for a cone pair
+// against 29 + 4 for the re-centred form it replaces.  For a < 0 (a ray inside a cone's
+// opening) this is the larger root, the entering one of the infinite solid; whenever it
+// lies outside the axial range the ray enters the finite solid through a cap disc, which
+// is the equator of a joint sphere / cap ellipsoid hit first, so the min over
+// primitives is unchanged.  NaN (no real root, or outside the axial range) never wins.
+// ---------------------------------------------------------------------------------------
+struct QuadLane {
+  float yp, d02, a02, by, ed0, ed1, ea0, ea1, eb0;
+  float lzy, lzl, nclz, hl;  // axial (cones / cylinder)
+};
+template <bool AXIAL>
+__device__ __forceinline__ QuadLane quad_lane(const float* __restrict__ r, float dx) {
+  const float4 r0 = *reinterpret_cast<const float4*>(r + 0);   // xp yp d00 d10
+  const float4 r1 = *reinterpret_cast<const float4*>(r + 4);   // d01 d20 d11 d02
+  const float4 r2 = *reinterpret_cast<const float4*>(r + 8);   // b0 bx by clz
+  const float4 r3 = *reinterpret_cast<const float4*>(r + 12);  // a00 a10 a01 a20
+  float a11, a02;
+  QuadLane q;
+  if (AXIAL) {
+    const float4 r4 = *reinterpret_cast<const float4*>(r + 16);  // a11 a02 lzx lzy
+    const float2 r5 = *reinterpret_cast<const float2*>(r + 20);  // lz1 hl
+    a11 = r4.x;
+    a02 = r4.y;
+    q.lzy = r4.w;
+    q.lzl = fmaf(r4.z, dx, r5.x);
+    q.nclz = -r2.w;
+    q.hl = r5.y;
+  } else {
+    const float2 r4 = *reinterpret_cast<const float2*>(r + 16);  // a11 a02
+    a11 = r4.x;
+    a02 = r4.y;
   }
+  const float xq = dx - r0.x;
+  q.yp = r0.y;
+  q.d02 = r1.w;
+  q.a02 = a02;
+  q.by = r2.z;
+  q.ed0 = fmaf(fmaf(r1.y, xq, r0.w), xq, r0.z);
+  q.ed1 = fmaf(r1.z, xq, r1.x);
+  q.ea0 = fmaf(fmaf(r3.w, xq, r3.y), xq, r3.x);
+  q.ea1 = fmaf(a11, xq, r3.z);
+  q.eb0 = fmaf(r2.y, xq, r2.x);
+  return q;
+}
+// One pixel pair (rows dy) of a quadric: the entering-root depth, NaN if none.
+template <bool AXIAL>
+__device__ __forceinline__ void quad_pair(const QuadLane& q, f2 dy, float& zb0, float& zb1) {
+  const f2 yq = sub2(dy, bc(q.yp));
+  const f2 D = fma2(fma2(bc(q.d02), yq, bc(q.ed1)), yq, bc(q.ed0));
+  const f2 A = fma2(fma2(bc(q.a02), yq, bc(q.ea1)), yq, bc(q.ea0));
+  const f2 B = fma2(bc(q.by), yq, bc(q.eb0));
+  const f2 t = mul2(sub2(B, sqrt2(D)), rcp2(A));
+  if (AXIAL) {
+    const f2 za = fma2(t, fma2(bc(q.lzy), dy, bc(q.lzl)), bc(q.nclz));
+    float za0, za1, t0, t1;
+    unpk(za, za0, za1);
+    unpk(t, t0, t1);
+    const float nan = __int_as_float(0x7fc00000);
+    zb0 = fminf(zb0, fabsf(za0) <= q.hl ? t0 : nan);
+    zb1 = fminf(zb1, fabsf(za1) <= q.hl ? t1 : nan);
+  } else {
+    float t0, t1;
+    unpk(t, t0, t1);
+    zb0 = fminf(zb0, t0);
+    zb1 = fminf(zb1, t1);
+  }
+}
+// The re-centred sphere test on one pixel pair (rows dy, 1 / |d|^2 idd; bx = dx c_x + c_z).
+__device__ __forceinline__ void sphere_pair(const float4 q, float dx, float bx, f2 dy, f2 idd,
+                                            float& zb0, float& zb1) {
+  const f2 tc = mul2(fma2(dy, bc(q.y), bc(bx)), idd);
+  const f2 ox = fma2(tc, bc(dx), bc(-q.x)), oy = fma2(tc, dy, bc(-q.y));
+  const f2 oz = add2(tc, bc(-q.z));
+  const f2 m = mul2(fma2(ox, ox, fma2(oy, oy, fma2(oz, oz, bc(-q.w)))), idd);
+  float m0, m1;
+  unpk(m, m0, m1);
+  float z0, z1;
+  unpk(fma2(m, pk(rsqrt_approx(-m0), rsqrt_approx(-m1)), tc), z0, z1);
+  zb0 = fminf(zb0, z0);
+  zb1 = fminf(zb1, z1);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -334,16 +393,58 @@ __device__ __forceinline__ uint3 cull_tile(const FkOut& fo, int X0, int Y0) {
   return make_uint3(lo & 0xFFFFFu, (lo >> 20) | ((hi & 0x7u) << 12), hi >> 3);
 }
 
-// BOTH: count the both-defined pixels (only the hp_eval_sums test hook reports them; the
-// cost needs just the r_m and o_s AND r_m counts and the numerator).
-// TMA: the observation-tile load, a.use_tma at run time (-1) or fixed at compile time (1:
-// TMA from the kernel-parameter descriptor — the persistent renderer).
+// Scoring of a lane's NPX pixels (rows rowb + 2 q of its column col in the observation
+// tile, ROWS rows of 16 words): r_m, o_s AND r_m, the clamped |o_d - r_d| numerator and
+// (BOTH) the both-defined count (AMB-1, -3, -4, -5).  Skipped for tiles where
+// nothing rendered.
+template <int NPX, bool BOTH>
+__device__ __forceinline__ void score_lane(const EvalArgs& a, const float* zb, uint32_t obs_s,
+                                           int col, int rowb, TileSums& acc) {
+  const float zfar = a.cam.zfar;
+  const float d_m = a.cost.d_m, clampv = a.cost.clampv;
+  const float qscale = a.cost.qscale, qmagic = a.cost.qmagic;
+  bool any = false;
+#pragma unroll
+  for (int q = 0; q < NPX; q++) any |= zb[q] <= zfar;
+  if (__any_sync(0xffffffffu, any)) {  // nothing rendered in this tile: nothing to score
+    // numerator: round(min(|dd|, clamp) 2^qbits) from the bits of an fp32 magic-number
+    // FFMA (exact: the sum lies in [2^23, 2^24], ulp 1), summed mod 2^32 and un-biased
+    // once (the true per-lane sum is < NPX * 2^22); no float-to-int conversion on the XU
+    unsigned int num = 0u - (unsigned)NPX * __float_as_uint(qmagic);
+#pragma unroll
+    for (int q = 0; q < NPX; q++) {
+      const uint32_t w = lds_u32(obs_s + 4u * ((rowb + 2 * q) * kTileW + col));
+      // o_d undefined is stored as NaN (kObsUndef), so diff is NaN exactly there; bit 31
+      // (o_s) is the float's sign, dropped by the absolute value
+      const float diff = fabsf(fabsf(__uint_as_float(w)) - zb[q]);
+      // off-image pixels have NaN rays and never hit (k_ray_table)
+      const bool hit = zb[q] <= zfar;
+      // r_m = 1 where |r_d - o_d| < d_m or o_d undefined (AMB-4, AMB-5):
+      // !(diff >= d_m) is true for NaN
+      const unsigned int rm = hit & !(diff >= d_m);
+      const bool both = hit & (diff == diff);
+      acc.rm += rm;
+      acc.and_ += rm & (w >> 31);
+      if (BOTH) acc.both += both;
+      num += __float_as_uint(fmaf(both ? fminf(diff, clampv) : 0.f, qscale, qmagic));
+    }
+    acc.num += num;
+  }
+}
+
+// One warp tile of 16 x 8 pixels (k_eval, the near-plane pass, the depth hooks): TMA the
+// observation tile, ray-cast the culled primitives, min depth, score.  Lane: column
+// lane & 15, rows lane >> 4 + {0, 2, 4, 6}.
+// CHK = false: the FAST records of fo (the hot path); CHK = true: exact solid semantics
+// near the camera from the EXACT records xr (instantiated only out of line, tiles_near).
+// BOTH: count the both-defined pixels (only the hp_eval_sums test hook reports them).
+// TMA: the observation-tile load, a.use_tma at run time (-1) or fixed at compile time (1).
 template <int MODE, bool CHK, bool BOTH = true, int TMA = -1>
 __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tmap,
-                                        const FkOut& fo, int X0, int Y0, uint3 km,
-                                        uint32_t obs_s, uint32_t bar_s, uint32_t& phase,
-                                        uint32_t dx_s, uint32_t dy_s, TileSums& acc,
-                                        int yoff = 0) {
+                                        const FkOut& fo, const FkExact* xr, int X0, int Y0,
+                                        uint3 km, uint32_t obs_s, uint32_t bar_s,
+                                        uint32_t& phase, uint32_t dx_s, uint32_t dy_s,
+                                        TileSums& acc, int yoff = 0) {
   const int lane = threadIdx.x & 31;
   const int col = lane & 15, rowb = lane >> 4;
   const float znear = a.cam.znear, zfar = a.cam.zfar;
@@ -376,17 +477,31 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
     L.zb[q] = zinit;
     L.zb[q + 1] = zinit;
   }
-  // CHK = false (the hot path): FK proved every primitive lies beyond z_near; CHK = true:
-  // exact solid semantics near the camera (instantiated only out of line, see tiles_near)
-  for (unsigned int m = msph; m; m &= m - 1) isect_sphere<CHK>(fo.rec[__ffs(m) - 1], L, znear);
-  // cones, then (fast path) the palm cylinder with its k = 0 specialisation (bitwise the
-  // cone formulas at k = 0; the exact near-plane path keeps the general code)
-  constexpr unsigned int kCylBit = 1u << (kCyl - kCone0);
-  for (unsigned int m = CHK ? mcone : (mcone & ~kCylBit); m; m &= m - 1)
-    isect_cone<CHK>(fo.rec[kCone0 + __ffs(m) - 1], L, znear);
-  if (!CHK && (mcone & kCylBit)) isect_cyl_fast(fo.rec[kCyl], L);
-  for (unsigned int m = mell; m; m &= m - 1)
-    isect_ellipsoid<CHK>(fo.rec[kEll0 + __ffs(m) - 1], L, znear);
+  if (CHK) {
+    // exact solid semantics (both roots, cone caps, [z_near, z_far]) from the EXACT records
+    for (unsigned int m = msph; m; m &= m - 1) isect_sphere<true>(xr->rec[__ffs(m) - 1], L, znear);
+    for (unsigned int m = mcone; m; m &= m - 1)
+      isect_cone<true>(xr->rec[kCone0 + __ffs(m) - 1], L, znear);
+    for (unsigned int m = mell; m; m &= m - 1)
+      isect_ellipsoid<true>(xr->rec[kEll0 + __ffs(m) - 1], L, znear);
+  } else {
+    for (unsigned int m = msph; m; m &= m - 1) {
+      const float4 q = *reinterpret_cast<const float4*>(fo.rec[__ffs(m) - 1]);
+      const float bx = fmaf(L.dx, q.x, q.z);
+      sphere_pair(q, L.dx, bx, L.dy[0], L.idd[0], L.zb[0], L.zb[1]);
+      sphere_pair(q, L.dx, bx, L.dy[1], L.idd[1], L.zb[2], L.zb[3]);
+    }
+    for (unsigned int m = mcone; m; m &= m - 1) {  // cones and the palm cylinder
+      const QuadLane Q = quad_lane<true>(fo.rec[kCone0 + __ffs(m) - 1], L.dx);
+      quad_pair<true>(Q, L.dy[0], L.zb[0], L.zb[1]);
+      quad_pair<true>(Q, L.dy[1], L.zb[2], L.zb[3]);
+    }
+    for (unsigned int m = mell; m; m &= m - 1) {
+      const QuadLane Q = quad_lane<false>(fo.rec[kEll0 + __ffs(m) - 1], L.dx);
+      quad_pair<false>(Q, L.dy[0], L.zb[0], L.zb[1]);
+      quad_pair<false>(Q, L.dy[1], L.zb[2], L.zb[3]);
+    }
+  }
 
   if (MODE == kModeDepth) {
 #pragma unroll
@@ -408,51 +523,101 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
       }
       __syncwarp();
     }
-    const float d_m = a.cost.d_m, clampv = a.cost.clampv;
-    const float qscale = a.cost.qscale, qmagic = a.cost.qmagic;
-    bool any = false;
-#pragma unroll
-    for (int q = 0; q < kPxPerLane; q++) any |= L.zb[q] <= zfar;
-    if (__any_sync(0xffffffffu, any)) {  // nothing rendered in this tile: nothing to score
-      // numerator: round(min(|dd|, clamp) 2^qbits) from the bits of an fp32 magic-number
-      // FFMA (exact: the sum lies in [2^23, 2^24], ulp 1), summed mod 2^32 and un-biased
-      // once (the true per-lane sum is < 4 * 2^22); no float-to-int conversion on the XU
-      unsigned int num = 0u - (unsigned)kPxPerLane * __float_as_uint(qmagic);
-#pragma unroll
-      for (int q = 0; q < kPxPerLane; q++) {
-        const uint32_t w = lds_u32(obs_s + 4u * ((rowb + 2 * q) * kTileW + col));
-        // o_d undefined is stored as NaN (kObsUndef), so diff is NaN exactly there
-        const float diff = fabsf(__uint_as_float(w & 0x7fffffffu) - L.zb[q]);
-        // off-image pixels have NaN rays and never hit (k_ray_table)
-        const bool hit = L.zb[q] <= zfar;
-        // r_m = 1 where |r_d - o_d| < d_m or o_d undefined (AMB-4, AMB-5):
-        // !(diff >= d_m) is true for NaN
-        const unsigned int rm = hit & !(diff >= d_m);
-        const bool both = hit & (diff == diff);
-        acc.rm += rm;
-        acc.and_ += rm & (w >> 31);
-        if (BOTH) acc.both += both;
-        num += __float_as_uint(fmaf(both ? fminf(diff, clampv) : 0.f, qscale, qmagic));
-      }
-      acc.num += num;
-    }
+    score_lane<kPxPerLane, BOTH>(a, L.zb, obs_s, col, rowb, acc);
   }
   __syncwarp();
 }
 
-// A warp's share of one particle's tiles.  Tiles come from the FK kernel's list
-// (nlist >= 0) or, when there is none, from the union grid with per-tile culling; the
-// warps of a CTA take them through the shared counter *next.
+// The batch renderer's warp BLOCK: 16 x 16 pixels = two 16 x 8 tiles with their own cull
+// masks (the over-test of 16 x 8 tiles) sharing one tile fetch, one 1 KB TMA observation
+// load, the ray set-up and each primitive's per-lane set-up.  Lane: column lane & 15,
+// rows lane >> 4 + {0, 2, ..., 14}; pairs 0, 1 are the top tile, 2, 3 the bottom.
+// ent: X0 | Y0 << 16, the top tile's prims 0..31, the bottom's, then 32..37 of the top in
+// bits 0..5 and of the bottom in bits 8..13 (k_fk_batch's block list).
+template <bool SUMS>
+__device__ __forceinline__ void do_block(const EvalArgs& a, const CUtensorMap* tmap,
+                                         const FkOut& fo, uint4 ent, uint32_t obs_s,
+                                         uint32_t bar_s, uint32_t& phase, uint32_t dx_s,
+                                         uint32_t dy_s, TileSums& acc, int yoff) {
+  const int lane = threadIdx.x & 31;
+  const int col = lane & 15, rowb = lane >> 4;
+  const int X0 = (int)(ent.x & 0xFFFFu), Y0 = (int)(ent.x >> 16);
+  const float zfar = a.cam.zfar;
+  const float zinit = __uint_as_float(__float_as_uint(zfar) + 1u);
+  HP_CHECK(yoff >= 0 && Y0 < a.cam.H && (X0 & 3) == 0);
+  tma_load_2d_elect_s(obs_s, tmap, X0, Y0 + yoff, bar_s, kTileW * kBlockH * 4);
+  const float dx = __uint_as_float(lds_u32(dx_s + 4u * X0));
+  const float ddx = fmaf(dx, dx, 1.f);
+  const float4 ya = lds_f4(dy_s + 16u * Y0);        // rows y, y+2, y+4, y+6
+  const float4 yb = lds_f4(dy_s + 16u * (Y0 + 8));  // rows y+8 .. y+14
+  const f2 dy[4] = {pk(ya.x, ya.y), pk(ya.z, ya.w), pk(yb.x, yb.y), pk(yb.z, yb.w)};
+  const f2 idd[4] = {pk(rcp_approx(fmaf(ya.x, ya.x, ddx)), rcp_approx(fmaf(ya.y, ya.y, ddx))),
+                     pk(rcp_approx(fmaf(ya.z, ya.z, ddx)), rcp_approx(fmaf(ya.w, ya.w, ddx))),
+                     pk(rcp_approx(fmaf(yb.x, yb.x, ddx)), rcp_approx(fmaf(yb.y, yb.y, ddx))),
+                     pk(rcp_approx(fmaf(yb.z, yb.z, ddx)), rcp_approx(fmaf(yb.w, yb.w, ddx)))};
+  float zb[8];
+#pragma unroll
+  for (int q = 0; q < 8; q++) zb[q] = zinit;
+  const unsigned int st = ent.y & 0xFFFFFu, sb = ent.z & 0xFFFFFu;
+  const unsigned int ct = (ent.y >> 20) | ((ent.w & 7u) << 12);
+  const unsigned int cb = (ent.z >> 20) | (((ent.w >> 8) & 7u) << 12);
+  const unsigned int et = (ent.w >> 3) & 7u, eb = (ent.w >> 11) & 7u;
+  for (unsigned int m = st | sb; m; m &= m - 1) {
+    const int j = __ffs(m) - 1;
+    const float4 q = *reinterpret_cast<const float4*>(fo.rec[j]);
+    const float bx = fmaf(dx, q.x, q.z);
+    if ((st >> j) & 1u) {
+      sphere_pair(q, dx, bx, dy[0], idd[0], zb[0], zb[1]);
+      sphere_pair(q, dx, bx, dy[1], idd[1], zb[2], zb[3]);
+    }
+    if ((sb >> j) & 1u) {
+      sphere_pair(q, dx, bx, dy[2], idd[2], zb[4], zb[5]);
+      sphere_pair(q, dx, bx, dy[3], idd[3], zb[6], zb[7]);
+    }
+  }
+  for (unsigned int m = ct | cb; m; m &= m - 1) {  // cones and the palm cylinder
+    const int j = __ffs(m) - 1;
+    const QuadLane Q = quad_lane<true>(fo.rec[kCone0 + j], dx);
+    if ((ct >> j) & 1u) {
+      quad_pair<true>(Q, dy[0], zb[0], zb[1]);
+      quad_pair<true>(Q, dy[1], zb[2], zb[3]);
+    }
+    if ((cb >> j) & 1u) {
+      quad_pair<true>(Q, dy[2], zb[4], zb[5]);
+      quad_pair<true>(Q, dy[3], zb[6], zb[7]);
+    }
+  }
+  for (unsigned int m = et | eb; m; m &= m - 1) {
+    const int j = __ffs(m) - 1;
+    const QuadLane Q = quad_lane<false>(fo.rec[kEll0 + j], dx);
+    if ((et >> j) & 1u) {
+      quad_pair<false>(Q, dy[0], zb[0], zb[1]);
+      quad_pair<false>(Q, dy[1], zb[2], zb[3]);
+    }
+    if ((eb >> j) & 1u) {
+      quad_pair<false>(Q, dy[2], zb[4], zb[5]);
+      quad_pair<false>(Q, dy[3], zb[6], zb[7]);
+    }
+  }
+  mbar_wait_s(bar_s, phase);
+  phase ^= 1u;
+  score_lane<8, SUMS>(a, zb, obs_s, col, rowb, acc);
+  __syncwarp();
+}
+
+// A warp's share of one particle's 16 x 8 tiles (k_eval, the near-plane pass): the union
+// grid with per-tile box culling; the warps of a CTA take tiles through the shared counter
+// *next.  xr: the EXACT records (read by the CHK instantiation only).
 struct TileRun {
   TileSums acc;
   uint32_t phase;
 };
-template <int MODE, bool CHK>
+template <int MODE, bool CHK, bool BOTH = true, int TMA = -1>
 __device__ __forceinline__ TileRun tile_loop(const EvalArgs& a, const CUtensorMap* tmap,
-                                             const FkOut& fo, const uint4* list, int nlist,
-                                             int first, int stride, int count, int* next,
-                                             uint32_t obs_s, uint32_t bar_s, uint32_t phase,
-                                             const float* s_dx, const float* s_dy, int yoff) {
+                                             const FkOut& fo, const FkExact* xr, int first,
+                                             int stride, int count, int* next, uint32_t obs_s,
+                                             uint32_t bar_s, uint32_t phase, const float* s_dx,
+                                             const float* s_dy, int yoff) {
   const int lane = threadIdx.x & 31;
   const TileGrid g(fo.ubox);
   TileRun r;
@@ -469,19 +634,11 @@ __device__ __forceinline__ TileRun tile_loop(const EvalArgs& a, const CUtensorMa
     int jn = 0;
     if (lane == 0) jn = atomicAdd(next, 1);  // the next tile, fetched early
     int X0, Y0;
-    uint3 km;
-    if (nlist >= 0) {
-      const uint4 it = list[j];
-      X0 = (int)(it.x & 0xFFFFu);
-      Y0 = (int)(it.x >> 16);
-      km = make_uint3(it.y, it.z, it.w);
-    } else {
-      g.origin(first + j * stride, X0, Y0);
-      km = cull_tile(fo, X0, Y0);
-    }
+    g.origin(first + j * stride, X0, Y0);
+    const uint3 km = cull_tile(fo, X0, Y0);
     if (km.x | km.y | km.z)  // no primitive box touches the tile: nothing to render or score
-      do_tile<MODE, CHK>(a, tmap, fo, X0, Y0, km, obs_s, bar_s, r.phase, dx_s, dy_s, r.acc,
-                         yoff);
+      do_tile<MODE, CHK, BOTH, TMA>(a, tmap, fo, xr, X0, Y0, km, obs_s, bar_s, r.phase, dx_s,
+                                    dy_s, r.acc, yoff);
     j = __shfl_sync(0xffffffffu, jn, 0);
   }
   return r;
@@ -492,42 +649,42 @@ __device__ __forceinline__ TileRun tile_loop(const EvalArgs& a, const CUtensorMa
 // loop's allocation.  The kernels' EvalArgs are __grid_constant__: no copy for the reference.
 template <int MODE>
 __device__ __noinline__ TileRun tiles_near(const EvalArgs& a, const CUtensorMap* tmap,
-                                           const FkOut& fo, const uint4* list, int nlist,
-                                           int first, int stride, int count, int* next,
-                                           uint32_t obs_s, uint32_t bar_s, uint32_t phase,
-                                           const float* s_dx, const float* s_dy, int yoff) {
-  return tile_loop<MODE, true>(a, tmap, fo, list, nlist, first, stride, count, next, obs_s,
-                               bar_s, phase, s_dx, s_dy, yoff);
+                                           const FkOut& fo, const FkExact* xr, int first,
+                                           int stride, int count, int* next, uint32_t obs_s,
+                                           uint32_t bar_s, uint32_t phase, const float* s_dx,
+                                           const float* s_dy, int yoff) {
+  return tile_loop<MODE, true>(a, tmap, fo, xr, first, stride, count, next, obs_s, bar_s,
+                               phase, s_dx, s_dy, yoff);
 }
 
 // NEARCODE = false (the speculative fit kernels): no near-plane code at all; a particle
 // that would need it raises a_.near_seen and the host re-runs the fit with NEARCODE = true.
 template <int MODE, bool NEARCODE = true>
 __device__ __forceinline__ TileRun run_tiles(const EvalArgs& a, const CUtensorMap* tmap,
-                                             const FkOut& fo, const uint4* list, int nlist,
-                                             int first, int stride, int count, int* next,
-                                             uint32_t obs_s, uint32_t bar_s, uint32_t phase,
-                                             const float* s_dx, const float* s_dy, int yoff) {
+                                             const FkOut& fo, const FkExact* xr, int first,
+                                             int stride, int count, int* next, uint32_t obs_s,
+                                             uint32_t bar_s, uint32_t phase, const float* s_dx,
+                                             const float* s_dy, int yoff) {
 #if HP_NEAR_TEST
-  return tile_loop<MODE, false>(a, tmap, fo, list, nlist, first, stride, count, next,
-                                obs_s, bar_s, phase, s_dx, s_dy, yoff);
+  return tile_loop<MODE, false>(a, tmap, fo, xr, first, stride, count, next, obs_s, bar_s,
+                                phase, s_dx, s_dy, yoff);
 #else
   if (!NEARCODE) {
     if (!fo.near_ok && threadIdx.x == 0 && a.near_seen) atomicOr(a.near_seen, 1);
-    return tile_loop<MODE, false>(a, tmap, fo, list, nlist, first, stride, count, next,
-                                  obs_s, bar_s, phase, s_dx, s_dy, yoff);
+    return tile_loop<MODE, false>(a, tmap, fo, xr, first, stride, count, next, obs_s, bar_s,
+                                  phase, s_dx, s_dy, yoff);
   }
   if (fo.near_ok)
-    return tile_loop<MODE, false>(a, tmap, fo, list, nlist, first, stride, count, next,
-                                  obs_s, bar_s, phase, s_dx, s_dy, yoff);
-  return tiles_near<MODE>(a, tmap, fo, list, nlist, first, stride, count, next, obs_s, bar_s,
-                          phase, s_dx, s_dy, yoff);
+    return tile_loop<MODE, false>(a, tmap, fo, xr, first, stride, count, next, obs_s, bar_s,
+                                  phase, s_dx, s_dy, yoff);
+  return tiles_near<MODE>(a, tmap, fo, xr, first, stride, count, next, obs_s, bar_s, phase,
+                          s_dx, s_dy, yoff);
 #endif
 }
 
 // Sum of a 64-bit value over the warp by two 32-bit REDUX: the low 24 bits and the rest.
 // Exact while every lane's value is < 2^51 (each part's 32-lane sum stays < 2^32): a lane's
-// numerator is < 2^24 per tile (4 pixels of <= 2^22) and a particle has < 2^17 tiles
+// numerator is < 2^25 per block (8 pixels of <= 2^22) and a particle has < 2^17 tiles
 // (the ray table limits the image to < 2^24 pixels).
 __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
   const unsigned int lo = __reduce_add_sync(0xffffffffu, (unsigned int)v & 0xFFFFFFu);
