@@ -146,8 +146,8 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
   const int p = blockIdx.x * kFkWarps + warp;  // one warp per particle
   if (p >= a.n) return;  // warp-uniform; only warp-local synchronisation below
   const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
-  fk_team<PoseT, 1>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk[warp], s_out[warp], nullptr,
-                    s_shp[warp]);
+  fk_team<PoseT, 1>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk[warp], s_out[warp],
+                    static_cast<FkExact*>(a.fkx_g) + p, s_shp[warp]);
   // the record leaves by one bulk copy while the warp builds the tile list: every lane
   // orders its record writes before the async proxy, then lane 0 issues the copy
   fence_proxy_async();
@@ -155,10 +155,6 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
   if (lane == 0)
     bulk_s2g(static_cast<FkOut*>(a.fk_g) + p, &s_out[warp], (uint32_t)sizeof(FkOut));
   FKPROF(4)
-  // a pose that may cross z_near (rare): its EXACT records for the near-plane pass, while
-  // the FK scratch still holds its frames
-  if (!s_out[warp].near_ok) fk_warp_exact(s_fk[warp], a.dims, a.cam, static_cast<FkExact*>(a.fkx_g) + p);
-  __syncwarp();
   uint2* band = reinterpret_cast<uint2*>(&s_fk[warp]);  // FK scratch is dead by now
   const float4* shp = s_shp[warp];
   __syncwarp();

@@ -230,31 +230,23 @@ __device__ __noinline__ void write_fast_quadric(float* rec, const double cen[3],
   }
 }
 
-// Records + box of device primitive j (see common.cuh for the order): `fast` (FAST layout,
-// may be null), `exact` (EXACT layout, may be null), `box` (may be null; then zmin is not
-// computed either).
-// shape (may be null): a cone's tile-list capsule (cone_capsule).
-__device__ __noinline__ void build_prim(int j, const FkScratch& s, const DimsD& dm, const CamParams& cam,
-                           float* fast, float* exact, int4* box, float& zmin,
-                           float4* shape = nullptr) {
-  float* rec = exact;  // the exact record (written only when requested)
-  if (rec)
+// Build record + box of device primitive j (see common.cuh for the order).
+// EXACT-layout record + box of device primitive j (see common.cuh for the order); shape
+// (may be null): a cone's tile-list capsule (cone_capsule).  fk_team converts the record
+// to the FAST layout afterwards (to_fast).
+__device__ void build_prim(int j, const FkScratch& s, const DimsD& dm,
+                                        const CamParams& cam, float* rec, int4& box,
+                                        float& zmin, float4* shape = nullptr) {
 #pragma unroll
-    for (int i = 0; i < kRec; i++) rec[i] = 0.f;
+  for (int i = 0; i < kRec; i++) rec[i] = 0.f;
   float gc[2][3], gA[2][3][3];
   int ng = 0;
   if (j < kCone0) {  // sphere at joint (f, k)
     int f = j >> 2, k = j & 3;
     double r = dm.rad[f][k];
     const double* c = s.J[f][k];
-    if (rec) {
-      put3(rec, kC, c);
-      rec[kR2] = (float)(r * r);
-    }
-    if (fast) {  // spheres keep the re-centred test: the fast record is the exact one's head
-      put3(fast, kC, c);
-      fast[kR2] = (float)(r * r);
-    }
+    put3(rec, kC, c);
+    rec[kR2] = (float)(r * r);
     for (int i = 0; i < 3; i++) gc[0][i] = (float)c[i];
     for (int a = 0; a < 3; a++)
       for (int b = 0; b < 3; b++) gA[0][a][b] = (a == b) ? (float)(r * r) : 0.f;
@@ -279,22 +271,15 @@ __device__ __noinline__ void build_prim(int j, const FkScratch& s, const DimsD& 
       e2[i] = s.Rs[f][k][i][2];
       m[i] = 0.5 * (J0[i] + J1[i]);
     }
+    put3(rec, kC, m);
     double rows[3][3] = {{e1[0], e1[1], e1[2]}, {e2[0], e2[1], e2[2]}, {ax[0], ax[1], ax[2]}};
-    if (rec) {
-      put3(rec, kC, m);
-      for (int a = 0; a < 3; a++) {
-        put3(rec, kM + 3 * a, rows[a]);
-        rec[kCl + a] = (float)(rows[a][0] * m[0] + rows[a][1] * m[1] + rows[a][2] * m[2]);
-      }
-      rec[kRm] = (float)(0.5 * (r0 + r1));
-      rec[kK] = (float)dm.cone_k[f][k];
-      rec[kHl] = (float)(0.5 * L);
+    for (int a = 0; a < 3; a++) {
+      put3(rec, kM + 3 * a, rows[a]);
+      rec[kCl + a] = (float)(rows[a][0] * m[0] + rows[a][1] * m[1] + rows[a][2] * m[2]);
     }
-    if (fast) {  // x^2 + y^2 - (r_m + k z)^2: Q = diag(1, 1, -k^2), g = (0, 0, -r_m k), h = -r_m^2
-      const double rm = 0.5 * (r0 + r1), kk = dm.cone_k[f][k];
-      const double q[3] = {1.0, 1.0, -kk * kk};
-      write_fast_quadric(fast, m, rows, q, -rm * kk, -rm * rm, true, 0.5 * L);
-    }
+    rec[kRm] = (float)(0.5 * (r0 + r1));
+    rec[kK] = (float)dm.cone_k[f][k];
+    rec[kHl] = (float)(0.5 * L);
     float axf[3] = {(float)ax[0], (float)ax[1], (float)ax[2]};
     for (int i = 0; i < 3; i++) {
       gc[0][i] = (float)J0[i];
@@ -312,6 +297,7 @@ __device__ __noinline__ void build_prim(int j, const FkScratch& s, const DimsD& 
       cz[i] = s.RW[i][2];
       m[i] = s.h[i] - 0.5 * dm.palm_len * cy[i];
     }
+    put3(rec, kC, m);
     double rows[3][3];
     const double iw = 1.0 / dm.palm_half_w, it = 1.0 / dm.palm_half_t;
     for (int i = 0; i < 3; i++) {
@@ -319,20 +305,13 @@ __device__ __noinline__ void build_prim(int j, const FkScratch& s, const DimsD& 
       rows[1][i] = cz[i] * it;
       rows[2][i] = cy[i];
     }
-    if (rec) {
-      put3(rec, kC, m);
-      for (int a = 0; a < 3; a++) {
-        put3(rec, kM + 3 * a, rows[a]);
-        rec[kCl + a] = (float)(rows[a][0] * m[0] + rows[a][1] * m[1] + rows[a][2] * m[2]);
-      }
-      rec[kRm] = 1.f;
-      rec[kK] = 0.f;
-      rec[kHl] = (float)(0.5 * dm.palm_len);
+    for (int a = 0; a < 3; a++) {
+      put3(rec, kM + 3 * a, rows[a]);
+      rec[kCl + a] = (float)(rows[a][0] * m[0] + rows[a][1] * m[1] + rows[a][2] * m[2]);
     }
-    if (fast) {  // (x/a)^2 + (z/b)^2 - 1 in the scaled rows: Q = diag(1, 1, 0), h = -1
-      const double q[3] = {1.0, 1.0, 0.0};
-      write_fast_quadric(fast, m, rows, q, 0.0, -1.0, true, 0.5 * dm.palm_len);
-    }
+    rec[kRm] = 1.f;
+    rec[kK] = 0.f;
+    rec[kHl] = (float)(0.5 * dm.palm_len);
     float cols[3][3], sd[3] = {(float)dm.palm_half_w, 0.f, (float)dm.palm_half_t};
     for (int i = 0; i < 3; i++) {
       cols[0][i] = (float)cx[i];
@@ -363,21 +342,12 @@ __device__ __noinline__ void build_prim(int j, const FkScratch& s, const DimsD& 
       sd[1] = dm.cap_half;
       sd[2] = dm.palm_half_t;
     }
-    double rows[3][3];
+    put3(rec, kC, c);
     for (int a = 0; a < 3; a++) {
       const double is = 1.0 / sd[a];
-      for (int i = 0; i < 3; i++) rows[a][i] = cols[a][i] * is;
-    }
-    if (rec) {
-      put3(rec, kC, c);
-      for (int a = 0; a < 3; a++) {
-        put3(rec, kM + 3 * a, rows[a]);
-        rec[kCl + a] = (float)(rows[a][0] * c[0] + rows[a][1] * c[1] + rows[a][2] * c[2]);
-      }
-    }
-    if (fast) {  // |l|^2 - 1
-      const double q[3] = {1.0, 1.0, 1.0};
-      write_fast_quadric(fast, c, rows, q, 0.0, -1.0, false, 0.0);
+      double row[3] = {cols[a][0] * is, cols[a][1] * is, cols[a][2] * is};
+      put3(rec, kM + 3 * a, row);
+      rec[kCl + a] = (float)(row[0] * c[0] + row[1] * c[1] + row[2] * c[2]);
     }
     float colf[3][3], sdf[3] = {(float)sd[0], (float)sd[1], (float)sd[2]};
     for (int a = 0; a < 3; a++)
@@ -386,7 +356,27 @@ __device__ __noinline__ void build_prim(int j, const FkScratch& s, const DimsD& 
     shape_from_axes(colf, sdf, gA[0]);
     ng = 1;
   }
-  if (box) *box = prim_box(ng, gc, gA, cam, zmin);
+  box = prim_box(ng, gc, gA, cam, zmin);
+}
+
+// In place: the EXACT record of quadric primitive j (fp32 geometry) becomes its FAST record
+// (polynomial coefficients computed in fp64 from that geometry).  Spheres keep their
+// record (the FAST sphere layout is the EXACT one's head).
+__device__ __noinline__ void to_fast(float* rec, int j) {
+  if (j < kCone0) return;
+  double c[3], M[3][3];
+  for (int i = 0; i < 3; i++) c[i] = rec[kC + i];
+  for (int a = 0; a < 3; a++)
+    for (int i = 0; i < 3; i++) M[a][i] = rec[kM + 3 * a + i];
+  if (j < kEll0) {  // cones and the cylinder (k = 0, r_m = 1 in its scaled rows):
+    // x^2 + y^2 - (r_m + k z)^2: Q = diag(1, 1, -k^2), g = (0, 0, -r_m k), h = -r_m^2
+    const double rm = rec[kRm], k = rec[kK], hl = rec[kHl];
+    const double q[3] = {1.0, 1.0, -k * k};
+    write_fast_quadric(rec, c, M, q, -rm * k, -rm * rm, true, hl);
+  } else {  // ellipsoids: |l|^2 - 1
+    const double q[3] = {1.0, 1.0, 1.0};
+    write_fast_quadric(rec, c, M, q, 0.0, -1.0, false, 0.0);
+  }
 }
 
 // FK on a team of 1 or 2 warps (warp 0 = the team leader).  pose: 26 values (float or
@@ -406,8 +396,10 @@ __device__ unsigned long long g_fkprof[16];
 #else
 #define FKPROF(i)
 #endif
-// xrec (may be null): also write the EXACT records (the near-plane path's).
+// xrec (may be null): also keep the EXACT records (the near-plane path's) — TEAM >= 2
+// always, TEAM 1 (k_fk_batch, xrec in global memory) only for a pose that is not near_ok.
 // shp (may be null): the cones' tile-list capsules [kNcone] (cone_capsule).
+// out.rec holds the FAST records on return.
 template <typename PoseT, int TEAM>
 __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam,
                         double kc_rest, FkScratch& s, FkOut& out, FkExact* xrec = nullptr,
@@ -495,9 +487,14 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
     const int j = j0 + lane;
     if (j < j1) {
       float zmin;
-      build_prim(j, s, dm, cam, out.rec[j], xrec ? xrec->rec[j] : nullptr, &out.box[j], zmin,
+      build_prim(j, s, dm, cam, out.rec[j], out.box[j], zmin,
                  shp && j >= kCone0 && j < kCyl ? shp + (j - kCone0) : nullptr);
       s.nearf[j] = zmin > cam.znear * 1.001f;
+      if (xrec)
+        for (int i = 0; i < kRec; i += 4)
+          *reinterpret_cast<float4*>(&xrec->rec[j][i]) =
+              *reinterpret_cast<const float4*>(&out.rec[j][i]);
+      to_fast(out.rec[j], j);
     }
     if (w != 0) {
       asm volatile("bar.arrive 1, %0;" ::"n"(32 * TEAM) : "memory");
@@ -513,10 +510,21 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
     for (int k = 0; k < nj; k++) {
       const int j = lane < 10 ? 2 * lane + k : lane + 10;
       float zmin;
-      build_prim(j, s, dm, cam, out.rec[j], xrec ? xrec->rec[j] : nullptr, &out.box[j], zmin,
+      build_prim(j, s, dm, cam, out.rec[j], out.box[j], zmin,
                  shp && j >= kCone0 && j < kCyl ? shp + (j - kCone0) : nullptr);
       s.nearf[j] = zmin > cam.znear * 1.001f;
     }
+    __syncwarp();
+    if (xrec) {  // a pose that may cross z_near keeps its EXACT records (global memory)
+      int nok = 1;
+      for (int j = lane; j < kNprim; j += 32) nok &= s.nearf[j];
+      if (!__all_sync(0xffffffffu, nok))
+        for (int i = lane; i < kNprim * kRec / 4; i += 32)
+          reinterpret_cast<float4*>(xrec->rec)[i] =
+              reinterpret_cast<const float4*>(out.rec)[i];
+    }
+    for (int k = 0; k < nj; k++) to_fast(out.rec[lane < 10 ? 2 * lane + k : lane + 10],
+                                         lane < 10 ? 2 * lane + k : lane + 10);
     __syncwarp();
   }
   FKPROF(3)
@@ -562,19 +570,6 @@ __device__ __forceinline__ void fk_warp(const PoseT* pose, const DimsD& dm, cons
                                         double kc_rest, FkScratch& s, FkOut& out,
                                         FkExact* xrec = nullptr) {
   fk_team<PoseT, 1>(pose, dm, cam, kc_rest, s, out, xrec);
-}
-
-// After fk_warp on a pose that is not near_ok: its EXACT records straight to global memory
-// (the FK scratch must still hold the pose's frames).  Same lane map as fk_team<1>.
-__device__ __forceinline__ void fk_warp_exact(const FkScratch& s, const DimsD& dm,
-                                              const CamParams& cam, FkExact* xg) {
-  const int lane = threadIdx.x & 31;
-  const int nj = lane < 10 ? 2 : (lane < 28 ? 1 : 0);
-  for (int k = 0; k < nj; k++) {
-    const int j = lane < 10 ? 2 * lane + k : lane + 10;
-    float zmin;
-    build_prim(j, s, dm, cam, nullptr, xg->rec[j], nullptr, zmin);
-  }
 }
 
 }  // namespace hp
