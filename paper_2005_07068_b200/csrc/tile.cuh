@@ -408,26 +408,46 @@ __device__ __forceinline__ void score_lane(const EvalArgs& a, const float* zb, u
   for (int q = 0; q < NPX; q++) any |= zb[q] <= zfar;
   if (__any_sync(0xffffffffu, any)) {  // nothing rendered in this tile: nothing to score
     // numerator: round(min(|dd|, clamp) 2^qbits) from the bits of an fp32 magic-number
-    // FFMA (exact: the sum lies in [2^23, 2^24], ulp 1), summed mod 2^32 and un-biased
-    // once (the true per-lane sum is < NPX * 2^22); no float-to-int conversion on the XU
-    unsigned int num = 0u - (unsigned)NPX * __float_as_uint(qmagic);
+    // FFMA (exact: the value lies in [2^23, 2^24], ulp 1) minus the magic's bits: no
+    // float-to-int conversion on the XU; every count is a predicated add
+    const unsigned int magic_bits = __float_as_uint(qmagic);
+    unsigned int num = 0u, both = 0u;
 #pragma unroll
     for (int q = 0; q < NPX; q++) {
       const uint32_t w = lds_u32(obs_s + 4u * ((rowb + 2 * q) * kTileW + col));
-      // o_d undefined is stored as NaN (kObsUndef), so diff is NaN exactly there; bit 31
-      // (o_s) is the float's sign, dropped by the absolute value
-      const float diff = fabsf(fabsf(__uint_as_float(w)) - zb[q]);
-      // off-image pixels have NaN rays and never hit (k_ray_table)
-      const bool hit = zb[q] <= zfar;
-      // r_m = 1 where |r_d - o_d| < d_m or o_d undefined (AMB-4, AMB-5):
-      // !(diff >= d_m) is true for NaN
-      const unsigned int rm = hit & !(diff >= d_m);
-      const bool both = hit & (diff == diff);
-      acc.rm += rm;
-      acc.and_ += rm & (w >> 31);
-      if (BOTH) acc.both += both;
-      num += __float_as_uint(fmaf(both ? fminf(diff, clampv) : 0.f, qscale, qmagic));
+      // diff = | |o| - z |: o_d undefined is stored as NaN (kObsUndef), so diff is NaN
+      // exactly there; bit 31 (o_s) is the float's sign, dropped by the absolute value.
+      // hit = z <= z_far (off-image pixels have NaN rays and never hit, k_ray_table).
+      // r_m = hit AND (diff < d_m OR o_d undefined) (AMB-4, AMB-5): "ltu" is
+      // true for NaN.  o_s AND r_m adds bit 31 of w.  Both depths defined: hit AND diff
+      // is a number; the numerator adds the bits of the magic-number FFMA minus the
+      // magic's (predicated adds only: no selects, no float-to-int conversion).
+      asm("{\n\t"
+          ".reg .pred ph, pr, pb, pa;\n\t"
+          ".reg .f32 d, c;\n\t"
+          ".reg .b32 t;\n\t"
+          "mov.b32 d, %4;\n\t"
+          "abs.f32 d, d;\n\t"
+          "sub.f32 d, d, %5;\n\t"
+          "abs.f32 d, d;\n\t"
+          "setp.le.f32 ph, %5, %6;\n\t"
+          "setp.ltu.and.f32 pr, d, %7, ph;\n\t"
+          "@pr add.u32 %0, %0, 1;\n\t"
+          "setp.lt.and.s32 pa, %4, 0, pr;\n\t"
+          "@pa add.u32 %1, %1, 1;\n\t"
+          "setp.num.and.f32 pb, d, d, ph;\n\t"
+          "@pb add.u32 %2, %2, 1;\n\t"
+          "min.f32 c, d, %8;\n\t"
+          "fma.rn.f32 c, c, %9, %10;\n\t"
+          "mov.b32 t, c;\n\t"
+          "sub.u32 t, t, %11;\n\t"
+          "@pb add.u32 %3, %3, t;\n\t"
+          "}"
+          : "+r"(acc.rm), "+r"(acc.and_), "+r"(both), "+r"(num)
+          : "r"(w), "f"(zb[q]), "f"(zfar), "f"(d_m), "f"(clampv), "f"(qscale), "f"(qmagic),
+            "r"(magic_bits));
     }
+    if (BOTH) acc.both += both;
     acc.num += num;
   }
 }
@@ -558,46 +578,61 @@ __device__ __forceinline__ void do_block(const EvalArgs& a, const CUtensorMap* t
   float zb[8];
 #pragma unroll
   for (int q = 0; q < 8; q++) zb[q] = zinit;
+  // masks per kind, split into primitives in both halves / the top only / the bottom only
+  // (no per-primitive half tests in the loops)
   const unsigned int st = ent.y & 0xFFFFFu, sb = ent.z & 0xFFFFFu;
   const unsigned int ct = (ent.y >> 20) | ((ent.w & 7u) << 12);
   const unsigned int cb = (ent.z >> 20) | (((ent.w >> 8) & 7u) << 12);
   const unsigned int et = (ent.w >> 3) & 7u, eb = (ent.w >> 11) & 7u;
-  for (unsigned int m = st | sb; m; m &= m - 1) {
-    const int j = __ffs(m) - 1;
-    const float4 q = *reinterpret_cast<const float4*>(fo.rec[j]);
+  const unsigned int s2 = st & sb, c2 = ct & cb, e2 = et & eb;
+  for (unsigned int m = s2; m; m &= m - 1) {
+    const float4 q = *reinterpret_cast<const float4*>(fo.rec[__ffs(m) - 1]);
     const float bx = fmaf(dx, q.x, q.z);
-    if ((st >> j) & 1u) {
-      sphere_pair(q, dx, bx, dy[0], idd[0], zb[0], zb[1]);
-      sphere_pair(q, dx, bx, dy[1], idd[1], zb[2], zb[3]);
-    }
-    if ((sb >> j) & 1u) {
-      sphere_pair(q, dx, bx, dy[2], idd[2], zb[4], zb[5]);
-      sphere_pair(q, dx, bx, dy[3], idd[3], zb[6], zb[7]);
-    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) sphere_pair(q, dx, bx, dy[k], idd[k], zb[2 * k], zb[2 * k + 1]);
   }
-  for (unsigned int m = ct | cb; m; m &= m - 1) {  // cones and the palm cylinder
-    const int j = __ffs(m) - 1;
-    const QuadLane Q = quad_lane<true>(fo.rec[kCone0 + j], dx);
-    if ((ct >> j) & 1u) {
-      quad_pair<true>(Q, dy[0], zb[0], zb[1]);
-      quad_pair<true>(Q, dy[1], zb[2], zb[3]);
-    }
-    if ((cb >> j) & 1u) {
-      quad_pair<true>(Q, dy[2], zb[4], zb[5]);
-      quad_pair<true>(Q, dy[3], zb[6], zb[7]);
-    }
+  for (unsigned int m = st ^ s2; m; m &= m - 1) {
+    const float4 q = *reinterpret_cast<const float4*>(fo.rec[__ffs(m) - 1]);
+    const float bx = fmaf(dx, q.x, q.z);
+#pragma unroll
+    for (int k = 0; k < 2; k++) sphere_pair(q, dx, bx, dy[k], idd[k], zb[2 * k], zb[2 * k + 1]);
   }
-  for (unsigned int m = et | eb; m; m &= m - 1) {
-    const int j = __ffs(m) - 1;
-    const QuadLane Q = quad_lane<false>(fo.rec[kEll0 + j], dx);
-    if ((et >> j) & 1u) {
-      quad_pair<false>(Q, dy[0], zb[0], zb[1]);
-      quad_pair<false>(Q, dy[1], zb[2], zb[3]);
-    }
-    if ((eb >> j) & 1u) {
-      quad_pair<false>(Q, dy[2], zb[4], zb[5]);
-      quad_pair<false>(Q, dy[3], zb[6], zb[7]);
-    }
+  for (unsigned int m = sb ^ s2; m; m &= m - 1) {
+    const float4 q = *reinterpret_cast<const float4*>(fo.rec[__ffs(m) - 1]);
+    const float bx = fmaf(dx, q.x, q.z);
+#pragma unroll
+    for (int k = 2; k < 4; k++) sphere_pair(q, dx, bx, dy[k], idd[k], zb[2 * k], zb[2 * k + 1]);
+  }
+  // cones and the palm cylinder
+  for (unsigned int m = c2; m; m &= m - 1) {
+    const QuadLane Q = quad_lane<true>(fo.rec[kCone0 + __ffs(m) - 1], dx);
+#pragma unroll
+    for (int k = 0; k < 4; k++) quad_pair<true>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
+  }
+  for (unsigned int m = ct ^ c2; m; m &= m - 1) {
+    const QuadLane Q = quad_lane<true>(fo.rec[kCone0 + __ffs(m) - 1], dx);
+#pragma unroll
+    for (int k = 0; k < 2; k++) quad_pair<true>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
+  }
+  for (unsigned int m = cb ^ c2; m; m &= m - 1) {
+    const QuadLane Q = quad_lane<true>(fo.rec[kCone0 + __ffs(m) - 1], dx);
+#pragma unroll
+    for (int k = 2; k < 4; k++) quad_pair<true>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
+  }
+  for (unsigned int m = e2; m; m &= m - 1) {
+    const QuadLane Q = quad_lane<false>(fo.rec[kEll0 + __ffs(m) - 1], dx);
+#pragma unroll
+    for (int k = 0; k < 4; k++) quad_pair<false>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
+  }
+  for (unsigned int m = et ^ e2; m; m &= m - 1) {
+    const QuadLane Q = quad_lane<false>(fo.rec[kEll0 + __ffs(m) - 1], dx);
+#pragma unroll
+    for (int k = 0; k < 2; k++) quad_pair<false>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
+  }
+  for (unsigned int m = eb ^ e2; m; m &= m - 1) {
+    const QuadLane Q = quad_lane<false>(fo.rec[kEll0 + __ffs(m) - 1], dx);
+#pragma unroll
+    for (int k = 2; k < 4; k++) quad_pair<false>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
   }
   mbar_wait_s(bar_s, phase);
   phase ^= 1u;
