@@ -317,9 +317,9 @@ __device__ __forceinline__ void quad_pair(const QuadLane& q, f2 dy, float& zb0, 
     float za0, za1, t0, t1;
     unpk(za, za0, za1);
     unpk(t, t0, t1);
-    const float nan = __int_as_float(0x7fc00000);
-    zb0 = fminf(zb0, fabsf(za0) <= q.hl ? t0 : nan);
-    zb1 = fminf(zb1, fabsf(za1) <= q.hl ? t1 : nan);
+    // a predicated min (no select): inside the axial range only
+    if (fabsf(za0) <= q.hl) zb0 = fminf(zb0, t0);
+    if (fabsf(za1) <= q.hl) zb1 = fminf(zb1, t1);
   } else {
     float t0, t1;
     unpk(t, t0, t1);
