@@ -271,6 +271,11 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   const uint32_t obs_s = HP_PIN(smem_u32(s_obs[warp])), bar_s = HP_PIN(smem_u32(&s_bar[warp]));
   const uint32_t dx_s = HP_PIN(smem_u32(s_dx + (lane & 15)));
   const uint32_t dy_s = HP_PIN(smem_u32(s_dy + 4 * (lane >> 4)));
+  // the lane's first observation pixel (column lane & 15, row lane >> 4) and the slots'
+  // shared bases, computed once (the compiler otherwise re-derives them per block)
+  const uint32_t obs_ls = HP_PIN(obs_s + 4u * ((lane >> 4) * kTileW + (lane & 15)));
+  const uint32_t tiles_s0 = smem_u32(s_tiles[0]), rec_s0 = smem_u32(s_out[0].rec);
+  const uint32_t next_s0 = smem_u32(&s_next[0]);
   for (int i = 0;; i++) {
     const int b = i & 1;
     mbar_wait(&s_full[b], (i >> 1) & 1);
@@ -287,12 +292,12 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
       // the union grid, both halves culled here
       const int nby = (g.ntiles / (g.tx > 0 ? g.tx : 1) + 1) >> 1;
       const int nt = NEAR ? g.ntiles : (nlist >= 0 ? nlist : g.tx * nby);
-      int t = 0;
-      if (lane == 0) t = atomicAdd(&s_next[b], 1);
-      t = __shfl_sync(0xffffffffu, t, 0);
+      const uint32_t next_s = next_s0 + 4u * b;
+      const uint32_t tiles_s = tiles_s0 + (uint32_t)sizeof(s_tiles[0]) * b;
+      const uint32_t rec_s = rec_s0 + (uint32_t)sizeof(FkOut) * b;
+      int t = warp_fetch_add1(next_s);
       while (t < nt) {
-        int tn = 0;
-        if (lane == 0) tn = atomicAdd(&s_next[b], 1);
+        const int tn = warp_fetch_add1(next_s);  // the next block, fetched early
         if (NEAR) {
           int X0, Y0;
           g.origin(t, X0, Y0);
@@ -304,7 +309,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
           uint4 ent;
           if (nlist >= 0) {
             HP_CHECK(t >= 0 && t < kMaxTiles);
-            ent = s_tiles[b][t];
+            ent = lds_u4_nv(tiles_s + 16u * t);
           } else {
             const int qy = t / g.tx, qx = t - qy * g.tx;
             const int X0 = g.x0 + qx * kTileW, Y0 = g.y0 + qy * kBlockH;
@@ -314,9 +319,10 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
                              ((kt.y >> 12) | (kt.z << 3)) | (((kb.y >> 12) | (kb.z << 3)) << 8));
           }
           if (ent.y | ent.z | ent.w)
-            do_block<SUMS>(a, &tmap, fo, ent, obs_s, bar_s, phase, dx_s, dy_s, acc, yoff);
+            do_block<SUMS>(a, &tmap, rec_s, ent, obs_s, obs_ls, bar_s, phase, dx_s, dy_s, acc,
+                           yoff);
         }
-        t = __shfl_sync(0xffffffffu, tn, 0);
+        t = tn;
       }
     }
     warp_reduce<SUMS>(acc);

@@ -246,6 +246,41 @@ __device__ __forceinline__ float4 lds_f4(uint32_t a) {
                : "r"(a));
   return v;
 }
+// Non-volatile shared loads (schedulable like plain loads) of data that does not change
+// while it is read (FK records, block lists).
+__device__ __forceinline__ float4 lds_f4_nv(uint32_t a) {
+  float4 v;
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float2 lds_f2_nv(uint32_t a) {
+  float2 v;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_u4_nv(uint32_t a) {
+  uint4 v;
+  asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "r"(a));
+  return v;
+}
+// Warp-collective: lane 0 adds 1 to the shared counter at address a; every lane gets the
+// old value (no divergent branch around the atomic).
+__device__ __forceinline__ int warp_fetch_add1(uint32_t a) {
+  int old = 0;
+  asm volatile(
+      "{\n.reg .pred p;\n.reg .u32 l;\n"
+      "mov.u32 l, %%laneid;\n"
+      "setp.eq.u32 p, l, 0;\n"
+      "@p atom.shared.add.u32 %0, [%1], 1;\n}"
+      : "+r"(old)
+      : "r"(a)
+      : "memory");
+  return __shfl_sync(0xffffffffu, old, 0);
+}
 __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }

@@ -271,16 +271,16 @@ struct QuadLane {
   float lzy, lzl, nclz, hl;  // axial (cones / cylinder)
 };
 template <bool AXIAL>
-__device__ __forceinline__ QuadLane quad_lane(const float* __restrict__ r, float dx) {
-  const float4 r0 = *reinterpret_cast<const float4*>(r + 0);   // xp yp d00 d10
-  const float4 r1 = *reinterpret_cast<const float4*>(r + 4);   // d01 d20 d11 d02
-  const float4 r2 = *reinterpret_cast<const float4*>(r + 8);   // b0 bx by clz
-  const float4 r3 = *reinterpret_cast<const float4*>(r + 12);  // a00 a10 a01 a20
+__device__ __forceinline__ QuadLane quad_lane(uint32_t r, float dx) {  // r: record address
+  const float4 r0 = lds_f4_nv(r + 0);   // xp yp d00 d10
+  const float4 r1 = lds_f4_nv(r + 16);  // d01 d20 d11 d02
+  const float4 r2 = lds_f4_nv(r + 32);  // b0 bx by clz
+  const float4 r3 = lds_f4_nv(r + 48);  // a00 a10 a01 a20
   float a11, a02;
   QuadLane q;
   if (AXIAL) {
-    const float4 r4 = *reinterpret_cast<const float4*>(r + 16);  // a11 a02 lzx lzy
-    const float2 r5 = *reinterpret_cast<const float2*>(r + 20);  // lz1 hl
+    const float4 r4 = lds_f4_nv(r + 64);  // a11 a02 lzx lzy
+    const float2 r5 = lds_f2_nv(r + 80);  // lz1 hl
     a11 = r4.x;
     a02 = r4.y;
     q.lzy = r4.w;
@@ -288,7 +288,7 @@ __device__ __forceinline__ QuadLane quad_lane(const float* __restrict__ r, float
     q.nclz = -r2.w;
     q.hl = r5.y;
   } else {
-    const float2 r4 = *reinterpret_cast<const float2*>(r + 16);  // a11 a02
+    const float2 r4 = lds_f2_nv(r + 64);  // a11 a02
     a11 = r4.x;
     a02 = r4.y;
   }
@@ -398,8 +398,8 @@ __device__ __forceinline__ uint3 cull_tile(const FkOut& fo, int X0, int Y0) {
 // (BOTH) the both-defined count (AMB-1, -3, -4, -5).  Skipped for tiles where
 // nothing rendered.
 template <int NPX, bool BOTH>
-__device__ __forceinline__ void score_lane(const EvalArgs& a, const float* zb, uint32_t obs_s,
-                                           int col, int rowb, TileSums& acc) {
+__device__ __forceinline__ void score_lane(const EvalArgs& a, const float* zb, uint32_t obs_ls,
+                                           TileSums& acc) {
   const float zfar = a.cam.zfar;
   const float d_m = a.cost.d_m, clampv = a.cost.clampv;
   const float qscale = a.cost.qscale, qmagic = a.cost.qmagic;
@@ -414,7 +414,7 @@ __device__ __forceinline__ void score_lane(const EvalArgs& a, const float* zb, u
     unsigned int num = 0u, both = 0u;
 #pragma unroll
     for (int q = 0; q < NPX; q++) {
-      const uint32_t w = lds_u32(obs_s + 4u * ((rowb + 2 * q) * kTileW + col));
+      const uint32_t w = lds_u32(obs_ls + 4u * (2 * q) * kTileW);
       // diff = | |o| - z |: o_d undefined is stored as NaN (kObsUndef), so diff is NaN
       // exactly there; bit 31 (o_s) is the float's sign, dropped by the absolute value.
       // hit = z <= z_far (off-image pixels have NaN rays and never hit, k_ray_table).
@@ -512,12 +512,12 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
       sphere_pair(q, L.dx, bx, L.dy[1], L.idd[1], L.zb[2], L.zb[3]);
     }
     for (unsigned int m = mcone; m; m &= m - 1) {  // cones and the palm cylinder
-      const QuadLane Q = quad_lane<true>(fo.rec[kCone0 + __ffs(m) - 1], L.dx);
+      const QuadLane Q = quad_lane<true>(smem_u32(fo.rec[kCone0 + __ffs(m) - 1]), L.dx);
       quad_pair<true>(Q, L.dy[0], L.zb[0], L.zb[1]);
       quad_pair<true>(Q, L.dy[1], L.zb[2], L.zb[3]);
     }
     for (unsigned int m = mell; m; m &= m - 1) {
-      const QuadLane Q = quad_lane<false>(fo.rec[kEll0 + __ffs(m) - 1], L.dx);
+      const QuadLane Q = quad_lane<false>(smem_u32(fo.rec[kEll0 + __ffs(m) - 1]), L.dx);
       quad_pair<false>(Q, L.dy[0], L.zb[0], L.zb[1]);
       quad_pair<false>(Q, L.dy[1], L.zb[2], L.zb[3]);
     }
@@ -543,7 +543,7 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
       }
       __syncwarp();
     }
-    score_lane<kPxPerLane, BOTH>(a, L.zb, obs_s, col, rowb, acc);
+    score_lane<kPxPerLane, BOTH>(a, L.zb, obs_s + 4u * (rowb * kTileW + col), acc);
   }
   __syncwarp();
 }
@@ -554,13 +554,13 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
 // rows lane >> 4 + {0, 2, ..., 14}; pairs 0, 1 are the top tile, 2, 3 the bottom.
 // ent: X0 | Y0 << 16, the top tile's prims 0..31, the bottom's, then 32..37 of the top in
 // bits 0..5 and of the bottom in bits 8..13 (k_fk_batch's block list).
+// rec_s: shared address of the particle's FAST records; obs_s: the warp's observation
+// buffer, obs_ls: this lane's first pixel in it (column lane & 15, row lane >> 4).
 template <bool SUMS>
 __device__ __forceinline__ void do_block(const EvalArgs& a, const CUtensorMap* tmap,
-                                         const FkOut& fo, uint4 ent, uint32_t obs_s,
-                                         uint32_t bar_s, uint32_t& phase, uint32_t dx_s,
-                                         uint32_t dy_s, TileSums& acc, int yoff) {
-  const int lane = threadIdx.x & 31;
-  const int col = lane & 15, rowb = lane >> 4;
+                                         uint32_t rec_s, uint4 ent, uint32_t obs_s,
+                                         uint32_t obs_ls, uint32_t bar_s, uint32_t& phase,
+                                         uint32_t dx_s, uint32_t dy_s, TileSums& acc, int yoff) {
   const int X0 = (int)(ent.x & 0xFFFFu), Y0 = (int)(ent.x >> 16);
   const float zfar = a.cam.zfar;
   const float zinit = __uint_as_float(__float_as_uint(zfar) + 1u);
@@ -571,10 +571,9 @@ __device__ __forceinline__ void do_block(const EvalArgs& a, const CUtensorMap* t
   const float4 ya = lds_f4(dy_s + 16u * Y0);        // rows y, y+2, y+4, y+6
   const float4 yb = lds_f4(dy_s + 16u * (Y0 + 8));  // rows y+8 .. y+14
   const f2 dy[4] = {pk(ya.x, ya.y), pk(ya.z, ya.w), pk(yb.x, yb.y), pk(yb.z, yb.w)};
-  const f2 idd[4] = {pk(rcp_approx(fmaf(ya.x, ya.x, ddx)), rcp_approx(fmaf(ya.y, ya.y, ddx))),
-                     pk(rcp_approx(fmaf(ya.z, ya.z, ddx)), rcp_approx(fmaf(ya.w, ya.w, ddx))),
-                     pk(rcp_approx(fmaf(yb.x, yb.x, ddx)), rcp_approx(fmaf(yb.y, yb.y, ddx))),
-                     pk(rcp_approx(fmaf(yb.z, yb.z, ddx)), rcp_approx(fmaf(yb.w, yb.w, ddx)))};
+  f2 idd[4];
+#pragma unroll
+  for (int k = 0; k < 4; k++) idd[k] = rcp2(fma2(dy[k], dy[k], bc(ddx)));  // 1 / |d|^2
   float zb[8];
 #pragma unroll
   for (int q = 0; q < 8; q++) zb[q] = zinit;
@@ -586,57 +585,57 @@ __device__ __forceinline__ void do_block(const EvalArgs& a, const CUtensorMap* t
   const unsigned int et = (ent.w >> 3) & 7u, eb = (ent.w >> 11) & 7u;
   const unsigned int s2 = st & sb, c2 = ct & cb, e2 = et & eb;
   for (unsigned int m = s2; m; m &= m - 1) {
-    const float4 q = *reinterpret_cast<const float4*>(fo.rec[__ffs(m) - 1]);
+    const float4 q = lds_f4_nv(rec_s + 4u * kRec * (__ffs(m) - 1));
     const float bx = fmaf(dx, q.x, q.z);
 #pragma unroll
     for (int k = 0; k < 4; k++) sphere_pair(q, dx, bx, dy[k], idd[k], zb[2 * k], zb[2 * k + 1]);
   }
   for (unsigned int m = st ^ s2; m; m &= m - 1) {
-    const float4 q = *reinterpret_cast<const float4*>(fo.rec[__ffs(m) - 1]);
+    const float4 q = lds_f4_nv(rec_s + 4u * kRec * (__ffs(m) - 1));
     const float bx = fmaf(dx, q.x, q.z);
 #pragma unroll
     for (int k = 0; k < 2; k++) sphere_pair(q, dx, bx, dy[k], idd[k], zb[2 * k], zb[2 * k + 1]);
   }
   for (unsigned int m = sb ^ s2; m; m &= m - 1) {
-    const float4 q = *reinterpret_cast<const float4*>(fo.rec[__ffs(m) - 1]);
+    const float4 q = lds_f4_nv(rec_s + 4u * kRec * (__ffs(m) - 1));
     const float bx = fmaf(dx, q.x, q.z);
 #pragma unroll
     for (int k = 2; k < 4; k++) sphere_pair(q, dx, bx, dy[k], idd[k], zb[2 * k], zb[2 * k + 1]);
   }
   // cones and the palm cylinder
   for (unsigned int m = c2; m; m &= m - 1) {
-    const QuadLane Q = quad_lane<true>(fo.rec[kCone0 + __ffs(m) - 1], dx);
+    const QuadLane Q = quad_lane<true>(rec_s + 4u * kRec * (kCone0 + __ffs(m) - 1), dx);
 #pragma unroll
     for (int k = 0; k < 4; k++) quad_pair<true>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
   }
   for (unsigned int m = ct ^ c2; m; m &= m - 1) {
-    const QuadLane Q = quad_lane<true>(fo.rec[kCone0 + __ffs(m) - 1], dx);
+    const QuadLane Q = quad_lane<true>(rec_s + 4u * kRec * (kCone0 + __ffs(m) - 1), dx);
 #pragma unroll
     for (int k = 0; k < 2; k++) quad_pair<true>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
   }
   for (unsigned int m = cb ^ c2; m; m &= m - 1) {
-    const QuadLane Q = quad_lane<true>(fo.rec[kCone0 + __ffs(m) - 1], dx);
+    const QuadLane Q = quad_lane<true>(rec_s + 4u * kRec * (kCone0 + __ffs(m) - 1), dx);
 #pragma unroll
     for (int k = 2; k < 4; k++) quad_pair<true>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
   }
   for (unsigned int m = e2; m; m &= m - 1) {
-    const QuadLane Q = quad_lane<false>(fo.rec[kEll0 + __ffs(m) - 1], dx);
+    const QuadLane Q = quad_lane<false>(rec_s + 4u * kRec * (kEll0 + __ffs(m) - 1), dx);
 #pragma unroll
     for (int k = 0; k < 4; k++) quad_pair<false>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
   }
   for (unsigned int m = et ^ e2; m; m &= m - 1) {
-    const QuadLane Q = quad_lane<false>(fo.rec[kEll0 + __ffs(m) - 1], dx);
+    const QuadLane Q = quad_lane<false>(rec_s + 4u * kRec * (kEll0 + __ffs(m) - 1), dx);
 #pragma unroll
     for (int k = 0; k < 2; k++) quad_pair<false>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
   }
   for (unsigned int m = eb ^ e2; m; m &= m - 1) {
-    const QuadLane Q = quad_lane<false>(fo.rec[kEll0 + __ffs(m) - 1], dx);
+    const QuadLane Q = quad_lane<false>(rec_s + 4u * kRec * (kEll0 + __ffs(m) - 1), dx);
 #pragma unroll
     for (int k = 2; k < 4; k++) quad_pair<false>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
   }
   mbar_wait_s(bar_s, phase);
   phase ^= 1u;
-  score_lane<8, SUMS>(a, zb, obs_s, col, rowb, acc);
+  score_lane<8, SUMS>(a, zb, obs_ls, acc);
   __syncwarp();
 }
 

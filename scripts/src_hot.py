@@ -1,5 +1,6 @@
 """Per-source-line warp-level instruction counts and stall samples of one kernel from an ncu
-report (`--print-source cuda,sass`).  python scripts/src_hot.py rep.ncu-rep kernel_regex [N]"""
+report (`--print-source cuda,sass`).
+    python scripts/src_hot.py rep.ncu-rep kernel_regex [N] [launch_index]"""
 import csv
 import io
 import subprocess
@@ -9,9 +10,10 @@ import sys
 def main():
     rep, kern = sys.argv[1], sys.argv[2]
     top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+    skip = sys.argv[4] if len(sys.argv) > 4 else "0"
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name",
-                          "regex:" + kern, "--print-source", "cuda,sass"],
-                         capture_output=True, text=True).stdout
+                          "regex:" + kern, "--launch-skip", skip, "--launch-count", "1",
+                          "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
     fname, rows = "?", []
     for r in csv.reader(io.StringIO(out)):
         if not r:
