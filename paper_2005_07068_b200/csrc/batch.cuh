@@ -130,37 +130,114 @@ __device__ __forceinline__ int build_block_list(const FkOut& fo, uint4* out, uin
 #define HP_FK_WARPS 4  // particles (warps) per k_fk_batch CTA
 #endif
 constexpr int kFkWarps = HP_FK_WARPS;
+static_assert(kFkWarps == 4, "k_fk_batch's work lists assume 4 poses per CTA");
+// One CTA of 4 warps scores FK for 4 poses cooperatively, with every phase laid out over
+// the CTA's 128 threads so that a warp runs one kind of work (no serialised branches of
+// different primitive kinds in a warp, few idle lanes):
+//   A  the 4 x 26 pose values and the 4 x 23 sincos (fp64), one per thread
+//   B  the 4 x 5 finger chains (fp64), one per thread
+//   C  the 4 x 38 EXACT records + boxes, sorted by kind: 80 spheres, 60 cones / cylinders,
+//      12 ellipsoids, in two passes of 128 threads
+//   C' (a pose that may cross z_near: its EXACT records to global memory, warp per pose)
+//   C" the 72 quadric records converted to the FAST layout (fp64), one pass
+//   D  per warp (= pose): union box, near-plane flag, kc; the record leaves by one bulk
+//      copy while the warp builds the pose's block list
 template <typename PoseT>
 __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
     k_fk_batch(const EvalArgs a) {
   __shared__ __align__(16) FkScratch s_fk[kFkWarps];
   __shared__ __align__(16) FkOut s_out[kFkWarps];
-  __shared__ __align__(16) float4 s_shp[kFkWarps][kNcone];  // cone capsules (fk_team)
+  __shared__ __align__(16) float4 s_shp[kFkWarps][kNcone];  // cone capsules
   static_assert(sizeof(FkScratch) >= 2 * kMaxBand * sizeof(uint2), "band masks alias s_fk");
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 #if HP_FK_PDL
   // the renderer (launched with programmatic stream serialisation) may start its prologue
   // on SMs this grid frees; it waits for this grid's completion before reading its output
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
-  const int p = blockIdx.x * kFkWarps + warp;  // one warp per particle
-  if (p >= a.n) return;  // warp-uniform; only warp-local synchronisation below
-  const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
-  fk_team<PoseT, 1>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk[warp], s_out[warp],
-                    static_cast<FkExact*>(a.fkx_g) + p, s_shp[warp]);
-  // the record leaves by one bulk copy while the warp builds the tile list: every lane
+  const int p0 = blockIdx.x * kFkWarps;
+  const int np = min(kFkWarps, a.n - p0);  // poses of this CTA (the last CTA may be short)
+  // ---- A: pose values and sincos ----
+  if (tid < np * kNdof) {
+    const int q = tid / kNdof, d = tid - q * kNdof;
+    const double v = (double)static_cast<const PoseT*>(a.poses)[(size_t)(p0 + q) * kNdof + d];
+    s_fk[q].h[d] = v;
+    if (d >= 3) sincos(v, &s_fk[q].sn[d], &s_fk[q].cs[d]);
+  }
+  __syncthreads();
+  // ---- B: finger chains ----
+  if (tid < np * 5) {
+    const int q = tid / 5, f = tid - q * 5;
+    int bad = 0;
+    for (int d = 0; d < kNdof; d++) bad |= !isfinite(s_fk[q].h[d]);
+    fk_finger_chain(s_fk[q], a.dims, f, bad);
+  }
+  __syncthreads();
+  // ---- C: EXACT records + boxes, kind-sorted items ----
+  constexpr int kNs = kFkWarps * kCone0, kNc = kFkWarps * (kEll0 - kCone0);
+  constexpr int kItems = kFkWarps * kNprim;
+#pragma unroll 1
+  for (int i = tid; i < kItems; i += kFkWarps * 32) {
+    int q, j;
+    if (i < kNs) {
+      q = i / kCone0;
+      j = i - q * kCone0;
+    } else if (i < kNs + kNc) {
+      const int k = i - kNs;
+      q = k / (kEll0 - kCone0);
+      j = kCone0 + k - q * (kEll0 - kCone0);
+    } else {
+      const int k = i - kNs - kNc;
+      q = k / (kNprim - kEll0);
+      j = kEll0 + k - q * (kNprim - kEll0);
+    }
+    if (q < np) {
+      float zmin;
+      build_prim(j, s_fk[q], a.dims, a.cam, s_out[q].rec[j], s_out[q].box[j], zmin,
+                 j >= kCone0 && j < kCyl ? &s_shp[q][j - kCone0] : nullptr);
+      s_fk[q].nearf[j] = zmin > a.cam.znear * 1.001f;
+    }
+  }
+  __syncthreads();
+  // ---- C': a pose that may cross z_near keeps its EXACT records (global memory) ----
+  if (warp < np) {
+    const int p = p0 + warp;
+    int nok = 1;
+    for (int j = lane; j < kNprim; j += 32) nok &= s_fk[warp].nearf[j];
+    if (!__all_sync(0xffffffffu, nok)) {
+      FkExact* xg = static_cast<FkExact*>(a.fkx_g) + p;
+      for (int i = lane; i < kNprim * kRec / 4; i += 32)
+        reinterpret_cast<float4*>(xg->rec)[i] = reinterpret_cast<const float4*>(s_out[warp].rec)[i];
+    }
+  }
+  __syncthreads();
+  // ---- C": FAST records of the quadrics (cones / cylinders first, then ellipsoids) ----
+  if (tid < kFkWarps * (kNprim - kCone0)) {
+    int q, j;
+    if (tid < kNc) {
+      q = tid / (kEll0 - kCone0);
+      j = kCone0 + tid - q * (kEll0 - kCone0);
+    } else {
+      const int k = tid - kNc;
+      q = k / (kNprim - kEll0);
+      j = kEll0 + k - q * (kNprim - kEll0);
+    }
+    if (q < np) to_fast(s_out[q].rec[j], j);
+  }
+  __syncthreads();
+  if (warp >= np) return;  // warp-uniform; only warp-local synchronisation below
+  // ---- D: per pose ----
+  const int p = p0 + warp;
+  fk_finish_warp(s_fk[warp], s_out[warp], a.cost.kc_rest);
+  // the record leaves by one bulk copy while the warp builds the block list: every lane
   // orders its record writes before the async proxy, then lane 0 issues the copy
   fence_proxy_async();
   __syncwarp();
   if (lane == 0)
     bulk_s2g(static_cast<FkOut*>(a.fk_g) + p, &s_out[warp], (uint32_t)sizeof(FkOut));
-  FKPROF(4)
   uint2* band = reinterpret_cast<uint2*>(&s_fk[warp]);  // FK scratch is dead by now
-  const float4* shp = s_shp[warp];
-  __syncwarp();
   const int cnt = build_block_list(s_out[warp], a.tiles_g + (size_t)p * kMaxTiles, band,
-                                   band + kMaxBand, shp);
-  FKPROF(5)
+                                   band + kMaxBand, s_shp[warp]);
   if (lane == 0) {
     int ntl = cnt;
     if (!s_out[warp].near_ok) {  // some primitive may cross z_near: the exact pass renders it
@@ -172,7 +249,6 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
     a.ntl_g[p] = ntl;
     bulk_wait_all();  // the record copy completes before the CTA's shared memory retires
   }
-  FKPROF(6)
 }
 
 // NEAR = false: the batch renderer, 16 x 16 warp blocks from k_fk_batch's block list (the

@@ -379,6 +379,106 @@ __device__ __noinline__ void to_fast(float* rec, int j) {
   }
 }
 
+// One warp: the union box of the 38 primitive boxes, the near-plane flag and kc(h) (P:L130,
+// AMB-7) of the pose in s / out.
+__device__ __forceinline__ void fk_finish_warp(const FkScratch& s, FkOut& out, double kc_rest) {
+  const int lane = threadIdx.x & 31;
+  // ---- warp 0: union box, near-plane flag, kc ----
+  // (the solid is the convex hull of its generators, so zmin bounds its nearest point; the
+  // 1e-3 relative slack covers the fp32 evaluation)
+  int near_ok = 1;
+  int4 u = make_int4(1 << 30, 1 << 30, -1, -1);
+  for (int j = lane; j < kNprim; j += 32) {
+    near_ok &= s.nearf[j];
+    const int4 b = out.box[j];
+    if (b.x <= b.z) {
+      u.x = min(u.x, b.x);
+      u.y = min(u.y, b.y);
+      u.z = max(u.z, b.z);
+      u.w = max(u.w, b.w);
+    }
+  }
+  near_ok = __all_sync(0xffffffffu, near_ok);
+  for (int off = 16; off; off >>= 1) {
+    u.x = min(u.x, __shfl_xor_sync(0xffffffffu, u.x, off));
+    u.y = min(u.y, __shfl_xor_sync(0xffffffffu, u.y, off));
+    u.z = max(u.z, __shfl_xor_sync(0xffffffffu, u.z, off));
+    u.w = max(u.w, __shfl_xor_sync(0xffffffffu, u.w, off));
+  }
+  if (lane == 0) {
+    if (s.bad || u.z < u.x) u = make_int4(1, 1, 0, 0);
+    out.ubox = u;
+    out.near_ok = near_ok && !s.bad;
+    // kc(h) = sum over (index,middle), (middle,ring), (ring,little) of -min(phi, 0)
+    double kc = 0.0;
+    for (int f = 1; f <= 3; f++) {
+      double phi = s.h[6 + 4 * f + 1] - s.h[6 + 4 * (f + 1) + 1] + kc_rest;
+      kc += -fmin(phi, 0.0);
+    }
+    out.kc = s.bad ? __longlong_as_double(0x7ff8000000000000ll) : kc;
+  }
+  __syncwarp();
+}
+
+// Phase B of FK for finger f (sincos of the pose already in s.sn / s.cs): R_W, the chain of
+// finger f in the camera frame (sparse column updates: B <- B Rz(MPz) touches columns 0, 1,
+// B <- B Rx(t) columns 1, 2; the segment runs along -B[:,1]), its joints and segment
+// frames.  f = 0 also stores R_W and the non-finite flag.
+__device__ __forceinline__ void fk_finger_chain(FkScratch& s, const DimsD& dm, int f, int bad) {
+    // R_W = Rz(th_z) Ry(th_y) Rx(th_x)  (AMB-10), written out
+    const double cx = s.cs[3], sx = s.sn[3], cy = s.cs[4], sy = s.sn[4], cz = s.cs[5],
+                 sz = s.sn[5];
+    const double r0[3] = {cy, sy * sx, sy * cx}, r1[3] = {0.0, cx, -sx},
+                 r2[3] = {-sy, cy * sx, cy * cx};  // rows of Ry Rx
+    double RW[3][3];
+    for (int j = 0; j < 3; j++) {
+      RW[0][j] = cz * r0[j] - sz * r1[j];
+      RW[1][j] = sz * r0[j] + cz * r1[j];
+      RW[2][j] = r2[j];
+    }
+    if (f == 0) {
+      for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) s.RW[i][j] = RW[i][j];
+      s.bad = bad;
+    }
+    // B = R_W R_f0 (camera-frame base frame of the finger)
+    double B[3][3];
+    if (f == 0) mat3_mul(RW, dm.RT0, B);
+    else
+      for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) B[i][j] = RW[i][j];
+    const int o = 6 + 4 * f;  // (MPx, MPz, PIP, DIP), Eq. (1)
+    {                         // B <- B Rz(MPz)
+      const double c = s.cs[o + 1], sn = s.sn[o + 1];
+      for (int i = 0; i < 3; i++) {
+        const double b0 = B[i][0], b1 = B[i][1];
+        B[i][0] = c * b0 + sn * b1;
+        B[i][1] = c * b1 - sn * b0;
+      }
+    }
+    double J[3];
+    for (int i = 0; i < 3; i++)
+      J[i] = s.h[i] + RW[i][0] * dm.base[f][0] + RW[i][1] * dm.base[f][1] +
+             RW[i][2] * dm.base[f][2];
+    for (int i = 0; i < 3; i++) s.J[f][0][i] = J[i];
+    for (int k = 0; k < 3; k++) {  // B <- B Rx(MPx | PIP | DIP); J += B (0, -L, 0)
+      const int ai = k == 0 ? o : o + 1 + k;
+      const double c = s.cs[ai], sn = s.sn[ai];
+      for (int i = 0; i < 3; i++) {
+        const double b1 = B[i][1], b2 = B[i][2];
+        B[i][1] = c * b1 + sn * b2;
+        B[i][2] = c * b2 - sn * b1;
+      }
+      const double L = dm.len[f][k];
+      for (int i = 0; i < 3; i++) {
+        J[i] -= L * B[i][1];
+        s.J[f][k + 1][i] = J[i];
+      }
+      for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) s.Rs[f][k][i][j] = B[i][j];
+    }
+  }
+
 // FK on a team of 1 or 2 warps (warp 0 = the team leader).  pose: 26 values (float or
 // double).  Writes `out`; `s` keeps the fp64 joints for the debug hook.
 //   phase A (warp 0): load the pose, sincos of the 23 angles (one per lane, fp64)
@@ -418,61 +518,7 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
     int bad = 0;
     if (lane < kNdof) bad = !isfinite(s.h[lane]);
     bad = __any_sync(0xffffffffu, bad);
-    if (lane < 5) {
-      // R_W = Rz(th_z) Ry(th_y) Rx(th_x)  (AMB-10), written out
-      const double cx = s.cs[3], sx = s.sn[3], cy = s.cs[4], sy = s.sn[4], cz = s.cs[5],
-                   sz = s.sn[5];
-      const double r0[3] = {cy, sy * sx, sy * cx}, r1[3] = {0.0, cx, -sx},
-                   r2[3] = {-sy, cy * sx, cy * cx};  // rows of Ry Rx
-      double RW[3][3];
-      for (int j = 0; j < 3; j++) {
-        RW[0][j] = cz * r0[j] - sz * r1[j];
-        RW[1][j] = sz * r0[j] + cz * r1[j];
-        RW[2][j] = r2[j];
-      }
-      const int f = lane;
-      if (f == 0) {
-        for (int i = 0; i < 3; i++)
-          for (int j = 0; j < 3; j++) s.RW[i][j] = RW[i][j];
-        s.bad = bad;
-      }
-      // B = R_W R_f0 (camera-frame base frame of the finger)
-      double B[3][3];
-      if (f == 0) mat3_mul(RW, dm.RT0, B);
-      else
-        for (int i = 0; i < 3; i++)
-          for (int j = 0; j < 3; j++) B[i][j] = RW[i][j];
-      const int o = 6 + 4 * f;  // (MPx, MPz, PIP, DIP), Eq. (1)
-      {                         // B <- B Rz(MPz)
-        const double c = s.cs[o + 1], sn = s.sn[o + 1];
-        for (int i = 0; i < 3; i++) {
-          const double b0 = B[i][0], b1 = B[i][1];
-          B[i][0] = c * b0 + sn * b1;
-          B[i][1] = c * b1 - sn * b0;
-        }
-      }
-      double J[3];
-      for (int i = 0; i < 3; i++)
-        J[i] = s.h[i] + RW[i][0] * dm.base[f][0] + RW[i][1] * dm.base[f][1] +
-               RW[i][2] * dm.base[f][2];
-      for (int i = 0; i < 3; i++) s.J[f][0][i] = J[i];
-      for (int k = 0; k < 3; k++) {  // B <- B Rx(MPx | PIP | DIP); J += B (0, -L, 0)
-        const int ai = k == 0 ? o : o + 1 + k;
-        const double c = s.cs[ai], sn = s.sn[ai];
-        for (int i = 0; i < 3; i++) {
-          const double b1 = B[i][1], b2 = B[i][2];
-          B[i][1] = c * b1 + sn * b2;
-          B[i][2] = c * b2 - sn * b1;
-        }
-        const double L = dm.len[f][k];
-        for (int i = 0; i < 3; i++) {
-          J[i] -= L * B[i][1];
-          s.J[f][k + 1][i] = J[i];
-        }
-        for (int i = 0; i < 3; i++)
-          for (int j = 0; j < 3; j++) s.Rs[f][k][i][j] = B[i][j];
-      }
-    }
+    if (lane < 5) fk_finger_chain(s, dm, lane, bad);
     __syncwarp();
     if (TEAM >= 2) asm volatile("bar.arrive 2, %0;" ::"n"(32 * TEAM) : "memory");
   } else if (TEAM >= 2) {
@@ -528,41 +574,7 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
     __syncwarp();
   }
   FKPROF(3)
-  // ---- warp 0: union box, near-plane flag, kc ----
-  // (the solid is the convex hull of its generators, so zmin bounds its nearest point; the
-  // 1e-3 relative slack covers the fp32 evaluation)
-  int near_ok = 1;
-  int4 u = make_int4(1 << 30, 1 << 30, -1, -1);
-  for (int j = lane; j < kNprim; j += 32) {
-    near_ok &= s.nearf[j];
-    const int4 b = out.box[j];
-    if (b.x <= b.z) {
-      u.x = min(u.x, b.x);
-      u.y = min(u.y, b.y);
-      u.z = max(u.z, b.z);
-      u.w = max(u.w, b.w);
-    }
-  }
-  near_ok = __all_sync(0xffffffffu, near_ok);
-  for (int off = 16; off; off >>= 1) {
-    u.x = min(u.x, __shfl_xor_sync(0xffffffffu, u.x, off));
-    u.y = min(u.y, __shfl_xor_sync(0xffffffffu, u.y, off));
-    u.z = max(u.z, __shfl_xor_sync(0xffffffffu, u.z, off));
-    u.w = max(u.w, __shfl_xor_sync(0xffffffffu, u.w, off));
-  }
-  if (lane == 0) {
-    if (s.bad || u.z < u.x) u = make_int4(1, 1, 0, 0);
-    out.ubox = u;
-    out.near_ok = near_ok && !s.bad;
-    // kc(h) = sum over (index,middle), (middle,ring), (ring,little) of -min(phi, 0)
-    double kc = 0.0;
-    for (int f = 1; f <= 3; f++) {
-      double phi = s.h[6 + 4 * f + 1] - s.h[6 + 4 * (f + 1) + 1] + kc_rest;
-      kc += -fmin(phi, 0.0);
-    }
-    out.kc = s.bad ? __longlong_as_double(0x7ff8000000000000ll) : kc;
-  }
-  __syncwarp();
+  fk_finish_warp(s, out, kc_rest);
 }
 
 template <typename PoseT>
