@@ -142,6 +142,20 @@ class ClockSampler:
                           "region"}
 
 
+def cpu_model() -> str:
+    """The host CPU model (recorded beside the core count)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
 def cpu_baseline(seconds: float, swarm: np.ndarray):
     """The oracle (culled mode, all host cores) on a bounded sample of the C4 workload."""
     import oracle as O
@@ -173,7 +187,7 @@ def cpu_baseline(seconds: float, swarm: np.ndarray):
         brute += len(swarm[brute % len(swarm):][:cores])
     brute_rate = brute / (time.perf_counter() - t2)
     return {"value": done / dt, "unit": "hyp/s", "cores": cores, "kind": "oracle",
-            "value_1core": one_rate, "value_brute": brute_rate,
+            "cpu_model": cpu_model(), "value_1core": one_rate, "value_brute": brute_rate,
             "sample": f"{done} poses of the C4 swarm in order (cycling after {len(swarm)}) at "
                       f"640x480, oracle culled mode (fp64, bitwise equal to brute force), "
                       f"{dt:.1f} s"}
@@ -184,8 +198,13 @@ def arm_config(world: int) -> dict:
     return {"workload": f"C4: 640x480 synthetic frame rendered from h_A, "
                         f"{PER_RANK}-pose mid-fit swarm per GPU (seed 7068)",
             "poses_per_gpu": PER_RANK, "resolution": "640x480",
-            "parallelism": f"particle-sharded x{world}, cost allgather",
-            "l2": "flushed between steps (256 MiB write, outside the events)"}
+            "parallelism": f"particle-sharded x{world}, cost allgather"}
+
+
+# how each arm treats L2 between timed steps (its own key: the workload config above is
+# identical for both arms)
+L2_GPU = "flushed between steps (256 MiB write, outside the events)"
+L2_CPU = "n/a (CPU oracle)"
 
 
 def run_reference(args):
@@ -211,8 +230,9 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(arm_config(args.gpus), l2="n/a (CPU oracle)"),
+            "config": arm_config(args.gpus), "l2": L2_CPU,
             "cpu_baseline": {"value": value, "unit": "hyp/s", "cores": cores, "kind": "oracle",
+                             "cpu_model": cpu_model(),
                              "sample": f"{sample} poses of the C4 swarm per step (a bounded "
                                        "slice of the workload), oracle culled mode"},
             "e2e": {"value": value, "unit": "hyp/s", "h2d_bytes_per_step": 0,
@@ -527,7 +547,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": arm_config(world),
+            "config": arm_config(world), "l2": L2_GPU,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": ncu_traffic(),
                          "kernel": "k_render_persist (render+score+cost; FK records and tile "
