@@ -184,15 +184,16 @@ __device__ __forceinline__ void put3(float* r, int off, const double v[3]) {
 // expansion point is the projection of cen, rounded to fp32 first so the coefficients
 // belong to the point the kernel subtracts.  axis (may be null): the axial row of M and
 // the half length (cones / cylinder).
-__device__ __noinline__ void write_fast_quadric(float* rec, const double cen[3], const double M[3][3],
+__device__ __forceinline__ void write_fast_quadric(float* rec, const double cen[3], const double M[3][3],
                                    const double q[3], double g2, double h, bool axial,
                                    double hl) {
   double cl[3];
   for (int a = 0; a < 3; a++) cl[a] = M[a][0] * cen[0] + M[a][1] * cen[1] + M[a][2] * cen[2];
-  float xp = 0.f, yp = 0.f;
+  float xp = 0.f, yp = 0.f;  // any fp32 point will do (the coefficients are computed for it)
   if (cen[2] > 1e-3) {
-    xp = (float)(cen[0] / cen[2]);
-    yp = (float)(cen[1] / cen[2]);
+    const float iz = __frcp_rn((float)cen[2]);
+    xp = (float)cen[0] * iz;
+    yp = (float)cen[1] * iz;
   }
   const double dp[3] = {(double)xp, (double)yp, 1.0};
   double m0[3], m1[3], dl[3];
@@ -362,7 +363,7 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm,
 // In place: the EXACT record of quadric primitive j (fp32 geometry) becomes its FAST record
 // (polynomial coefficients computed in fp64 from that geometry).  Spheres keep their
 // record (the FAST sphere layout is the EXACT one's head).
-__device__ __noinline__ void to_fast(float* rec, int j) {
+__device__ __forceinline__ void to_fast(float* rec, int j) {
   if (j < kCone0) return;
   double c[3], M[3][3];
   for (int i = 0; i < 3; i++) c[i] = rec[kC + i];
