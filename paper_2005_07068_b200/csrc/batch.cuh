@@ -173,58 +173,49 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
     fk_finger_chain(s_fk[q], a.dims, f, bad);
   }
   __syncthreads();
-  // ---- C: EXACT records + boxes, kind-sorted items ----
-  constexpr int kNs = kFkWarps * kCone0, kNc = kFkWarps * (kEll0 - kCone0);
-  constexpr int kItems = kFkWarps * kNprim;
+  // ---- C: records + boxes, kind-sorted items: the sphere records (EXACT = FAST) and boxes,
+  // the quadrics' boxes, then their FAST records straight from the frames (build_fast) ----
+  constexpr int kNs = kFkWarps * kCone0, kNq = kFkWarps * (kNprim - kCone0);
+  constexpr int kItems = kNs + 2 * kNq;
 #pragma unroll 1
   for (int i = tid; i < kItems; i += kFkWarps * 32) {
-    int q, j;
-    if (i < kNs) {
-      q = i / kCone0;
-      j = i - q * kCone0;
-    } else if (i < kNs + kNc) {
-      const int k = i - kNs;
-      q = k / (kEll0 - kCone0);
-      j = kCone0 + k - q * (kEll0 - kCone0);
+    if (i < kNs + kNq) {
+      int q, j;
+      if (i < kNs) {
+        q = i / kCone0;
+        j = i - q * kCone0;
+      } else {
+        const int k = i - kNs;
+        q = k / (kNprim - kCone0);
+        j = kCone0 + k - q * (kNprim - kCone0);
+      }
+      if (q < np) {
+        float zmin, xr[kRec];  // a quadric's EXACT record is not kept here (see C')
+        build_prim(j, s_fk[q], a.dims, a.cam, j < kCone0 ? s_out[q].rec[j] : xr,
+                   s_out[q].box[j], zmin,
+                   j >= kCone0 && j < kCyl ? &s_shp[q][j - kCone0] : nullptr);
+        s_fk[q].nearf[j] = zmin > a.cam.znear * 1.001f;
+      }
     } else {
-      const int k = i - kNs - kNc;
-      q = k / (kNprim - kEll0);
-      j = kEll0 + k - q * (kNprim - kEll0);
-    }
-    if (q < np) {
-      float zmin;
-      build_prim(j, s_fk[q], a.dims, a.cam, s_out[q].rec[j], s_out[q].box[j], zmin,
-                 j >= kCone0 && j < kCyl ? &s_shp[q][j - kCone0] : nullptr);
-      s_fk[q].nearf[j] = zmin > a.cam.znear * 1.001f;
+      const int k = i - kNs - kNq;
+      const int q = k / (kNprim - kCone0), j = kCone0 + k - q * (kNprim - kCone0);
+      if (q < np) build_fast(j, s_fk[q], a.dims, s_out[q].rec[j]);
     }
   }
   __syncthreads();
-  // ---- C': a pose that may cross z_near keeps its EXACT records (global memory) ----
+  // ---- C': a pose that may cross z_near (rare) keeps its EXACT records (global memory) ----
   if (warp < np) {
-    const int p = p0 + warp;
     int nok = 1;
     for (int j = lane; j < kNprim; j += 32) nok &= s_fk[warp].nearf[j];
     if (!__all_sync(0xffffffffu, nok)) {
-      FkExact* xg = static_cast<FkExact*>(a.fkx_g) + p;
-      for (int i = lane; i < kNprim * kRec / 4; i += 32)
-        reinterpret_cast<float4*>(xg->rec)[i] = reinterpret_cast<const float4*>(s_out[warp].rec)[i];
+      FkExact* xg = static_cast<FkExact*>(a.fkx_g) + p0 + warp;
+      for (int j = lane; j < kNprim; j += 32) {
+        float zmin;
+        int4 box;
+        build_prim(j, s_fk[warp], a.dims, a.cam, xg->rec[j], box, zmin, nullptr);
+      }
     }
   }
-  __syncthreads();
-  // ---- C": FAST records of the quadrics (cones / cylinders first, then ellipsoids) ----
-  if (tid < kFkWarps * (kNprim - kCone0)) {
-    int q, j;
-    if (tid < kNc) {
-      q = tid / (kEll0 - kCone0);
-      j = kCone0 + tid - q * (kEll0 - kCone0);
-    } else {
-      const int k = tid - kNc;
-      q = k / (kNprim - kEll0);
-      j = kEll0 + k - q * (kNprim - kEll0);
-    }
-    if (q < np) to_fast(s_out[q].rec[j], j);
-  }
-  __syncthreads();
   if (warp >= np) return;  // warp-uniform; only warp-local synchronisation below
   // ---- D: per pose ----
   const int p = p0 + warp;

@@ -11,7 +11,7 @@ namespace hp {
 // (S > 1 splits per particle keep every SM busy) and for the depth-image hooks.
 // ---------------------------------------------------------------------------------------
 #ifndef HP_EVAL_FK_TEAM
-#define HP_EVAL_FK_TEAM 3  // k_eval's FK team: warps 0..2 (one primitive kind per warp)
+#define HP_EVAL_FK_TEAM 4  // k_eval's FK team: warps 0..3 (fk_team<4>)
 #endif
 constexpr int kEvalFkTeam = HP_EVAL_FK_TEAM;
 template <int NW, typename PoseT, int MODE, bool NEARCODE = true>
@@ -49,12 +49,10 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
         pso_update_warp(a.pso, p, a.pso_k, a.x_in, a.v_in, a.x_out, a.v_out, sidx == 0, s_pose,
                         /*deferred=*/true);
       __syncwarp();
-      fk_team<double, kEvalFkTeam>(s_pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out,
-                                   NEARCODE ? &s_x : nullptr);
+      fk_team<double, kEvalFkTeam>(s_pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out, &s_x);
     } else {
       const PoseT* pose = static_cast<const PoseT*>(a.poses) + (size_t)p * kNdof;
-      fk_team<PoseT, kEvalFkTeam>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out,
-                                  NEARCODE ? &s_x : nullptr);
+      fk_team<PoseT, kEvalFkTeam>(pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out, &s_x);
     }
   } else {
     // while the FK team runs: stage the per-column / per-row ray directions (k_ray_table)

@@ -360,21 +360,64 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm,
   box = prim_box(ng, gc, gA, cam, zmin);
 }
 
-// In place: the EXACT record of quadric primitive j (fp32 geometry) becomes its FAST record
-// (polynomial coefficients computed in fp64 from that geometry).  Spheres keep their
-// record (the FAST sphere layout is the EXACT one's head).
-__device__ __forceinline__ void to_fast(float* rec, int j) {
-  if (j < kCone0) return;
+// FAST record of quadric primitive j (cone / cylinder / ellipsoid, j >= kCone0) straight
+// from the fp64 FK geometry (the same frames build_prim uses), independent of the EXACT
+// record and the box, so a team can build both in parallel.  Spheres: their FAST record is
+// the EXACT record's head (build_prim).
+__device__ __forceinline__ void build_fast(int j, const FkScratch& s, const DimsD& dm,
+                                           float* rec) {
   double c[3], M[3][3];
-  for (int i = 0; i < 3; i++) c[i] = rec[kC + i];
-  for (int a = 0; a < 3; a++)
-    for (int i = 0; i < 3; i++) M[a][i] = rec[kM + 3 * a + i];
-  if (j < kEll0) {  // cones and the cylinder (k = 0, r_m = 1 in its scaled rows):
+  if (j < kCyl) {  // truncated cone J_k -> J_{k+1}: rows e1, e2, axis; midpoint origin
+    int f, k;
+    if (j < 32) {
+      f = 1 + (j - kCone0) / 3;
+      k = (j - kCone0) % 3;
+    } else {
+      f = 0;
+      k = j - 32 + 1;
+    }
+    for (int i = 0; i < 3; i++) {
+      M[0][i] = s.Rs[f][k][i][0];
+      M[1][i] = s.Rs[f][k][i][2];
+      M[2][i] = -s.Rs[f][k][i][1];
+      c[i] = 0.5 * (s.J[f][k][i] + s.J[f][k + 1][i]);
+    }
     // x^2 + y^2 - (r_m + k z)^2: Q = diag(1, 1, -k^2), g = (0, 0, -r_m k), h = -r_m^2
-    const double rm = rec[kRm], k = rec[kK], hl = rec[kHl];
-    const double q[3] = {1.0, 1.0, -k * k};
-    write_fast_quadric(rec, c, M, q, -rm * k, -rm * rm, true, hl);
-  } else {  // ellipsoids: |l|^2 - 1
+    const double rm = 0.5 * (dm.rad[f][k] + dm.rad[f][k + 1]), kk = dm.cone_k[f][k];
+    const double q[3] = {1.0, 1.0, -kk * kk};
+    write_fast_quadric(rec, c, M, q, -rm * kk, -rm * rm, true, 0.5 * dm.len[f][k]);
+  } else if (j == kCyl) {  // palm: (x/a)^2 + (z/b)^2 - 1, axial y_H in [-len, 0]
+    const double iw = 1.0 / dm.palm_half_w, it = 1.0 / dm.palm_half_t;
+    for (int i = 0; i < 3; i++) {
+      M[0][i] = s.RW[i][0] * iw;
+      M[1][i] = s.RW[i][2] * it;
+      M[2][i] = s.RW[i][1];
+      c[i] = s.h[i] - 0.5 * dm.palm_len * s.RW[i][1];
+    }
+    const double q[3] = {1.0, 1.0, 0.0};
+    write_fast_quadric(rec, c, M, q, 0.0, -1.0, true, 0.5 * dm.palm_len);
+  } else {  // ellipsoids: |l|^2 - 1 with rows = axes / semi-axes
+    double sd[3];
+    if (j == kEll0) {
+      for (int i = 0; i < 3; i++) c[i] = 0.5 * (s.J[0][0][i] + s.J[0][1][i]);
+      for (int a = 0; a < 3; a++)
+        for (int i = 0; i < 3; i++) M[a][i] = s.Rs[0][0][i][a];
+      sd[0] = dm.th_x;
+      sd[1] = 0.5 * dm.len[0][0];
+      sd[2] = dm.th_z;
+    } else {
+      const double yc = j == kEll0 + 1 ? 0.0 : -dm.palm_len;
+      for (int i = 0; i < 3; i++) c[i] = s.h[i] + yc * s.RW[i][1];
+      for (int a = 0; a < 3; a++)
+        for (int i = 0; i < 3; i++) M[a][i] = s.RW[i][a];
+      sd[0] = dm.palm_half_w;
+      sd[1] = dm.cap_half;
+      sd[2] = dm.palm_half_t;
+    }
+    for (int a = 0; a < 3; a++) {
+      const double is = 1.0 / sd[a];
+      for (int i = 0; i < 3; i++) M[a][i] *= is;
+    }
     const double q[3] = {1.0, 1.0, 1.0};
     write_fast_quadric(rec, c, M, q, 0.0, -1.0, false, 0.0);
   }
@@ -506,7 +549,7 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
                         double kc_rest, FkScratch& s, FkOut& out, FkExact* xrec = nullptr,
                         float4* shp = nullptr) {
   FKPROF(0)
-  static_assert(TEAM >= 1 && TEAM <= 3, "FK teams of 1..3 warps (warps 0..TEAM-1 of the CTA)");
+  static_assert(TEAM == 1 || TEAM == 4, "FK teams of 1 or 4 warps (warps 0..TEAM-1 of the CTA)");
   const int lane = threadIdx.x & 31, w = TEAM >= 2 ? (int)(threadIdx.x >> 5) : 0;
   if (w == 0) {
     if (lane < kNdof) {
@@ -528,20 +571,23 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
   FKPROF(2)
   // ---- phase C: records + boxes ----
   if (TEAM >= 2) {
-    // TEAM 2: warp 0 spheres, warp 1 the 18 others; TEAM 3: spheres | cones | the rest
-    const int j0 = w == 0 ? 0 : (w == 1 ? kCone0 : kCyl);
-    const int j1 = w == 0 ? kCone0 : (w == 1 ? (TEAM == 3 ? kCyl : kNprim) : kNprim);
-    const int j = j0 + lane;
-    if (j < j1) {
-      float zmin;
-      build_prim(j, s, dm, cam, out.rec[j], out.box[j], zmin,
-                 shp && j >= kCone0 && j < kCyl ? shp + (j - kCone0) : nullptr);
-      s.nearf[j] = zmin > cam.znear * 1.001f;
-      if (xrec)
-        for (int i = 0; i < kRec; i += 4)
-          *reinterpret_cast<float4*>(&xrec->rec[j][i]) =
-              *reinterpret_cast<const float4*>(&out.rec[j][i]);
-      to_fast(out.rec[j], j);
+    // TEAM 4: warp 0 the 20 spheres (record = EXACT head = FAST), warp 1 the 14 cones and
+    // warp 2 the cylinder + 3 ellipsoids (EXACT records into xrec, boxes), warp 3 the 18
+    // FAST quadric records straight from the frames, in parallel with warps 1-2
+    if (w == 3) {
+      if (lane < kNprim - kCone0) build_fast(kCone0 + lane, s, dm, out.rec[kCone0 + lane]);
+    } else {
+      const int j0 = w == 0 ? 0 : (w == 1 ? kCone0 : kCyl);
+      const int j1 = w == 0 ? kCone0 : (w == 1 ? kCyl : kNprim);
+      const int j = j0 + lane;
+      if (j < j1) {
+        float zmin;
+        float* xr = xrec->rec[j];
+        build_prim(j, s, dm, cam, xr, out.box[j], zmin, nullptr);
+        s.nearf[j] = zmin > cam.znear * 1.001f;
+        if (j < kCone0)  // spheres: the FAST record is the EXACT one's head
+          *reinterpret_cast<float4*>(out.rec[j]) = *reinterpret_cast<const float4*>(xr);
+      }
     }
     if (w != 0) {
       asm volatile("bar.arrive 1, %0;" ::"n"(32 * TEAM) : "memory");
@@ -570,8 +616,7 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
           reinterpret_cast<float4*>(xrec->rec)[i] =
               reinterpret_cast<const float4*>(out.rec)[i];
     }
-    for (int k = 0; k < nj; k++) to_fast(out.rec[lane < 10 ? 2 * lane + k : lane + 10],
-                                         lane < 10 ? 2 * lane + k : lane + 10);
+    if (lane < kNprim - kCone0) build_fast(kCone0 + lane, s, dm, out.rec[kCone0 + lane]);
     __syncwarp();
   }
   FKPROF(3)
