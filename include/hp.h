@@ -255,6 +255,10 @@ hp_status hp_pso_state(hp_ctx* ctx, int32_t particles, int32_t D, double* X, dou
  * output may be NULL.  Synchronous. */
 hp_status hp_debug_fk(hp_ctx* ctx, const double* pose, float* records, int32_t* boxes,
                       double* joints, double* kc);
+/* The FK output record k_fk_batch left for pose p of the last batch-path evaluation
+ * (records [38][24] FAST layout, boxes [38][4]), host buffers, synchronous: the batch path's
+ * FK against hp_debug_fk's. */
+hp_status hp_debug_batch_fk(hp_ctx* ctx, int64_t p, float* records, int32_t* boxes);
 /* Depth image [H][W] fp32 (device) of the pose pose_dev (device fp32 [26]) produced by
  * the same tile/culling/intersection code as hp_eval_costs.  Async. */
 hp_status hp_debug_render(hp_ctx* ctx, const float* pose_dev, float* depth_dev, void* stream);

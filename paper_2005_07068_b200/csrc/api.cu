@@ -1023,6 +1023,19 @@ hp_status hp_eval_sums_f64(hp_ctx* ctx, const double* poses, int64_t n, uint64_t
   return eval_common(ctx, poses, n, nullptr, costs64, sums, (cudaStream_t)stream, 0, true);
 }
 
+hp_status hp_debug_batch_fk(hp_ctx* ctx, int64_t p, float* records, int32_t* boxes) {
+  ARG(ctx && p >= 0 && p < ctx->max_n, "hp_debug_batch_fk: bad argument");
+  cudaSetDevice(ctx->device);
+  CK(cudaStreamSynchronize(ctx->st));
+  CK(cudaDeviceSynchronize());
+  std::vector<char> buf(fk_record_bytes());
+  CK(cudaMemcpy(buf.data(), static_cast<char*>(ctx->fk_g) + (size_t)p * fk_record_bytes(),
+                buf.size(), cudaMemcpyDeviceToHost));
+  if (records) memcpy(records, buf.data(), kNprim * kRec * sizeof(float));
+  if (boxes) memcpy(boxes, buf.data() + kNprim * kRec * sizeof(float), kNprim * 16);
+  return HP_OK;
+}
+
 hp_status hp_debug_fk(hp_ctx* ctx, const double* pose, float* records, int32_t* boxes,
                       double* joints, double* kc) {
   ARG(ctx && pose, "hp_debug_fk: NULL argument");

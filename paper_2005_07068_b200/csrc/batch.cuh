@@ -190,10 +190,14 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
         j = kCone0 + k - q * (kNprim - kCone0);
       }
       if (q < np) {
-        float zmin, xr[kRec];  // a quadric's EXACT record is not kept here (see C')
-        build_prim(j, s_fk[q], a.dims, a.cam, j < kCone0 ? s_out[q].rec[j] : xr,
-                   s_out[q].box[j], zmin,
-                   j >= kCone0 && j < kCyl ? &s_shp[q][j - kCone0] : nullptr);
+        float zmin;
+        if (j < kCone0) {  // a sphere's EXACT record is its FAST record
+          build_prim(j, s_fk[q], a.dims, a.cam, s_out[q].rec[j], s_out[q].box[j], zmin);
+        } else {  // a quadric's EXACT record is not kept here (see C')
+          float xr[kRec];
+          build_prim(j, s_fk[q], a.dims, a.cam, xr, s_out[q].box[j], zmin,
+                     j < kCyl ? &s_shp[q][j - kCone0] : nullptr);
+        }
         s_fk[q].nearf[j] = zmin > a.cam.znear * 1.001f;
       }
     } else {
@@ -202,6 +206,9 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
       if (q < np) build_fast(j, s_fk[q], a.dims, s_out[q].rec[j]);
     }
   }
+  // the records were written by every thread of the CTA: each orders its writes before the
+  // async proxy (the bulk copy in D) before the barrier
+  fence_proxy_async();
   __syncthreads();
   // ---- C': a pose that may cross z_near (rare) keeps its EXACT records (global memory) ----
   if (warp < np) {

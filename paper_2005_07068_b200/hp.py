@@ -94,6 +94,7 @@ def lib(path: str | None = None) -> C.CDLL:
             "hp_pso_fit": [_VP, C.POINTER(PsoParams), _VP, _VP, _VP, _VP, _VP],
             "hp_pso_state": [_VP, C.c_int32, C.c_int32, _VP, _VP, _VP, _VP],
             "hp_debug_fk": [_VP, _VP, _VP, _VP, _VP, _VP],
+            "hp_debug_batch_fk": [_VP, C.c_int64, _VP, _VP],
             "hp_debug_render": [_VP, _VP, _VP, _VP],
             "hp_debug_pso_sphere": [_VP, C.c_int32, _VP, _VP, _VP, _VP, C.c_int32, C.c_int32, _VP,
                                     C.POINTER(PsoParams), _VP, _VP, _VP, _VP, _VP],
@@ -139,7 +140,7 @@ def exported_symbols():
             "hp_bounds", "hp_create", "hp_set_observation", "hp_render_observation",
             "hp_eval_costs", "hp_eval_costs_host", "hp_eval_sums", "hp_eval_sums_f64", "hp_pso_fit",
             "hp_pso_state",
-            "hp_debug_fk", "hp_debug_render", "hp_debug_pso_sphere", "hp_last_launch_count",
+            "hp_debug_fk", "hp_debug_batch_fk", "hp_debug_render", "hp_debug_pso_sphere", "hp_last_launch_count",
             "hp_splits_for", "hp_last_error", "hp_destroy", "hp_shard_range",
             "hp_nccl_available", "hp_get_nccl_id", "hp_shard", "hp_track",
             "hp_set_timing", "hp_last_kernel_ms", "hp_set_observations",
@@ -599,6 +600,14 @@ class Context:
         _check(self._L.hp_debug_fk(self._h, h.ctypes.data, rec.ctypes.data, boxes.ctypes.data,
                                    joints.ctypes.data, C.byref(kc)), self._h, self._L)
         return rec, boxes, joints, kc.value
+
+    def debug_batch_fk(self, p: int):
+        """(records, boxes) k_fk_batch wrote for pose p of the last batch-path call."""
+        rec = np.zeros((NPRIM, REC_FLOATS), dtype=np.float32)
+        boxes = np.zeros((NPRIM, 4), dtype=np.int32)
+        _check(self._L.hp_debug_batch_fk(self._h, p, rec.ctypes.data, boxes.ctypes.data),
+               self._h, self._L)
+        return rec, boxes
 
     def debug_render(self, pose_dev, stream=None):
         import torch

@@ -102,6 +102,26 @@ def test_fk_boxes_tight():
                        for b in (O.prim_box(p, cam, 1) for p in prims))
 
 
+def test_batch_fk_records_equal_the_fk_hook():
+    """k_fk_batch's FK output (records, boxes; hp_debug_batch_fk) for every pose of a batch-path
+    call equals the single-pose FK hook's (the same FK device functions): spheres and boxes
+    bit for bit, quadric FAST coefficients to fp32 rounding.  A CTA-cooperative FK that
+    dropped or misplaced a record fails here before any pixel is scored."""
+    ctx = ctx_for(320, 240)
+    obs = obs_for(W.H_A, 320, 240)
+    poses = np.concatenate([np.stack([W.NAMED[k] for k in sorted(W.NAMED)]),
+                            W.swarm_c4(600)]).astype(np.float32)
+    gpu_costs(ctx, obs, poses)
+    assert ctx.last_launch_count() == 3  # the batch path ran
+    for i in list(range(len(W.NAMED))) + [100, 333, 606]:
+        rb, bb = ctx.debug_batch_fk(i)
+        rd, bd, _, _ = ctx.debug_fk(poses[i].astype(np.float64))
+        assert np.array_equal(bb, bd), i
+        assert np.array_equal(rb[:20, :4], rd[:20, :4]), i
+        np.testing.assert_allclose(rb[20:35, :22], rd[20:35, :22], rtol=2e-6, atol=1e-6)
+        np.testing.assert_allclose(rb[35:, :18], rd[35:, :18], rtol=2e-6, atol=1e-6)
+
+
 # ------------------------------------------------------------------------------ depth
 def _depth_parity(w, h, poses):
     ctx = ctx_for(w, h)
