@@ -327,16 +327,26 @@ def run_ours(args):
     #      k and k + 1 overlapped (one call's FK under the other's render tail); inputs
     #      resident, no flush between the overlapped calls ----
     pipelined = None
-    if world == 1 and args.steps >= 4:
+    if args.steps >= 4:
+        # N > 1: two particle-sharded contexts (two NCCL communicators), so the allgather of
+        # call k on one stream overlaps the scoring of call k + 1 on the other
         ctx2 = hp.Context(WIDTH, HEIGHT, max_particles=PER_RANK)
         ctx2.set_observation(depth, mask)
-        costs2 = torch.empty_like(costs)
+        if world > 1:
+            ctx2.shard(rank, world)
+            first, PP, out1 = sctx, P_all, all_costs
+            out2 = torch.empty_like(all_costs)
+        else:
+            first, PP, out1 = ctx, P, costs
+            out2 = torch.empty_like(costs)
         sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
-        pairs = [(ctx, costs, sa), (ctx2, costs2, sb)]
+        pairs = [(first, out1, sa), (ctx2, out2, sb)]
         for k in range(4):
             c_, o_, st_ = pairs[k & 1]
-            c_.eval_costs(P, out=o_, stream=st_)
+            c_.eval_costs(PP, out=o_, stream=st_)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -344,15 +354,23 @@ def run_ours(args):
         sb.wait_event(e0)
         for k in range(args.steps):
             c_, o_, st_ = pairs[k & 1]
-            c_.eval_costs(P, out=o_, stream=st_)
+            c_.eval_costs(PP, out=o_, stream=st_)
         ea.record(sa)
         eb.record(sb)
         torch.cuda.synchronize()
-        pms = max(e0.elapsed_time(ea), e0.elapsed_time(eb)) / args.steps
-        pipelined = {"value": PER_RANK / (pms * 1e-3), "unit": "hyp/s", "ms_per_call": pms,
+        pt = torch.tensor([max(e0.elapsed_time(ea), e0.elapsed_time(eb)) / args.steps],
+                          dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(pt, op=dist.ReduceOp.MAX)
+        pms = float(pt[0])
+        pipelined = {"value": PER_RANK * world / (pms * 1e-3), "unit": "hyp/s",
+                     "ms_per_call": pms,
                      "config": "two contexts on two streams, alternating calls on the C4 "
-                               "batch; inputs resident in HBM, no L2 flush between the "
-                               "overlapped calls"}
+                               "batch" + (" (each particle-sharded: the allgather of one call "
+                                          "overlaps the other call's scoring)" if world > 1
+                                          else "") +
+                               "; inputs resident in HBM, no L2 flush between the overlapped "
+                               "calls; max over ranks"}
         del ctx2
 
     # ---- cold box: the same call on a first-generation swarm uniform in
