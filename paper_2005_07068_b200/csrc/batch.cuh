@@ -123,6 +123,9 @@ __device__ __forceinline__ int build_block_list(const FkOut& fo, uint4* out, uin
 #ifndef HP_PIN
 #define HP_PIN(x) pin_u32(x)
 #endif
+#ifndef HP_FETCH
+#define HP_FETCH 2  // renderer blocks a warp takes per shared-counter atomic
+#endif
 #ifndef HP_FK_PDL
 #define HP_FK_PDL 1  // programmatic dependent launch of k_render_persist after k_fk_batch
 #endif
@@ -369,9 +372,15 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
       const uint32_t next_s = next_s0 + 4u * b;
       const uint32_t tiles_s = tiles_s0 + (uint32_t)sizeof(s_tiles[0]) * b;
       const uint32_t rec_s = rec_s0 + (uint32_t)sizeof(FkOut) * b;
-      int t = warp_fetch_add1(next_s);
+      // blocks are taken HP_FETCH at a time (one shared atomic per HP_FETCH blocks)
+      constexpr int kF = NEAR ? 1 : HP_FETCH;
+      int t = warp_fetch_add<kF>(next_s), tend = t + kF;  // this warp's blocks [t, tend)
       while (t < nt) {
-        const int tn = warp_fetch_add1(next_s);  // the next block, fetched early
+        int tn = t + 1;
+        if (tn >= tend) {  // the next range, fetched early
+          tn = warp_fetch_add<kF>(next_s);
+          tend = tn + kF;
+        }
         if (NEAR) {
           int X0, Y0;
           g.origin(t, X0, Y0);

@@ -269,18 +269,20 @@ __device__ __forceinline__ uint4 lds_u4_nv(uint32_t a) {
 }
 // Warp-collective: lane 0 adds 1 to the shared counter at address a; every lane gets the
 // old value (no divergent branch around the atomic).
-__device__ __forceinline__ int warp_fetch_add1(uint32_t a) {
+template <int INC = 1>
+__device__ __forceinline__ int warp_fetch_add(uint32_t a) {
   int old = 0;
   asm volatile(
       "{\n.reg .pred p;\n.reg .u32 l;\n"
       "mov.u32 l, %%laneid;\n"
       "setp.eq.u32 p, l, 0;\n"
-      "@p atom.shared.add.u32 %0, [%1], 1;\n}"
+      "@p atom.shared.add.u32 %0, [%1], %2;\n}"
       : "+r"(old)
-      : "r"(a)
+      : "r"(a), "n"(INC)
       : "memory");
   return __shfl_sync(0xffffffffu, old, 0);
 }
+__device__ __forceinline__ int warp_fetch_add1(uint32_t a) { return warp_fetch_add<1>(a); }
 __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
