@@ -1,0 +1,11 @@
+#!/bin/bash
+# Round-2 evidence run (under gpurun): the full default bench line, the ncu launch list of a
+# short bench run, and one ncu --set full capture each of k_render_persist and k_fk_batch.
+set -x
+python bench.py > gpurun_out/r2_bench.json 2> gpurun_out/r2_bench.err
+S="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --fit-seeds 2 --track-frames 5 --frames 4"
+$S > gpurun_out/r2_short.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/r2_launches.csv $S > gpurun_out/r2_launches.log 2>&1
+bash scripts/prof_render.sh r2
+bash scripts/prof_fk.sh r2
