@@ -355,7 +355,11 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   const uint32_t next_s0 = smem_u32(&s_next[0]);
   for (int i = 0;; i++) {
     const int b = i & 1;
+#if HP_SLOT_SLEEP
+    mbar_wait_sleep(&s_full[b], (i >> 1) & 1);  // suspended, not spinning on issue slots
+#else
     mbar_wait(&s_full[b], (i >> 1) & 1);
+#endif
     const int p = s_pid[b];
     if (p >= a.n) break;
     const FkOut& fo = s_out[b];
