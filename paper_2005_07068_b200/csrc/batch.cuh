@@ -367,15 +367,21 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     const int yoff = frame_of(a, p) * a.cam.H;
     TileSums acc;
     if (nlist != -2) {
-      const TileGrid g(fo.ubox, nlist < 0);  // the tile origins only without a list
       // NEAR: every 16 x 8 tile of the union grid, culled here; otherwise the block list,
       // or (a close-up pose with more blocks than the list holds) every 16 x 16 block of
-      // the union grid, both halves culled here
-      const int nby = (g.ntiles / (g.tx > 0 ? g.tx : 1) + 1) >> 1;
-      const int nt = NEAR ? g.ntiles : (nlist >= 0 ? nlist : g.tx * nby);
-      const uint32_t next_s = next_s0 + 4u * b;
-      const uint32_t tiles_s = tiles_s0 + (uint32_t)sizeof(s_tiles[0]) * b;
-      const uint32_t rec_s = rec_s0 + (uint32_t)sizeof(FkOut) * b;
+      // the union grid, both halves culled here.  The union grid (and its division) only
+      // where it is used.
+      TileGrid g;
+      int nt = nlist;
+      if (NEAR || nlist < 0) {
+        g = TileGrid(fo.ubox);
+        nt = NEAR ? g.ntiles : g.tx * ((g.ntiles / (g.tx > 0 ? g.tx : 1) + 1) >> 1);
+      }
+      // the slot's shared addresses pinned in registers: the primitive loops address
+      // records as [rec_s + index * record size] instead of re-deriving the slot base
+      const uint32_t next_s = HP_PIN(next_s0 + 4u * b);
+      const uint32_t tiles_s = HP_PIN(tiles_s0 + (uint32_t)sizeof(s_tiles[0]) * b);
+      const uint32_t rec_s = HP_PIN(rec_s0 + (uint32_t)sizeof(FkOut) * b);
       // blocks are taken HP_FETCH at a time (one shared atomic per HP_FETCH blocks)
       constexpr int kF = NEAR ? 1 : HP_FETCH;
       int t = warp_fetch_add<kF>(next_s), tend = t + kF;  // this warp's blocks [t, tend)

@@ -353,8 +353,9 @@ struct TileSums {
 // Tile geometry of a particle: the union box's x0 rounded down to 4 px, because a TMA box
 // must start 16-byte aligned in global memory (an unaligned start faults on sm_100a).
 struct TileGrid {
-  int x0, y0, tx, ntiles;
-  unsigned int magic;  // floor(2^32 / tx): t / tx = umulhi(t, magic) + {0, 1}
+  int x0 = 0, y0 = 0, tx = 0, ntiles = 0;
+  unsigned int magic = 0u;  // floor(2^32 / tx): t / tx = umulhi(t, magic) + {0, 1}
+  TileGrid() = default;
   // need_origin = false: only the tile counts (origin() is not called; skips the division)
   __device__ __forceinline__ explicit TileGrid(int4 ub, bool need_origin = true) {
     x0 = ub.x & ~3;
