@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = [os.path.join(HERE, "csrc", f) for f in ("kernels.cu", "pso.cu", "api.cu")]
 DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "fk.cuh", "pso.cuh",
-                                                      "tile.cuh", "eval.cuh", "batch.cuh")] + [
+                                                      "tile.cuh", "eval.cuh", "fit.cuh", "batch.cuh")] + [
     os.path.join(os.path.dirname(HERE), "include", "hp.h")]
 LIB = os.path.join(HERE, "libhp.so")
 # debug build for the single-GPU loopback test of the sharded paths (include/hp.h

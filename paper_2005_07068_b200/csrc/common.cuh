@@ -158,6 +158,11 @@ struct EvalArgs {
                                   // -2: queued for the near-plane pass)
   int* near_list;                 // [n] particles whose primitives may cross z_near
   unsigned int* near_count;       // their number (reset by the near-plane pass)
+  // persistent fit (k_fit): per-CTA sums [2][grid][4] and per-particle evaluated position +
+  // kc [2][N][32], both double-buffered by generation parity; the grid-barrier counter
+  unsigned long long* fit_part;
+  double* fit_xpub;
+  unsigned int* fit_bar;
 };
 
 // Debug builds (-DHP_DEBUG_CHECKS=1): device-side bounds checks that trap (the GPU test
@@ -380,6 +385,10 @@ cudaError_t launch_unpack_obs(const uint32_t* obs, int W, int H, int pitch_words
 cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUtensorMap* map,
                         cudaStream_t st, cudaEvent_t* tev = nullptr,
                         const CUtensorMap* map16 = nullptr);
+// persistent fit (k_fit, fit.cuh): one cooperative launch of a.S * N CTAs; exact = the
+// near-plane code compiled in.  fit_blocks_per_sm: resident k_fit CTAs per SM (0: unusable)
+cudaError_t launch_fit(const EvalArgs& a, const CUtensorMap* map, bool exact, cudaStream_t st);
+int fit_blocks_per_sm(const CamParams& cam, int N);
 cudaError_t launch_fk_debug(const double* pose_dev, const DimsD& dims, const CamParams& cam,
                             float* rec, int* boxes, double* joints, double* kc,
                             cudaStream_t st);

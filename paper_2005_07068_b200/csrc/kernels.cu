@@ -173,6 +173,7 @@ __global__ void k_depth_to_mask(const float* __restrict__ depth, uint8_t* __rest
 
 #include "tile.cuh"
 #include "eval.cuh"
+#include "fit.cuh"
 #include "batch.cuh"
 
 namespace hp {
@@ -211,6 +212,38 @@ static void set_carveouts() {
   cfg(k_eval<kEvalWarps, double, kModeCost, false>);
   cfg(k_eval<kEvalWarps, float, kModeDepth>);
   cfg(k_eval<kEvalWarps, double, kModeDepth>);
+  cfg(k_fit<false>);
+  cfg(k_fit<true>);
+}
+
+static size_t fit_dyn_bytes(const CamParams& cam, int N) {
+  return (size_t)ray_floats(cam.W, cam.H) * sizeof(float) + (size_t)N * kNdof * sizeof(double);
+}
+
+int fit_blocks_per_sm(const CamParams& cam, int N) {
+  set_carveouts();
+  if (N > kFitMaxN) return 0;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fit<false>, kFitWarps * 32,
+                                                    fit_dyn_bytes(cam, N)) != cudaSuccess)
+    return 0;
+  return nb;
+}
+
+cudaError_t launch_fit(const EvalArgs& a, const CUtensorMap* map, bool exact, cudaStream_t st) {
+  set_carveouts();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.S * a.pso.N));
+  cfg.blockDim = dim3(kFitWarps * 32);
+  cfg.dynamicSmemBytes = fit_dyn_bytes(a.cam, a.pso.N);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // every CTA resident: the grid barrier
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return exact ? cudaLaunchKernelEx(&cfg, k_fit<true>, a, *map)
+               : cudaLaunchKernelEx(&cfg, k_fit<false>, a, *map);
 }
 
 size_t fk_record_bytes() { return sizeof(FkOut); }
