@@ -258,21 +258,32 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
 // those (exact-solid path from their EXACT records; 16 x 8 tiles, box 16 x 8)
 // in a second, normally empty launch, so the near-plane code never shares a register
 // allocation with the hot loop.
+#ifndef HP_SLOTS
+#define HP_SLOTS 2  // particle slots per renderer CTA (FK record + block list each)
+#endif
+constexpr int kSlots = HP_SLOTS;
+// dynamic shared memory of k_render_persist: the ray table, then the slots' block lists
+__host__ __device__ constexpr size_t render_dyn_bytes(int W, int H) {
+  return (size_t)ray_floats(W, H) * sizeof(float) + (size_t)kSlots * kMaxTiles * 16;
+}
 template <int NW, bool NEAR, bool SUMS>
 __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     k_render_persist(const __grid_constant__ EvalArgs a,
                      const __grid_constant__ CUtensorMap tmap) {
-  __shared__ __align__(16) FkOut s_out[2];
-  __shared__ __align__(16) FkExact s_x[NEAR ? 2 : 1];
-  __shared__ __align__(16) uint4 s_tiles[2][NEAR ? 1 : kMaxTiles];
+  __shared__ __align__(16) FkOut s_out[kSlots];
+  __shared__ __align__(16) FkExact s_x[NEAR ? kSlots : 1];
   __shared__ __align__(128) uint32_t s_obs[NW][kTileW * (NEAR ? kTileH : kBlockH)];
   __shared__ __align__(8) uint64_t s_bar[NW];
-  __shared__ __align__(8) uint64_t s_full[2];
+  __shared__ __align__(8) uint64_t s_full[kSlots];
   // per-warp partial sums of the particle in slot b: r_m, o_s AND r_m, numerator lo, hi
-  __shared__ __align__(16) uint4 s_part[2][NW];
-  __shared__ unsigned int s_pboth[2][NW];  // both-defined count (SUMS only)
-  __shared__ int s_next[2], s_done[2], s_pid[2], s_ntl[2];
+  __shared__ __align__(16) uint4 s_part[kSlots][NW];
+  __shared__ unsigned int s_pboth[kSlots][NW];  // both-defined count (SUMS only)
+  __shared__ int s_next[kSlots], s_done[kSlots], s_pid[kSlots], s_ntl[kSlots];
   extern __shared__ float s_ray[];
+  // the slots' block lists follow the ray table (16-byte aligned: ray_floats is a multiple
+  // of 4)
+  uint4(*s_tiles)[kMaxTiles] =
+      reinterpret_cast<uint4(*)[kMaxTiles]>(s_ray + ray_floats(a.cam.W, a.cam.H));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* s_dx = s_ray;
@@ -324,7 +335,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   }
   if (threadIdx.x == 0) {
     for (int w = 0; w < NW; w++) mbar_init(&s_bar[w], 1);
-    for (int b = 0; b < 2; b++) {
+    for (int b = 0; b < kSlots; b++) {
       mbar_init(&s_full[b], 1);
       s_next[b] = 0;
       s_done[b] = 0;
@@ -334,8 +345,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
 #if HP_FK_PDL
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous grid is complete
 #endif
-    issue(0);
-    issue(1);
+    for (int b = 0; b < kSlots; b++) issue(b);
   }
   {
     const int n4 = ray_floats(a.cam.W, a.cam.H) / 4;
@@ -354,11 +364,12 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   const uint32_t tiles_s0 = smem_u32(s_tiles[0]), rec_s0 = smem_u32(s_out[0].rec);
   const uint32_t next_s0 = smem_u32(&s_next[0]);
   for (int i = 0;; i++) {
-    const int b = i & 1;
+    const int b = kSlots == 2 ? (i & 1) : i % kSlots;
+    const uint32_t par = (kSlots == 2 ? (i >> 1) : i / kSlots) & 1;
 #if HP_SLOT_SLEEP
-    mbar_wait_sleep(&s_full[b], (i >> 1) & 1);  // suspended, not spinning on issue slots
+    mbar_wait_sleep(&s_full[b], par);  // suspended, not spinning on issue slots
 #else
-    mbar_wait(&s_full[b], (i >> 1) & 1);
+    mbar_wait(&s_full[b], par);
 #endif
     const int p = s_pid[b];
     if (p >= a.n) break;
@@ -445,7 +456,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
         s_next[b] = 0;
         s_done[b] = 0;
         fence_proxy_async();  // every warp's generic reads of slot b precede the refill
-        issue(b);             // particle i + 2 into the freed slot
+        issue(b);             // particle i + kSlots into the freed slot
       }
     }
     __syncwarp();

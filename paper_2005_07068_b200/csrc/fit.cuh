@@ -136,10 +136,16 @@ __global__ void __launch_bounds__(kFitWarps * 32, 1)
   __shared__ double s_bv[kFitWarps];
   __shared__ int s_bi[kFitWarps];
   __shared__ int s_g_idx, s_final, s_mark;
+  // the hand model and the PSO parameters in shared memory: read every generation, and
+  // kernel-parameter (constant-bank) reads that miss the constant cache after the tile loop
+  // cost a round trip each on the generation's critical path
+  __shared__ DimsD s_dims;
+  __shared__ PsoDev s_ps;
+  __shared__ PsoDyn s_dyn;
   extern __shared__ float s_ray[];  // the ray table, then every particle's evaluated position
 
-  const PsoDev& ps = a.pso;
-  const int N = ps.N, D = ps.D, K = ps.K;
+  const PsoDev& ps = s_ps;
+  const int N = a.pso.N, D = a.pso.D, K = a.pso.K;
   const int G = gridDim.x, S = a.S;
   const int p = blockIdx.x % N, sidx = blockIdx.x / N;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -147,7 +153,7 @@ __global__ void __launch_bounds__(kFitWarps * 32, 1)
   const float* s_dy = s_ray + ray_dx_len(a.cam.W);
   double(*s_xall)[kNdof] =
       reinterpret_cast<double(*)[kNdof]>(s_ray + ray_floats(a.cam.W, a.cam.H));
-  const PsoDyn dyn = *ps.dyn;
+  const PsoDyn& dyn = s_dyn;
 
   // ---- prologue: ray table, mbarriers, bounds, generation-0 position of particle p ----
   {
@@ -155,6 +161,14 @@ __global__ void __launch_bounds__(kFitWarps * 32, 1)
     for (int i = tid; i < n4; i += kFitWarps * 32)
       reinterpret_cast<float4*>(s_ray)[i] = __ldg(reinterpret_cast<const float4*>(a.ray) + i);
   }
+  for (int i = tid; i < (int)(sizeof(DimsD) / sizeof(double)); i += kFitWarps * 32)
+    reinterpret_cast<double*>(&s_dims)[i] = reinterpret_cast<const double*>(&a.dims)[i];
+  if (tid == 0) {
+    s_ps = a.pso;
+    s_dyn = *a.pso.dyn;
+  }
+  __syncthreads();
+  const DimsD& dims = s_dims;
   if (tid == 0) {
     for (int w = 0; w < kFitWarps; w++) mbar_init(&s_bar[w], 1);
     fence_mbar_init();
@@ -182,7 +196,7 @@ __global__ void __launch_bounds__(kFitWarps * 32, 1)
         pso_update_own(ps, dyn, s_pose, s_v, s_pb, s_g, s_lo, s_hi, s_rd[k & 1], s_mark != 0);
       __syncwarp();
       FITPROF_CLK(k, 5)
-      fk_team<double, kEvalFkTeam>(s_pose, a.dims, a.cam, a.cost.kc_rest, s_fk, s_out, &s_xr);
+      fk_team<double, kEvalFkTeam>(s_pose, dims, a.cam, a.cost.kc_rest, s_fk, s_out, &s_xr);
     } else if (warp == kEvalFkTeam) {  // next generation's draws, while the team runs FK
       if (lane == 0) s_next = 0;
       if (k + 1 < K) pso_draws_own(ps, dyn, p, k + 1, s_lo, s_hi, s_rd[(k + 1) & 1]);
@@ -224,13 +238,18 @@ __global__ void __launch_bounds__(kFitWarps * 32, 1)
     fit_grid_sync(a.fit_bar, (unsigned)(k + 1) * (unsigned)G);
     FITPROF_MAX(k, 3)
     // ---- 4. bookkeeping, redundantly in every CTA ----
-    for (int idx = tid; idx < N * D; idx += kFitWarps * 32) {
-      const int i = idx / D, d = idx - i * D;
-      s_xall[i][d] = __ldcg(a.fit_xpub + ((size_t)buf * N + i) * 32 + d);
-    }
+    // the particle threads (warps 0 .. nwp - 1) load the sums and compute the costs; the
+    // other warps copy every particle's evaluated position (for the gbest) meanwhile
+    const int nwp = (N + 31) >> 5;
     double bv = INFINITY;
     int bi = 0x7fffffff;
-    for (int i = tid; i < N; i += kFitWarps * 32) {
+    if (warp >= nwp) {
+      for (int idx = tid - 32 * nwp; idx < N * D; idx += (kFitWarps - nwp) * 32) {
+        const int i = idx / D, d = idx - i * D;
+        s_xall[i][d] = __ldcg(a.fit_xpub + ((size_t)buf * N + i) * 32 + d);
+      }
+    } else if (tid < N) {
+      const int i = tid;
       unsigned long long v0 = 0, v1 = 0, v2 = 0, v3 = 0;
       for (int s = 0; s < S; s++) {
         const ulonglong2* q = reinterpret_cast<const ulonglong2*>(
@@ -245,13 +264,13 @@ __global__ void __launch_bounds__(kFitWarps * 32, 1)
       const double kc = __ldcg(a.fit_xpub + ((size_t)buf * N + i) * 32 + 31);
       double e = finalize_cost(a, i, v, kc);  // Eq. (4)-(5); the fit's EvalArgs store nothing
       if (isnan(e)) e = INFINITY;
-      const bool imp = k == 0 || e < s_pc[i];
-      if (imp) s_pc[i] = e;
+      const double pc_old = s_pc[i];
+      const bool imp = k == 0 || e < pc_old;
+      const double pc = imp ? e : pc_old;
+      s_pc[i] = pc;
       s_imp[i] = imp;
-      if (s_pc[i] < bv) {  // i ascending per thread: the lowest index wins ties
-        bv = s_pc[i];
-        bi = i;
-      }
+      bv = pc;
+      bi = i;
     }
     FITPROF_CLK(k, 6)
 #pragma unroll

@@ -199,14 +199,16 @@ static void set_carveouts() {
   if (done) return;
   done = true;
   const int pct = cudaSharedmemCarveoutMaxShared;
-  auto cfg = [&](auto f) {
+  auto cfg = [&](auto f, size_t extra = 0) {
     cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxRayBytes);
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(kMaxRayBytes + extra));
   };
-  cfg(k_render_persist<kRenderWarps, false, false>);
-  cfg(k_render_persist<kRenderWarps, true, false>);
-  cfg(k_render_persist<kRenderWarps, false, true>);
-  cfg(k_render_persist<kRenderWarps, true, true>);
+  const size_t tiles = (size_t)kSlots * kMaxTiles * 16;  // the renderer's block lists
+  cfg(k_render_persist<kRenderWarps, false, false>, tiles);
+  cfg(k_render_persist<kRenderWarps, true, false>, tiles);
+  cfg(k_render_persist<kRenderWarps, false, true>, tiles);
+  cfg(k_render_persist<kRenderWarps, true, true>, tiles);
   cfg(k_eval<kEvalWarps, float, kModeCost>);
   cfg(k_eval<kEvalWarps, double, kModeCost>);
   cfg(k_eval<kEvalWarps, double, kModeCost, false>);
@@ -262,7 +264,7 @@ int eval_blocks_per_sm(const CamParams& cam) {
 int persist_blocks_per_sm(const CamParams& cam) {
   set_carveouts();
   int nb = 0;
-  const size_t dyn = (size_t)ray_floats(cam.W, cam.H) * sizeof(float);
+  const size_t dyn = render_dyn_bytes(cam.W, cam.H);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb,
                                                     k_render_persist<kRenderWarps, false, false>,
                                                     kRenderWarps * 32, dyn) != cudaSuccess)
@@ -334,11 +336,12 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     if (e != cudaSuccess) return e;
     if (tev) cudaEventRecord(tev[1], st);
     const dim3 pgrid((unsigned)(a.persist_grid < a.n ? a.persist_grid : a.n));
+    const size_t rdyn = render_dyn_bytes(a.cam.W, a.cam.H);
 #if HP_FK_PDL
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = pgrid;
     cfg.blockDim = rblock;
-    cfg.dynamicSmemBytes = dyn;
+    cfg.dynamicSmemBytes = rdyn;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -356,13 +359,13 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     if (e != cudaSuccess) return e;
 #else
     if (a.sums_out) {
-      k_render_persist<kRenderWarps, false, true><<<pgrid, rblock, dyn, st>>>(a, *map16);
+      k_render_persist<kRenderWarps, false, true><<<pgrid, rblock, rdyn, st>>>(a, *map16);
       k_render_persist<kRenderWarps, true, true><<<dim3(pgrid.x < 148u ? pgrid.x : 148u), rblock,
-                                                 dyn, st>>>(a, *map);
+                                                 rdyn, st>>>(a, *map);
     } else {
-      k_render_persist<kRenderWarps, false, false><<<pgrid, rblock, dyn, st>>>(a, *map16);
+      k_render_persist<kRenderWarps, false, false><<<pgrid, rblock, rdyn, st>>>(a, *map16);
       k_render_persist<kRenderWarps, true, false><<<dim3(pgrid.x < 148u ? pgrid.x : 148u), rblock,
-                                                  dyn, st>>>(a, *map);
+                                                  rdyn, st>>>(a, *map);
     }
 #endif
     if (tev) cudaEventRecord(tev[2], st);
