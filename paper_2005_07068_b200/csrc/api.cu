@@ -516,7 +516,7 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   CKC(launch_ray_table(ctx->camp, ctx->ray, ctx->st));
   CKC(cudaMalloc(&ctx->fk_g, (size_t)max_particles * fk_record_bytes()));
   CKC(cudaMalloc(&ctx->fkx_g, (size_t)max_particles * fk_exact_bytes()));
-  CKC(cudaMalloc(&ctx->tiles_g, (size_t)max_particles * kMaxTiles * sizeof(uint4)));
+  CKC(cudaMalloc(&ctx->tiles_g, (size_t)max_particles * kMaxTiles * 2 * sizeof(uint4)));
   CKC(cudaMalloc(&ctx->ntl_g, (size_t)max_particles * sizeof(int)));
   CKC(cudaMalloc(&ctx->pcount, 4 * sizeof(unsigned int)));
   CKC(cudaMemset(ctx->pcount, 0, 4 * sizeof(unsigned int)));

@@ -52,10 +52,9 @@ __device__ __forceinline__ uint2 tile_mask(uint2 c, uint2 r, int X0, int Y0, con
 }
 
 // The particle's non-empty 16 x 16 blocks of its union grid (16 x 8 tiles, rows paired),
-// each with its two halves' masks: uint4 (X0 | Y0 << 16, top prims 0..31, bottom prims
-// 0..31, top 32..37 | bottom 32..37 << 8).  Returns the count, or -1 (too large: the
-// renderer culls per tile).
-__device__ __forceinline__ int build_block_list(const FkOut& fo, uint4* out, uint2* s_cm,
+// each with its two halves' masks split per kind (BlockEnt, tile.cuh).  Returns the count,
+// or -1 (too large: the renderer culls per tile).
+__device__ __forceinline__ int build_block_list(const FkOut& fo, BlockEnt* out, uint2* s_cm,
                                                 uint2* s_rm, const float4* shp) {
   const int lane = threadIdx.x & 31;
   const TileGrid g(fo.ubox);
@@ -112,8 +111,10 @@ __device__ __forceinline__ int build_block_list(const FkOut& fo, uint4* out, uin
     const unsigned int bal = __ballot_sync(0xffffffffu, ne);
     if (ne) {
       HP_CHECK(cnt + __popc(bal & ((1u << lane) - 1u)) < kMaxTiles);
-      out[cnt + __popc(bal & ((1u << lane) - 1u))] =
-          make_uint4((unsigned)X0 | ((unsigned)Y0 << 16), top.x, bot.x, top.y | (bot.y << 8));
+      const BlockEnt e = make_block_ent(X0, Y0, split_kinds(top), split_kinds(bot));
+      BlockEnt* dst = out + cnt + __popc(bal & ((1u << lane) - 1u));
+      dst->a = e.a;
+      dst->b = e.b;
     }
     cnt += __popc(bal);
   }
@@ -237,7 +238,8 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
   if (lane == 0)
     bulk_s2g(static_cast<FkOut*>(a.fk_g) + p, &s_out[warp], (uint32_t)sizeof(FkOut));
   uint2* band = reinterpret_cast<uint2*>(&s_fk[warp]);  // FK scratch is dead by now
-  const int cnt = build_block_list(s_out[warp], a.tiles_g + (size_t)p * kMaxTiles, band,
+  const int cnt = build_block_list(s_out[warp],
+                                   reinterpret_cast<BlockEnt*>(a.tiles_g) + (size_t)p * kMaxTiles, band,
                                    band + kMaxBand, s_shp[warp]);
   if (lane == 0) {
     int ntl = cnt;
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
 constexpr int kSlots = HP_SLOTS;
 // dynamic shared memory of k_render_persist: the ray table, then the slots' block lists
 __host__ __device__ constexpr size_t render_dyn_bytes(int W, int H) {
-  return (size_t)ray_floats(W, H) * sizeof(float) + (size_t)kSlots * kMaxTiles * 16;
+  return (size_t)ray_floats(W, H) * sizeof(float) + (size_t)kSlots * kMaxTiles * sizeof(BlockEnt);
 }
 template <int NW, bool NEAR, bool SUMS>
 __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
@@ -282,8 +284,8 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   extern __shared__ float s_ray[];
   // the slots' block lists follow the ray table (16-byte aligned: ray_floats is a multiple
   // of 4)
-  uint4(*s_tiles)[kMaxTiles] =
-      reinterpret_cast<uint4(*)[kMaxTiles]>(s_ray + ray_floats(a.cam.W, a.cam.H));
+  BlockEnt(*s_tiles)[kMaxTiles] =
+      reinterpret_cast<BlockEnt(*)[kMaxTiles]>(s_ray + ray_floats(a.cam.W, a.cam.H));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* s_dx = s_ray;
@@ -306,14 +308,16 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
         mbar_arrive(&s_full[b]);
         return;
       }
-      const uint32_t lb = ntl > 0 ? (uint32_t)ntl * 16u : 0u;
+      const uint32_t lb = ntl > 0 ? (uint32_t)ntl * (uint32_t)sizeof(BlockEnt) : 0u;
       const uint32_t xb = NEAR ? (uint32_t)sizeof(FkExact) : 0u;
       mbar_expect_tx(&s_full[b], (uint32_t)sizeof(FkOut) + lb + xb);
       bulk_g2s(&s_out[b], static_cast<const FkOut*>(a.fk_g) + p, (uint32_t)sizeof(FkOut),
                &s_full[b]);
       if (NEAR)
         bulk_g2s(&s_x[NEAR ? b : 0], static_cast<const FkExact*>(a.fkx_g) + p, xb, &s_full[b]);
-      if (lb) bulk_g2s(s_tiles[b], a.tiles_g + (size_t)p * kMaxTiles, lb, &s_full[b]);
+      if (lb)
+        bulk_g2s(s_tiles[b], reinterpret_cast<const BlockEnt*>(a.tiles_g) + (size_t)p * kMaxTiles,
+                 lb, &s_full[b]);
     } else {
       mbar_arrive(&s_full[b]);  // terminator: complete the phase without data
     }
@@ -410,19 +414,20 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
             do_tile<kModeCost, true, SUMS, 1>(a, &tmap, fo, &s_x[NEAR ? b : 0], X0, Y0, km,
                                               obs_s, bar_s, phase, dx_s, dy_s, acc, yoff);
         } else {
-          uint4 ent;
+          BlockEnt ent;
+          bool any = true;  // listed blocks are non-empty
           if (nlist >= 0) {
             HP_CHECK(t >= 0 && t < kMaxTiles);
-            ent = lds_u4_nv(tiles_s + 16u * t);
+            ent.a = lds_u4_nv(tiles_s + (uint32_t)sizeof(BlockEnt) * t);
+            ent.b = lds_u4_nv(tiles_s + (uint32_t)sizeof(BlockEnt) * t + 16u);
           } else {
             const int qy = t / g.tx, qx = t - qy * g.tx;
             const int X0 = g.x0 + qx * kTileW, Y0 = g.y0 + qy * kBlockH;
             const uint3 kt = cull_tile(fo, X0, Y0), kb = cull_tile(fo, X0, Y0 + kTileH);
-            ent = make_uint4((unsigned)X0 | ((unsigned)Y0 << 16), kt.x | (kt.y << 20),
-                             kb.x | (kb.y << 20),
-                             ((kt.y >> 12) | (kt.z << 3)) | (((kb.y >> 12) | (kb.z << 3)) << 8));
+            ent = make_block_ent(X0, Y0, kt, kb);
+            any = (kt.x | kt.y | kt.z | kb.x | kb.y | kb.z) != 0;
           }
-          if (ent.y | ent.z | ent.w)
+          if (any)
             do_block<SUMS>(a, &tmap, rec_s, ent, obs_s, obs_ls, bar_s, phase, dx_s, dy_s, acc,
                            yoff);
         }

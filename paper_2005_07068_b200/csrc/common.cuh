@@ -152,8 +152,8 @@ struct EvalArgs {
   // k_render_persist bulk-copies them into shared memory
   void* fk_g;                     // FkOut [n] (16-byte aligned records)
   void* fkx_g;                    // FkExact [n]: exact records, written for near-plane poses
-  uint4* tiles_g;                 // [n][kMaxTiles] 16x16 blocks: X0 | Y0 << 16, the top
-                                  // half's prims 0..31, the bottom's, both halves' 32..37
+  uint4* tiles_g;                 // [n][kMaxTiles] 16x16 blocks, 32 bytes each (BlockEnt,
+                                  // tile.cuh: the origin and the masks split per kind)
   int* ntl_g;                     // [n] tile-list length (-1: box too large, cull on the fly;
                                   // -2: queued for the near-plane pass)
   int* near_list;                 // [n] particles whose primitives may cross z_near

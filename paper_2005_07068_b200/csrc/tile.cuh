@@ -549,19 +549,40 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
   __syncwarp();
 }
 
+// A block-list entry (32 bytes): the block origin and its primitive masks already split
+// the way the renderer's loops take them — per kind, the primitives in both 16 x 8 halves,
+// in the top half only and in the bottom half only — so the loops start without decoding.
+//   a = (X0 | Y0 << 16, spheres both, spheres top only, spheres bottom only)
+//   b = (cones both, cones top only, cones bottom only, ellipsoids both | top << 8 |
+//        bottom << 16)
+// (spheres = prims 0..19, cones + the palm cylinder = 20..34, ellipsoids = 35..37)
+struct BlockEnt {
+  uint4 a, b;
+};
+__device__ __forceinline__ BlockEnt make_block_ent(int X0, int Y0, uint3 top, uint3 bot) {
+  const unsigned s2 = top.x & bot.x, c2 = top.y & bot.y, e2 = top.z & bot.z;
+  BlockEnt e;
+  e.a = make_uint4((unsigned)X0 | ((unsigned)Y0 << 16), s2, top.x ^ s2, bot.x ^ s2);
+  e.b = make_uint4(c2, top.y ^ c2, bot.y ^ c2, e2 | ((top.z ^ e2) << 8) | ((bot.z ^ e2) << 16));
+  return e;
+}
+// The 38-bit half-block mask (lo: prims 0..31, hi: 32..37) split by kind.
+__device__ __forceinline__ uint3 split_kinds(uint2 m) {
+  return make_uint3(m.x & 0xFFFFFu, (m.x >> 20) | ((m.y & 7u) << 12), m.y >> 3);
+}
+
 // The batch renderer's warp BLOCK: 16 x 16 pixels = two 16 x 8 tiles with their own cull
 // masks (the over-test of 16 x 8 tiles) sharing one tile fetch, one 1 KB TMA observation
 // load, the ray set-up and each primitive's per-lane set-up.  Lane: column lane & 15,
 // rows lane >> 4 + {0, 2, ..., 14}; pairs 0, 1 are the top tile, 2, 3 the bottom.
-// ent: X0 | Y0 << 16, the top tile's prims 0..31, the bottom's, then 32..37 of the top in
-// bits 0..5 and of the bottom in bits 8..13 (k_fk_batch's block list).
 // rec_s: shared address of the particle's FAST records; obs_s: the warp's observation
 // buffer, obs_ls: this lane's first pixel in it (column lane & 15, row lane >> 4).
 template <bool SUMS>
 __device__ __forceinline__ void do_block(const EvalArgs& a, const CUtensorMap* tmap,
-                                         uint32_t rec_s, uint4 ent, uint32_t obs_s,
+                                         uint32_t rec_s, BlockEnt e, uint32_t obs_s,
                                          uint32_t obs_ls, uint32_t bar_s, uint32_t& phase,
                                          uint32_t dx_s, uint32_t dy_s, TileSums& acc, int yoff) {
+  const uint4 ent = e.a;
   const int X0 = (int)(ent.x & 0xFFFFu), Y0 = (int)(ent.x >> 16);
   const float zfar = a.cam.zfar;
   const float zinit = __uint_as_float(__float_as_uint(zfar) + 1u);
@@ -580,24 +601,22 @@ __device__ __forceinline__ void do_block(const EvalArgs& a, const CUtensorMap* t
   for (int q = 0; q < 8; q++) zb[q] = zinit;
   // masks per kind, split into primitives in both halves / the top only / the bottom only
   // (no per-primitive half tests in the loops)
-  const unsigned int st = ent.y & 0xFFFFFu, sb = ent.z & 0xFFFFFu;
-  const unsigned int ct = (ent.y >> 20) | ((ent.w & 7u) << 12);
-  const unsigned int cb = (ent.z >> 20) | (((ent.w >> 8) & 7u) << 12);
-  const unsigned int et = (ent.w >> 3) & 7u, eb = (ent.w >> 11) & 7u;
-  const unsigned int s2 = st & sb, c2 = ct & cb, e2 = et & eb;
+  const unsigned int s2 = ent.y, s_t = ent.z, s_b = ent.w;
+  const unsigned int c2 = e.b.x, c_t = e.b.y, c_b = e.b.z;
+  const unsigned int e2 = e.b.w & 0xFFu, e_t = (e.b.w >> 8) & 0xFFu, e_b = e.b.w >> 16;
   for (unsigned int m = s2; m; m &= m - 1) {
     const float4 q = lds_f4_nv(rec_s + 4u * kRec * (__ffs(m) - 1));
     const float bx = fmaf(dx, q.x, q.z);
 #pragma unroll
     for (int k = 0; k < 4; k++) sphere_pair(q, dx, bx, dy[k], idd[k], zb[2 * k], zb[2 * k + 1]);
   }
-  for (unsigned int m = st ^ s2; m; m &= m - 1) {
+  for (unsigned int m = s_t; m; m &= m - 1) {
     const float4 q = lds_f4_nv(rec_s + 4u * kRec * (__ffs(m) - 1));
     const float bx = fmaf(dx, q.x, q.z);
 #pragma unroll
     for (int k = 0; k < 2; k++) sphere_pair(q, dx, bx, dy[k], idd[k], zb[2 * k], zb[2 * k + 1]);
   }
-  for (unsigned int m = sb ^ s2; m; m &= m - 1) {
+  for (unsigned int m = s_b; m; m &= m - 1) {
     const float4 q = lds_f4_nv(rec_s + 4u * kRec * (__ffs(m) - 1));
     const float bx = fmaf(dx, q.x, q.z);
 #pragma unroll
@@ -609,12 +628,12 @@ __device__ __forceinline__ void do_block(const EvalArgs& a, const CUtensorMap* t
 #pragma unroll
     for (int k = 0; k < 4; k++) quad_pair<true>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
   }
-  for (unsigned int m = ct ^ c2; m; m &= m - 1) {
+  for (unsigned int m = c_t; m; m &= m - 1) {
     const QuadLane Q = quad_lane<true>(rec_s + 4u * kRec * (kCone0 + __ffs(m) - 1), dx);
 #pragma unroll
     for (int k = 0; k < 2; k++) quad_pair<true>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
   }
-  for (unsigned int m = cb ^ c2; m; m &= m - 1) {
+  for (unsigned int m = c_b; m; m &= m - 1) {
     const QuadLane Q = quad_lane<true>(rec_s + 4u * kRec * (kCone0 + __ffs(m) - 1), dx);
 #pragma unroll
     for (int k = 2; k < 4; k++) quad_pair<true>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
@@ -624,12 +643,12 @@ __device__ __forceinline__ void do_block(const EvalArgs& a, const CUtensorMap* t
 #pragma unroll
     for (int k = 0; k < 4; k++) quad_pair<false>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
   }
-  for (unsigned int m = et ^ e2; m; m &= m - 1) {
+  for (unsigned int m = e_t; m; m &= m - 1) {
     const QuadLane Q = quad_lane<false>(rec_s + 4u * kRec * (kEll0 + __ffs(m) - 1), dx);
 #pragma unroll
     for (int k = 0; k < 2; k++) quad_pair<false>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
   }
-  for (unsigned int m = eb ^ e2; m; m &= m - 1) {
+  for (unsigned int m = e_b; m; m &= m - 1) {
     const QuadLane Q = quad_lane<false>(rec_s + 4u * kRec * (kEll0 + __ffs(m) - 1), dx);
 #pragma unroll
     for (int k = 2; k < 4; k++) quad_pair<false>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
