@@ -140,8 +140,8 @@ static_assert(kFkWarps == 4, "k_fk_batch's work lists assume 4 poses per CTA");
 // different primitive kinds in a warp, few idle lanes):
 //   A  the 4 x 26 pose values and the 4 x 23 sincos (fp64), one per thread
 //   B  the 4 x 5 finger chains (fp64), one per thread
-//   C  the 4 x 38 EXACT records + boxes, sorted by kind: 80 spheres, 60 cones / cylinders,
-//      12 ellipsoids, in two passes of 128 threads
+//   C  the 4 x 38 boxes and FAST records, sorted by kind: 80 spheres (box + record), 72
+//      quadric boxes, 72 quadric records, in passes of 128 threads
 //   C' (a pose that may cross z_near: its EXACT records to global memory, warp per pose)
 //   C" the 72 quadric records converted to the FAST layout (fp64), one pass
 //   D  per warp (= pose): union box, near-plane flag, kc; the record leaves by one bulk
@@ -195,8 +195,9 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
       }
       if (q < np) {
         float zmin;
-        if (j < kCone0) {  // a sphere's EXACT record is its FAST record
+        if (j < kCone0) {  // a sphere: box (the EXACT record is discarded), then FAST record
           build_prim(j, s_fk[q], a.dims, a.cam, s_out[q].rec[j], s_out[q].box[j], zmin);
+          build_fast(j, s_fk[q], a.dims, s_out[q].rec[j]);
         } else {  // a quadric's EXACT record is not kept here (see C')
           float xr[kRec];
           build_prim(j, s_fk[q], a.dims, a.cam, xr, s_out[q].box[j], zmin,

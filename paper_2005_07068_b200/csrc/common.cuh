@@ -57,19 +57,23 @@ constexpr uint64_t kEllMask = ((1ull << 38) - 1) ^ ((1ull << 35) - 1);
 //   [13..15] c_l = M c
 //   [16] r_mid  [17] slope k  [18] half length (cone / cylinder)
 enum RecField { kC = 0, kR2 = 3, kM = 4, kCl = 13, kRm = 16, kK = 17, kHl = 18 };
-// FAST record layout (FkOut.rec, the hot loops; DESIGN §9 "polynomial form").  Spheres keep
-// [c, r^2] (fields kC, kR2 above: the re-centred sphere test).  Ellipsoids, cones and the
-// palm cylinder: with local coordinates l = M (p - c), implicit F(l) = l'Q l + 2 g.l + h and
-// the pixel ray p = t d, d = (x, y, 1), F = 0 reads a t^2 - 2 b t + c0 = 0 with
-//   a = dl'Q dl, b = dl'Q cl - g.dl, c0 = cl'Q cl - 2 g.cl + h   (dl = M d, cl = M c),
-// entering root t = (b - sqrt(D)) / a, D = b^2 - a c0.  a and D are quadratic, b affine in
-// (x, y); FK expands them in fp64 about the projected centre (xp, yp) and stores fp32
-// coefficients of x' = x - xp, y' = y - yp (all terms O(D) over the primitive's box, so the
-// fp32 Horner evaluation does not cancel):
-//   [0] xp [1] yp  [2..7] D: d00 d10 d01 d20 d11 d02  [8..10] b: b0 bx by  [11] cl_z
-//   [12..17] a: a00 a10 a01 a20 a11 a02  [18..20] axis row of M (raw x, y, 1 coefficients:
-//   the axial coordinate at t is t (lzx x + lzy y + lz1) - cl_z)  [21] half length
-enum FastField { kFxp = 0, kFyp = 1, kFd = 2, kFb = 8, kFclz = 11, kFa = 12, kFlz = 18, kFhl = 21 };
+// FAST record layout (FkOut.rec, the hot loops; DESIGN §9 "inverse-depth polynomial form"),
+// the same for every kind (spheres, ellipsoids, cones, the palm cylinder): with local
+// coordinates l = M (p - c), implicit F(l) = l'Q l + 2 g.l + h and the pixel ray p = t d,
+// d = (x, y, 1), F = 0 reads a t^2 - 2 b t + c0 = 0 with
+//   a = dl'Q dl, b = dl'Q cl - g.dl, c0 = cl'Q cl - 2 g.cl + h   (dl = M d, cl = M c).
+// c0 = F(camera) does not depend on the pixel, so in the inverse depth s = 1 / t the same
+// equation is c0 s^2 - 2 b s + a = 0 and the root t = (b - sqrt(D)) / a the renderer wants
+// (the entering root) is s = (b + sqrt(D)) / c0, D = b^2 - a c0: no per-pixel division, and
+// the nearest hit is the LARGEST s.  D is quadratic, b affine in (x, y); FK expands them in
+// fp64 about the projected centre (xp, yp) and stores fp32 coefficients of x' = x - xp,
+// y' = y - yp (all terms O(D) over the primitive's box: the fp32 Horner evaluation does not
+// cancel), b pre-scaled by 1 / c0:
+//   [0] xp [1] yp  [2..7] D: d00 d10 d01 d20 d11 d02  [8..10] b / c0: b0 bx by  [11] 1 / c0
+//   cones / cylinder: [12..14] (axis row of M) / hl (raw x, y, 1 coefficients)
+//   [15] -cl_z / hl — the axial coordinate at the hit is within [-hl, hl] iff
+//   |s (-cl_z / hl) + (lzx x + lzy y + lz1) / hl| <= s.
+enum FastField { kFxp = 0, kFyp = 1, kFd = 2, kFb = 8, kFic0 = 11, kFlz = 12, kFnclz = 15 };
 
 struct CamParams {
   int W, H;

@@ -179,11 +179,11 @@ __device__ __forceinline__ void put3(float* r, int off, const double v[3]) {
   r[off + 2] = (float)v[2];
 }
 
-// FAST record of a quadric primitive (common.cuh "FAST record layout"): local origin cen,
-// rows of M, Q = diag(q), g = (0, 0, g2), h; fp64 throughout, fp32 coefficients out.  The
-// expansion point is the projection of cen, rounded to fp32 first so the coefficients
-// belong to the point the kernel subtracts.  axis (may be null): the axial row of M and
-// the half length (cones / cylinder).
+// FAST record of a primitive (common.cuh "FAST record layout"): local origin cen, rows of
+// M, Q = diag(q), g = (0, 0, g2), h; fp64 throughout, fp32 coefficients out.  The expansion
+// point is the projection of cen, rounded to fp32 first so the coefficients belong to the
+// point the kernel subtracts.  axial: cones / cylinder (the axial row of M and the half
+// length hl).
 __device__ __forceinline__ void write_fast_quadric(float* rec, const double cen[3], const double M[3][3],
                                    const double q[3], double g2, double h, bool axial,
                                    double hl) {
@@ -213,22 +213,24 @@ __device__ __forceinline__ void write_fast_quadric(float* rec, const double cen[
   const double D[6] = {b0 * b0 - c0 * A[0],       2.0 * b0 * bx - c0 * A[1],
                        2.0 * b0 * by - c0 * A[2], bx * bx - c0 * A[3],
                        2.0 * bx * by - c0 * A[4], by * by - c0 * A[5]};
+  const double ic0 = 1.0 / c0;
   rec[kFxp] = xp;
   rec[kFyp] = yp;
-  for (int i = 0; i < 6; i++) {
-    rec[kFd + i] = (float)D[i];
-    rec[kFa + i] = (float)A[i];
-  }
-  rec[kFb + 0] = (float)b0;
-  rec[kFb + 1] = (float)bx;
-  rec[kFb + 2] = (float)by;
-  rec[kFclz] = (float)cl[2];
+  for (int i = 0; i < 6; i++) rec[kFd + i] = (float)D[i];
+  rec[kFb + 0] = (float)(b0 * ic0);
+  rec[kFb + 1] = (float)(bx * ic0);
+  rec[kFb + 2] = (float)(by * ic0);
+  rec[kFic0] = (float)ic0;
   if (axial) {
-    rec[kFlz + 0] = (float)M[2][0];
-    rec[kFlz + 1] = (float)M[2][1];
-    rec[kFlz + 2] = (float)M[2][2];
-    rec[kFhl] = (float)hl;
+    const double ih = 1.0 / hl;
+    rec[kFlz + 0] = (float)(M[2][0] * ih);
+    rec[kFlz + 1] = (float)(M[2][1] * ih);
+    rec[kFlz + 2] = (float)(M[2][2] * ih);
+    rec[kFnclz] = (float)(-cl[2] * ih);
+  } else {
+    for (int i = kFlz; i <= kFnclz; i++) rec[i] = 0.f;
   }
+  for (int i = kFnclz + 1; i < kRec; i++) rec[i] = 0.f;  // unused: deterministic records
 }
 
 // Build record + box of device primitive j (see common.cuh for the order).
@@ -360,14 +362,22 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm,
   box = prim_box(ng, gc, gA, cam, zmin);
 }
 
-// FAST record of quadric primitive j (cone / cylinder / ellipsoid, j >= kCone0) straight
-// from the fp64 FK geometry (the same frames build_prim uses), independent of the EXACT
-// record and the box, so a team can build both in parallel.  Spheres: their FAST record is
-// the EXACT record's head (build_prim).
+// FAST record of primitive j straight from the fp64 FK geometry (the same frames build_prim
+// uses), independent of the EXACT record and the box, so a team can build both in
+// parallel.
 __device__ __forceinline__ void build_fast(int j, const FkScratch& s, const DimsD& dm,
                                            float* rec) {
   double c[3], M[3][3];
-  if (j < kCyl) {  // truncated cone J_k -> J_{k+1}: rows e1, e2, axis; midpoint origin
+  if (j < kCone0) {  // sphere at joint (f, k): |p - c|^2 - r^2, M = I
+    const int f = j >> 2, k = j & 3;
+    const double r = dm.rad[f][k];
+    for (int i = 0; i < 3; i++) {
+      c[i] = s.J[f][k][i];
+      for (int a = 0; a < 3; a++) M[a][i] = a == i ? 1.0 : 0.0;
+    }
+    const double q[3] = {1.0, 1.0, 1.0};
+    write_fast_quadric(rec, c, M, q, 0.0, -r * r, false, 0.0);
+  } else if (j < kCyl) {  // truncated cone J_k -> J_{k+1}: rows e1, e2, axis; midpoint origin
     int f, k;
     if (j < 32) {
       f = 1 + (j - kCone0) / 3;
@@ -571,7 +581,7 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
   FKPROF(2)
   // ---- phase C: records + boxes ----
   if (TEAM >= 2) {
-    // TEAM 4: warp 0 the 20 spheres (record = EXACT head = FAST), warp 1 the 14 cones and
+    // TEAM 4: warp 0 the 20 spheres (EXACT + box, then FAST), warp 1 the 14 cones and
     // warp 2 the cylinder + 3 ellipsoids (EXACT records into xrec, boxes), warp 3 the 18
     // FAST quadric records straight from the frames, in parallel with warps 1-2
     if (w == 3) {
@@ -585,8 +595,7 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
         float* xr = xrec->rec[j];
         build_prim(j, s, dm, cam, xr, out.box[j], zmin, nullptr);
         s.nearf[j] = zmin > cam.znear * 1.001f;
-        if (j < kCone0)  // spheres: the FAST record is the EXACT one's head
-          *reinterpret_cast<float4*>(out.rec[j]) = *reinterpret_cast<const float4*>(xr);
+        if (j < kCone0) build_fast(j, s, dm, out.rec[j]);  // spheres: FAST on warp 0
       }
     }
     if (w != 0) {
@@ -617,6 +626,7 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
               reinterpret_cast<const float4*>(out.rec)[i];
     }
     if (lane < kNprim - kCone0) build_fast(kCone0 + lane, s, dm, out.rec[kCone0 + lane]);
+    if (lane < kCone0) build_fast(lane, s, dm, out.rec[lane]);  // spheres (EXACT copied above)
     __syncwarp();
   }
   FKPROF(3)

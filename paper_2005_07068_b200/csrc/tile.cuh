@@ -256,91 +256,70 @@ __device__ __forceinline__ f2 rcp2(f2 x) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Fast path, ellipsoids / cones / the palm cylinder: the polynomial form (common.cuh FAST
-// record layout).  Per lane (one column x): x' = x - xp and the y-Horner coefficients of D
-// and a, b's affine part; per pixel pair: y' = y - yp, D, a by Horner in y', b, the entering
-// root t = (b - sqrt(D)) / a — 10 packed fp32x2 instructions and 4 MUFU for a cone pair
-// against 29 + 4 for the re-centred form it replaces.  For a < 0 (a ray inside a cone's
-// opening) this is the larger root, the entering one of the infinite solid; whenever it
-// lies outside the axial range the ray enters the finite solid through a cap disc, which
-// is the equator of a joint sphere / cap ellipsoid hit first, so the min over
-// primitives is unchanged.  NaN (no real root, or outside the axial range) never wins.
+// Fast path, every primitive kind: the inverse-depth polynomial form (common.cuh FAST record
+// layout).  Per lane (one column x): x' = x - xp and the y-Horner coefficients of D, b's
+// affine part (b pre-scaled by 1 / c0), for cones the axial line's x part; per pixel pair:
+// y' = y - yp, D by Horner, the inverse depth s = sqrt(D) / c0 + b / c0 of the entering
+// root t = (b - sqrt(D)) / a (the same root: s = 1 / t), and the running MAXIMUM of s —
+// 6 packed fp32x2 instructions and 2 MUFU for a sphere / ellipsoid pair, 8 + 2 FSETP for a
+// cone, against 14-17 and 4 MUFU for the depth form (no per-pixel 1 / a, no 1 / |d|^2).  The
+// depth is 1 / s once per pixel after all primitives.  For a < 0 (a ray inside a cone's
+// opening) the root is the larger one, the entering one of the infinite solid; whenever it
+// lies outside the axial range the ray enters the finite solid through a cap disc, which is
+// the equator of a joint sphere / cap ellipsoid hit first, so the max over
+// primitives is unchanged.  NaN (no real root) never wins; neither does a negative s (a
+// root behind the camera) nor one outside the axial range.
 // ---------------------------------------------------------------------------------------
 struct QuadLane {
-  float yp, d02, a02, by, ed0, ed1, ea0, ea1, eb0;
-  float lzy, lzl, nclz, hl;  // axial (cones / cylinder)
+  float yp, d02, by, ic0, ed0, ed1, eb0;
+  float lzy, lzl, nclz;  // axial (cones / cylinder), scaled by 1 / hl
 };
 template <bool AXIAL>
 __device__ __forceinline__ QuadLane quad_lane(uint32_t r, float dx) {  // r: record address
   const float4 r0 = lds_f4_nv(r + 0);   // xp yp d00 d10
   const float4 r1 = lds_f4_nv(r + 16);  // d01 d20 d11 d02
-  const float4 r2 = lds_f4_nv(r + 32);  // b0 bx by clz
-  const float4 r3 = lds_f4_nv(r + 48);  // a00 a10 a01 a20
-  float a11, a02;
+  const float4 r2 = lds_f4_nv(r + 32);  // b0 bx by ic0 (b / c0)
   QuadLane q;
   if (AXIAL) {
-    const float4 r4 = lds_f4_nv(r + 64);  // a11 a02 lzx lzy
-    const float2 r5 = lds_f2_nv(r + 80);  // lz1 hl
-    a11 = r4.x;
-    a02 = r4.y;
-    q.lzy = r4.w;
-    q.lzl = fmaf(r4.z, dx, r5.x);
-    q.nclz = -r2.w;
-    q.hl = r5.y;
-  } else {
-    const float2 r4 = lds_f2_nv(r + 64);  // a11 a02
-    a11 = r4.x;
-    a02 = r4.y;
+    const float4 r3 = lds_f4_nv(r + 48);  // lzx lzy lz1 nclz (/ hl)
+    q.lzy = r3.y;
+    q.lzl = fmaf(r3.x, dx, r3.z);
+    q.nclz = r3.w;
   }
   const float xq = dx - r0.x;
   q.yp = r0.y;
   q.d02 = r1.w;
-  q.a02 = a02;
   q.by = r2.z;
+  q.ic0 = r2.w;
   q.ed0 = fmaf(fmaf(r1.y, xq, r0.w), xq, r0.z);
   q.ed1 = fmaf(r1.z, xq, r1.x);
-  q.ea0 = fmaf(fmaf(r3.w, xq, r3.y), xq, r3.x);
-  q.ea1 = fmaf(a11, xq, r3.z);
   q.eb0 = fmaf(r2.y, xq, r2.x);
   return q;
 }
-// One pixel pair (rows dy) of a quadric: the entering-root depth, NaN if none.
+// One pixel pair (rows dy): the inverse depth of the entering root, kept if larger.
 template <bool AXIAL>
-__device__ __forceinline__ void quad_pair(const QuadLane& q, f2 dy, float& zb0, float& zb1) {
+__device__ __forceinline__ void quad_pair(const QuadLane& q, f2 dy, float& sb0, float& sb1) {
   const f2 yq = sub2(dy, bc(q.yp));
   const f2 D = fma2(fma2(bc(q.d02), yq, bc(q.ed1)), yq, bc(q.ed0));
-  const f2 A = fma2(fma2(bc(q.a02), yq, bc(q.ea1)), yq, bc(q.ea0));
   const f2 B = fma2(bc(q.by), yq, bc(q.eb0));
-  const f2 t = mul2(sub2(B, sqrt2(D)), rcp2(A));
+  const f2 s = fma2(sqrt2(D), bc(q.ic0), B);  // NaN when D < 0: no hit
+  float s0, s1;
+  unpk(s, s0, s1);
   if (AXIAL) {
-    const f2 za = fma2(t, fma2(bc(q.lzy), dy, bc(q.lzl)), bc(q.nclz));
-    float za0, za1, t0, t1;
-    unpk(za, za0, za1);
-    unpk(t, t0, t1);
-    // a predicated min (no select): inside the axial range only
-    if (fabsf(za0) <= q.hl) zb0 = fminf(zb0, t0);
-    if (fabsf(za1) <= q.hl) zb1 = fminf(zb1, t1);
+    // axial coordinate within [-hl, hl]: |s (-cl_z / hl) + (axis . d) / hl| <= s (false for
+    // NaN and for s < 0); a predicated max, no select
+    const f2 xv = fma2(bc(q.nclz), s, fma2(bc(q.lzy), dy, bc(q.lzl)));
+    float x0, x1;
+    unpk(xv, x0, x1);
+    if (fabsf(x0) <= s0) sb0 = fmaxf(sb0, s0);
+    if (fabsf(x1) <= s1) sb1 = fmaxf(sb1, s1);
   } else {
-    float t0, t1;
-    unpk(t, t0, t1);
-    zb0 = fminf(zb0, t0);
-    zb1 = fminf(zb1, t1);
+    sb0 = fmaxf(sb0, s0);
+    sb1 = fmaxf(sb1, s1);
   }
 }
-// The re-centred sphere test on one pixel pair (rows dy, 1 / |d|^2 idd; bx = dx c_x + c_z).
-__device__ __forceinline__ void sphere_pair(const float4 q, float dx, float bx, f2 dy, f2 idd,
-                                            float& zb0, float& zb1) {
-  const f2 tc = mul2(fma2(dy, bc(q.y), bc(bx)), idd);
-  const f2 ox = fma2(tc, bc(dx), bc(-q.x)), oy = fma2(tc, dy, bc(-q.y));
-  const f2 oz = add2(tc, bc(-q.z));
-  const f2 m = mul2(fma2(ox, ox, fma2(oy, oy, fma2(oz, oz, bc(-q.w)))), idd);
-  float m0, m1;
-  unpk(m, m0, m1);
-  float z0, z1;
-  unpk(fma2(m, pk(rsqrt_approx(-m0), rsqrt_approx(-m1)), tc), z0, z1);
-  zb0 = fminf(zb0, z0);
-  zb1 = fminf(zb1, z1);
-}
+// Depth of the nearest hit from the largest inverse depth: 1 / s (0 -> +inf: no hit).
+__device__ __forceinline__ float depth_of(float sb) { return rcp_approx(sb); }
 
 // ---------------------------------------------------------------------------------------
 // One warp tile: TMA the observation tile, cull, ray-cast, min-depth, score.
@@ -487,16 +466,18 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
   HP_CHECK((X0 & 3) == 0);  // TMA boxes start 16-byte aligned
   // the ray table by shared address: dx_s = &dx[lane's column], dy_s = &dy4[lane's row]
   L.dx = __uint_as_float(lds_u32(dx_s + 4u * X0));
-  const float ddx = fmaf(L.dx, L.dx, 1.f);
   const float4 dy4 = lds_f4(dy_s + 16u * Y0);  // rows y, y+2, y+4, y+6
   const float dyv[4] = {dy4.x, dy4.y, dy4.z, dy4.w};
 #pragma unroll
   for (int q = 0; q < kPxPerLane; q += 2) {
     const float dy0 = dyv[q], dy1 = dyv[q + 1];
     L.dy[q / 2] = pk(dy0, dy1);
-    L.idd[q / 2] = pk(rcp_approx(fmaf(dy0, dy0, ddx)), rcp_approx(fmaf(dy1, dy1, ddx)));
-    L.zb[q] = zinit;
-    L.zb[q + 1] = zinit;
+    if (CHK) {  // the exact path's depth form needs 1 / |d|^2; the fast path none
+      const float ddx = fmaf(L.dx, L.dx, 1.f);
+      L.idd[q / 2] = pk(rcp_approx(fmaf(dy0, dy0, ddx)), rcp_approx(fmaf(dy1, dy1, ddx)));
+    }
+    L.zb[q] = CHK ? zinit : 0.f;  // fast path: the largest inverse depth so far
+    L.zb[q + 1] = CHK ? zinit : 0.f;
   }
   if (CHK) {
     // exact solid semantics (both roots, cone caps, [z_near, z_far]) from the EXACT records
@@ -507,10 +488,9 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
       isect_ellipsoid<true>(xr->rec[kEll0 + __ffs(m) - 1], L, znear);
   } else {
     for (unsigned int m = msph; m; m &= m - 1) {
-      const float4 q = *reinterpret_cast<const float4*>(fo.rec[__ffs(m) - 1]);
-      const float bx = fmaf(L.dx, q.x, q.z);
-      sphere_pair(q, L.dx, bx, L.dy[0], L.idd[0], L.zb[0], L.zb[1]);
-      sphere_pair(q, L.dx, bx, L.dy[1], L.idd[1], L.zb[2], L.zb[3]);
+      const QuadLane Q = quad_lane<false>(smem_u32(fo.rec[__ffs(m) - 1]), L.dx);
+      quad_pair<false>(Q, L.dy[0], L.zb[0], L.zb[1]);
+      quad_pair<false>(Q, L.dy[1], L.zb[2], L.zb[3]);
     }
     for (unsigned int m = mcone; m; m &= m - 1) {  // cones and the palm cylinder
       const QuadLane Q = quad_lane<true>(smem_u32(fo.rec[kCone0 + __ffs(m) - 1]), L.dx);
@@ -522,6 +502,8 @@ __device__ __forceinline__ void do_tile(const EvalArgs& a, const CUtensorMap* tm
       quad_pair<false>(Q, L.dy[0], L.zb[0], L.zb[1]);
       quad_pair<false>(Q, L.dy[1], L.zb[2], L.zb[3]);
     }
+#pragma unroll
+    for (int q = 0; q < kPxPerLane; q++) L.zb[q] = depth_of(L.zb[q]);
   }
 
   if (MODE == kModeDepth) {
@@ -584,43 +566,34 @@ __device__ __forceinline__ void do_block(const EvalArgs& a, const CUtensorMap* t
                                          uint32_t dx_s, uint32_t dy_s, TileSums& acc, int yoff) {
   const uint4 ent = e.a;
   const int X0 = (int)(ent.x & 0xFFFFu), Y0 = (int)(ent.x >> 16);
-  const float zfar = a.cam.zfar;
-  const float zinit = __uint_as_float(__float_as_uint(zfar) + 1u);
   HP_CHECK(yoff >= 0 && Y0 < a.cam.H && (X0 & 3) == 0);
   tma_load_2d_elect_s(obs_s, tmap, X0, Y0 + yoff, bar_s, kTileW * kBlockH * 4);
   const float dx = __uint_as_float(lds_u32(dx_s + 4u * X0));
-  const float ddx = fmaf(dx, dx, 1.f);
   const float4 ya = lds_f4(dy_s + 16u * Y0);        // rows y, y+2, y+4, y+6
   const float4 yb = lds_f4(dy_s + 16u * (Y0 + 8));  // rows y+8 .. y+14
   const f2 dy[4] = {pk(ya.x, ya.y), pk(ya.z, ya.w), pk(yb.x, yb.y), pk(yb.z, yb.w)};
-  f2 idd[4];
+  float zb[8];  // the largest inverse depth so far, then the depth
 #pragma unroll
-  for (int k = 0; k < 4; k++) idd[k] = rcp2(fma2(dy[k], dy[k], bc(ddx)));  // 1 / |d|^2
-  float zb[8];
-#pragma unroll
-  for (int q = 0; q < 8; q++) zb[q] = zinit;
+  for (int q = 0; q < 8; q++) zb[q] = 0.f;
   // masks per kind, split into primitives in both halves / the top only / the bottom only
   // (no per-primitive half tests in the loops)
   const unsigned int s2 = ent.y, s_t = ent.z, s_b = ent.w;
   const unsigned int c2 = e.b.x, c_t = e.b.y, c_b = e.b.z;
   const unsigned int e2 = e.b.w & 0xFFu, e_t = (e.b.w >> 8) & 0xFFu, e_b = e.b.w >> 16;
   for (unsigned int m = s2; m; m &= m - 1) {
-    const float4 q = lds_f4_nv(rec_s + 4u * kRec * (__ffs(m) - 1));
-    const float bx = fmaf(dx, q.x, q.z);
+    const QuadLane Q = quad_lane<false>(rec_s + 4u * kRec * (__ffs(m) - 1), dx);
 #pragma unroll
-    for (int k = 0; k < 4; k++) sphere_pair(q, dx, bx, dy[k], idd[k], zb[2 * k], zb[2 * k + 1]);
+    for (int k = 0; k < 4; k++) quad_pair<false>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
   }
   for (unsigned int m = s_t; m; m &= m - 1) {
-    const float4 q = lds_f4_nv(rec_s + 4u * kRec * (__ffs(m) - 1));
-    const float bx = fmaf(dx, q.x, q.z);
+    const QuadLane Q = quad_lane<false>(rec_s + 4u * kRec * (__ffs(m) - 1), dx);
 #pragma unroll
-    for (int k = 0; k < 2; k++) sphere_pair(q, dx, bx, dy[k], idd[k], zb[2 * k], zb[2 * k + 1]);
+    for (int k = 0; k < 2; k++) quad_pair<false>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
   }
   for (unsigned int m = s_b; m; m &= m - 1) {
-    const float4 q = lds_f4_nv(rec_s + 4u * kRec * (__ffs(m) - 1));
-    const float bx = fmaf(dx, q.x, q.z);
+    const QuadLane Q = quad_lane<false>(rec_s + 4u * kRec * (__ffs(m) - 1), dx);
 #pragma unroll
-    for (int k = 2; k < 4; k++) sphere_pair(q, dx, bx, dy[k], idd[k], zb[2 * k], zb[2 * k + 1]);
+    for (int k = 2; k < 4; k++) quad_pair<false>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
   }
   // cones and the palm cylinder
   for (unsigned int m = c2; m; m &= m - 1) {
@@ -653,6 +626,8 @@ __device__ __forceinline__ void do_block(const EvalArgs& a, const CUtensorMap* t
 #pragma unroll
     for (int k = 2; k < 4; k++) quad_pair<false>(Q, dy[k], zb[2 * k], zb[2 * k + 1]);
   }
+#pragma unroll
+  for (int q = 0; q < 8; q++) zb[q] = depth_of(zb[q]);
   mbar_wait_s(bar_s, phase);
   phase ^= 1u;
   score_lane<8, SUMS>(a, zb, obs_ls, acc);

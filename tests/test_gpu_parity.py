@@ -104,8 +104,8 @@ def test_fk_boxes_tight():
 
 def test_batch_fk_records_equal_the_fk_hook():
     """k_fk_batch's FK output (records, boxes; hp_debug_batch_fk) for every pose of a batch-path
-    call equals the single-pose FK hook's (the same FK device functions): spheres and boxes
-    bit for bit, quadric FAST coefficients to fp32 rounding.  A CTA-cooperative FK that
+    call equals the single-pose FK hook's (the same FK device functions): boxes bit for bit,
+    FAST coefficients to fp32 rounding.  A CTA-cooperative FK that
     dropped or misplaced a record fails here before any pixel is scored."""
     ctx = ctx_for(320, 240)
     obs = obs_for(W.H_A, 320, 240)
@@ -117,9 +117,11 @@ def test_batch_fk_records_equal_the_fk_hook():
         rb, bb = ctx.debug_batch_fk(i)
         rd, bd, _, _ = ctx.debug_fk(poses[i].astype(np.float64))
         assert np.array_equal(bb, bd), i
-        assert np.array_equal(rb[:20, :4], rd[:20, :4]), i
-        np.testing.assert_allclose(rb[20:35, :22], rd[20:35, :22], rtol=2e-6, atol=1e-6)
-        np.testing.assert_allclose(rb[35:, :18], rd[35:, :18], rtol=2e-6, atol=1e-6)
+        # FAST records (16 fields, common.cuh): fp32 rounding of the fp64 coefficients, per
+        # field relative to the field's scale over the pose (1 / c0 ~ 1e-6, D ~ 1e4)
+        scale = np.max(np.abs(rd[:, :16]), axis=0, keepdims=True)
+        assert np.all(np.abs(rb[:, :16] - rd[:, :16]) <= 2e-6 * np.abs(rd[:, :16]) + 1e-7 * scale), i
+        assert not np.any(rb[:, 16:]) and not np.any(rd[:, 16:]), i  # unused fields are zero
 
 
 # ------------------------------------------------------------------------------ depth
