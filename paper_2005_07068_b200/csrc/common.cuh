@@ -20,7 +20,10 @@ constexpr int kRec = 24;   // floats per primitive record (96 B)
 constexpr int kPxPerLane = HP_PX;       // pixels per lane (one column, every other row)
 constexpr int kTileW = 16;              // warp tile: 16 x (2 * kPxPerLane) pixels
 constexpr int kTileH = 2 * kPxPerLane;
-constexpr int kMaxTiles = 512;          // producer block list capacity per particle
+#ifndef HP_MAX_TILES
+#define HP_MAX_TILES 256
+#endif
+constexpr int kMaxTiles = HP_MAX_TILES;  // block-list capacity per particle (16 x 16 blocks)
 constexpr int kBlockH = 2 * kTileH;     // the batch renderer's warp block: two 16 x 8 tiles
                                         // (top / bottom half, each with its own cull masks)
 constexpr int kRayPad = 16;             // ray-table slack for tiles overhanging the image

@@ -186,7 +186,7 @@ namespace hp {
 #endif
 constexpr int kEvalWarps = HP_NW;
 #ifndef HP_RENDER_NW
-#define HP_RENDER_NW 16  // warps per k_render_persist CTA (2 CTAs per SM at 64 registers)
+#define HP_RENDER_NW 8  // warps per k_render_persist CTA (4 CTAs per SM at 64 registers)
 #endif
 constexpr int kRenderWarps = HP_RENDER_NW;
 

@@ -409,7 +409,8 @@ def test_pso_hand_fit_parity_c2_c3(res):
 
 
 def test_batch_path_close_up_poses_beyond_tile_list_capacity():
-    """Hands close to the camera have union boxes of more than kMaxTiles (512) 16x8 tiles;
+    """Hands close to the camera have union boxes of more than kMaxTiles (256) 16x16 blocks
+    (512 16x8 tiles);
     the FK kernel then hands the renderer no tile list and it culls every tile itself.
     Mixed into a batch large enough for the persistent path (S = 1)."""
     ctx = ctx_for(640, 480)
