@@ -309,14 +309,16 @@ hp_status hp_shard_loopback(hp_ctx* ctx, const char* group, int32_t rank, int32_
 int64_t hp_last_launch_count(const hp_ctx* ctx);
 /* Per-launch device timing of the evaluation (bench.py's roofline leg).
    hp_set_timing(ctx, 1) makes every later hp_eval_costs / hp_eval_costs_host / hp_eval_sums
-   record three CUDA events on the stream the kernels run on: before the first launch,
-   between the two launches of the batch path (k_fk_batch | k_render_persist), after the
-   last. hp_last_kernel_ms waits for the last event and returns ms[0] = first launch
-   (k_fk_batch; 0 on single-launch paths) and ms[1] = the renderer / fused kernel.
-   HP_ERR_STATE if no timed evaluation was enqueued since timing was switched on.
-   Timing adds two event records per call; leave it off outside measurement. */
+   record four CUDA events on the stream the kernels run on: before the first launch,
+   between the launches of the batch path (k_fk_batch | k_render_persist | its near-plane
+   pass), after the last. hp_last_kernel_ms waits for the last event and returns ms[0] =
+   first launch (k_fk_batch; 0 on single-launch paths), ms[1] = the renderer / fused kernel
+   alone, ms[2] = the near-plane pass (0 on single-launch paths).  HP_ERR_STATE if no timed
+   evaluation was enqueued since timing was switched on.  Timing adds event records between
+   the launches (the programmatic-dependent-launch overlap between them is lost); leave it off
+   outside measurement. */
 hp_status hp_set_timing(hp_ctx* ctx, int32_t on);
-hp_status hp_last_kernel_ms(hp_ctx* ctx, float ms[2]);
+hp_status hp_last_kernel_ms(hp_ctx* ctx, float ms[3]);
 
 /* Split factor S (CTAs per particle) used for n poses. */
 int32_t hp_splits_for(const hp_ctx* ctx, int64_t n);

@@ -185,7 +185,7 @@ struct hp_ctx {
   int sync_debug = 0;  // HP_SYNC_DEBUG=1: synchronise after every launch
   int use_pdl = 1;     // programmatic dependent launch between PSO generations (HP_NO_PDL=1)
   int zero_copy = 1;   // host path: kernels access mapped pinned buffers (HP_NO_ZEROCOPY=1)
-  cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};  // hp_set_timing: per-launch events
+  cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};  // hp_set_timing: per launch
   int timing = 0;
   int timed = 0;  // the last hp_eval_costs / hp_eval_sums recorded tev
   std::string err;
@@ -317,16 +317,17 @@ hp_status hp_set_timing(hp_ctx* ctx, int32_t on) {
   return HP_OK;
 }
 
-hp_status hp_last_kernel_ms(hp_ctx* ctx, float ms[2]) {
+hp_status hp_last_kernel_ms(hp_ctx* ctx, float ms[3]) {
   ARG(ctx && ms, "hp_last_kernel_ms: NULL argument");
   if (!ctx->timed) {
     ctx->err = "hp_last_kernel_ms: no timed evaluation (hp_set_timing(ctx, 1) first)";
     return HP_ERR_STATE;
   }
   cudaSetDevice(ctx->device);
-  CK(cudaEventSynchronize(ctx->tev[2]));
+  CK(cudaEventSynchronize(ctx->tev[3]));
   CK(cudaEventElapsedTime(&ms[0], ctx->tev[0], ctx->tev[1]));
   CK(cudaEventElapsedTime(&ms[1], ctx->tev[1], ctx->tev[2]));
+  CK(cudaEventElapsedTime(&ms[2], ctx->tev[2], ctx->tev[3]));
   return HP_OK;
 }
 
@@ -530,6 +531,8 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
     if (atoi(e)) ctx->zero_copy = 0;
   if (const char* e = getenv("HP_NO_PERSIST"))
     if (atoi(e)) ctx->persist_grid = 0;
+  if (const char* e = getenv("HP_PERSIST_GRID"))  // A/B: the renderer's CTA count
+    if (atoi(e) > 0) ctx->persist_grid = atoi(e);
   // the persistent renderer always loads observation tiles by TMA from its kernel-parameter
   // descriptor (compile time); the HP_NO_TMA / HP_TMA_MODE A/B switches use k_eval
   if (ctx->use_tma != 1) ctx->persist_grid = 0;

@@ -265,9 +265,16 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
 #define HP_SLOTS 2  // particle slots per renderer CTA (FK record + block list each)
 #endif
 constexpr int kSlots = HP_SLOTS;
-// dynamic shared memory of k_render_persist: the ray table, then the slots' block lists
-__host__ __device__ constexpr size_t render_dyn_bytes(int W, int H) {
-  return (size_t)ray_floats(W, H) * sizeof(float) + (size_t)kSlots * kMaxTiles * sizeof(BlockEnt);
+#ifndef HP_RAY_GLOBAL
+#define HP_RAY_GLOBAL 0  // 1: the block renderer reads the ray table through L1, not shared
+#endif
+// dynamic shared memory of k_render_persist: the ray table (the near pass, or HP_RAY_GLOBAL
+// = 0), then the slots' block lists
+__host__ __device__ constexpr size_t render_ray_bytes(int W, int H, bool near) {
+  return near || !HP_RAY_GLOBAL ? (size_t)ray_floats(W, H) * sizeof(float) : 0;
+}
+__host__ __device__ constexpr size_t render_dyn_bytes(int W, int H, bool near = false) {
+  return render_ray_bytes(W, H, near) + (size_t)kSlots * kMaxTiles * sizeof(BlockEnt);
 }
 template <int NW, bool NEAR, bool SUMS>
 __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
@@ -285,8 +292,8 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   extern __shared__ float s_ray[];
   // the slots' block lists follow the ray table (16-byte aligned: ray_floats is a multiple
   // of 4)
-  BlockEnt(*s_tiles)[kMaxTiles] =
-      reinterpret_cast<BlockEnt(*)[kMaxTiles]>(s_ray + ray_floats(a.cam.W, a.cam.H));
+  BlockEnt(*s_tiles)[kMaxTiles] = reinterpret_cast<BlockEnt(*)[kMaxTiles]>(
+      reinterpret_cast<char*>(s_ray) + render_ray_bytes(a.cam.W, a.cam.H, NEAR));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* s_dx = s_ray;
@@ -352,7 +359,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
 #endif
     for (int b = 0; b < kSlots; b++) issue(b);
   }
-  {
+  if (NEAR || !HP_RAY_GLOBAL) {
     const int n4 = ray_floats(a.cam.W, a.cam.H) / 4;
     for (int i = threadIdx.x; i < n4; i += NW * 32)
       reinterpret_cast<float4*>(s_ray)[i] = __ldg(reinterpret_cast<const float4*>(a.ray) + i);
@@ -363,6 +370,11 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   const uint32_t obs_s = HP_PIN(smem_u32(s_obs[warp])), bar_s = HP_PIN(smem_u32(&s_bar[warp]));
   const uint32_t dx_s = HP_PIN(smem_u32(s_dx + (lane & 15)));
   const uint32_t dy_s = HP_PIN(smem_u32(s_dy + 4 * (lane >> 4)));
+#if HP_RAY_GLOBAL
+  // the lane's column / first row in the global ray table (L1-resident)
+  const float* ray_x = a.ray + (lane & 15);
+  const float4* ray_y = reinterpret_cast<const float4*>(a.ray + ray_dx_len(a.cam.W)) + (lane >> 4);
+#endif
   // the lane's first observation pixel (column lane & 15, row lane >> 4) and the slots'
   // shared bases, computed once (the compiler otherwise re-derives them per block)
   const uint32_t obs_ls = HP_PIN(obs_s + 4u * ((lane >> 4) * kTileW + (lane & 15)));
@@ -429,8 +441,13 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
             any = (kt.x | kt.y | kt.z | kb.x | kb.y | kb.z) != 0;
           }
           if (any)
+#if HP_RAY_GLOBAL
+            do_block<SUMS, true>(a, &tmap, rec_s, ent, obs_s, obs_ls, bar_s, phase, dx_s, dy_s,
+                                 acc, yoff, ray_x, ray_y);
+#else
             do_block<SUMS>(a, &tmap, rec_s, ent, obs_s, obs_ls, bar_s, phase, dx_s, dy_s, acc,
                            yoff);
+#endif
         }
         t = tn;
       }

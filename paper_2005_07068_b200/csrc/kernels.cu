@@ -204,7 +204,7 @@ static void set_carveouts() {
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(kMaxRayBytes + extra));
   };
-  const size_t tiles = (size_t)kSlots * kMaxTiles * 16;  // the renderer's block lists
+  const size_t tiles = (size_t)kSlots * kMaxTiles * sizeof(BlockEnt);  // the block lists
   cfg(k_render_persist<kRenderWarps, false, false>, tiles);
   cfg(k_render_persist<kRenderWarps, true, false>, tiles);
   cfg(k_render_persist<kRenderWarps, false, true>, tiles);
@@ -336,7 +336,8 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     if (e != cudaSuccess) return e;
     if (tev) cudaEventRecord(tev[1], st);
     const dim3 pgrid((unsigned)(a.persist_grid < a.n ? a.persist_grid : a.n));
-    const size_t rdyn = render_dyn_bytes(a.cam.W, a.cam.H);
+    const size_t rdyn = render_dyn_bytes(a.cam.W, a.cam.H),
+                 ndyn = render_dyn_bytes(a.cam.W, a.cam.H, true);  // the near pass
 #if HP_FK_PDL
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = pgrid;
@@ -352,23 +353,27 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     e = sums ? cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, false, true>, a, *map16)
              : cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, false, false>, a, *map16);
     if (e != cudaSuccess) return e;
+    if (tev) cudaEventRecord(tev[2], st);  // the renderer alone (timing mode only)
     // the near-plane pass (exits at once when k_fk_batch queued nothing)
     cfg.gridDim = dim3((unsigned)(pgrid.x < 148u ? pgrid.x : 148u));
+    cfg.dynamicSmemBytes = ndyn;
     e = sums ? cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, true, true>, a, *map)
              : cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, true, false>, a, *map);
     if (e != cudaSuccess) return e;
 #else
     if (a.sums_out) {
       k_render_persist<kRenderWarps, false, true><<<pgrid, rblock, rdyn, st>>>(a, *map16);
+      if (tev) cudaEventRecord(tev[2], st);
       k_render_persist<kRenderWarps, true, true><<<dim3(pgrid.x < 148u ? pgrid.x : 148u), rblock,
-                                                 rdyn, st>>>(a, *map);
+                                                 ndyn, st>>>(a, *map);
     } else {
       k_render_persist<kRenderWarps, false, false><<<pgrid, rblock, rdyn, st>>>(a, *map16);
+      if (tev) cudaEventRecord(tev[2], st);
       k_render_persist<kRenderWarps, true, false><<<dim3(pgrid.x < 148u ? pgrid.x : 148u), rblock,
-                                                  rdyn, st>>>(a, *map);
+                                                  ndyn, st>>>(a, *map);
     }
 #endif
-    if (tev) cudaEventRecord(tev[2], st);
+    if (tev) cudaEventRecord(tev[3], st);
     return cudaGetLastError();
   } else if (mode == kModeCost && a.pdl && pose_double) {
     cudaLaunchConfig_t cfg = {};
@@ -385,7 +390,10 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
         a.near_seen ? cudaLaunchKernelEx(&cfg, k_eval<kEvalWarps, double, kModeCost, false>, a,
                                          *map)
                     : cudaLaunchKernelEx(&cfg, k_eval<kEvalWarps, double, kModeCost>, a, *map);
-    if (tev) cudaEventRecord(tev[2], st);
+    if (tev) {
+      cudaEventRecord(tev[2], st);
+      cudaEventRecord(tev[3], st);  // single-kernel path: empty last interval
+    }
     return e;
   } else if (mode == kModeCost) {
     if (pose_double && a.near_seen)
@@ -400,7 +408,10 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     else
       k_eval<kEvalWarps, float, kModeDepth><<<grid, block, dyn, st>>>(a, *map);
   }
-  if (tev) cudaEventRecord(tev[2], st);
+  if (tev) {
+    cudaEventRecord(tev[2], st);
+    cudaEventRecord(tev[3], st);  // single-kernel path: empty last interval
+  }
   return cudaGetLastError();
 }
 

@@ -339,7 +339,7 @@ struct TileGrid {
   __device__ __forceinline__ explicit TileGrid(int4 ub, bool need_origin = true) {
     x0 = ub.x & ~3;
     y0 = ub.y;
-    const int bw = ub.z - x0 + 1, bh = ub.w - ub.y + 1;
+    const int bw = ub.z - x0 + 1, bh = ub.w - y0 + 1;
     tx = bw > 0 ? (bw + kTileW - 1) / kTileW : 0;
     const int ty = bh > 0 ? (bh + kTileH - 1) / kTileH : 0;
     ntiles = tx * ty;
@@ -559,18 +559,21 @@ __device__ __forceinline__ uint3 split_kinds(uint2 m) {
 // rows lane >> 4 + {0, 2, ..., 14}; pairs 0, 1 are the top tile, 2, 3 the bottom.
 // rec_s: shared address of the particle's FAST records; obs_s: the warp's observation
 // buffer, obs_ls: this lane's first pixel in it (column lane & 15, row lane >> 4).
-template <bool SUMS>
+template <bool SUMS, bool RG = false>
 __device__ __forceinline__ void do_block(const EvalArgs& a, const CUtensorMap* tmap,
                                          uint32_t rec_s, BlockEnt e, uint32_t obs_s,
                                          uint32_t obs_ls, uint32_t bar_s, uint32_t& phase,
-                                         uint32_t dx_s, uint32_t dy_s, TileSums& acc, int yoff) {
+                                         uint32_t dx_s, uint32_t dy_s, TileSums& acc, int yoff,
+                                         const float* ray_x = nullptr,
+                                         const float4* ray_y = nullptr) {
   const uint4 ent = e.a;
   const int X0 = (int)(ent.x & 0xFFFFu), Y0 = (int)(ent.x >> 16);
   HP_CHECK(yoff >= 0 && Y0 < a.cam.H && (X0 & 3) == 0);
   tma_load_2d_elect_s(obs_s, tmap, X0, Y0 + yoff, bar_s, kTileW * kBlockH * 4);
-  const float dx = __uint_as_float(lds_u32(dx_s + 4u * X0));
-  const float4 ya = lds_f4(dy_s + 16u * Y0);        // rows y, y+2, y+4, y+6
-  const float4 yb = lds_f4(dy_s + 16u * (Y0 + 8));  // rows y+8 .. y+14
+  // RG: the ray table through L1 (global), else the CTA's shared copy
+  const float dx = RG ? __ldg(ray_x + X0) : __uint_as_float(lds_u32(dx_s + 4u * X0));
+  const float4 ya = RG ? __ldg(ray_y + Y0) : lds_f4(dy_s + 16u * Y0);  // rows y .. y+6
+  const float4 yb = RG ? __ldg(ray_y + Y0 + 8) : lds_f4(dy_s + 16u * (Y0 + 8));  // y+8 ..
   const f2 dy[4] = {pk(ya.x, ya.y), pk(ya.z, ya.w), pk(yb.x, yb.y), pk(yb.z, yb.w)};
   float zb[8];  // the largest inverse depth so far, then the depth
 #pragma unroll
@@ -630,7 +633,13 @@ __device__ __forceinline__ void do_block(const EvalArgs& a, const CUtensorMap* t
   for (int q = 0; q < 8; q++) zb[q] = depth_of(zb[q]);
   mbar_wait_s(bar_s, phase);
   phase ^= 1u;
+#if HP_HALF_SCORE
+  // each 16 x 8 half scored only if something was rendered in it
+  score_lane<4, SUMS>(a, zb, obs_ls, acc);
+  score_lane<4, SUMS>(a, zb + 4, obs_ls + 4u * 8 * kTileW, acc);
+#else
   score_lane<8, SUMS>(a, zb, obs_ls, acc);
+#endif
   __syncwarp();
 }
 

@@ -485,11 +485,12 @@ class Context:
         """Record per-launch CUDA events around every later evaluation (hp_set_timing)."""
         _check(self._L.hp_set_timing(self._h, 1 if on else 0), self._h, self._L)
 
-    def last_kernel_ms(self) -> tuple[float, float]:
-        """(first launch, renderer) device ms of the last timed evaluation."""
-        ms = (C.c_float * 2)()
+    def last_kernel_ms(self) -> tuple[float, float, float]:
+        """(first launch, renderer alone, near-plane pass) device ms of the last timed
+        evaluation."""
+        ms = (C.c_float * 3)()
         _check(self._L.hp_last_kernel_ms(self._h, ms), self._h, self._L)
-        return float(ms[0]), float(ms[1])
+        return float(ms[0]), float(ms[1]), float(ms[2])
 
     # -- PSO
     def pso_fit(self, seed: int = 0, particles: int = 64, generations: int = 30,
