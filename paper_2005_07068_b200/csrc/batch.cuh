@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
 // in a second, normally empty launch, so the near-plane code never shares a register
 // allocation with the hot loop.
 #ifndef HP_SLOTS
-#define HP_SLOTS 2  // particle slots per renderer CTA (FK record + block list each)
+#define HP_SLOTS 3  // particle slots per renderer CTA (FK record + block list each)
 #endif
 constexpr int kSlots = HP_SLOTS;
 #ifndef HP_RAY_GLOBAL
@@ -452,6 +452,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
         t = tn;
       }
     }
+    unpack_counts(acc);
     warp_reduce<SUMS>(acc);
     // publish this warp's partial sums; the last warp to arrive (acq_rel counter: its
     // acquire sees every other warp's partials) reduces them and refills the slot

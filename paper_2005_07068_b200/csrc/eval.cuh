@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS_EVAL / NW)
   GENPROF_MAX(2)
   if (MODE != kModeCost) return;
   // ---- reduction: warp shuffles, one atomic per sum per CTA ----
+  unpack_counts(acc);
   warp_reduce(acc);
   if (lane == 0) {
     s_red[warp][0] = acc.rm;

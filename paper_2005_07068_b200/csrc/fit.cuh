@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(kFitWarps * 32, 1)
     }
     FITPROF_MAX(k, 2)
     // ---- 3. publish the CTA's sums (+ position and kc); grid barrier ----
+    unpack_counts(acc);
     warp_reduce(acc);
     if (lane == 0) {
       s_red[warp][0] = acc.rm;

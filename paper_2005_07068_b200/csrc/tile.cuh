@@ -402,28 +402,30 @@ __device__ __forceinline__ void score_lane(const EvalArgs& a, const float* zb, u
       // true for NaN.  o_s AND r_m adds bit 31 of w.  Both depths defined: hit AND diff
       // is a number; the numerator adds the bits of the magic-number FFMA minus the
       // magic's (predicated adds only: no selects, no float-to-int conversion).
+      // r_m and o_s AND r_m in one packed counter (one PRMT + one predicated add): the
+      // increment is 1 + (o_s ? 0xFFFF0000 : 0) — o_s's sign bit replicated into the high
+      // half — so the counter holds r_m - (o_s AND r_m) 2^16 (unpack_counts)
       asm("{\n\t"
-          ".reg .pred ph, pr, pb, pa;\n\t"
+          ".reg .pred ph, pr, pb;\n\t"
           ".reg .f32 d, c;\n\t"
           ".reg .b32 t;\n\t"
-          "mov.b32 d, %4;\n\t"
+          "mov.b32 d, %3;\n\t"
           "abs.f32 d, d;\n\t"
-          "sub.f32 d, d, %5;\n\t"
+          "sub.f32 d, d, %4;\n\t"
           "abs.f32 d, d;\n\t"
-          "setp.le.f32 ph, %5, %6;\n\t"
-          "setp.ltu.and.f32 pr, d, %7, ph;\n\t"
-          "@pr add.u32 %0, %0, 1;\n\t"
-          "setp.lt.and.s32 pa, %4, 0, pr;\n\t"
-          "@pa add.u32 %1, %1, 1;\n\t"
+          "setp.le.f32 ph, %4, %5;\n\t"
+          "setp.ltu.and.f32 pr, d, %6, ph;\n\t"
+          "prmt.b32 t, %3, 1, 0xBB54;\n\t"
+          "@pr add.u32 %0, %0, t;\n\t"
           "setp.num.and.f32 pb, d, d, ph;\n\t"
-          "@pb add.u32 %2, %2, 1;\n\t"
-          "min.f32 c, d, %8;\n\t"
-          "fma.rn.f32 c, c, %9, %10;\n\t"
+          "@pb add.u32 %1, %1, 1;\n\t"
+          "min.f32 c, d, %7;\n\t"
+          "fma.rn.f32 c, c, %8, %9;\n\t"
           "mov.b32 t, c;\n\t"
-          "sub.u32 t, t, %11;\n\t"
-          "@pb add.u32 %3, %3, t;\n\t"
+          "sub.u32 t, t, %10;\n\t"
+          "@pb add.u32 %2, %2, t;\n\t"
           "}"
-          : "+r"(acc.rm), "+r"(acc.and_), "+r"(both), "+r"(num)
+          : "+r"(acc.rm), "+r"(both), "+r"(num)
           : "r"(w), "f"(zb[q]), "f"(zfar), "f"(d_m), "f"(clampv), "f"(qscale), "f"(qmagic),
             "r"(magic_bits));
     }
@@ -728,6 +730,13 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
   const unsigned int lo = __reduce_add_sync(0xffffffffu, (unsigned int)v & 0xFFFFFFu);
   const unsigned int hi = __reduce_add_sync(0xffffffffu, (unsigned int)(v >> 24));
   return ((unsigned long long)hi << 24) + lo;
+}
+// The lane's packed counter (score_lane: rm holds r_m - (o_s AND r_m) 2^16, both < 2^16
+// per lane) split into the two counts; once per lane before warp_reduce.
+__device__ __forceinline__ void unpack_counts(TileSums& s) {
+  const unsigned int p = s.rm;
+  s.rm = p & 0xFFFFu;
+  s.and_ = (0u - (p >> 16)) & 0xFFFFu;
 }
 template <bool BOTH = true>
 __device__ __forceinline__ void warp_reduce(TileSums& s) {
