@@ -299,30 +299,36 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   const float* s_dx = s_ray;
   const float* s_dy = s_ray + ray_dx_len(a.cam.W);
   unsigned int* const counter = a.pcount + (NEAR ? 2 : 0);  // [taken, CTAs exited]
-  // one thread: take the next particle and pull its FK record + tile list into slot b
-  auto issue = [&](int b) {
+  // one thread: take the next particle (k: a counter value already taken, or -1) and pull
+  // its FK record + tile list into slot b.  The record's copy starts before the list
+  // length is known (expect_tx without arrival; the arrival follows with the list bytes)
+  auto issue = [&](int b, int kt) {
     int p = a.n;
+    const unsigned k = kt >= 0 ? (unsigned)kt : atomicAdd(counter, 1u);
     if (NEAR) {
-      const unsigned k = atomicAdd(counter, 1u);
       if (k < __ldcg(a.near_count)) p = __ldcg(a.near_list + k);
     } else {
-      p = (int)atomicAdd(counter, 1u);
+      p = (int)k;
     }
     s_pid[b] = p;
     if (p < a.n) {
-      const int ntl = NEAR ? -1 : __ldcg(a.ntl_g + p);  // NEAR: cull every tile
-      s_ntl[b] = ntl;
-      if (ntl == -2) {  // queued for the near-plane pass: nothing to fetch
-        mbar_arrive(&s_full[b]);
+      if (NEAR) {
+        mbar_expect_tx(&s_full[b], (uint32_t)(sizeof(FkOut) + sizeof(FkExact)));
+        bulk_g2s(&s_out[b], static_cast<const FkOut*>(a.fk_g) + p, (uint32_t)sizeof(FkOut),
+                 &s_full[b]);
+        bulk_g2s(&s_x[NEAR ? b : 0], static_cast<const FkExact*>(a.fkx_g) + p,
+                 (uint32_t)sizeof(FkExact), &s_full[b]);
+        s_ntl[b] = -1;  // NEAR: cull every tile
         return;
       }
-      const uint32_t lb = ntl > 0 ? (uint32_t)ntl * (uint32_t)sizeof(BlockEnt) : 0u;
-      const uint32_t xb = NEAR ? (uint32_t)sizeof(FkExact) : 0u;
-      mbar_expect_tx(&s_full[b], (uint32_t)sizeof(FkOut) + lb + xb);
+      mbar_expect_tx_only(&s_full[b], (uint32_t)sizeof(FkOut));
       bulk_g2s(&s_out[b], static_cast<const FkOut*>(a.fk_g) + p, (uint32_t)sizeof(FkOut),
                &s_full[b]);
-      if (NEAR)
-        bulk_g2s(&s_x[NEAR ? b : 0], static_cast<const FkExact*>(a.fkx_g) + p, xb, &s_full[b]);
+      const int ntl = __ldcg(a.ntl_g + p);
+      s_ntl[b] = ntl;
+      // ntl == -2: queued for the near-plane pass (the record is not used); -1: no list
+      const uint32_t lb = ntl > 0 ? (uint32_t)ntl * (uint32_t)sizeof(BlockEnt) : 0u;
+      mbar_expect_tx(&s_full[b], lb);
       if (lb)
         bulk_g2s(s_tiles[b], reinterpret_cast<const BlockEnt*>(a.tiles_g) + (size_t)p * kMaxTiles,
                  lb, &s_full[b]);
@@ -357,7 +363,8 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
 #if HP_FK_PDL
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous grid is complete
 #endif
-    for (int b = 0; b < kSlots; b++) issue(b);
+    const unsigned k0 = atomicAdd(counter, (unsigned)kSlots);  // the first poses, one atomic
+    for (int b = 0; b < kSlots; b++) issue(b, (int)(k0 + b));
   }
   if (NEAR || !HP_RAY_GLOBAL) {
     const int n4 = ray_floats(a.cam.W, a.cam.H) / 4;
@@ -480,7 +487,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
         s_next[b] = 0;
         s_done[b] = 0;
         fence_proxy_async();  // every warp's generic reads of slot b precede the refill
-        issue(b);             // particle i + kSlots into the freed slot
+        issue(b, -1);         // particle i + kSlots into the freed slot
       }
     }
     __syncwarp();
