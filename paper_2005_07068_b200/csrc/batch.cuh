@@ -483,11 +483,13 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
       warp_reduce<SUMS>(t);
       if (lane == 0) {
         const unsigned long long v[4] = {t.rm, t.and_, t.num, t.both};
-        if (nlist != -2) finalize_cost(a, p, v, fo.kc);  // queued ones: the near pass
+        const double kc = fo.kc;  // read before the refill overwrites the slot
         s_next[b] = 0;
         s_done[b] = 0;
         fence_proxy_async();  // every warp's generic reads of slot b precede the refill
-        issue(b, -1);         // particle i + kSlots into the freed slot
+        issue(b, -1);         // particle i + kSlots into the freed slot (before the cost:
+                              // the refill's latency is the warps' critical path)
+        if (nlist != -2) finalize_cost(a, p, v, kc);  // queued ones: the near pass
       }
     }
     __syncwarp();
