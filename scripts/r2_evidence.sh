@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-2 evidence run (under gpurun): the full default bench line, the ncu launch list of a
+# Round-2 evidence run (final build) (under gpurun): the full default bench line, the ncu launch list of a
 # short bench run, and one ncu --set full capture each of k_render_persist and k_fk_batch.
 set -x
 python bench.py > gpurun_out/r2_bench.json 2> gpurun_out/r2_bench.err
@@ -9,3 +9,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/r2_launches.csv $S > gpurun_out/r2_launches.log 2>&1
 bash scripts/prof_render.sh r2
 bash scripts/prof_fk.sh r2
+ncu -i gpurun_out/prof_r2.ncu-rep --page source --csv --kernel-name regex:k_render_persist \
+    --launch-count 1 --print-source sass > gpurun_out/r2_render_src_sass.csv 2>&1
+bash scripts/prof_fit.sh r2
+python scripts/fit_time.py > gpurun_out/r2_fit_time.txt 2>&1
