@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--fit-seeds", type=int, default=10)
+    ap.add_argument("--fit-seeds", type=int, default=50)
     ap.add_argument("--no-fit", action="store_true")
     ap.add_argument("--track-frames", type=int, default=100)
     ap.add_argument("--frames", type=int, default=8,
@@ -79,9 +79,9 @@ def ncu_traffic():
         return None
 
 
-def walg_per_hyp():
+def walg_per_hyp(key="c4_640x480"):
     with open(os.path.join(ROOT, "profiles", "walg.json")) as f:
-        return json.load(f)["c4_640x480"]["flops_per_hyp"]
+        return json.load(f)[key]["flops_per_hyp"]
 
 
 class ClockSampler:
@@ -431,6 +431,28 @@ def run_ours(args):
                          f"{args.fit_seeds} seeds", "last_best_cost": r.best_cost,
                "launches_per_fit": ctx.last_launch_count(),
                "paper_context": "0.8 s/frame on AMD HD5870M + i7-740QM, 64 x 30 (P:L197)"}
+        # the fit against the same FP32 roofline: W_alg of the poses a C3 fit evaluates
+        # (profiles/walg.json "c3_fit_640x480", the oracle's PSO) x 64 x 40 / the fit's time
+        try:
+            wfit = walg_per_hyp("c3_fit_640x480")
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            peak = sms * 128 * 2 * 1965e6 / 1e12
+            ach = wfit * 64 * 40 / (fit["ms_per_frame"] * 1e-3) / 1e12
+            fit["roofline"] = {"achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                               "frac": ach / peak, "walg_per_hyp": wfit,
+                               "note": "host wall clock per fit (launch and result copy "
+                                       "included); FP32 peak at 1965 MHz"}
+        except (OSError, KeyError):
+            pass
+        # the paper's cold start: particles drawn from the whole Tables 1-2 box
+        ctx.pso_fit(seed=0, particles=64, generations=40)
+        cms = []
+        for s in range(min(args.fit_seeds, 20)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ctx.pso_fit(seed=s + 1, particles=64, generations=40)
+            cms.append(1e3 * (time.perf_counter() - t0))
+        fit["cold_init_ms_per_frame"] = statistics.median(cms)
         # M2's smaller configurations: C1 160x120 16 x 10, C2 320x240 64 x 40
         for name, (fw, fh, fn, fk) in (("C1", (160, 120, 16, 10)), ("C2", (320, 240, 64, 40))):
             cctx = hp.Context(fw, fh, max_particles=fn)

@@ -581,11 +581,15 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
   FKPROF(2)
   // ---- phase C: records + boxes ----
   if (TEAM >= 2) {
-    // TEAM 4: warp 0 the 20 spheres (EXACT + box, then FAST), warp 1 the 14 cones and
-    // warp 2 the cylinder + 3 ellipsoids (EXACT records into xrec, boxes), warp 3 the 18
-    // FAST quadric records straight from the frames, in parallel with warps 1-2
+    // TEAM 4: warp 0 the 20 spheres' EXACT records + boxes, warp 1 the 14 cones' and warp 2
+    // the cylinder's + 3 ellipsoids' (EXACT records into xrec, boxes), warp 3 the 18 FAST
+    // quadric records straight from the frames, and warp 2's idle lanes the 20 spheres'
+    // FAST records, all in parallel (no warp builds two records per lane)
     if (w == 3) {
       if (lane < kNprim - kCone0) build_fast(kCone0 + lane, s, dm, out.rec[kCone0 + lane]);
+    } else if (w == 2 && lane >= kNprim - kCyl) {
+      const int j = lane - (kNprim - kCyl);  // lanes 4..23: spheres 0..19
+      if (j < kCone0) build_fast(j, s, dm, out.rec[j]);
     } else {
       const int j0 = w == 0 ? 0 : (w == 1 ? kCone0 : kCyl);
       const int j1 = w == 0 ? kCone0 : (w == 1 ? kCyl : kNprim);
@@ -595,7 +599,6 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
         float* xr = xrec->rec[j];
         build_prim(j, s, dm, cam, xr, out.box[j], zmin, nullptr);
         s.nearf[j] = zmin > cam.znear * 1.001f;
-        if (j < kCone0) build_fast(j, s, dm, out.rec[j]);  // spheres: FAST on warp 0
       }
     }
     if (w != 0) {

@@ -35,6 +35,22 @@ def main():
     out["h_A_640x480"] = mean_walg(W.H_A[None], cam)
     for res in ("160x120", "320x240"):
         out[f"h_A_{res}"] = mean_walg(W.H_A[None], O.camera(*W.RESOLUTIONS[res]))
+    # C3: every pose a 64 x 40 fit evaluates (the oracle's PSO on the oracle's costs, local
+    # init box, seeds 1 and 2; bench.py's pso_fit leg divides it by the fit's time)
+    obs = O.synthesize(W.H_A, cam)
+    lo, hi = O.bounds()
+    c, rad = W.local_init_box()
+    ilo, ihi = np.maximum(lo, c - rad), np.minimum(hi, c + rad)
+    seen = []
+
+    def objective(X):
+        seen.append(np.array(X))
+        return O.eval_batch(X, obs)
+
+    for seed in (1, 2):
+        O.pso_run(26, lo, hi, ilo, ihi, 6, 26,
+                  O.default_pso(seed=seed, particles=64, generations=40), objective)
+    out["c3_fit_640x480"] = mean_walg(np.concatenate(seen), cam)
     path = os.path.join(ROOT, "profiles", "walg.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
