@@ -276,6 +276,15 @@ __host__ __device__ constexpr size_t render_ray_bytes(int W, int H, bool near) {
 __host__ __device__ constexpr size_t render_dyn_bytes(int W, int H, bool near = false) {
   return render_ray_bytes(W, H, near) + (size_t)kSlots * kMaxTiles * sizeof(BlockEnt);
 }
+#if HP_TAIL_PROF
+// per CTA: globaltimer at entry, then per warp at loop exit (main pass only)
+__device__ unsigned long long g_tailprof[1024][1 + 16];
+__device__ __forceinline__ unsigned long long tail_time() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 template <int NW, bool NEAR, bool SUMS>
 __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     k_render_persist(const __grid_constant__ EvalArgs a,
@@ -296,6 +305,12 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
       reinterpret_cast<char*>(s_ray) + render_ray_bytes(a.cam.W, a.cam.H, NEAR));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if HP_TAIL_PROF
+  if (!NEAR && threadIdx.x == 0 && blockIdx.x < 1024) {
+    g_tailprof[blockIdx.x][0] = tail_time();
+    for (int q = 9; q < 17; q++) g_tailprof[blockIdx.x][q] = 0;
+  }
+#endif
   const float* s_dx = s_ray;
   const float* s_dy = s_ray + ray_dx_len(a.cam.W);
   unsigned int* const counter = a.pcount + (NEAR ? 2 : 0);  // [taken, CTAs exited]
@@ -333,6 +348,10 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
         bulk_g2s(s_tiles[b], reinterpret_cast<const BlockEnt*>(a.tiles_g) + (size_t)p * kMaxTiles,
                  lb, &s_full[b]);
     } else {
+#if HP_TAIL_PROF
+      if (!NEAR && blockIdx.x < 1024 && g_tailprof[blockIdx.x][16] == 0)
+        g_tailprof[blockIdx.x][16] = tail_time();  // the first terminator claim
+#endif
       mbar_arrive(&s_full[b]);  // terminator: complete the phase without data
     }
   };
@@ -490,10 +509,27 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
         issue(b, -1);         // particle i + kSlots into the freed slot (before the cost:
                               // the refill's latency is the warps' critical path)
         if (nlist != -2) finalize_cost(a, p, v, kc);  // queued ones: the near pass
+#if HP_TAIL_PROF
+        if (!NEAR && blockIdx.x < 1024) {  // smid, particles, blocks, last two finish times
+          unsigned long long* r = g_tailprof[blockIdx.x];
+          unsigned smid;
+          asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+          r[9] = smid;
+          r[10] += 1;
+          r[11] += nlist >= 0 ? nlist : 1000;
+          r[12] = r[13];
+          r[13] = tail_time();
+          r[14] = p;
+          r[15] = (unsigned)nlist;
+        }
+#endif
       }
     }
     __syncwarp();
   }
+#if HP_TAIL_PROF
+  if (!NEAR && lane == 0 && blockIdx.x < 1024) g_tailprof[blockIdx.x][1 + warp] = tail_time();
+#endif
   // the last CTA to leave resets the counters for the next launch
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -116,6 +116,9 @@ extern "C" int hp_debug_fit_clk(long long* out) {
 #define FITPROF_MAX(k, i)
 #endif
 
+#ifndef HP_FIT_DRAW_WARP
+#define HP_FIT_DRAW_WARP kEvalFkTeam  // the warp drawing generation k + 1's numbers
+#endif
 template <bool NEARCODE>
 __global__ void __launch_bounds__(kFitWarps * 32, 1)
     k_fit(const __grid_constant__ EvalArgs a, const __grid_constant__ CUtensorMap tmap) {
@@ -142,6 +145,8 @@ __global__ void __launch_bounds__(kFitWarps * 32, 1)
   __shared__ DimsD s_dims;
   __shared__ PsoDev s_ps;
   __shared__ PsoDyn s_dyn;
+  __shared__ CamParams s_cam;  // FK's camera and kc rest term (no constant-bank reads per
+  __shared__ double s_kcrest;  // generation: the parameter lines leave the constant cache)
   extern __shared__ float s_ray[];  // the ray table, then every particle's evaluated position
 
   const PsoDev& ps = s_ps;
@@ -166,6 +171,8 @@ __global__ void __launch_bounds__(kFitWarps * 32, 1)
   if (tid == 0) {
     s_ps = a.pso;
     s_dyn = *a.pso.dyn;
+    s_cam = a.cam;
+    s_kcrest = a.cost.kc_rest;
   }
   __syncthreads();
   const DimsD& dims = s_dims;
@@ -196,8 +203,10 @@ __global__ void __launch_bounds__(kFitWarps * 32, 1)
         pso_update_own(ps, dyn, s_pose, s_v, s_pb, s_g, s_lo, s_hi, s_rd[k & 1], s_mark != 0);
       __syncwarp();
       FITPROF_CLK(k, 5)
-      fk_team<double, kEvalFkTeam>(s_pose, dims, a.cam, a.cost.kc_rest, s_fk, s_out, &s_xr);
-    } else if (warp == kEvalFkTeam) {  // next generation's draws, while the team runs FK
+      // EXACT records only for the exact (near-plane) instantiation
+      fk_team<double, kEvalFkTeam>(s_pose, dims, s_cam, s_kcrest, s_fk, s_out,
+                                   NEARCODE ? &s_xr : nullptr);
+    } else if (warp == HP_FIT_DRAW_WARP) {  // next generation's draws, while the team runs FK
       if (lane == 0) s_next = 0;
       if (k + 1 < K) pso_draws_own(ps, dyn, p, k + 1, s_lo, s_hi, s_rd[(k + 1) & 1]);
     }

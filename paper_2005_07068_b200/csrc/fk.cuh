@@ -433,6 +433,13 @@ __device__ __forceinline__ void build_fast(int j, const FkScratch& s, const Dims
   }
 }
 
+#if HP_FK_PROF
+__device__ unsigned long long g_fkprof[16];
+#define FKPROF(i) \
+  if (blockIdx.x == 7 && threadIdx.x == 0) g_fkprof[i] = clock64();
+#else
+#define FKPROF(i)
+#endif
 // One warp: the union box of the 38 primitive boxes, the near-plane flag and kc(h) (P:L130,
 // AMB-7) of the pose in s / out.
 __device__ __forceinline__ void fk_finish_warp(const FkScratch& s, FkOut& out, double kc_rest) {
@@ -452,6 +459,7 @@ __device__ __forceinline__ void fk_finish_warp(const FkScratch& s, FkOut& out, d
       u.w = max(u.w, b.w);
     }
   }
+  FKPROF(5)
   near_ok = __all_sync(0xffffffffu, near_ok);
   for (int off = 16; off; off >>= 1) {
     u.x = min(u.x, __shfl_xor_sync(0xffffffffu, u.x, off));
@@ -459,6 +467,7 @@ __device__ __forceinline__ void fk_finish_warp(const FkScratch& s, FkOut& out, d
     u.z = max(u.z, __shfl_xor_sync(0xffffffffu, u.z, off));
     u.w = max(u.w, __shfl_xor_sync(0xffffffffu, u.w, off));
   }
+  FKPROF(6)
   if (lane == 0) {
     if (s.bad || u.z < u.x) u = make_int4(1, 1, 0, 0);
     out.ubox = u;
@@ -543,13 +552,6 @@ __device__ __forceinline__ void fk_finger_chain(FkScratch& s, const DimsD& dm, i
 //           warp 1; TEAM 3: spheres | cones | cylinder + ellipsoids, one kind per warp, so no
 //           warp serialises the branches of several kinds;
 //           warp 1, in parallel), then the union box, the near-plane flag and kc(h)
-#if HP_FK_PROF
-__device__ unsigned long long g_fkprof[16];
-#define FKPROF(i) \
-  if (blockIdx.x == 7 && threadIdx.x == 0) g_fkprof[i] = clock64();
-#else
-#define FKPROF(i)
-#endif
 // xrec (may be null): also keep the EXACT records (the near-plane path's) — TEAM >= 2
 // always, TEAM 1 (k_fk_batch, xrec in global memory) only for a pose that is not near_ok.
 // shp (may be null): the cones' tile-list capsules [kNcone] (cone_capsule).
@@ -596,8 +598,12 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
       const int j = j0 + lane;
       if (j < j1) {
         float zmin;
-        float* xr = xrec->rec[j];
-        build_prim(j, s, dm, cam, xr, out.box[j], zmin, nullptr);
+        if (xrec) {
+          build_prim(j, s, dm, cam, xrec->rec[j], out.box[j], zmin, nullptr);
+        } else {  // no EXACT records wanted: dead stores to a local array (removed)
+          float xl[kRec];
+          build_prim(j, s, dm, cam, xl, out.box[j], zmin, nullptr);
+        }
         s.nearf[j] = zmin > cam.znear * 1.001f;
       }
     }
@@ -634,6 +640,7 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
   }
   FKPROF(3)
   fk_finish_warp(s, out, kc_rest);
+  FKPROF(4)
 }
 
 template <typename PoseT>

@@ -357,6 +357,9 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     // the near-plane pass (exits at once when k_fk_batch queued nothing)
     cfg.gridDim = dim3((unsigned)(pgrid.x < 148u ? pgrid.x : 148u));
     cfg.dynamicSmemBytes = ndyn;
+#if HP_SKIP_NEAR_TEST  // A/B measurement only: what the (normally empty) near pass costs
+    if (0)
+#endif
     e = sums ? cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, true, true>, a, *map)
              : cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, true, false>, a, *map);
     if (e != cudaSuccess) return e;
@@ -415,6 +418,11 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
   return cudaGetLastError();
 }
 
+#if HP_TAIL_PROF
+extern "C" int hp_debug_tail_prof(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_tailprof, sizeof(g_tailprof));
+}
+#endif
 #if HP_FK_PROF
 extern "C" int hp_debug_fk_prof(unsigned long long* out) {
   return (int)cudaMemcpyFromSymbol(out, g_fkprof, sizeof(g_fkprof));

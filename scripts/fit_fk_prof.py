@@ -19,8 +19,11 @@ for s in range(3):
 torch.cuda.synchronize()
 out = (C.c_ulonglong * 16)()
 hp.hp.lib().hp_debug_fk_prof(out)
-t = [out[i] for i in range(4)]
-names = ["pose+sincos", "chains (B)", "records (C)"]
-for i in range(3):
+t = [out[i] for i in range(5)]
+t_all = [out[i] for i in range(16)]
+names = ["pose+sincos", "chains (B)", "records (C)", "union box, kc"]
+for i in range(4):
     print(f"{names[i]:12s} {(t[i + 1] - t[i]) / 1965:.2f} us")
-print(f"total        {(t[3] - t[0]) / 1965:.2f} us")
+for i, n in ((5, "finish: loads"), (6, "finish: shfl")):
+    print(f"{n:14s} {(t_all[i] - t_all[3]) / 1965:.2f} us")
+print(f"total        {(t[4] - t[0]) / 1965:.2f} us")
