@@ -461,12 +461,10 @@ __device__ __forceinline__ void fk_finish_warp(const FkScratch& s, FkOut& out, d
   }
   FKPROF(5)
   near_ok = __all_sync(0xffffffffu, near_ok);
-  for (int off = 16; off; off >>= 1) {
-    u.x = min(u.x, __shfl_xor_sync(0xffffffffu, u.x, off));
-    u.y = min(u.y, __shfl_xor_sync(0xffffffffu, u.y, off));
-    u.z = max(u.z, __shfl_xor_sync(0xffffffffu, u.z, off));
-    u.w = max(u.w, __shfl_xor_sync(0xffffffffu, u.w, off));
-  }
+  u.x = __reduce_min_sync(0xffffffffu, u.x);  // redux.sync: one instruction per bound
+  u.y = __reduce_min_sync(0xffffffffu, u.y);
+  u.z = __reduce_max_sync(0xffffffffu, u.z);
+  u.w = __reduce_max_sync(0xffffffffu, u.w);
   FKPROF(6)
   if (lane == 0) {
     if (s.bad || u.z < u.x) u = make_int4(1, 1, 0, 0);
