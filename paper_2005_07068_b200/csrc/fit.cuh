@@ -105,9 +105,11 @@ __device__ long long g_fitclk[64][2][8];
 extern "C" int hp_debug_fit_clk(long long* out) {
   return (int)cudaMemcpyFromSymbol(out, g_fitclk, sizeof(g_fitclk));
 }
-#define FITPROF_CLK(k, i)                                                      \
-  if (threadIdx.x == 0 && (k) < 64 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) \
-    g_fitclk[(k)][blockIdx.x == 0 ? 0 : 1][i] = clock64();
+// stamps staged in shared memory (a global store per stamp would add a constant-bank load
+// of the symbol's address, which misses: the loop's code evicts it), copied out at the end
+__shared__ long long s_fitclk[64][8];
+#define FITPROF_CLK(k, i) \
+  if (threadIdx.x == 0 && (k) < 64) s_fitclk[(k)][i] = clock64();
 #define FITPROF_MIN(k, i) FITPROF_CLK(k, i)
 #define FITPROF_MAX(k, i) FITPROF_CLK(k, i)
 #else
@@ -350,6 +352,11 @@ __global__ void __launch_bounds__(kFitWarps * 32, 1)
     FITPROF_MAX(k, 4)
     if (s_final) break;
   }
+#if HP_GEN_PROF
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+    for (int q = 0; q < 64 * 8; q++)
+      g_fitclk[q / 8][blockIdx.x == 0 ? 0 : 1][q % 8] = s_fitclk[q / 8][q % 8];
+#endif
   // ---- the final state for the host (hp_pso_state): split 0 of every particle, gbest ----
   if (sidx == 0 && tid < D) {
     const size_t id = (size_t)p * D + tid;

@@ -367,7 +367,10 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm,
 // parallel.
 __device__ __forceinline__ void build_fast(int j, const FkScratch& s, const DimsD& dm,
                                            float* rec) {
-  double c[3], M[3][3];
+  // the kinds differ only in the quadric's frame and coefficients: one write_fast_quadric
+  // call after the branches, so a warp holding several kinds runs its arithmetic once
+  double c[3], M[3][3], q[3], g2, h, hl;
+  bool axial;
   if (j < kCone0) {  // sphere at joint (f, k): |p - c|^2 - r^2, M = I
     const int f = j >> 2, k = j & 3;
     const double r = dm.rad[f][k];
@@ -375,8 +378,13 @@ __device__ __forceinline__ void build_fast(int j, const FkScratch& s, const Dims
       c[i] = s.J[f][k][i];
       for (int a = 0; a < 3; a++) M[a][i] = a == i ? 1.0 : 0.0;
     }
-    const double q[3] = {1.0, 1.0, 1.0};
-    write_fast_quadric(rec, c, M, q, 0.0, -r * r, false, 0.0);
+    q[0] = 1.0;
+    q[1] = 1.0;
+    q[2] = 1.0;
+    g2 = 0.0;
+    h = -r * r;
+    axial = false;
+    hl = 0.0;
   } else if (j < kCyl) {  // truncated cone J_k -> J_{k+1}: rows e1, e2, axis; midpoint origin
     int f, k;
     if (j < 32) {
@@ -394,8 +402,13 @@ __device__ __forceinline__ void build_fast(int j, const FkScratch& s, const Dims
     }
     // x^2 + y^2 - (r_m + k z)^2: Q = diag(1, 1, -k^2), g = (0, 0, -r_m k), h = -r_m^2
     const double rm = 0.5 * (dm.rad[f][k] + dm.rad[f][k + 1]), kk = dm.cone_k[f][k];
-    const double q[3] = {1.0, 1.0, -kk * kk};
-    write_fast_quadric(rec, c, M, q, -rm * kk, -rm * rm, true, 0.5 * dm.len[f][k]);
+    q[0] = 1.0;
+    q[1] = 1.0;
+    q[2] = -kk * kk;
+    g2 = -rm * kk;
+    h = -rm * rm;
+    axial = true;
+    hl = 0.5 * dm.len[f][k];
   } else if (j == kCyl) {  // palm: (x/a)^2 + (z/b)^2 - 1, axial y_H in [-len, 0]
     const double iw = 1.0 / dm.palm_half_w, it = 1.0 / dm.palm_half_t;
     for (int i = 0; i < 3; i++) {
@@ -404,8 +417,13 @@ __device__ __forceinline__ void build_fast(int j, const FkScratch& s, const Dims
       M[2][i] = s.RW[i][1];
       c[i] = s.h[i] - 0.5 * dm.palm_len * s.RW[i][1];
     }
-    const double q[3] = {1.0, 1.0, 0.0};
-    write_fast_quadric(rec, c, M, q, 0.0, -1.0, true, 0.5 * dm.palm_len);
+    q[0] = 1.0;
+    q[1] = 1.0;
+    q[2] = 0.0;
+    g2 = 0.0;
+    h = -1.0;
+    axial = true;
+    hl = 0.5 * dm.palm_len;
   } else {  // ellipsoids: |l|^2 - 1 with rows = axes / semi-axes
     double sd[3];
     if (j == kEll0) {
@@ -428,15 +446,22 @@ __device__ __forceinline__ void build_fast(int j, const FkScratch& s, const Dims
       const double is = 1.0 / sd[a];
       for (int i = 0; i < 3; i++) M[a][i] *= is;
     }
-    const double q[3] = {1.0, 1.0, 1.0};
-    write_fast_quadric(rec, c, M, q, 0.0, -1.0, false, 0.0);
+    q[0] = 1.0;
+    q[1] = 1.0;
+    q[2] = 1.0;
+    g2 = 0.0;
+    h = -1.0;
+    axial = false;
+    hl = 0.0;
   }
+  write_fast_quadric(rec, c, M, q, g2, h, axial, hl);
 }
 
 #if HP_FK_PROF
 __device__ unsigned long long g_fkprof[16];
+__shared__ unsigned long long s_fkprof[16];  // staged in shared memory (see fit.cuh)
 #define FKPROF(i) \
-  if (blockIdx.x == 7 && threadIdx.x == 0) g_fkprof[i] = clock64();
+  if (blockIdx.x == 7 && threadIdx.x == 0) s_fkprof[i] = clock64();
 #else
 #define FKPROF(i)
 #endif
@@ -639,6 +664,10 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
   FKPROF(3)
   fk_finish_warp(s, out, kc_rest);
   FKPROF(4)
+#if HP_FK_PROF
+  if (blockIdx.x == 7 && threadIdx.x == 0)
+    for (int q = 0; q < 16; q++) g_fkprof[q] = s_fkprof[q];
+#endif
 }
 
 template <typename PoseT>
