@@ -11,7 +11,7 @@ namespace hp {
 // (S > 1 splits per particle keep every SM busy) and for the depth-image hooks.
 // ---------------------------------------------------------------------------------------
 #ifndef HP_EVAL_FK_TEAM
-#define HP_EVAL_FK_TEAM 4  // k_eval's FK team: warps 0..3 (fk_team<4>)
+#define HP_EVAL_FK_TEAM 5  // k_eval's / k_fit's FK team: warps 0..4 (fk_team<5>)
 #endif
 constexpr int kEvalFkTeam = HP_EVAL_FK_TEAM;
 template <int NW, typename PoseT, int MODE, bool NEARCODE = true>

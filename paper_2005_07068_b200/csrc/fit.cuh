@@ -11,7 +11,7 @@ namespace hp {
 // Every CTA keeps its particle's swarm state (x, v, pbest) and the swarm-wide pbest costs
 // and gbest in shared memory; per generation:
 //   1. warp 0: Eq. (6)-(7) update of the CTA's particle (k >= 1; every split computes the
-//      same bits), warps 0-3: FK of that pose into shared memory (fk_team)
+//      same bits), warps 0-4: FK of that pose into shared memory (fk_team)
 //   2. all warps: the split's share of the particle's 16 x 8 tiles (run_tiles)
 //   3. the CTA's integer sums (and, split 0, the evaluated position and kc) to global
 //      memory, double-buffered by generation parity; one grid barrier

@@ -584,7 +584,8 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
                         double kc_rest, FkScratch& s, FkOut& out, FkExact* xrec = nullptr,
                         float4* shp = nullptr) {
   FKPROF(0)
-  static_assert(TEAM == 1 || TEAM == 4, "FK teams of 1 or 4 warps (warps 0..TEAM-1 of the CTA)");
+  static_assert(TEAM == 1 || TEAM == 4 || TEAM == 5,
+                "FK teams of 1, 4 or 5 warps (warps 0..TEAM-1 of the CTA)");
   const int lane = threadIdx.x & 31, w = TEAM >= 2 ? (int)(threadIdx.x >> 5) : 0;
   if (w == 0) {
     if (lane < kNdof) {
@@ -610,9 +611,12 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
     // the cylinder's + 3 ellipsoids' (EXACT records into xrec, boxes), warp 3 the 18 FAST
     // quadric records straight from the frames, and warp 2's idle lanes the 20 spheres'
     // FAST records, all in parallel (no warp builds two records per lane)
+    // TEAM 5: the spheres' FAST records on warp 4 instead (warp 2: the boxes only)
     if (w == 3) {
       if (lane < kNprim - kCone0) build_fast(kCone0 + lane, s, dm, out.rec[kCone0 + lane]);
-    } else if (w == 2 && lane >= kNprim - kCyl) {
+    } else if (w == 4) {
+      if (lane < kCone0) build_fast(lane, s, dm, out.rec[lane]);
+    } else if (TEAM == 4 && w == 2 && lane >= kNprim - kCyl) {
       const int j = lane - (kNprim - kCyl);  // lanes 4..23: spheres 0..19
       if (j < kCone0) build_fast(j, s, dm, out.rec[j]);
     } else {
