@@ -168,6 +168,8 @@ struct hp_ctx {
   void* fkx_g = nullptr;           // FkExact [max_n] (near-plane poses only)
   uint4* tiles_g = nullptr;        // [max_n][kMaxTiles]
   int* ntl_g = nullptr;            // [max_n]
+  unsigned int* fk_ready = nullptr;  // [max_n] batch FK readiness epochs
+  unsigned int* fk_epoch = nullptr;  // the batch launch epoch
   int* near_list = nullptr;        // [max_n] near-plane pass queue
   double* kc_g = nullptr;          // [max_n] kc per particle (fused PSO generations)
   unsigned int* near_count = nullptr;
@@ -354,7 +356,8 @@ void hp_destroy(hp_ctx* ctx) {
                  ctx->poses32, ctx->costs32, ctx->scratch, ctx->X, ctx->V, ctx->P, ctx->Pc,
                  ctx->E, ctx->G, ctx->Gc, ctx->trace, ctx->bnd, ctx->centre, ctx->mark,
                  ctx->flags, ctx->dyn, ctx->tmap_g, ctx->ray, ctx->pcount, ctx->X2,
-                 ctx->V2, ctx->gcount, ctx->fk_g, ctx->fkx_g, ctx->tiles_g, ctx->ntl_g, ctx->near_list,
+                 ctx->V2, ctx->gcount, ctx->fk_g, ctx->fkx_g, ctx->tiles_g, ctx->ntl_g, ctx->fk_ready,
+                 ctx->fk_epoch, ctx->near_list,
                  ctx->near_count, ctx->kc_g, ctx->pimp, ctx->gsel, ctx->fit_part,
                  ctx->fit_xpub, ctx->fit_bar};
   for (void* p : dev)
@@ -519,6 +522,13 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
   CKC(cudaMalloc(&ctx->fkx_g, (size_t)max_particles * fk_exact_bytes()));
   CKC(cudaMalloc(&ctx->tiles_g, (size_t)max_particles * kMaxTiles * 2 * sizeof(uint4)));
   CKC(cudaMalloc(&ctx->ntl_g, (size_t)max_particles * sizeof(int)));
+  CKC(cudaMalloc(&ctx->fk_ready, (size_t)max_particles * sizeof(unsigned int)));
+  CKC(cudaMemset(ctx->fk_ready, 0, (size_t)max_particles * sizeof(unsigned int)));
+  CKC(cudaMalloc(&ctx->fk_epoch, sizeof(unsigned int)));
+  {
+    const unsigned int one = 1;  // epoch 1: no flag holds it yet
+    CKC(cudaMemcpy(ctx->fk_epoch, &one, sizeof(one), cudaMemcpyHostToDevice));
+  }
   CKC(cudaMalloc(&ctx->pcount, 4 * sizeof(unsigned int)));
   CKC(cudaMemset(ctx->pcount, 0, 4 * sizeof(unsigned int)));
   CKC(cudaMalloc(&ctx->near_list, (size_t)max_particles * sizeof(int)));
@@ -749,6 +759,8 @@ static EvalArgs base_args(hp_ctx* ctx) {
   a.fkx_g = ctx->fkx_g;
   a.tiles_g = ctx->tiles_g;
   a.ntl_g = ctx->ntl_g;
+  a.fk_ready = ctx->fk_ready;
+  a.fk_epoch = ctx->fk_epoch;
   a.near_list = ctx->near_list;
   a.near_count = ctx->near_count;
   a.fit_part = ctx->fit_part;

@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
   const int cnt = build_block_list(s_out[warp],
                                    reinterpret_cast<BlockEnt*>(a.tiles_g) + (size_t)p * kMaxTiles, band,
                                    band + kMaxBand, s_shp[warp]);
+  __syncwarp();  // the warp's list (and C' record) stores precede lane 0's release
   if (lane == 0) {
     int ntl = cnt;
     if (!s_out[warp].near_ok) {  // some primitive may cross z_near: the exact pass renders it
@@ -251,7 +252,10 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
       ntl = -2;
     }
     a.ntl_g[p] = ntl;
-    bulk_wait_all();  // the record copy completes before the CTA's shared memory retires
+    bulk_wait_all();  // the record's bulk write is complete (and the CTA's shared memory free)
+    fence_proxy_async_global();
+    // publish: the renderer (already running, PDL) may take pose p from here on
+    st_release_u32(a.fk_ready + p, __ldcg(a.fk_epoch));
   }
 }
 
@@ -298,6 +302,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   __shared__ __align__(16) uint4 s_part[kSlots][NW];
   __shared__ unsigned int s_pboth[kSlots][NW];  // both-defined count (SUMS only)
   __shared__ int s_next[kSlots], s_done[kSlots], s_pid[kSlots], s_ntl[kSlots];
+  __shared__ int s_fkdone;  // k_fk_batch's grid is known complete (griddepcontrol.wait ran)
   extern __shared__ float s_ray[];
   // the slots' block lists follow the ray table (16-byte aligned: ray_floats is a multiple
   // of 4)
@@ -317,7 +322,10 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   // one thread: take the next particle (k: a counter value already taken, or -1) and pull
   // its FK record + tile list into slot b.  The record's copy starts before the list
   // length is known (expect_tx without arrival; the arrival follows with the list bytes)
-  auto issue = [&](int b, int kt) {
+  unsigned epoch = 0;  // thread 0: this launch's FK epoch (the first poses' flags)
+  // ready: the pose's FK is known to be published (after griddepcontrol.wait); otherwise
+  // (the first poses, taken while k_fk_batch may still run) wait for its flag first
+  auto issue = [&](int b, int kt, bool ready) {
     int p = a.n;
     const unsigned k = kt >= 0 ? (unsigned)kt : atomicAdd(counter, 1u);
     if (NEAR) {
@@ -335,6 +343,10 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
                  (uint32_t)sizeof(FkExact), &s_full[b]);
         s_ntl[b] = -1;  // NEAR: cull every tile
         return;
+      }
+      if (!ready) {  // wait for this launch's epoch in the pose's flag
+        while (ld_acquire_u32(a.fk_ready + p) != epoch) __nanosleep(256);
+        fence_proxy_async_global();  // the record's bulk read below sees FK's bulk write
       }
       mbar_expect_tx_only(&s_full[b], (uint32_t)sizeof(FkOut));
       bulk_g2s(&s_out[b], static_cast<const FkOut*>(a.fk_g) + p, (uint32_t)sizeof(FkOut),
@@ -379,11 +391,16 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     }
     fence_mbar_init();
     prefetch_tmap(&tmap);
+    s_fkdone = 0;
+    // the first poses, one atomic; with PDL this grid starts on SMs k_fk_batch frees, so
+    // each first pose waits for its own FK flag instead of the whole FK grid (NEAR: the
+    // previous grid is complete first)
 #if HP_FK_PDL
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous grid is complete
+    if (NEAR) asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
-    const unsigned k0 = atomicAdd(counter, (unsigned)kSlots);  // the first poses, one atomic
-    for (int b = 0; b < kSlots; b++) issue(b, (int)(k0 + b));
+    epoch = NEAR ? 0u : __ldcg(a.fk_epoch);  // advanced only by the previous launch's end
+    const unsigned k0 = atomicAdd(counter, (unsigned)kSlots);
+    for (int b = 0; b < kSlots; b++) issue(b, (int)(k0 + b), NEAR || !HP_FK_PDL || !a.fk_wait);
   }
   if (NEAR || !HP_RAY_GLOBAL) {
     const int n4 = ray_floats(a.cam.W, a.cam.H) / 4;
@@ -506,7 +523,16 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
         s_next[b] = 0;
         s_done[b] = 0;
         fence_proxy_async();  // every warp's generic reads of slot b precede the refill
-        issue(b, -1);         // particle i + kSlots into the freed slot (before the cost:
+#if HP_FK_PDL
+        // k_fk_batch complete before this refill reads its outputs: the first refilling
+        // thread of the CTA waits for the grid (griddepcontrol.wait) and says so through
+        // shared memory (release / acquire at CTA scope), later ones only read that
+        if (!NEAR && ld_acquire_cta_s32(&s_fkdone) == 0) {
+          asm volatile("griddepcontrol.wait;" ::: "memory");
+          st_release_cta_s32(&s_fkdone, 1);
+        }
+#endif
+        issue(b, -1, true);   // particle i + kSlots into the freed slot (before the cost:
                               // the refill's latency is the warps' critical path)
         if (nlist != -2) finalize_cost(a, p, v, kc);  // queued ones: the near pass
 #if HP_TAIL_PROF
@@ -538,6 +564,7 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
       counter[0] = 0;
       counter[1] = 0;
       if (NEAR) *a.near_count = 0;
+      else *a.fk_epoch += 1u;  // the next batch launch's flags
       __threadfence();
     }
   }

@@ -155,6 +155,8 @@ struct EvalArgs {
   int* near_seen;                 // non-null: speculative fit kernel (no near-plane code);
                                   // set when a particle needed it
   int pdl;                        // launched with programmatic dependent launch
+  int fk_wait;                    // renderer launched under k_fk_batch (PDL): its first poses
+                                  // wait for their FK flags (0: k_fk_batch is complete)
   // two-kernel batch path: k_fk_batch writes each particle's FK output and tile list here,
   // k_render_persist bulk-copies them into shared memory
   void* fk_g;                     // FkOut [n] (16-byte aligned records)
@@ -163,6 +165,9 @@ struct EvalArgs {
                                   // tile.cuh: the origin and the masks split per kind)
   int* ntl_g;                     // [n] tile-list length (-1: box too large, cull on the fly;
                                   // -2: queued for the near-plane pass)
+  unsigned int* fk_ready;         // [n] k_fk_batch -> renderer readiness: the launch epoch once
+                                  // pose p's record, list and ntl are published (st.release)
+  unsigned int* fk_epoch;         // the batch launch's epoch (the renderer's last CTA advances it)
   int* near_list;                 // [n] particles whose primitives may cross z_near
   unsigned int* near_count;       // their number (reset by the near-plane pass)
   // persistent fit (k_fit): per-CTA sums [2][grid][4] and per-particle evaluated position +
@@ -215,6 +220,30 @@ __device__ __forceinline__ int atom_add_acq_rel_cta(int* p, int v) {
                : "r"(smem_u32(p)), "r"(v)
                : "memory");
   return old;
+}
+__device__ __forceinline__ int ld_acquire_cta_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_s32(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -348,10 +348,15 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    // timing mode: the renderer alone, launched after k_fk_batch completed (no PDL, so its
+    // first poses need no FK flags); otherwise it starts on the SMs k_fk_batch frees
+    cfg.numAttrs = tev ? 0 : 1;
+    EvalArgs ar = a;
+    ar.fk_wait = tev ? 0 : 1;
     const bool sums = a.sums_out != nullptr;
-    e = sums ? cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, false, true>, a, *map16)
-             : cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, false, false>, a, *map16);
+    e = sums ? cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, false, true>, ar, *map16)
+             : cudaLaunchKernelEx(&cfg, k_render_persist<kRenderWarps, false, false>, ar, *map16);
+    cfg.numAttrs = 1;
     if (e != cudaSuccess) return e;
     if (tev) cudaEventRecord(tev[2], st);  // the renderer alone (timing mode only)
     // the near-plane pass (exits at once when k_fk_batch queued nothing)
