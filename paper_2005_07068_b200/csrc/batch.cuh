@@ -265,6 +265,9 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
 // those (exact-solid path from their EXACT records; 16 x 8 tiles, box 16 x 8)
 // in a second, normally empty launch, so the near-plane code never shares a register
 // allocation with the hot loop.
+#ifndef HP_STATIC_FIRST
+#define HP_STATIC_FIRST 1  // CTA i's first poses are kSlots i + b (no atomic on the start path)
+#endif
 #ifndef HP_SLOTS
 #define HP_SLOTS 3  // particle slots per renderer CTA (FK record + block list each)
 #endif
@@ -327,7 +330,10 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
   // (the first poses, taken while k_fk_batch may still run) wait for its flag first
   auto issue = [&](int b, int kt, bool ready) {
     int p = a.n;
-    const unsigned k = kt >= 0 ? (unsigned)kt : atomicAdd(counter, 1u);
+    const unsigned k =
+        kt >= 0 ? (unsigned)kt
+                : atomicAdd(counter, 1u) +
+                      (!NEAR && HP_STATIC_FIRST ? (unsigned)kSlots * gridDim.x : 0u);
     if (NEAR) {
       if (k < __ldcg(a.near_count)) p = __ldcg(a.near_list + k);
     } else {
@@ -399,7 +405,8 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
     if (NEAR) asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
     epoch = NEAR ? 0u : __ldcg(a.fk_epoch);  // advanced only by the previous launch's end
-    const unsigned k0 = atomicAdd(counter, (unsigned)kSlots);
+    const unsigned k0 = NEAR || !HP_STATIC_FIRST ? atomicAdd(counter, (unsigned)kSlots)
+                                                 : (unsigned)kSlots * blockIdx.x;
     for (int b = 0; b < kSlots; b++) issue(b, (int)(k0 + b), NEAR || !HP_FK_PDL || !a.fk_wait);
   }
   if (NEAR || !HP_RAY_GLOBAL) {
