@@ -404,7 +404,9 @@ __global__ void __launch_bounds__(NW * 32, HP_MINB_WARPS / NW)
 #if HP_FK_PDL
     if (NEAR) asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
-    epoch = NEAR ? 0u : __ldcg(a.fk_epoch);  // advanced only by the previous launch's end
+    // this launch's FK epoch (advanced only by the previous launch's end); needed only when
+    // the first poses wait for their flags
+    epoch = NEAR || !a.fk_wait ? 0u : __ldcg(a.fk_epoch);
     const unsigned k0 = NEAR || !HP_STATIC_FIRST ? atomicAdd(counter, (unsigned)kSlots)
                                                  : (unsigned)kSlots * blockIdx.x;
     for (int b = 0; b < kSlots; b++) issue(b, (int)(k0 + b), NEAR || !HP_FK_PDL || !a.fk_wait);
