@@ -468,9 +468,12 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
       dd.len[f][i] = d.seg_len[f][i];
     }
     for (int i = 0; i < 4; i++) dd.rad[f][i] = d.radius[f][i];
-    for (int i = 0; i < 3; i++)
+    for (int i = 0; i < 3; i++) {
       dd.cone_k[f][i] = (dd.rad[f][i + 1] - dd.rad[f][i]) / dd.len[f][i];
+      dd.inv_hl[f][i] = 1.0 / (0.5 * dd.len[f][i]);
+    }
   }
+  dd.inv_hl_palm = 1.0 / (0.5 * d.palm_len);
   dd.th_x = d.thumb_ell_x;
   dd.th_z = d.thumb_ell_z;
   {  // R_T0 = Rz(yaw) Ry(pitch)

@@ -89,6 +89,8 @@ struct DimsD {
   double th_x, th_z;
   double RT0[3][3];  // thumb base frame Rz(yaw) Ry(pitch), host fp64
   double cone_k[5][3];  // (r_{k+1} - r_k) / L_k, the cone slopes (host fp64)
+  double inv_hl[5][3];  // 1 / (L_k / 2): the cones' inverse half lengths (host fp64)
+  double inv_hl_palm;   // 1 / (palm_len / 2)
 };
 
 struct CostD {

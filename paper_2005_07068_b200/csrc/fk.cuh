@@ -185,8 +185,8 @@ __device__ __forceinline__ void put3(float* r, int off, const double v[3]) {
 // point the kernel subtracts.  axial: cones / cylinder (the axial row of M and the half
 // length hl).
 __device__ __forceinline__ void write_fast_quadric(float* rec, const double cen[3], const double M[3][3],
-                                   const double q[3], double g2, double h, bool axial,
-                                   double hl) {
+                                   double q2, double g2, double h, bool axial,
+                                   double ihl) {
   double cl[3];
   for (int a = 0; a < 3; a++) cl[a] = M[a][0] * cen[0] + M[a][1] * cen[1] + M[a][2] * cen[2];
   float xp = 0.f, yp = 0.f;  // any fp32 point will do (the coefficients are computed for it)
@@ -202,8 +202,8 @@ __device__ __forceinline__ void write_fast_quadric(float* rec, const double cen[
     m1[a] = M[a][1];
     dl[a] = M[a][0] * dp[0] + M[a][1] * dp[1] + M[a][2];
   }
-  auto QX = [&](const double u[3], const double v[3]) {
-    return q[0] * u[0] * v[0] + q[1] * u[1] * v[1] + q[2] * u[2] * v[2];
+  auto QX = [&](const double u[3], const double v[3]) {  // Q = diag(1, 1, q2)
+    return u[0] * v[0] + u[1] * v[1] + q2 * u[2] * v[2];
   };
   const double A[6] = {QX(dl, dl), 2.0 * QX(m0, dl), 2.0 * QX(m1, dl),
                        QX(m0, m0), 2.0 * QX(m0, m1), QX(m1, m1)};
@@ -222,7 +222,7 @@ __device__ __forceinline__ void write_fast_quadric(float* rec, const double cen[
   rec[kFb + 2] = (float)(by * ic0);
   rec[kFic0] = (float)ic0;
   if (axial) {
-    const double ih = 1.0 / hl;
+    const double ih = ihl;  // 1 / the half length (host fp64)
     rec[kFlz + 0] = (float)(M[2][0] * ih);
     rec[kFlz + 1] = (float)(M[2][1] * ih);
     rec[kFlz + 2] = (float)(M[2][2] * ih);
@@ -369,7 +369,7 @@ __device__ __forceinline__ void build_fast(int j, const FkScratch& s, const Dims
                                            float* rec) {
   // the kinds differ only in the quadric's frame and coefficients: one write_fast_quadric
   // call after the branches, so a warp holding several kinds runs its arithmetic once
-  double c[3], M[3][3], q[3], g2, h, hl;
+  double c[3], M[3][3], q2, g2, h, ihl;  // Q = diag(1, 1, q2)
   bool axial;
   if (j < kCone0) {  // sphere at joint (f, k): |p - c|^2 - r^2, M = I
     const int f = j >> 2, k = j & 3;
@@ -378,13 +378,11 @@ __device__ __forceinline__ void build_fast(int j, const FkScratch& s, const Dims
       c[i] = s.J[f][k][i];
       for (int a = 0; a < 3; a++) M[a][i] = a == i ? 1.0 : 0.0;
     }
-    q[0] = 1.0;
-    q[1] = 1.0;
-    q[2] = 1.0;
+    q2 = 1.0;
     g2 = 0.0;
     h = -r * r;
     axial = false;
-    hl = 0.0;
+    ihl = 0.0;
   } else if (j < kCyl) {  // truncated cone J_k -> J_{k+1}: rows e1, e2, axis; midpoint origin
     int f, k;
     if (j < 32) {
@@ -402,13 +400,11 @@ __device__ __forceinline__ void build_fast(int j, const FkScratch& s, const Dims
     }
     // x^2 + y^2 - (r_m + k z)^2: Q = diag(1, 1, -k^2), g = (0, 0, -r_m k), h = -r_m^2
     const double rm = 0.5 * (dm.rad[f][k] + dm.rad[f][k + 1]), kk = dm.cone_k[f][k];
-    q[0] = 1.0;
-    q[1] = 1.0;
-    q[2] = -kk * kk;
+    q2 = -kk * kk;
     g2 = -rm * kk;
     h = -rm * rm;
     axial = true;
-    hl = 0.5 * dm.len[f][k];
+    ihl = dm.inv_hl[f][k];
   } else if (j == kCyl) {  // palm: (x/a)^2 + (z/b)^2 - 1, axial y_H in [-len, 0]
     const double iw = 1.0 / dm.palm_half_w, it = 1.0 / dm.palm_half_t;
     for (int i = 0; i < 3; i++) {
@@ -417,13 +413,11 @@ __device__ __forceinline__ void build_fast(int j, const FkScratch& s, const Dims
       M[2][i] = s.RW[i][1];
       c[i] = s.h[i] - 0.5 * dm.palm_len * s.RW[i][1];
     }
-    q[0] = 1.0;
-    q[1] = 1.0;
-    q[2] = 0.0;
+    q2 = 0.0;
     g2 = 0.0;
     h = -1.0;
     axial = true;
-    hl = 0.5 * dm.palm_len;
+    ihl = dm.inv_hl_palm;
   } else {  // ellipsoids: |l|^2 - 1 with rows = axes / semi-axes
     double sd[3];
     if (j == kEll0) {
@@ -446,15 +440,13 @@ __device__ __forceinline__ void build_fast(int j, const FkScratch& s, const Dims
       const double is = 1.0 / sd[a];
       for (int i = 0; i < 3; i++) M[a][i] *= is;
     }
-    q[0] = 1.0;
-    q[1] = 1.0;
-    q[2] = 1.0;
+    q2 = 1.0;
     g2 = 0.0;
     h = -1.0;
     axial = false;
-    hl = 0.0;
+    ihl = 0.0;
   }
-  write_fast_quadric(rec, c, M, q, g2, h, axial, hl);
+  write_fast_quadric(rec, c, M, q2, g2, h, axial, ihl);
 }
 
 #if HP_FK_PROF
