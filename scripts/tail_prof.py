@@ -49,9 +49,3 @@ term = (r[:, 16].astype(np.float64) - t0)
 print("first terminator claim (us): min %.2f median %.2f max %.2f" % (term.min() / 1e3, np.median(term) / 1e3, term.max() / 1e3))
 rem = cta_end - term
 print("CTA end - its first terminator (us): p10 %.2f p50 %.2f p90 %.2f max %.2f" % tuple(np.percentile(rem, q) / 1e3 for q in (10, 50, 90, 100)))
-# per-particle vs per-block cost: CTA busy time ~ a * blocks + b * particles (CTAs whose
-# first pose started after FK, i.e. all of them run from the common FK end to their end)
-busy = cta_end - np.median(st[:, 0] if st.ndim > 1 else st)
-X = np.stack([r[:, 11].astype(np.float64), r[:, 10].astype(np.float64)], axis=1)
-coef, *_ = np.linalg.lstsq(X, busy, rcond=None)
-print("fit: CTA busy (us) = %.4f x blocks + %.3f x particles" % (coef[0] / 1e3, coef[1] / 1e3))
