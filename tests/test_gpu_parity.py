@@ -565,3 +565,30 @@ def test_anisotropic_off_centre_camera_batch_split_and_oracle():
     co, so, _, _ = oracle_eval(obs, swarm[sample])
     check_sample(sums, c64, so, co, swarm, sample, cam, obs, max_edge=2)
     ctx.close()
+
+
+def test_batch_path_back_to_back_batches_never_see_stale_fk_output():
+    """The renderer starts under k_fk_batch (PDL) and its first poses wait for per-pose ready
+    flags that hold the launch's epoch: back-to-back batches of different poses
+    and sizes through one context must give exactly the bits each batch gives in a fresh
+    context — a stale flag would hand the renderer the previous batch's records."""
+    obs = obs_for(W.H_A, 640, 480)
+    a = W.swarm_c4(4096, seed=7068).astype(np.float32)
+    b = W.swarm_c4(4096, seed=11).astype(np.float32)
+    c = W.cold_box(4096, seed=12).astype(np.float32)
+    seq = [a, b, b[:1500], c, a[:2600], b, c, a]
+    ref = {}
+    for i, X in enumerate(seq):
+        fresh = hp.Context(640, 480, max_particles=4096)
+        fresh.set_observation(obs.depth, obs.mask)
+        ref[i] = fresh.eval_costs(torch.tensor(X, device="cuda")).cpu().numpy()
+        assert fresh.last_launch_count() == 3, "batch path not taken"
+        fresh.close()
+    ctx = hp.Context(640, 480, max_particles=4096)
+    ctx.set_observation(obs.depth, obs.mask)
+    for rep in range(2):
+        for i, X in enumerate(seq):
+            got = ctx.eval_costs(torch.tensor(X, device="cuda")).cpu().numpy()
+            assert ctx.last_launch_count() == 3
+            assert np.array_equal(got, ref[i]), (rep, i)
+    ctx.close()
