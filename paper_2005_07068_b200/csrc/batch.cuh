@@ -7,13 +7,16 @@ namespace hp {
 
 // ---------------------------------------------------------------------------------------
 // Two-kernel batch path for large swarms.
-//   k_fk_batch      : one warp per particle — FK (fp64) and the particle's list of
+//   k_fk_batch      : four particles per CTA — FK (fp64) and each particle's list of
 //                     non-empty 16 x 16 blocks with the cull masks of their two 16 x 8
-//                     halves, written to global memory (L2-resident).
+//                     halves, written to global memory (L2-resident), then a per-particle
+//                     ready flag (the launch epoch, st.release).
 //   k_render_persist: persistent CTAs, ALL warps render.  Per particle one thread pulls the
 //                     FK record and tile list into shared memory with 1-D TMA bulk copies
-//                     (double-buffered: particle i + 2 is fetched as soon as particle i is
-//                     finished, while i + 1 renders), so no warp ever waits on FK latency.
+//                     (three slots: particle i + 3 is fetched as soon as particle i is
+//                     finished, while i + 1 and i + 2 render), so no warp waits on FK
+//                     latency; launched under k_fk_batch (PDL), its first particles wait
+//                     for their own flags, not for the whole FK grid.
 // ---------------------------------------------------------------------------------------
 // A tile (qx, qy) overlaps primitive j iff column qx's x-range and row qy's y-range both
 // overlap box j — the same four compares as cull_tile — so the tile masks are the AND of

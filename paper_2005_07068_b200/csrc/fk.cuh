@@ -557,18 +557,16 @@ __device__ __forceinline__ void fk_finger_chain(FkScratch& s, const DimsD& dm, i
     }
   }
 
-// FK on a team of 1 or 2 warps (warp 0 = the team leader).  pose: 26 values (float or
+// FK on a team of 1, 4 or 5 warps (warp 0 = the team leader).  pose: 26 values (float or
 // double).  Writes `out`; `s` keeps the fp64 joints for the debug hook.
 //   phase A (warp 0): load the pose, sincos of the 23 angles (one per lane, fp64)
 //   phase B (warp 0, lanes 0..4): the finger chains directly in the camera frame with
 //           sparse column updates: B <- B Rz(MPz) touches columns 0, 1, B <- B Rx(t)
 //           columns 1, 2 (the segment runs along -B[:,1])
-//   phase C: the 38 records + fp32 screen boxes (TEAM 2: spheres on warp 0, the rest on
-//           warp 1; TEAM 3: spheres | cones | cylinder + ellipsoids, one kind per warp, so no
-//           warp serialises the branches of several kinds;
-//           warp 1, in parallel), then the union box, the near-plane flag and kc(h)
+//   phase C: the 38 FAST records + fp32 screen boxes, one kind of work per warp (TEAM 4 / 5,
+//           below), then on warp 0 the union box, the near-plane flag and kc(h)
 // xrec (may be null): also keep the EXACT records (the near-plane path's) — TEAM >= 2
-// always, TEAM 1 (k_fk_batch, xrec in global memory) only for a pose that is not near_ok.
+// when given, TEAM 1 (the debug hook) only for a pose that is not near_ok.
 // shp (may be null): the cones' tile-list capsules [kNcone] (cone_capsule).
 // out.rec holds the FAST records on return.
 template <typename PoseT, int TEAM>
@@ -599,8 +597,8 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
   FKPROF(2)
   // ---- phase C: records + boxes ----
   if (TEAM >= 2) {
-    // TEAM 4: warp 0 the 20 spheres' EXACT records + boxes, warp 1 the 14 cones' and warp 2
-    // the cylinder's + 3 ellipsoids' (EXACT records into xrec, boxes), warp 3 the 18 FAST
+    // TEAM 4: warp 0 the 20 spheres' boxes (+ EXACT records into xrec when it is given),
+    // warp 1 the 14 cones', warp 2 the cylinder's + 3 ellipsoids', warp 3 the 18 FAST
     // quadric records straight from the frames, and warp 2's idle lanes the 20 spheres'
     // FAST records, all in parallel (no warp builds two records per lane)
     // TEAM 5: the spheres' FAST records on warp 4 instead (warp 2: the boxes only)
