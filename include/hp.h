@@ -315,7 +315,9 @@ int64_t hp_last_launch_count(const hp_ctx* ctx);
    first launch (k_fk_batch; 0 on single-launch paths), ms[1] = the renderer / fused kernel
    alone, ms[2] = the near-plane pass (0 on single-launch paths).  HP_ERR_STATE if no timed
    evaluation was enqueued since timing was switched on.  Timing adds event records between
-   the launches (the programmatic-dependent-launch overlap between them is lost); leave it off
+   the launches and launches the renderer after k_fk_batch has completed (no programmatic
+   dependent launch, so its first poses skip the per-pose FK ready flags): ms[1] is the
+   renderer alone, and the FK / render overlap of the untimed path is lost; leave it off
    outside measurement. */
 hp_status hp_set_timing(hp_ctx* ctx, int32_t on);
 hp_status hp_last_kernel_ms(hp_ctx* ctx, float ms[3]);
