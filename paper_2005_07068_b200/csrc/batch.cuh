@@ -149,9 +149,26 @@ static_assert(kFkWarps == 4, "k_fk_batch's work lists assume 4 poses per CTA");
 //   C" the 72 quadric records converted to the FAST layout (fp64), one pass
 //   D  per warp (= pose): union box, near-plane flag, kc; the record leaves by one bulk
 //      copy while the warp builds the pose's block list
+#if HP_FKB_PROF
+// clock64 stamps of k_fk_batch's phases (CTA 300, thread 0), staged in shared memory
+__device__ long long g_fkbprof[16];
+__device__ unsigned long long g_fkbcta[1024][2];  // per CTA: globaltimer at start / end
+__device__ __forceinline__ unsigned long long fkb_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define FKBPROF(i) \
+  if (blockIdx.x == 300 && threadIdx.x == 0) s_fkbp[i] = clock64();
+#else
+#define FKBPROF(i)
+#endif
 template <typename PoseT>
 __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
     k_fk_batch(const EvalArgs a) {
+#if HP_FKB_PROF
+  __shared__ long long s_fkbp[16];
+#endif
   __shared__ __align__(16) FkScratch s_fk[kFkWarps];
   __shared__ __align__(16) FkOut s_out[kFkWarps];
   __shared__ __align__(16) float4 s_shp[kFkWarps][kNcone];  // cone capsules
@@ -164,6 +181,10 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
 #endif
   const int p0 = blockIdx.x * kFkWarps;
   const int np = min(kFkWarps, a.n - p0);  // poses of this CTA (the last CTA may be short)
+  FKBPROF(0)
+#if HP_FKB_PROF
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_fkbcta[blockIdx.x][0] = fkb_gtime();
+#endif
   // ---- A: pose values and sincos ----
   if (tid < np * kNdof) {
     const int q = tid / kNdof, d = tid - q * kNdof;
@@ -172,6 +193,7 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
     if (d >= 3) sincos(v, &s_fk[q].sn[d], &s_fk[q].cs[d]);
   }
   __syncthreads();
+  FKBPROF(1)
   // ---- B: finger chains ----
   if (tid < np * 5) {
     const int q = tid / 5, f = tid - q * 5;
@@ -180,6 +202,7 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
     fk_finger_chain(s_fk[q], a.dims, f, bad);
   }
   __syncthreads();
+  FKBPROF(2)
   // ---- C: records + boxes, kind-sorted items: the sphere records (EXACT = FAST) and boxes,
   // the quadrics' boxes, then their FAST records straight from the frames (build_fast) ----
   constexpr int kNs = kFkWarps * kCone0, kNq = kFkWarps * (kNprim - kCone0);
@@ -218,6 +241,7 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
   // async proxy (the bulk copy in D) before the barrier
   fence_proxy_async();
   __syncthreads();
+  FKBPROF(3)
   // ---- C': a pose that may cross z_near (rare) keeps its EXACT records (global memory) ----
   if (warp < np) {
     int nok = 1;
@@ -234,7 +258,9 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
   if (warp >= np) return;  // warp-uniform; only warp-local synchronisation below
   // ---- D: per pose ----
   const int p = p0 + warp;
+  FKBPROF(4)
   fk_finish_warp(s_fk[warp], s_out[warp], a.cost.kc_rest);
+  FKBPROF(5)
   // the record leaves by one bulk copy while the warp builds the block list: every lane
   // orders its record writes before the async proxy, then lane 0 issues the copy
   fence_proxy_async();
@@ -245,6 +271,7 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
   const int cnt = build_block_list(s_out[warp],
                                    reinterpret_cast<BlockEnt*>(a.tiles_g) + (size_t)p * kMaxTiles, band,
                                    band + kMaxBand, s_shp[warp]);
+  FKBPROF(6)
   __syncwarp();  // the warp's list (and C' record) stores precede lane 0's release
   if (lane == 0) {
     int ntl = cnt;
@@ -259,6 +286,12 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
     fence_proxy_async_global();
     // publish: the renderer (already running, PDL) may take pose p from here on
     st_release_u32(a.fk_ready + p, __ldcg(a.fk_epoch));
+    FKBPROF(7)
+#if HP_FKB_PROF
+    if (blockIdx.x < 1024) atomicMax(&g_fkbcta[blockIdx.x][1], fkb_gtime());
+    if (blockIdx.x == 300 && threadIdx.x == 0)
+      for (int q = 0; q < 8; q++) g_fkbprof[q] = s_fkbp[q];
+#endif
   }
 }
 

@@ -423,6 +423,14 @@ cudaError_t launch_eval(const EvalArgs& a, bool pose_double, int mode, const CUt
   return cudaGetLastError();
 }
 
+#if HP_FKB_PROF
+extern "C" int hp_debug_fkb_prof(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_fkbprof, sizeof(g_fkbprof));
+}
+extern "C" int hp_debug_fkb_cta(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_fkbcta, sizeof(g_fkbcta));
+}
+#endif
 #if HP_TAIL_PROF
 extern "C" int hp_debug_tail_prof(unsigned long long* out) {
   return (int)cudaMemcpyFromSymbol(out, g_tailprof, sizeof(g_tailprof));
