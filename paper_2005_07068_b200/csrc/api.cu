@@ -485,6 +485,13 @@ hp_status hp_create(const hp_intrinsics* cam, const hp_hand_dims* dims, const hp
       for (int j = 0; j < 3; j++)
         dd.RT0[i][j] = Rz[i][0] * Ry[0][j] + Rz[i][1] * Ry[1][j] + Rz[i][2] * Ry[2][j];
   }
+  // inverse semi-axes (IEEE divisions here give the bits the kernels would compute)
+  dd.inv_sd[0][0] = 1.0 / dd.th_x;
+  dd.inv_sd[0][1] = 1.0 / (0.5 * dd.len[0][0]);
+  dd.inv_sd[0][2] = 1.0 / dd.th_z;
+  dd.inv_sd[1][0] = 1.0 / dd.palm_half_w;
+  dd.inv_sd[1][1] = 1.0 / dd.cap_half;
+  dd.inv_sd[1][2] = 1.0 / dd.palm_half_t;
   const hp_cost_params& c = ctx->cost;
   {
     CostD& cd = ctx->costd;

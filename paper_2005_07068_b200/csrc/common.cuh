@@ -91,6 +91,8 @@ struct DimsD {
   double cone_k[5][3];  // (r_{k+1} - r_k) / L_k, the cone slopes (host fp64)
   double inv_hl[5][3];  // 1 / (L_k / 2): the cones' inverse half lengths (host fp64)
   double inv_hl_palm;   // 1 / (palm_len / 2)
+  double inv_sd[2][3];  // inverse semi-axes: [0] the thumb ellipsoid (th_x, L_00 / 2, th_z),
+                        // [1] the palm caps / cylinder (palm_half_w, cap_half, palm_half_t)
 };
 
 struct CostD {

@@ -302,7 +302,7 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm,
     }
     put3(rec, kC, m);
     double rows[3][3];
-    const double iw = 1.0 / dm.palm_half_w, it = 1.0 / dm.palm_half_t;
+    const double iw = dm.inv_sd[1][0], it = dm.inv_sd[1][2];  // 1 / semi-axes (host)
     for (int i = 0; i < 3; i++) {
       rows[0][i] = cx[i] * iw;
       rows[1][i] = cz[i] * it;
@@ -347,7 +347,7 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm,
     }
     put3(rec, kC, c);
     for (int a = 0; a < 3; a++) {
-      const double is = 1.0 / sd[a];
+      const double is = dm.inv_sd[j == kEll0 ? 0 : 1][a];  // 1 / sd[a] (host)
       double row[3] = {cols[a][0] * is, cols[a][1] * is, cols[a][2] * is};
       put3(rec, kM + 3 * a, row);
       rec[kCl + a] = (float)(row[0] * c[0] + row[1] * c[1] + row[2] * c[2]);
@@ -406,7 +406,7 @@ __device__ __forceinline__ void build_fast(int j, const FkScratch& s, const Dims
     axial = true;
     ihl = dm.inv_hl[f][k];
   } else if (j == kCyl) {  // palm: (x/a)^2 + (z/b)^2 - 1, axial y_H in [-len, 0]
-    const double iw = 1.0 / dm.palm_half_w, it = 1.0 / dm.palm_half_t;
+    const double iw = dm.inv_sd[1][0], it = dm.inv_sd[1][2];  // 1 / semi-axes (host)
     for (int i = 0; i < 3; i++) {
       M[0][i] = s.RW[i][0] * iw;
       M[1][i] = s.RW[i][2] * it;
@@ -418,26 +418,19 @@ __device__ __forceinline__ void build_fast(int j, const FkScratch& s, const Dims
     h = -1.0;
     axial = true;
     ihl = dm.inv_hl_palm;
-  } else {  // ellipsoids: |l|^2 - 1 with rows = axes / semi-axes
-    double sd[3];
+  } else {  // ellipsoids: |l|^2 - 1 with rows = axes / semi-axes (dm.inv_sd)
     if (j == kEll0) {
       for (int i = 0; i < 3; i++) c[i] = 0.5 * (s.J[0][0][i] + s.J[0][1][i]);
       for (int a = 0; a < 3; a++)
         for (int i = 0; i < 3; i++) M[a][i] = s.Rs[0][0][i][a];
-      sd[0] = dm.th_x;
-      sd[1] = 0.5 * dm.len[0][0];
-      sd[2] = dm.th_z;
     } else {
       const double yc = j == kEll0 + 1 ? 0.0 : -dm.palm_len;
       for (int i = 0; i < 3; i++) c[i] = s.h[i] + yc * s.RW[i][1];
       for (int a = 0; a < 3; a++)
         for (int i = 0; i < 3; i++) M[a][i] = s.RW[i][a];
-      sd[0] = dm.palm_half_w;
-      sd[1] = dm.cap_half;
-      sd[2] = dm.palm_half_t;
     }
     for (int a = 0; a < 3; a++) {
-      const double is = 1.0 / sd[a];
+      const double is = dm.inv_sd[j == kEll0 ? 0 : 1][a];  // 1 / sd[a] (host)
       for (int i = 0; i < 3; i++) M[a][i] *= is;
     }
     q2 = 1.0;
