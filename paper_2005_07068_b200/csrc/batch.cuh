@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kFkWarps * 32, 32 / kFkWarps)
         float zmin;
         if (j < kCone0) {  // a sphere: box (the EXACT record is discarded), then FAST record
           build_prim(j, s_fk[q], a.dims, a.cam, s_out[q].rec[j], s_out[q].box[j], zmin);
-          build_fast(j, s_fk[q], a.dims, s_out[q].rec[j]);
+          build_fast_sphere(j, s_fk[q], a.dims, s_out[q].rec[j]);
         } else {  // a quadric's EXACT record is not kept here (see C')
           float xr[kRec];
           build_prim(j, s_fk[q], a.dims, a.cam, xr, s_out[q].box[j], zmin,

@@ -365,6 +365,21 @@ __device__ void build_prim(int j, const FkScratch& s, const DimsD& dm,
 // FAST record of primitive j straight from the fp64 FK geometry (the same frames build_prim
 // uses), independent of the EXACT record and the box, so a team can build both in
 // parallel.
+// The sphere at joint (f, k) = primitive j < kCone0: |p - c|^2 - r^2 with M = I, Q = I —
+// its own call, so the constants fold (the general builder's runtime M = I would cost a full
+// quadric expansion); the same values as build_fast's sphere branch.
+__device__ __forceinline__ void build_fast_sphere(int j, const FkScratch& s, const DimsD& dm,
+                                                  float* rec) {
+  const int f = j >> 2, k = j & 3;
+  const double r = dm.rad[f][k];
+  double c[3], M[3][3];
+  for (int i = 0; i < 3; i++) {
+    c[i] = s.J[f][k][i];
+    for (int a = 0; a < 3; a++) M[a][i] = a == i ? 1.0 : 0.0;
+  }
+  write_fast_quadric(rec, c, M, 1.0, 0.0, -r * r, false, 0.0);
+}
+
 __device__ __forceinline__ void build_fast(int j, const FkScratch& s, const DimsD& dm,
                                            float* rec) {
   // the kinds differ only in the quadric's frame and coefficients: one write_fast_quadric
@@ -598,10 +613,10 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
     if (w == 3) {
       if (lane < kNprim - kCone0) build_fast(kCone0 + lane, s, dm, out.rec[kCone0 + lane]);
     } else if (w == 4) {
-      if (lane < kCone0) build_fast(lane, s, dm, out.rec[lane]);
+      if (lane < kCone0) build_fast_sphere(lane, s, dm, out.rec[lane]);
     } else if (TEAM == 4 && w == 2 && lane >= kNprim - kCyl) {
       const int j = lane - (kNprim - kCyl);  // lanes 4..23: spheres 0..19
-      if (j < kCone0) build_fast(j, s, dm, out.rec[j]);
+      if (j < kCone0) build_fast_sphere(j, s, dm, out.rec[j]);
     } else {
       const int j0 = w == 0 ? 0 : (w == 1 ? kCone0 : kCyl);
       const int j1 = w == 0 ? kCone0 : (w == 1 ? kCyl : kNprim);
@@ -645,7 +660,7 @@ __device__ void fk_team(const PoseT* pose, const DimsD& dm, const CamParams& cam
               reinterpret_cast<const float4*>(out.rec)[i];
     }
     if (lane < kNprim - kCone0) build_fast(kCone0 + lane, s, dm, out.rec[kCone0 + lane]);
-    if (lane < kCone0) build_fast(lane, s, dm, out.rec[lane]);  // spheres (EXACT copied above)
+    if (lane < kCone0) build_fast_sphere(lane, s, dm, out.rec[lane]);  // (EXACT copied above)
     __syncwarp();
   }
   FKPROF(3)
