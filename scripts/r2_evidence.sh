@@ -16,3 +16,4 @@ bash scripts/prof_fit.sh r2
 python scripts/fit_time.py > gpurun_out/r2_fit_time.txt 2>&1
 [ -e build_prof/tail.so ] && HP_LIB=build_prof/tail.so timeout 120 python scripts/tail_prof.py > gpurun_out/r2_tail.txt 2>&1
 [ -e build_prof/genprof.so ] && HP_LIB=build_prof/genprof.so timeout 120 python scripts/fit_prof.py > gpurun_out/r2_fit_phases.txt 2>&1
+[ -e build_prof/fkb.so ] && HP_LIB=build_prof/fkb.so timeout 120 python scripts/fkb_prof.py > gpurun_out/r2_fk_phases.txt 2>&1
